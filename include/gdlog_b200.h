@@ -1,0 +1,355 @@
+/*
+ * gdlog_b200.h — C-ABI of the B200-native GDlog semi-naive fixpoint hot path.
+ *
+ * This is the drop-in boundary.  The reference (`arraylog`,
+ * /root/reference/proj/include/arraylog) has no FFI of its own: its boundary
+ * is a header-only C++ API.  Every entry point below replaces one reference
+ * function or method; the replaced interface is cited as  file:line  relative
+ * to proj/include/arraylog/.  The C++ wrapper that restores the reference
+ * signatures on top of this ABI is include/arraylog_b200/arraylog_b200.hpp,
+ * the Python mirror is paper_2311_02206_b200/arraylog.py.
+ *
+ * Conventions
+ *  - No exceptions cross the boundary.  Every call returns a gd_status; the
+ *    message of the last failure is gd_last_error(ctx), and for
+ *    GD_ERR_BUDGET the phase name ("index", "join", "dedup", "difference",
+ *    "merge", "other") is gd_last_error_phase(ctx).  The status codes map
+ *    1:1 to the reference's exception types (types.hpp:19-72).
+ *  - Tuples cross the boundary as flat row-major uint64_t arrays
+ *    (tuple_array::data, tuple_array.hpp:19-51) plus a row count and an
+ *    arity; `canonical` flags mirror tuple_array::canonical.
+ *  - "host" pointers are ordinary CPU memory (pinned or pageable); the
+ *    `_device` variants take device pointers on the context's device.
+ *  - All device work is ordered on the context's stream.  A context (and the
+ *    engines created from it) is not thread-safe: one host thread per ctx,
+ *    like the reference's single-threaded orchestration (engine.hpp:34-39).
+ *  - `workers` / `stride_rows` knobs are accepted and ignored: results never
+ *    depend on them (acceptance criterion 7).
+ */
+#ifndef GDLOG_B200_H
+#define GDLOG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GD_ABI_VERSION 1
+
+/* Fixed maxima of the plan blob (plan.hpp:18-58).  The built-in programs
+ * (builtins.hpp:13-41) need arity 2, 2 steps, 3 variants, 1 filter. */
+#define GD_MAX_ARITY 8
+#define GD_MAX_FILTERS 8
+#define GD_MAX_STEPS 6
+#define GD_MAX_VARIANTS 8
+
+typedef enum gd_status {
+    GD_OK = 0,
+    GD_ERR_LOGIC = 1,       /* std::logic_error: precondition / internal fault */
+    GD_ERR_CONFIG = 2,      /* config_error   (types.hpp:19)  */
+    GD_ERR_USAGE = 3,       /* usage_error    (types.hpp:24)  */
+    GD_ERR_LOAD = 4,        /* load_error     (types.hpp:29)  */
+    GD_ERR_PLAN = 5,        /* plan_error     (types.hpp:34)  */
+    GD_ERR_BUDGET = 6,      /* budget_error   (types.hpp:40-72), phase via gd_last_error_phase */
+    GD_ERR_CUDA = 7,        /* CUDA runtime failure (no reference equivalent) */
+    GD_ERR_UNSUPPORTED = 8, /* shape the device encoding cannot hold */
+    GD_ERR_INVALID_ARG = 9  /* null pointer / bad handle at the C boundary */
+} gd_status;
+
+/* ------------------------------------------------------------------ */
+/* Context                                                              */
+
+typedef struct gd_ctx gd_ctx;
+
+/* Creates a context on CUDA device `device`.  `stream` is a cudaStream_t
+ * (0 = create a private non-blocking stream).  Fails with GD_ERR_CUDA when
+ * no device is present: there is no CPU fallback. */
+gd_status gd_ctx_create(int device, void* stream, gd_ctx** out);
+gd_status gd_ctx_destroy(gd_ctx* ctx);
+const char* gd_last_error(const gd_ctx* ctx);
+const char* gd_last_error_phase(const gd_ctx* ctx);
+int gd_abi_version(void);
+/* Number of kernels this context has launched (for the bench's gpu_launches). */
+uint64_t gd_ctx_kernel_launches(const gd_ctx* ctx);
+gd_status gd_ctx_synchronize(gd_ctx* ctx);
+
+/* ------------------------------------------------------------------ */
+/* Join-spec and plan data (ra.hpp:18-66, plan.hpp:18-58)              */
+
+typedef enum gd_operand_kind {
+    GD_OUTER_COL = 0, /* operand::outer(c)    ra.hpp:25 */
+    GD_INNER_COL = 1, /* operand::inner(c)    ra.hpp:28 */
+    GD_CONSTANT = 2   /* operand::constant(v) ra.hpp:31 */
+} gd_operand_kind;
+
+typedef struct gd_operand {
+    uint32_t kind;   /* gd_operand_kind */
+    uint32_t column;
+    uint64_t value;
+} gd_operand;
+
+/* row_filter (ra.hpp:48-54): (lhs == rhs) must equal require_equal. */
+typedef struct gd_filter {
+    gd_operand lhs;
+    gd_operand rhs;
+    uint32_t require_equal;
+    uint32_t reserved;
+} gd_filter;
+
+/* join_step (plan.hpp:31-39). */
+typedef struct gd_join_step {
+    uint32_t inner_rel;                 /* relation id */
+    uint32_t join_column_count;         /* 0 = Cartesian */
+    uint32_t inner_perm[GD_MAX_ARITY];  /* first arity(inner_rel) entries used */
+    uint32_t proj_arity;
+    uint32_t nfilters;
+    gd_operand proj[GD_MAX_ARITY];
+    gd_filter filters[GD_MAX_FILTERS];
+} gd_join_step;
+
+typedef enum gd_version { GD_FULL = 0, GD_DELTA = 1 } gd_version; /* plan.hpp:18 */
+
+/* rule_variant (plan.hpp:43-50). nsteps == 0: select/project off the source. */
+typedef struct gd_variant {
+    uint32_t src_rel;
+    uint32_t src_version;               /* gd_version */
+    uint32_t src_perm[GD_MAX_ARITY];
+    uint32_t nsteps;
+    uint32_t sel_arity;
+    uint32_t nsel_filters;
+    uint32_t reserved;
+    gd_join_step steps[GD_MAX_STEPS];
+    gd_operand sel_proj[GD_MAX_ARITY];
+    gd_filter sel_filters[GD_MAX_FILTERS];
+} gd_variant;
+
+/* rule_plan (plan.hpp:52-58). */
+typedef struct gd_rule_plan {
+    uint32_t rule_index;
+    uint32_t head_rel;
+    uint32_t head_arity;
+    uint32_t recursive;
+    uint32_t nvariants;
+    uint32_t reserved;
+    gd_variant variants[GD_MAX_VARIANTS];
+} gd_rule_plan;
+
+/* ------------------------------------------------------------------ */
+/* Kernel-level entry points (unit parity; host buffers in and out)     */
+/* Each call uploads its inputs, runs the sm_100a kernels, downloads.   */
+
+/* slot_key() of the first `ncols` columns of each row (hash.hpp:28-60),
+ * bit-exact with the reference Murmur3 mix. out[n]. */
+gd_status gd_prefix_hash(gd_ctx* ctx, const uint64_t* rows, uint64_t n,
+                         uint32_t arity, uint32_t ncols, uint64_t* out);
+
+/* canonicalize (tuple_array.hpp:73-133): sort + dedup.  out has room for
+ * n*arity values; *out_n receives the distinct row count. */
+gd_status gd_canonicalize(gd_ctx* ctx, const uint64_t* rows, uint64_t n,
+                          uint32_t arity, uint64_t* out, uint64_t* out_n);
+
+/* permute_columns (ra.hpp:426-454). rel must be canonical. */
+gd_status gd_permute_columns(gd_ctx* ctx, const uint64_t* rows, uint64_t n,
+                             uint32_t arity, int canonical,
+                             const uint32_t* perm, uint32_t perm_len,
+                             uint64_t* out, uint64_t* out_n);
+
+/* group_starts (index_map.hpp:46-66). out_starts has room for n entries. */
+gd_status gd_group_starts(gd_ctx* ctx, const uint64_t* rows, uint64_t n,
+                          uint32_t arity, int canonical, uint32_t prefix_len,
+                          uint64_t* out_starts, uint64_t* out_count);
+
+/* build_index (index_map.hpp:74-124) + range_lookup (container.hpp:52-89):
+ * builds the device HISA index over the canonical rows, then answers one
+ * lookup per key (keys: nkeys x prefix_len row-major).  Also reports the
+ * index's slot_count() and occupied() (index_map.hpp:30-39). */
+gd_status gd_index_lookup(gd_ctx* ctx, const uint64_t* rows, uint64_t n,
+                          uint32_t arity, int canonical, uint32_t prefix_len,
+                          double load_factor, const uint64_t* keys,
+                          uint64_t nkeys, uint32_t key_len, uint64_t* out_start,
+                          uint64_t* out_count, uint64_t* out_slot_count,
+                          uint64_t* out_occupied);
+
+/* One side of a join_spec (ra.hpp:60-66): a relation_container with an
+ * optional index of prefix `index_prefix_len` (0 = no index). */
+typedef struct gd_container_view {
+    const uint64_t* rows;
+    uint64_t n;
+    uint32_t arity;
+    uint32_t canonical;
+    uint32_t index_prefix_len;
+    uint32_t reserved;
+    double load_factor;
+} gd_container_view;
+
+typedef struct gd_join_spec {
+    uint32_t join_column_count;
+    uint32_t proj_arity;
+    uint32_t nfilters;
+    uint32_t reserved;
+    gd_operand proj[GD_MAX_ARITY];
+    gd_filter filters[GD_MAX_FILTERS];
+} gd_join_spec;
+
+/* join_count (ra.hpp:141-182). */
+gd_status gd_join_count(gd_ctx* ctx, const gd_container_view* outer,
+                        const gd_container_view* inner,
+                        const gd_join_spec* spec, uint64_t* out_total);
+
+/* join_materialize (ra.hpp:189-263): out must hold exactly
+ * out_capacity_rows * proj_arity values; a mismatch with the join size is
+ * GD_ERR_LOGIC ("output capacity mismatch").  Row order equals the
+ * reference: outer-row order, then inner-range order. */
+gd_status gd_join_materialize(gd_ctx* ctx, const gd_container_view* outer,
+                              const gd_container_view* inner,
+                              const gd_join_spec* spec, uint64_t* out,
+                              uint64_t out_capacity_rows);
+
+/* select_project (ra.hpp:267-293). out room: n * proj_arity. */
+gd_status gd_select_project(gd_ctx* ctx, const uint64_t* rows, uint64_t n,
+                            uint32_t arity, const gd_operand* proj,
+                            uint32_t proj_arity, const gd_filter* filters,
+                            uint32_t nfilters, uint64_t* out, uint64_t* out_n);
+
+/* merge_sorted (ra.hpp:299-381): disjoint canonical union.  buffer_rows is
+ * the caller's merge-buffer capacity (too small -> GD_ERR_LOGIC); out holds
+ * (nf + nd) * arity values.  Overlapping inputs -> GD_ERR_LOGIC. */
+gd_status gd_merge_sorted(gd_ctx* ctx, const uint64_t* full, uint64_t nf,
+                          int full_canonical, const uint64_t* delta,
+                          uint64_t nd, int delta_canonical, uint32_t arity,
+                          uint64_t buffer_rows, uint64_t* out);
+
+/* difference (ra.hpp:386-422): rows of new_rel absent from full. */
+gd_status gd_difference(gd_ctx* ctx, const uint64_t* new_rows, uint64_t nn,
+                        int new_canonical, const uint64_t* full, uint64_t nf,
+                        int full_canonical, uint32_t arity, uint64_t* out,
+                        uint64_t* out_n);
+
+/* ------------------------------------------------------------------ */
+/* Engine (engine.hpp:25-277): the performance entry.                   */
+
+/* engine_config (engine.hpp:25-32). memory_budget_bytes = UINT64_MAX is
+ * "unlimited" (budget.hpp:19). */
+typedef struct gd_engine_config {
+    uint64_t memory_budget_bytes;
+    uint32_t ebm_enabled;
+    uint32_t alpha;
+    double load_factor;
+    uint32_t workers;     /* accepted, ignored */
+    uint32_t reserved;
+    uint64_t stride_rows; /* accepted, ignored */
+} gd_engine_config;
+
+/* run_stats (stats.hpp:21-46) plus device-only counters. phase_seconds is
+ * indexed in kPhaseOrder: index, join, dedup, difference, merge, other. */
+typedef struct gd_run_stats {
+    double phase_seconds[6];
+    double total_seconds;
+    uint64_t iterations;
+    uint64_t buffer_allocations;
+    uint64_t charge_events;
+    uint64_t peak_tracked_bytes;
+    uint64_t peak_temp_bytes;
+    /* device extras */
+    uint64_t join_tuples;        /* sum over all join steps of output rows */
+    uint64_t device_bytes_peak;  /* peak bytes held in the device arena */
+    double kernel_seconds[6];    /* CUDA-event time per phase */
+    uint64_t algo_bytes[6];      /* algorithmic HBM bytes per phase */
+} gd_run_stats;
+
+/* Per-iteration counters of one recursive relation:
+ * delta_in = |Δ| consumed, join = J rows appended, new_unique = N,
+ * delta_out = D, full_after = |F| after the merge. */
+typedef struct gd_iter_record {
+    uint64_t delta_in;
+    uint64_t join;
+    uint64_t new_unique;
+    uint64_t delta_out;
+    uint64_t full_after;
+} gd_iter_record;
+
+typedef struct gd_engine gd_engine;
+
+/* engine(program, engine_config) (engine.hpp:66-88).  Relations are ids
+ * 0..nrels-1 with their arities, an EDB flag (edb_decl, program.hpp:73) and
+ * their names (nullable: "r<id>").  Names only order the per-iteration
+ * copy refresh like the reference's name-keyed relation map
+ * (engine.hpp:209-210) and label errors. */
+gd_status gd_engine_create(gd_ctx* ctx, const gd_engine_config* cfg,
+                           uint32_t nrels, const uint32_t* arities,
+                           const uint32_t* is_edb, const char* const* names,
+                           gd_engine** out);
+gd_status gd_engine_destroy(gd_engine* eng);
+
+/* set_plans / override_plans (engine.hpp:97-101, 300-310). */
+gd_status gd_engine_set_plans(gd_engine* eng, const gd_rule_plan* plans,
+                              uint32_t nplans);
+
+/* load_edb (engine.hpp:107-128): rejects the kEmptySlot sentinel
+ * (GD_ERR_LOAD), canonicalizes when canonical == 0. */
+gd_status gd_engine_load_edb(gd_engine* eng, uint32_t rel,
+                             const uint64_t* rows, uint64_t n, int canonical);
+gd_status gd_engine_load_edb_device(gd_engine* eng, uint32_t rel,
+                                    const uint64_t* d_rows, uint64_t n,
+                                    int canonical);
+
+/* seed / iterate_to_fixpoint / run (engine.hpp:130-257). */
+gd_status gd_engine_seed(gd_engine* eng);
+gd_status gd_engine_iterate(gd_engine* eng);
+gd_status gd_engine_run(gd_engine* eng);
+
+/* relation(name) (engine.hpp:259-264): row count, then download into a
+ * host (or device) buffer of count*arity values. */
+gd_status gd_engine_relation_count(gd_engine* eng, uint32_t rel, uint64_t* n);
+gd_status gd_engine_relation_download(gd_engine* eng, uint32_t rel,
+                                      uint64_t* out, uint64_t capacity_rows);
+gd_status gd_engine_relation_download_device(gd_engine* eng, uint32_t rel,
+                                             uint64_t* d_out,
+                                             uint64_t capacity_rows);
+/* Order-independent 64-bit digest of a relation, computed on the device
+ * (sum of fmix64(row hash)); used by the bench to check full-size runs
+ * without a download. */
+gd_status gd_engine_relation_digest(gd_engine* eng, uint32_t rel,
+                                    uint64_t* digest);
+
+/* stats() (engine.hpp:270-277). */
+gd_status gd_engine_stats(gd_engine* eng, gd_run_stats* out);
+/* run_stats::delta_history entry of one recursive relation. */
+gd_status gd_engine_delta_history(gd_engine* eng, uint32_t rel, uint64_t* out,
+                                  uint64_t capacity, uint64_t* len);
+gd_status gd_engine_iter_log(gd_engine* eng, uint32_t rel, gd_iter_record* out,
+                             uint64_t capacity, uint64_t* len);
+/* Encoding chosen at seed time: bits per column, key words, dictionary. */
+gd_status gd_engine_encoding(gd_engine* eng, uint32_t* bits,
+                             uint32_t* key_words, uint32_t* dictionary);
+
+/* ------------------------------------------------------------------ */
+/* Hash-partitioned multi-GPU mode.                     */
+/* Every IDB tuple lives on rank owner(t) = fmix64(digest(t)) % nranks;  */
+/* EDB relations are replicated.  One iteration is split in two halves   */
+/* around the caller's all-to-all (NCCL via torch.distributed):           */
+/*   begin: joins on the local Δ, route rows to owners, local dedup;      */
+/*          send buffer = encoded keys grouped by destination rank.       */
+/*   end:   merge received keys into the local full; new local Δ.         */
+
+gd_status gd_engine_set_partition(gd_engine* eng, uint32_t rank,
+                                  uint32_t nranks);
+/* Number of 64-bit words per exchanged tuple (1 or 2). */
+gd_status gd_engine_exchange_words(gd_engine* eng, uint32_t* words);
+/* Runs the local half of one iteration.  send_counts[nranks] receives the
+ * row count for each destination; *d_send points to the device send
+ * buffer (valid until the next call). */
+gd_status gd_engine_partition_begin(gd_engine* eng, uint64_t* send_counts,
+                                    const void** d_send);
+gd_status gd_engine_partition_end(gd_engine* eng, const void* d_recv,
+                                  uint64_t recv_rows, uint64_t* local_delta);
+/* Global termination is decided by the caller (all-reduce of local Δ). */
+gd_status gd_engine_partition_finish(gd_engine* eng);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GDLOG_B200_H */

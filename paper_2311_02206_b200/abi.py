@@ -1,0 +1,226 @@
+"""ctypes mirror of include/gdlog_b200.h (the C-ABI of libgdlog_b200.so).
+
+Struct layouts here must match the header byte for byte; tests/test_abi.py
+checks the sizes against the C compiler's view.  Loading the library is
+explicit and loud: there is no CPU fallback for the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+GD_MAX_ARITY = 8
+GD_MAX_FILTERS = 8
+GD_MAX_STEPS = 6
+GD_MAX_VARIANTS = 8
+
+GD_OK = 0
+GD_ERR_LOGIC = 1
+GD_ERR_CONFIG = 2
+GD_ERR_USAGE = 3
+GD_ERR_LOAD = 4
+GD_ERR_PLAN = 5
+GD_ERR_BUDGET = 6
+GD_ERR_CUDA = 7
+GD_ERR_UNSUPPORTED = 8
+GD_ERR_INVALID_ARG = 9
+
+GD_OUTER_COL = 0
+GD_INNER_COL = 1
+GD_CONSTANT = 2
+GD_FULL = 0
+GD_DELTA = 1
+
+PHASES = ("index", "join", "dedup", "difference", "merge", "other")  # stats.hpp:15-16
+
+u32 = C.c_uint32
+u64 = C.c_uint64
+
+
+class gd_operand(C.Structure):
+    _fields_ = [("kind", u32), ("column", u32), ("value", u64)]
+
+
+class gd_filter(C.Structure):
+    _fields_ = [("lhs", gd_operand), ("rhs", gd_operand), ("require_equal", u32), ("reserved", u32)]
+
+
+class gd_join_step(C.Structure):
+    _fields_ = [
+        ("inner_rel", u32),
+        ("join_column_count", u32),
+        ("inner_perm", u32 * GD_MAX_ARITY),
+        ("proj_arity", u32),
+        ("nfilters", u32),
+        ("proj", gd_operand * GD_MAX_ARITY),
+        ("filters", gd_filter * GD_MAX_FILTERS),
+    ]
+
+
+class gd_variant(C.Structure):
+    _fields_ = [
+        ("src_rel", u32),
+        ("src_version", u32),
+        ("src_perm", u32 * GD_MAX_ARITY),
+        ("nsteps", u32),
+        ("sel_arity", u32),
+        ("nsel_filters", u32),
+        ("reserved", u32),
+        ("steps", gd_join_step * GD_MAX_STEPS),
+        ("sel_proj", gd_operand * GD_MAX_ARITY),
+        ("sel_filters", gd_filter * GD_MAX_FILTERS),
+    ]
+
+
+class gd_rule_plan(C.Structure):
+    _fields_ = [
+        ("rule_index", u32),
+        ("head_rel", u32),
+        ("head_arity", u32),
+        ("recursive", u32),
+        ("nvariants", u32),
+        ("reserved", u32),
+        ("variants", gd_variant * GD_MAX_VARIANTS),
+    ]
+
+
+class gd_container_view(C.Structure):
+    _fields_ = [
+        ("rows", C.c_void_p),
+        ("n", u64),
+        ("arity", u32),
+        ("canonical", u32),
+        ("index_prefix_len", u32),
+        ("reserved", u32),
+        ("load_factor", C.c_double),
+    ]
+
+
+class gd_join_spec(C.Structure):
+    _fields_ = [
+        ("join_column_count", u32),
+        ("proj_arity", u32),
+        ("nfilters", u32),
+        ("reserved", u32),
+        ("proj", gd_operand * GD_MAX_ARITY),
+        ("filters", gd_filter * GD_MAX_FILTERS),
+    ]
+
+
+class gd_engine_config(C.Structure):
+    _fields_ = [
+        ("memory_budget_bytes", u64),
+        ("ebm_enabled", u32),
+        ("alpha", u32),
+        ("load_factor", C.c_double),
+        ("workers", u32),
+        ("reserved", u32),
+        ("stride_rows", u64),
+    ]
+
+
+class gd_run_stats(C.Structure):
+    _fields_ = [
+        ("phase_seconds", C.c_double * 6),
+        ("total_seconds", C.c_double),
+        ("iterations", u64),
+        ("buffer_allocations", u64),
+        ("charge_events", u64),
+        ("peak_tracked_bytes", u64),
+        ("peak_temp_bytes", u64),
+        ("join_tuples", u64),
+        ("device_bytes_peak", u64),
+        ("kernel_seconds", C.c_double * 6),
+        ("algo_bytes", u64 * 6),
+    ]
+
+
+class gd_iter_record(C.Structure):
+    _fields_ = [
+        ("delta_in", u64),
+        ("join", u64),
+        ("new_unique", u64),
+        ("delta_out", u64),
+        ("full_after", u64),
+    ]
+
+
+P = C.c_void_p
+PU64 = C.POINTER(u64)
+PU32 = C.POINTER(u32)
+
+# name -> (restype, argtypes); the full exported surface of gdlog_b200.h.
+SIGNATURES = {
+    "gd_abi_version": (C.c_int, []),
+    "gd_ctx_create": (C.c_int, [C.c_int, P, C.POINTER(P)]),
+    "gd_ctx_destroy": (C.c_int, [P]),
+    "gd_last_error": (C.c_char_p, [P]),
+    "gd_last_error_phase": (C.c_char_p, [P]),
+    "gd_ctx_kernel_launches": (u64, [P]),
+    "gd_ctx_synchronize": (C.c_int, [P]),
+    "gd_prefix_hash": (C.c_int, [P, P, u64, u32, u32, P]),
+    "gd_canonicalize": (C.c_int, [P, P, u64, u32, P, PU64]),
+    "gd_permute_columns": (C.c_int, [P, P, u64, u32, C.c_int, P, u32, P, PU64]),
+    "gd_group_starts": (C.c_int, [P, P, u64, u32, C.c_int, u32, P, PU64]),
+    "gd_index_lookup": (C.c_int, [P, P, u64, u32, C.c_int, u32, C.c_double, P, u64, u32, P, P, PU64, PU64]),
+    "gd_join_count": (C.c_int, [P, C.POINTER(gd_container_view), C.POINTER(gd_container_view),
+                                C.POINTER(gd_join_spec), PU64]),
+    "gd_join_materialize": (C.c_int, [P, C.POINTER(gd_container_view), C.POINTER(gd_container_view),
+                                      C.POINTER(gd_join_spec), P, u64]),
+    "gd_select_project": (C.c_int, [P, P, u64, u32, C.POINTER(gd_operand), u32, C.POINTER(gd_filter), u32,
+                                    P, PU64]),
+    "gd_merge_sorted": (C.c_int, [P, P, u64, C.c_int, P, u64, C.c_int, u32, u64, P]),
+    "gd_difference": (C.c_int, [P, P, u64, C.c_int, P, u64, C.c_int, u32, P, PU64]),
+    "gd_engine_create": (C.c_int, [P, C.POINTER(gd_engine_config), u32, PU32, PU32, C.POINTER(C.c_char_p),
+                                   C.POINTER(P)]),
+    "gd_engine_destroy": (C.c_int, [P]),
+    "gd_engine_set_plans": (C.c_int, [P, C.POINTER(gd_rule_plan), u32]),
+    "gd_engine_load_edb": (C.c_int, [P, u32, P, u64, C.c_int]),
+    "gd_engine_load_edb_device": (C.c_int, [P, u32, P, u64, C.c_int]),
+    "gd_engine_seed": (C.c_int, [P]),
+    "gd_engine_iterate": (C.c_int, [P]),
+    "gd_engine_run": (C.c_int, [P]),
+    "gd_engine_relation_count": (C.c_int, [P, u32, PU64]),
+    "gd_engine_relation_download": (C.c_int, [P, u32, P, u64]),
+    "gd_engine_relation_download_device": (C.c_int, [P, u32, P, u64]),
+    "gd_engine_relation_digest": (C.c_int, [P, u32, PU64]),
+    "gd_engine_stats": (C.c_int, [P, C.POINTER(gd_run_stats)]),
+    "gd_engine_delta_history": (C.c_int, [P, u32, P, u64, PU64]),
+    "gd_engine_iter_log": (C.c_int, [P, u32, C.POINTER(gd_iter_record), u64, PU64]),
+    "gd_engine_encoding": (C.c_int, [P, PU32, PU32, PU32]),
+    "gd_engine_set_partition": (C.c_int, [P, u32, u32]),
+    "gd_engine_exchange_words": (C.c_int, [P, PU32]),
+    "gd_engine_partition_begin": (C.c_int, [P, P, C.POINTER(P)]),
+    "gd_engine_partition_end": (C.c_int, [P, P, u64, PU64]),
+    "gd_engine_partition_finish": (C.c_int, [P]),
+}
+
+PKG_DIR = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("GDLOG_B200_LIB", PKG_DIR / "lib" / "libgdlog_b200.so"))
+
+_lib = None
+
+
+def load_library(path: Path | str | None = None) -> C.CDLL:
+    """Loads libgdlog_b200.so (built in-tree by __graft_entry__.build()).
+
+    Raises RuntimeError when the library is missing: the product path has
+    no CPU fallback.
+    """
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"libgdlog_b200.so not found at {p}; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+    lib = C.CDLL(str(p))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib

@@ -1,0 +1,922 @@
+// engine.cu — the semi-naive fixpoint driver on the device
+// (engine::seed / iterate_to_fixpoint / refresh_copies / execute_chain /
+// merge_into_full, engine.hpp:137-542), templated on the packed key type.
+//
+// Per iteration, for every recursive relation:
+//   join   : join_probe (fused count+scan) + load-balanced materialize,
+//            written straight into the head's new-tuple accumulator;
+//   dedup  : onesweep radix sort of the accumulator (only significant bits);
+//   diff+merge: ONE merge-path pass: F' = F U N and Δ = unique(N) \ F
+//            (the adjacent-unique of canonicalize, difference and
+//            merge_sorted of the reference fused), into ping-pong buffers.
+// Indexed copies with a non-identity permutation are maintained
+// incrementally (sorted permuted Δ merged into the copy)
+// and their HISA index rebuilt; identity copies alias the full relation.
+// The logical-byte accountant and EBM bookkeeping replay the reference's
+// charges in the same order (accounting.h).
+#include <cstring>
+#include <set>
+
+#include "engine.h"
+#include "ops.h"
+
+namespace gd {
+
+namespace {
+
+inline u64 rb(u64 rows, u32 arity) { return rows * arity * 8ull; }  // tuple_array::byte_size
+
+inline bool is_identity(const u32* p, u32 k) {
+    for (u32 i = 0; i < k; ++i)
+        if (p[i] != i) return false;
+    return true;
+}
+
+using CopyKey = std::pair<std::vector<u32>, u32>;
+
+// Grows a device buffer to hold `need` elements, preserving the first
+// `keep` elements.
+template <typename K>
+void ensure_keep(Ctx& c, DevBuf<K>& b, u64 need, u64 keep) {
+    if (b.p && b.cap >= need) return;
+    u64 cap = std::max<u64>(need + need / 4, 1024);
+    DevBuf<K> nb(c, cap);
+    if (keep && b.p) c.d2d(nb.p, b.p, keep * sizeof(K));
+    b = std::move(nb);
+}
+template <typename K>
+void ensure_discard(Ctx& c, DevBuf<K>& b, u64 need) {
+    if (b.p && b.cap >= need) return;
+    b.reserve_discard(c, std::max<u64>(need + need / 4, 1024));
+}
+
+template <typename K>
+struct CopyState {
+    std::vector<u32> perm;
+    u32 prefix = 0;
+    bool identity = false;
+    DevBuf<K> rows, alt;
+    u64 n = 0;
+    DevIndex<K> index;
+    u64 bytes = 0;  // accounted container bytes (engine.hpp:44-47)
+    bool built = false;
+    u64 synced_gen = 0;
+};
+
+template <typename K>
+struct RelDev {
+    DevBuf<K> full, full_alt;
+    u64 full_n = 0;
+    DevBuf<K> delta, delta_alt;
+    u64 delta_n = 0;
+    DevBuf<K> new_acc;
+    u64 new_n = 0;
+    std::map<CopyKey, CopyState<K>> copies;
+    bool dirty = true;
+    u64 merge_gen = 0;
+    bool last_merge_was_delta = false;
+};
+
+template <typename K>
+class Impl final : public ImplBase {
+public:
+    explicit Impl(Engine& e) : E(e), c(e.c), bits(e.enc.e.bits) {
+        const u32 nrels = (u32)E.info_.size();
+        rels.resize(nrels);
+        // Constant encodings (every plan constant is in the dictionary).
+        for (const auto& p : E.plans_) for_each_constant(p, [&](u64 v) { encode_const(v); });
+        // Indexed copies registered by set_plans (engine.hpp:300-310).
+        for (const auto& p : E.plans_)
+            for (u32 v = 0; v < p.nvariants; ++v)
+                for (u32 s = 0; s < p.variants[v].nsteps; ++s) {
+                    const gd_join_step& st = p.variants[v].steps[s];
+                    const u32 ar = E.info_[st.inner_rel].arity;
+                    CopyKey key{std::vector<u32>(st.inner_perm, st.inner_perm + ar), st.join_column_count};
+                    auto& cp = rels[st.inner_rel].copies[key];
+                    cp.perm = key.first;
+                    cp.prefix = key.second;
+                    cp.identity = is_identity(st.inner_perm, ar);
+                }
+        // EDB rows: pack under the engine encoding; order is preserved, so
+        // canonical raw rows stay canonical (no re-sort).
+        for (u32 r = 0; r < nrels; ++r) {
+            if (!E.info_[r].is_edb) continue;
+            const u64 n = E.raw_n[r];
+            auto& st = rels[r];
+            ensure_discard(c, st.full, n);
+            if (n) pack_rows<K>(c, E.raw[r].p, n, E.info_[r].arity, E.enc.e, st.full.p);
+            st.full_n = n;
+            E.raw[r].release();
+        }
+    }
+
+    // ------------------------------------------------------------------
+    void seed() override {
+        // nonrecursive_topo_order, engine.hpp:322-353
+        std::vector<u32> nonrec;
+        for (u32 i = 0; i < E.plans_.size(); ++i)
+            if (!E.plans_[i].recursive) nonrec.push_back(i);
+        std::vector<bool> done(nonrec.size(), false);
+        size_t ndone = 0;
+        while (ndone < nonrec.size()) {
+            bool progressed = false;
+            for (size_t i = 0; i < nonrec.size(); ++i) {
+                if (done[i]) continue;
+                const gd_rule_plan& pi = E.plans_[nonrec[i]];
+                bool ready = true;
+                for (size_t j = 0; j < nonrec.size() && ready; ++j) {
+                    if (done[j] || j == i) continue;
+                    const u32 h = E.plans_[nonrec[j]].head_rel;
+                    if (!E.info_[h].is_edb && reads(pi, h)) ready = false;
+                }
+                if (!ready) continue;
+                done[i] = true;
+                ++ndone;
+                progressed = true;
+                seed_rule(pi);
+            }
+            if (!progressed) throw_logic("nonrecursive rules form a dependency cycle");
+        }
+        // delta := full for every IDB (engine.hpp:170-174)
+        for (u32 r = 0; r < rels.size(); ++r) {
+            if (E.info_[r].is_edb) continue;
+            auto& st = rels[r];
+            ensure_discard(c, st.delta, st.full_n);
+            if (st.full_n) c.d2d(st.delta.p, st.full.p, st.full_n * sizeof(K));
+            assign_delta(r, st.full_n, "other");
+            st.delta_n = st.full_n;
+        }
+        check_temp_watermark();
+        if (E.nranks > 1) keep_owned();
+    }
+
+    // Partitioned mode: each rank keeps the IDB tuples it owns
+    // (owner = hash(tuple) % nranks); EDB relations stay replicated.
+    void keep_owned() {
+        for (u32 r = 0; r < rels.size(); ++r) {
+            if (E.info_[r].is_edb) continue;
+            auto& st = rels[r];
+            if (st.full_n == 0) continue;
+            DevBuf<u32> own(c, st.full_n);
+            DevBuf<uint8_t> flags(c, st.full_n);
+            owner_of<K>(c, st.full.p, st.full_n, E.nranks, own.p);
+            owner_flags(c, own.p, st.full_n, E.rank, flags.p);
+            DevBuf<K> kept(c, st.full_n);
+            const u64 m = compact_flagged<K>(c, st.full.p, flags.p, st.full_n, kept.p);
+            st.full.swap(kept);
+            st.full_n = m;
+            ensure_discard(c, st.delta, m);
+            if (m) c.d2d(st.delta.p, st.full.p, m * sizeof(K));
+            st.delta_n = m;
+        }
+    }
+
+    void iterate() override {
+        std::vector<u32> rec;
+        for (const auto& p : E.plans_)
+            if (p.recursive && std::find(rec.begin(), rec.end(), p.head_rel) == rec.end()) rec.push_back(p.head_rel);
+        // refresh order = the reference's name-keyed map order
+        std::vector<u32> by_name(rels.size());
+        for (u32 i = 0; i < by_name.size(); ++i) by_name[i] = i;
+        std::sort(by_name.begin(), by_name.end(),
+                  [&](u32 a, u32 b) { return E.info_[a].name < E.info_[b].name; });
+
+        for (;;) {
+            bool active = false;
+            for (u32 r : rec) active |= rels[r].delta_n > 0;
+            if (!active) break;
+            ++E.iterations;
+            std::vector<u64> delta_in(rec.size());
+            for (size_t i = 0; i < rec.size(); ++i) {
+                delta_in[i] = rels[rec[i]].delta_n;
+                E.info_[rec[i]].history.push_back(delta_in[i]);
+            }
+            // (1) refresh indexed copies
+            for (u32 r : by_name)
+                if (rels[r].dirty) refresh_copies(r);
+            // (2) every variant of every recursive rule on the deltas
+            std::vector<u64> joined(rels.size(), 0);
+            for (const auto& p : E.plans_) {
+                if (!p.recursive) continue;
+                auto& head = rels[p.head_rel];
+                for (u32 v = 0; v < p.nvariants; ++v) {
+                    const gd_variant& var = p.variants[v];
+                    if (var.src_version == GD_DELTA && rels[var.src_rel].delta_n == 0) continue;
+                    u64 m = 0;
+                    execute_chain(var, head.new_acc, head.new_n, &m);
+                    joined[p.head_rel] += m;
+                    append_new(p.head_rel, m);
+                }
+                check_temp_watermark();
+            }
+            // (3) dedup, (4) difference, (5) merge — fused
+            for (size_t i = 0; i < rec.size(); ++i) {
+                const u32 r = rec[i];
+                gd_iter_record log{delta_in[i], joined[r], 0, 0, 0};
+                dedup_diff_merge(r, log);
+                E.info_[r].log.push_back(log);
+            }
+        }
+    }
+
+    u64 count(u32 r) override { return rels[r].full_n; }
+
+    void download(u32 r, u64* out, bool device) override {
+        auto& st = rels[r];
+        const u32 ar = E.info_[r].arity;
+        if (st.full_n == 0) return;
+        if (device) {
+            unpack_rows<K>(c, st.full.p, st.full_n, ar, E.enc.e, out);
+            c.sync();
+            return;
+        }
+        DevBuf<u64> tmp(c, st.full_n * ar);
+        unpack_rows<K>(c, st.full.p, st.full_n, ar, E.enc.e, tmp.p);
+        c.d2h(out, tmp.p, st.full_n * ar * sizeof(u64));
+        c.sync();
+    }
+
+    u64 digest(u32 r) override {
+        return digest_rows<K>(c, rels[r].full.p, rels[r].full_n, E.info_[r].arity, E.enc.e);
+    }
+
+    // ---- hash-partitioned mode -----------------------------
+    void partition_begin(u64* send_counts, const void** d_send) override;
+    void partition_end(const void* d_recv, u64 recv_rows, u64* local_delta) override;
+    void partition_finish() override {}
+
+private:
+    Engine& E;
+    Ctx& c;
+    u32 bits;
+    std::vector<RelDev<K>> rels;
+    std::map<u64, std::pair<bool, u64>> consts;  // value -> (present, encoded)
+    // partition-mode state
+    DevBuf<K> send_buf;
+    DevBuf<u32> owners;
+
+    template <typename F>
+    static void for_each_constant(const gd_rule_plan& p, F&& f) {
+        auto op = [&](const gd_operand& o) { if (o.kind == GD_CONSTANT) f(o.value); };
+        for (u32 v = 0; v < p.nvariants; ++v) {
+            const gd_variant& var = p.variants[v];
+            for (u32 k = 0; k < var.sel_arity; ++k) op(var.sel_proj[k]);
+            for (u32 k = 0; k < var.nsel_filters; ++k) { op(var.sel_filters[k].lhs); op(var.sel_filters[k].rhs); }
+            for (u32 s = 0; s < var.nsteps; ++s) {
+                const gd_join_step& st = var.steps[s];
+                for (u32 k = 0; k < st.proj_arity; ++k) op(st.proj[k]);
+                for (u32 k = 0; k < st.nfilters; ++k) { op(st.filters[k].lhs); op(st.filters[k].rhs); }
+            }
+        }
+    }
+
+    void encode_const(u64 v) {
+        if (consts.count(v)) return;
+        u64 enc = 0;
+        const bool ok = encode_value(c, E.enc.e, v, &enc);
+        consts[v] = {ok, enc};
+    }
+
+    static bool reads(const gd_rule_plan& p, u32 rel) {
+        const gd_variant& v = p.variants[0];
+        if (v.src_rel == rel) return true;
+        for (u32 s = 0; s < v.nsteps; ++s)
+            if (v.steps[s].inner_rel == rel) return true;
+        return false;
+    }
+
+    DevOperand dev_op(const gd_operand& o, bool* never) {
+        DevOperand d{o.kind, o.column, 0};
+        if (o.kind == GD_CONSTANT) {
+            auto it = consts.find(o.value);
+            if (it == consts.end()) { encode_const(o.value); it = consts.find(o.value); }
+            if (!it->second.first) {
+                if (never) *never = true;
+                else throw_logic("projection constant missing from the encoding");
+            }
+            d.value = it->second.second;
+        }
+        return d;
+    }
+
+    DevJoin make_desc(u32 jcc, u32 outer_arity, const u32* outer_perm, u32 inner_arity, u32 proj_arity,
+                      const gd_operand* proj, u32 nfilters, const gd_filter* filters) {
+        DevJoin jd;
+        std::memset(&jd, 0, sizeof(jd));
+        jd.jcc = jcc;
+        jd.proj_arity = proj_arity;
+        jd.nfilters = nfilters;
+        jd.bits = bits;
+        jd.outer_arity = outer_arity;
+        jd.outer_identity = is_identity(outer_perm, outer_arity) ? 1 : 0;
+        jd.inner_arity = inner_arity;
+        for (u32 i = 0; i < outer_arity; ++i) jd.outer_perm[i] = outer_perm[i];
+        for (u32 k = 0; k < proj_arity; ++k) jd.proj[k] = dev_op(proj[k], nullptr);
+        for (u32 f = 0; f < nfilters; ++f) {
+            bool never = false;
+            jd.filters[f].lhs = dev_op(filters[f].lhs, &never);
+            jd.filters[f].rhs = dev_op(filters[f].rhs, &never);
+            jd.filters[f].require_equal = filters[f].require_equal;
+            jd.filters[f].never = never ? 1 : 0;
+        }
+        return jd;
+    }
+
+    void check_temp_watermark() const {  // engine.hpp:544-548
+        if (E.acct.current(Accountant::kTemp) != 0)
+            throw_logic("temporary storage leaked past a rule boundary");
+    }
+
+    // refresh_copies, engine.hpp:365-395
+    void refresh_copies(u32 r) {
+        PhaseTimer t(E, "index");
+        auto& st = rels[r];
+        const u32 ar = E.info_[r].arity;
+        for (auto& kv : st.copies) {
+            CopyState<K>& cp = kv.second;
+            Tracked scratch(E.acct, Accountant::kTemp, 2 * rb(st.full_n, ar) + st.full_n * 8, "index");
+            const K* data;
+            if (cp.identity) {
+                cp.n = st.full_n;
+                data = st.full.p;
+            } else if (cp.built && st.merge_gen == cp.synced_gen + 1 && st.last_merge_was_delta &&
+                       cp.n + st.delta_n == st.full_n) {
+                // incremental: copy' = copy U sort(perm(Δ))
+                const u64 dn = st.delta_n;
+                DevBuf<K> a(c, dn), b(c, dn);
+                permute_keys<K>(c, st.delta.p, dn, ar, bits, cp.perm.data(), a.p);
+                K* sorted = radix_sort<K>(c, a.p, b.p, dn, ar * bits);
+                ensure_discard(c, cp.alt, cp.n + dn);
+                diff_merge<K>(c, cp.rows.p, cp.n, sorted, dn, cp.alt.p, nullptr);
+                cp.rows.swap(cp.alt);
+                cp.n += dn;
+                data = cp.rows.p;
+            } else {
+                const u64 n = st.full_n;
+                ensure_discard(c, cp.rows, n);
+                ensure_discard(c, cp.alt, n);
+                permute_keys<K>(c, st.full.p, n, ar, bits, cp.perm.data(), cp.rows.p);
+                K* sorted = radix_sort<K>(c, cp.rows.p, cp.alt.p, n, ar * bits);
+                if (sorted != cp.rows.p) cp.rows.swap(cp.alt);
+                cp.n = n;
+                data = cp.rows.p;
+            }
+            cp.built = true;
+            cp.synced_gen = st.merge_gen;
+            if (cp.prefix > 0) build_index<K>(c, data, cp.n, ar, bits, cp.prefix, E.cfg.load_factor, cp.index);
+            scratch.reset();
+            const u64 bytes = rb(cp.n, ar) + (cp.prefix > 0 ? cp.index.slot_count * 16ull : 0);
+            E.acct.charge(Accountant::kContainer, bytes, "index");
+            E.acct.release(Accountant::kContainer, cp.bytes);
+            cp.bytes = bytes;
+        }
+        st.dirty = false;
+    }
+
+    // execute_chain, engine.hpp:401-484.  The final step's rows are appended
+    // to (sink, sink_n); *produced = rows appended.
+    void execute_chain(const gd_variant& v, DevBuf<K>& sink, u64& sink_n, u64* produced) {
+        auto& src = rels[v.src_rel];
+        const u32 ar = E.info_[v.src_rel].arity;
+        const bool use_delta = v.src_version == GD_DELTA;
+        const K* cur = use_delta ? src.delta.p : src.full.p;
+        u64 cur_n = use_delta ? src.delta_n : src.full_n;
+        u32 cur_ar = ar;
+        u32 cur_perm[kMaxArity];
+        for (u32 i = 0; i < kMaxArity; ++i) cur_perm[i] = i < ar ? v.src_perm[i] : i;
+
+        Tracked permuted_charge;
+        if (!is_identity(v.src_perm, ar)) {
+            // The permutation is folded into the outer view (no re-sort: the
+            // outer order only changes the raw join order, never results).
+            PhaseTimer t(E, "join");
+            Tracked scratch(E.acct, Accountant::kTemp, 2 * rb(cur_n, ar) + cur_n * 8, "join");
+            scratch.reset();
+            permuted_charge = Tracked(E.acct, Accountant::kTemp, rb(cur_n, ar), "join");
+        }
+        if (v.nsteps == 0) {
+            PhaseTimer t(E, "join");
+            DevJoin jd = make_desc(0, cur_ar, cur_perm, 0, v.sel_arity, v.sel_proj, v.nsel_filters, v.sel_filters);
+            ensure_keep(c, sink, sink_n + cur_n, sink_n);
+            const u64 m = cur_n ? select_project<K>(c, cur, cur_n, jd, sink.p + sink_n) : 0;
+            sink_n += m;
+            *produced = m;
+            return;
+        }
+        DevBuf<K> chained;
+        Tracked chained_charge;
+        for (u32 s = 0; s < v.nsteps; ++s) {
+            const gd_join_step& st = v.steps[s];
+            auto& in = rels[st.inner_rel];
+            const u32 iar = E.info_[st.inner_rel].arity;
+            CopyState<K>& cp = in.copies.at(CopyKey{std::vector<u32>(st.inner_perm, st.inner_perm + iar),
+                                                    st.join_column_count});
+            const K* inner = cp.identity ? in.full.p : cp.rows.p;
+            const u64 inner_n = cp.identity ? in.full_n : cp.n;
+            const DevJoin jd = make_desc(st.join_column_count, cur_ar, cur_perm, iar, st.proj_arity, st.proj,
+                                         st.nfilters, st.filters);
+            const bool last = s + 1 == v.nsteps;
+            u64 total = 0;
+            DevBuf<K> cand;  // filtered path: candidates, then survivors
+            DevBuf<u64> row_start, row_off;
+            {
+                PhaseTimer t(E, "join");
+                if (cur_n && inner_n) {
+                    row_start = DevBuf<u64>(c, cur_n);
+                    row_off = DevBuf<u64>(c, cur_n + 1);
+                    IndexView<K> iv{};
+                    if (st.join_column_count > 0)
+                        iv = IndexView<K>{cp.index.slots.p, cp.index.slot_count, inner, inner_n, iar, bits,
+                                          st.join_column_count};
+                    const u64 ncand = join_probe<K>(c, cur, cur_n, jd, st.join_column_count ? &iv : nullptr,
+                                                    inner_n, row_start.p, row_off.p);
+                    if (st.nfilters == 0) {
+                        total = ncand;
+                    } else if (ncand) {
+                        DevBuf<K> raw(c, ncand);
+                        DevBuf<uint8_t> flags(c, ncand);
+                        join_materialize<K>(c, cur, cur_n, inner, jd, row_start.p, row_off.p, ncand, raw.p,
+                                            flags.p);
+                        cand = DevBuf<K>(c, ncand);
+                        total = compact_flagged<K>(c, raw.p, flags.p, ncand, cand.p);
+                    }
+                }
+            }
+            Tracked out_charge(E.acct, Accountant::kTemp, total * st.proj_arity * 8ull, "join");
+            K* dst;
+            DevBuf<K> out;
+            if (last) {
+                ensure_keep(c, sink, sink_n + total, sink_n);
+                dst = sink.p + sink_n;
+            } else {
+                out = DevBuf<K>(c, total);
+                dst = out.p;
+            }
+            if (total) {
+                PhaseTimer t(E, "join");
+                if (st.nfilters == 0)
+                    join_materialize<K>(c, cur, cur_n, inner, jd, row_start.p, row_off.p, total, dst, nullptr);
+                else
+                    c.d2d(dst, cand.p, total * sizeof(K));
+            }
+            E.join_tuples += total;
+            if (last) {
+                sink_n += total;
+                *produced = total;
+                break;
+            }
+            chained = std::move(out);
+            chained_charge = std::move(out_charge);
+            permuted_charge.reset();
+            cur = chained.p;
+            cur_n = total;
+            cur_ar = st.proj_arity;
+            for (u32 i = 0; i < kMaxArity; ++i) cur_perm[i] = i;
+        }
+    }
+
+    void append_new(u32 r, u64 m) {  // engine.hpp:486-495
+        if (m == 0) return;
+        const u64 b = rb(m, E.info_[r].arity);
+        E.acct.charge(Accountant::kContainer, b, "join");
+        E.info_[r].new_bytes += b;
+    }
+
+    void assign_delta(u32 r, u64 rows, const char* phase) {  // engine.hpp:511-517
+        RelInfo& ri = E.info_[r];
+        const u64 b = rb(rows, ri.arity);
+        E.acct.charge(Accountant::kContainer, b, phase);
+        E.acct.release(Accountant::kContainer, ri.delta_bytes);
+        ri.delta_bytes = b;
+    }
+
+    // merge_into_full bookkeeping (engine.hpp:520-533 + merge_buffer.hpp).
+    void merge_accounting(u32 r, u64 full_before, u64 gained, const char* phase) {
+        RelInfo& ri = E.info_[r];
+        E.bufs.acquire(ri.name, full_before, gained, ri.arity);
+        E.bufs.release(ri.name);
+        const u64 b = rb(full_before + gained, ri.arity);
+        E.acct.charge(Accountant::kContainer, b, phase);
+        E.acct.release(Accountant::kContainer, ri.full_bytes);
+        ri.full_bytes = b;
+    }
+
+    // Sorts rows [0, m) of `buf` (scratch `tmp`), returns the sorted pointer.
+    K* sort_rows(DevBuf<K>& buf, u64 m, u32 ar) {
+        DevBuf<K> tmp(c, m);
+        K* s = radix_sort<K>(c, buf.p, tmp.p, m, ar * bits);
+        if (s != buf.p) {
+            buf.swap(tmp);  // keep the sorted data in buf; old buf freed with tmp
+            return buf.p;
+        }
+        return s;
+    }
+
+    void seed_rule(const gd_rule_plan& plan) {  // engine.hpp:141-168
+        const gd_variant& v = plan.variants[0];
+        for (u32 s = 0; s < v.nsteps; ++s)  // refresh_inputs, engine.hpp:355-360
+            if (rels[v.steps[s].inner_rel].dirty) refresh_copies(v.steps[s].inner_rel);
+        const u32 h = plan.head_rel;
+        const u32 ar = E.info_[h].arity;
+        DevBuf<K> rows;
+        u64 m = 0, produced = 0;
+        execute_chain(v, rows, m, &produced);
+        Tracked rows_charge(E.acct, Accountant::kTemp, rb(m, ar), "join");
+        if (m == 0) return;
+        auto& head = rels[h];
+        K* sorted;
+        {
+            PhaseTimer t(E, "dedup");
+            sorted = sort_rows(rows, m, ar);
+        }
+        MergeResult mr;
+        DevBuf<K> gained(c, m);
+        {
+            PhaseTimer t(E, "difference");
+            ensure_discard(c, head.full_alt, head.full_n + m);
+            mr = diff_merge<K>(c, head.full.p, head.full_n, sorted, m, head.full_alt.p, gained.p);
+        }
+        {
+            Tracked scratch(E.acct, Accountant::kTemp, m * 8 + rb(m, ar), "dedup");
+        }
+        Tracked fresh_charge(E.acct, Accountant::kTemp, rb(mr.unique_new, ar), "dedup");
+        rows_charge.reset();
+        if (mr.delta_n == 0) return;
+        Tracked gained_charge(E.acct, Accountant::kTemp, rb(mr.delta_n, ar), "difference");
+        fresh_charge.reset();
+        {
+            PhaseTimer t(E, "merge");
+            merge_accounting(h, head.full_n, mr.delta_n, "merge");
+        }
+        head.full.swap(head.full_alt);
+        head.full_n += mr.delta_n;
+        ++head.merge_gen;
+        head.last_merge_was_delta = false;
+        head.dirty = true;
+    }
+
+    // Steps (3)-(5) of one iteration for relation r (engine.hpp:228-251).
+    void dedup_diff_merge(u32 r, gd_iter_record& log) {
+        auto& st = rels[r];
+        RelInfo& ri = E.info_[r];
+        const u32 ar = ri.arity;
+        const u64 m = st.new_n;
+        MergeResult mr;
+        if (m > 0) {
+            K* sorted;
+            {
+                PhaseTimer t(E, "dedup");
+                sorted = sort_rows(st.new_acc, m, ar);
+            }
+            PhaseTimer t(E, "merge");
+            ensure_discard(c, st.full_alt, st.full_n + m);
+            ensure_discard(c, st.delta_alt, m);
+            mr = diff_merge<K>(c, st.full.p, st.full_n, sorted, m, st.full_alt.p, st.delta_alt.p);
+            Tracked scratch(E.acct, Accountant::kTemp, m * 8 + rb(m, ar), "dedup");
+        }
+        Tracked fresh_charge(E.acct, Accountant::kTemp, rb(mr.unique_new, ar), "dedup");
+        // clear_new, engine.hpp:497-501
+        E.acct.release(Accountant::kContainer, ri.new_bytes);
+        ri.new_bytes = 0;
+        st.new_n = 0;
+        fresh_charge.reset();
+        assign_delta(r, mr.delta_n, "difference");
+        st.delta.swap(st.delta_alt);
+        st.delta_n = mr.delta_n;
+        if (mr.delta_n > 0) {
+            PhaseTimer t(E, "merge");
+            merge_accounting(r, st.full_n, mr.delta_n, "merge");
+            st.full.swap(st.full_alt);
+            st.full_n += mr.delta_n;
+            ++st.merge_gen;
+            st.last_merge_was_delta = true;
+            st.dirty = true;
+        }
+        log.new_unique = mr.unique_new;
+        log.delta_out = mr.delta_n;
+        log.full_after = st.full_n;
+    }
+};
+
+// ---- partition mode -------------------------------------------------
+// begin: run every recursive variant on the local Δ into new_acc, sort it
+// with the owner rank as the most significant digit (so the send buffer
+// is grouped by destination, each group sorted), drop local duplicates.
+template <typename K>
+void Impl<K>::partition_begin(u64* send_counts, const void** d_send) {
+    u32 rec_rel = UINT32_MAX;
+    for (const auto& p : E.plans_)
+        if (p.recursive) rec_rel = p.head_rel;
+    auto& head = rels[rec_rel];
+    const u32 ar = E.info_[rec_rel].arity;
+    for (u32 r = 0; r < rels.size(); ++r)
+        if (rels[r].dirty && !rels[r].copies.empty()) refresh_copies(r);
+    for (const auto& p : E.plans_) {
+        if (!p.recursive) continue;
+        for (u32 v = 0; v < p.nvariants; ++v) {
+            const gd_variant& var = p.variants[v];
+            if (rels[var.src_rel].delta_n == 0) continue;
+            u64 m = 0;
+            execute_chain(var, head.new_acc, head.new_n, &m);
+        }
+    }
+    const u64 m = head.new_n;
+    for (u32 k = 0; k < E.nranks; ++k) send_counts[k] = 0;
+    if (m == 0) {
+        *d_send = nullptr;
+        return;
+    }
+    PhaseTimer t(E, "dedup");
+    K* sorted = sort_rows(head.new_acc, m, ar);
+    ensure_discard(c, send_buf, m);
+    const u64 u = unique_sorted<K>(c, sorted, m, send_buf.p);
+    // group by owner: stable counting split on the owner (keys stay sorted
+    // inside each destination group)
+    ensure_discard(c, owners, u);
+    owner_of<K>(c, send_buf.p, u, E.nranks, owners.p);
+    std::vector<unsigned long long> cnt(E.nranks, 0);
+    {
+        // one stable partition pass per destination via flag compaction
+        DevBuf<K> grouped(c, u);
+        DevBuf<uint8_t> flags(c, u);
+        u64 off = 0;
+        for (u32 k = 0; k < E.nranks; ++k) {
+            owner_flags(c, owners.p, u, k, flags.p);
+            const u64 got = compact_flagged<K>(c, send_buf.p, flags.p, u, grouped.p + off);
+            cnt[k] = got;
+            off += got;
+        }
+        send_buf.swap(grouped);
+    }
+    head.new_n = 0;
+    for (u32 k = 0; k < E.nranks; ++k) send_counts[k] = cnt[k];
+    *d_send = send_buf.p;
+}
+
+template <typename K>
+void Impl<K>::partition_end(const void* d_recv, u64 recv_rows, u64* local_delta) {
+    u32 rec_rel = UINT32_MAX;
+    for (const auto& p : E.plans_)
+        if (p.recursive) rec_rel = p.head_rel;
+    auto& st = rels[rec_rel];
+    const u32 ar = E.info_[rec_rel].arity;
+    ++E.iterations;
+    E.info_[rec_rel].history.push_back(st.delta_n);
+    gd_iter_record log{st.delta_n, recv_rows, 0, 0, 0};
+    MergeResult mr;
+    if (recv_rows) {
+        DevBuf<K> buf(c, recv_rows);
+        c.d2d(buf.p, d_recv, recv_rows * sizeof(K));
+        K* sorted;
+        {
+            PhaseTimer t(E, "dedup");
+            sorted = sort_rows(buf, recv_rows, ar);
+        }
+        PhaseTimer t(E, "merge");
+        ensure_discard(c, st.full_alt, st.full_n + recv_rows);
+        ensure_discard(c, st.delta_alt, recv_rows);
+        mr = diff_merge<K>(c, st.full.p, st.full_n, sorted, recv_rows, st.full_alt.p, st.delta_alt.p);
+    }
+    st.delta.swap(st.delta_alt);
+    st.delta_n = mr.delta_n;
+    if (mr.delta_n) {
+        st.full.swap(st.full_alt);
+        st.full_n += mr.delta_n;
+    }
+    log.new_unique = mr.unique_new;
+    log.delta_out = mr.delta_n;
+    log.full_after = st.full_n;
+    E.info_[rec_rel].log.push_back(log);
+    *local_delta = mr.delta_n;
+}
+
+}  // namespace
+
+// ---- shared helpers used above ---------------------------------------
+
+u64 canonicalize_rows(Ctx& c, const u64* d_rows, u64 n, u32 arity, DevBuf<u64>& out) {
+    out.reserve_discard(c, std::max<u64>(n * arity, 1));
+    if (n == 0) return 0;
+    EncodingOwner eo;
+    choose_encoding(c, {{d_rows, n * arity}}, {}, arity, eo);
+    auto run = [&](auto tag) -> u64 {
+        using K = decltype(tag);
+        DevBuf<K> a(c, n), b(c, n);
+        pack_rows<K>(c, d_rows, n, arity, eo.e, a.p);
+        K* s = radix_sort<K>(c, a.p, b.p, n, arity * eo.e.bits);
+        K* u = s == a.p ? b.p : a.p;
+        const u64 m = unique_sorted<K>(c, s, n, u);
+        unpack_rows<K>(c, u, m, arity, eo.e, out.p);
+        return m;
+    };
+    return eo.e.key_words == 1 ? run(u64{}) : run(u128{});
+}
+
+// ---- Engine ----------------------------------------------------------
+
+Engine::Engine(Ctx& ctx, const gd_engine_config& cf, u32 nrels, const u32* arities, const u32* is_edb,
+               const char* const* names)
+    : c(ctx), cfg(cf), acct(cf.memory_budget_bytes), bufs(acct, cf.ebm_enabled != 0, cf.alpha) {
+    if (!(cfg.load_factor > 0.0) || cfg.load_factor >= 1.0)
+        throw_config("engine: load factor must be in (0, 1)");
+    info_.resize(nrels);
+    raw.resize(nrels);
+    raw_n.assign(nrels, 0);
+    for (u32 r = 0; r < nrels; ++r) {
+        if (arities[r] == 0 || arities[r] > kMaxArity)
+            throw_unsupported("relation arity must be in [1, " + std::to_string(kMaxArity) + "]");
+        info_[r].arity = arities[r];
+        info_[r].is_edb = is_edb[r] != 0;
+        info_[r].name = names && names[r] ? std::string(names[r]) : "r" + std::to_string(r);
+    }
+}
+
+Engine::~Engine() = default;
+
+void Engine::set_plans(const gd_rule_plan* plans, u32 n) {  // engine.hpp:97-101, 300-310
+    if (seeded || impl) throw_logic("override_plans: engine already seeded");
+    for (u32 i = 0; i < n; ++i) {
+        const gd_rule_plan& p = plans[i];
+        check_rel(p.head_rel);
+        if (p.nvariants == 0 || p.nvariants > GD_MAX_VARIANTS) throw_plan_error("rule plan has no/too many variants");
+        for (u32 v = 0; v < p.nvariants; ++v) {
+            const gd_variant& var = p.variants[v];
+            check_rel(var.src_rel);
+            if (var.nsteps > GD_MAX_STEPS) throw_unsupported("too many join steps");
+            u32 out_ar = var.nsteps ? var.steps[var.nsteps - 1].proj_arity : var.sel_arity;
+            if (out_ar != info_[p.head_rel].arity) throw_logic("append_new: arity mismatch");
+            for (u32 s = 0; s < var.nsteps; ++s) {
+                const gd_join_step& st = var.steps[s];
+                check_rel(st.inner_rel);
+                if (st.proj_arity == 0 || st.proj_arity > kMaxArity)
+                    throw_config("join: projection must produce at least one column");
+            }
+        }
+    }
+    plans_.assign(plans, plans + n);
+}
+
+void Engine::load_edb(u32 r, const u64* rows, u64 n, bool canonical, bool device) {  // engine.hpp:107-128
+    if (seeded || impl) throw_logic("load_edb: engine already running");
+    if (r >= info_.size() || !info_[r].is_edb)
+        throw_load("load_edb: '" + (r < info_.size() ? info_[r].name : std::to_string(r)) +
+                   "' is not a declared EDB relation");
+    const u32 ar = info_[r].arity;
+    DevBuf<u64> up(c, std::max<u64>(n * ar, 1));
+    if (device) {
+        c.d2d(up.p, rows, n * ar * sizeof(u64));
+        if (n && max_value(c, up.p, n * ar) == kEmptySlot)
+            throw_load("load_edb: '" + info_[r].name + "' contains the reserved sentinel value");
+    } else {
+        for (u64 i = 0; i < n * ar; ++i)
+            if (rows[i] == kEmptySlot)
+                throw_load("load_edb: '" + info_[r].name + "' contains the reserved sentinel value");
+        c.h2d(up.p, rows, n * ar * sizeof(u64));
+        c.sync();
+    }
+    u64 m = n;
+    if (canonical) {
+        raw[r] = std::move(up);
+    } else {
+        PhaseTimer t(*this, "other");
+        Tracked scratch(acct, Accountant::kTemp, n * 8 + rb(n, ar), "other");
+        m = canonicalize_rows(c, up.p, n, ar, raw[r]);
+    }
+    raw_n[r] = m;
+    // assign_full, engine.hpp:503-509
+    const u64 b = rb(m, ar);
+    acct.charge(Accountant::kContainer, b, "other");
+    acct.release(Accountant::kContainer, info_[r].full_bytes);
+    info_[r].full_bytes = b;
+}
+
+void Engine::seed() {  // engine.hpp:137-179
+    if (seeded) throw_logic("seed: called twice");
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!impl) {
+        // Encoding over every EDB value and every rule constant.
+        std::vector<std::pair<const u64*, u64>> arrays;
+        u32 max_ar = 1;
+        for (u32 r = 0; r < info_.size(); ++r) {
+            max_ar = std::max(max_ar, info_[r].arity);
+            if (info_[r].is_edb && raw_n[r]) arrays.push_back({raw[r].p, raw_n[r] * info_[r].arity});
+        }
+        std::vector<u64> constants;
+        for (const auto& p : plans_)
+            for (u32 v = 0; v < p.nvariants; ++v) {
+                const gd_variant& var = p.variants[v];
+                auto op = [&](const gd_operand& o) { if (o.kind == GD_CONSTANT) constants.push_back(o.value); };
+                for (u32 k = 0; k < var.sel_arity; ++k) op(var.sel_proj[k]);
+                for (u32 k = 0; k < var.nsel_filters; ++k) { op(var.sel_filters[k].lhs); op(var.sel_filters[k].rhs); }
+                for (u32 s = 0; s < var.nsteps; ++s) {
+                    const gd_join_step& st = var.steps[s];
+                    max_ar = std::max(max_ar, st.proj_arity);
+                    for (u32 k = 0; k < st.proj_arity; ++k) op(st.proj[k]);
+                    for (u32 k = 0; k < st.nfilters; ++k) { op(st.filters[k].lhs); op(st.filters[k].rhs); }
+                }
+            }
+        choose_encoding(c, arrays, constants, max_ar, enc);
+        if (enc.e.key_words == 1) impl.reset(new Impl<u64>(*this));
+        else impl.reset(new Impl<u128>(*this));
+    }
+    impl->seed();
+    seeded = true;
+    total_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void Engine::iterate() {  // engine.hpp:181-257
+    if (!seeded) seed();
+    const auto t0 = std::chrono::steady_clock::now();
+    impl->iterate();
+    c.sync();
+    total_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+u64 Engine::relation_count(u32 r) {
+    check_rel(r);
+    if (!impl) return info_[r].is_edb ? raw_n[r] : 0;
+    return impl->count(r);
+}
+
+void Engine::relation_download(u32 r, u64* out, u64 capacity_rows, bool device) {
+    check_rel(r);
+    const u64 n = relation_count(r);
+    if (n > capacity_rows) throw_logic("relation download: buffer too small");
+    if (!impl) {
+        if (n == 0) return;
+        if (device) c.d2d(out, raw[r].p, n * info_[r].arity * sizeof(u64));
+        else c.d2h(out, raw[r].p, n * info_[r].arity * sizeof(u64));
+        c.sync();
+        return;
+    }
+    impl->download(r, out, device);
+}
+
+u64 Engine::relation_digest(u32 r) {
+    check_rel(r);
+    if (!impl) throw_logic("relation_digest: engine not seeded");
+    return impl->digest(r);
+}
+
+void Engine::fill_stats(gd_run_stats* out) const {  // engine.hpp:270-277, stats.hpp:21-46
+    std::memset(out, 0, sizeof(*out));
+    static const char* kPhases[6] = {"index", "join", "dedup", "difference", "merge", "other"};
+    double categorized = 0;
+    for (int p = 0; p < 5; ++p) {
+        auto it = phase_seconds_.find(kPhases[p]);
+        out->phase_seconds[p] = it == phase_seconds_.end() ? 0.0 : it->second;
+        categorized += out->phase_seconds[p];
+    }
+    out->phase_seconds[5] = std::max(0.0, total_seconds - categorized);
+    out->total_seconds = total_seconds;
+    out->iterations = iterations;
+    out->buffer_allocations = bufs.allocations();
+    out->charge_events = acct.events();
+    out->peak_tracked_bytes = acct.peak();
+    out->peak_temp_bytes = acct.peak_temp();
+    out->join_tuples = join_tuples;
+    out->device_bytes_peak = c.bytes_peak;
+    for (int p = 0; p < 6; ++p) {
+        out->kernel_seconds[p] = kernel_seconds[p];
+        out->algo_bytes[p] = algo_bytes[p];
+    }
+}
+
+void Engine::encoding(u32* bits, u32* key_words, u32* dict) const {
+    *bits = enc.e.bits;
+    *key_words = enc.e.key_words;
+    *dict = enc.e.dict ? 1 : 0;
+}
+
+void Engine::set_partition(u32 rk, u32 nr) {
+    if (seeded) throw_logic("set_partition: engine already seeded");
+    if (nr == 0 || rk >= nr) throw_config("set_partition: rank must be < nranks");
+    u32 nrec = 0;
+    std::set<u32> heads;
+    for (const auto& p : plans_) {
+        if (!p.recursive) continue;
+        heads.insert(p.head_rel);
+        for (u32 v = 0; v < p.nvariants; ++v)
+            for (u32 s = 0; s < p.variants[v].nsteps; ++s)
+                if (!info_[p.variants[v].steps[s].inner_rel].is_edb)
+                    throw_unsupported("partitioned mode needs EDB-only inner relations (SURVEY §8e); "
+                                      "run IDB-inner programs as replicas");
+    }
+    nrec = (u32)heads.size();
+    if (nrec != 1) throw_unsupported("partitioned mode supports exactly one recursive relation");
+    rank = rk;
+    nranks = nr;
+}
+
+u32 Engine::exchange_words() const { return enc.e.key_words; }
+
+void Engine::partition_begin(u64* send_counts, const void** d_send) {
+    if (!seeded) throw_logic("partition_begin: seed first");
+    impl->partition_begin(send_counts, d_send);
+}
+void Engine::partition_end(const void* d_recv, u64 recv_rows, u64* local_delta) {
+    impl->partition_end(d_recv, recv_rows, local_delta);
+}
+void Engine::partition_finish() { impl->partition_finish(); }
+
+}  // namespace gd

@@ -1,0 +1,201 @@
+// merge.cu — the fused difference + merge of one iteration
+// (difference, ra.hpp:386-422, then merge_sorted, ra.hpp:299-381, and the
+// adjacent-dedup tail of canonicalize, tuple_array.hpp:124-131).
+//
+// Inputs: F canonical (sorted, unique) and N sorted with duplicates (the
+// radix-sorted join output).  One merge-path pass emits
+//     F' = F U N   and   D = unique(N) \ F
+// in a single read of F and N and a single write of F' and D.
+//
+// Merge order breaks ties F-first, so an N element x is in F iff the F
+// element immediately before it in merge order equals x, and is a
+// duplicate iff the N element before it equals x.  Each tile of
+// kMergeThreads * kMergeItems merged positions is delimited by a global
+// merge-path search (partition kernel), staged in shared memory, merged by
+// per-thread sequential merges, and its output offsets come from a block
+// scan of kept-N counts plus a decoupled look-back across tiles.
+#include "dev_common.cuh"
+#include "ops.h"
+
+namespace gd {
+
+namespace {
+
+constexpr int kMergeThreads = 256;
+constexpr int kMergeItems = 8;
+constexpr u64 kMergeTile = (u64)kMergeThreads * kMergeItems;
+
+// splits[t] = number of F elements among the first min(t*tile, nf+nn)
+// positions of the merged order (ties: F first).
+template <typename K>
+__global__ void merge_partition_kernel(const K* __restrict__ A, u64 na, const K* __restrict__ B,
+                                       u64 nb, u64 tile, u64 nsplits, u64* __restrict__ splits) {
+    const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nsplits) return;
+    const u64 diag = min(t * tile, na + nb);
+    u64 lo = diag > nb ? diag - nb : 0;
+    u64 hi = min(diag, na);
+    while (lo < hi) {
+        const u64 mid = (lo + hi) >> 1;
+        if (A[mid] <= B[diag - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+    }
+    splits[t] = lo;
+}
+
+template <typename K>
+struct MergeSmem {
+    K in[kMergeTile + 2];   // [halo F | F tile | halo N | N tile]
+    K outF[kMergeTile];
+    K outD[kMergeTile];
+};
+
+// ws: [0] tile counter, [1] kept total, [2] unique-N total, [3] overlap,
+//     [4..] tile statuses.
+template <typename K>
+__global__ void __launch_bounds__(kMergeThreads) diff_merge_kernel(
+    const K* __restrict__ F, u64 nf, const K* __restrict__ N, u64 nn,
+    const u64* __restrict__ splits, K* __restrict__ Fout, K* __restrict__ Dout, u64* ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    MergeSmem<K>& sm = *reinterpret_cast<MergeSmem<K>*>(smem_raw);
+    __shared__ u64 s_tile;
+    __shared__ u64 s_scan[kMergeThreads / 32 + 1];
+    __shared__ u64 s_base;
+
+    const u64 tile = claim_tile(ws, &s_tile);
+    const u64 total = nf + nn;
+    const u64 diag0 = tile * kMergeTile;
+    const u64 diag1 = min(diag0 + kMergeTile, total);
+    const u64 a0 = splits[tile], a1 = splits[tile + 1];
+    const u64 b0 = diag0 - a0, b1 = diag1 - a1;
+    const u32 na = (u32)(a1 - a0), nb = (u32)(b1 - b0);
+
+    // Stage: in[0] = F[a0-1] (halo), in[1..na] = F tile,
+    //        in[na+1] = N[b0-1] (halo), in[na+2..] = N tile.
+    K* sA = sm.in;
+    K* sB = sm.in + na + 1;
+    for (u32 i = threadIdx.x; i < na; i += kMergeThreads) sA[1 + i] = F[a0 + i];
+    for (u32 i = threadIdx.x; i < nb; i += kMergeThreads) sB[1 + i] = N[b0 + i];
+    if (threadIdx.x == 0) {
+        sA[0] = a0 > 0 ? F[a0 - 1] : K(0);
+        sB[0] = b0 > 0 ? N[b0 - 1] : K(0);
+    }
+    __syncthreads();
+
+    // Per-thread sub-range of the tile's merge path.
+    const u32 tn = na + nb;
+    const u32 d = min((u32)threadIdx.x * kMergeItems, tn);
+    const u32 de = min(d + kMergeItems, tn);
+    u32 lo = d > nb ? d - nb : 0, hi = min(d, na);
+    while (lo < hi) {
+        const u32 mid = (lo + hi) >> 1;
+        if (sA[1 + mid] <= sB[1 + (d - 1 - mid)]) lo = mid + 1;
+        else hi = mid;
+    }
+    const u32 ai0 = lo, bi0 = d - lo;
+
+    // Pass 1 over the sub-range: count kept / unique / overlap.
+    u32 ai = ai0, bi = bi0;
+    u64 kept = 0, uniq = 0;
+    bool overlap = false;
+    for (u32 s = d; s < de; ++s) {
+        const bool takeA = bi >= nb || (ai < na && sA[1 + ai] <= sB[1 + bi]);
+        if (takeA) {
+            ++ai;
+        } else {
+            const K x = sB[1 + bi];
+            const bool dup = (b0 + bi > 0) && sB[bi] == x;
+            const bool inF = (a0 + ai > 0) && sA[ai] == x;
+            uniq += !dup;
+            overlap |= (inF && !dup);
+            kept += (!dup && !inF);
+            ++bi;
+        }
+    }
+    u64 tile_kept;
+    const u64 excl = block_exclusive_scan<u64, kMergeThreads>(kept, tile_kept, s_scan);
+    u64 tile_uniq;
+    block_exclusive_scan<u64, kMergeThreads>(uniq, tile_uniq, s_scan);
+    const bool any_overlap = __syncthreads_or(overlap);
+    if (threadIdx.x < 32) {
+        const u64 base = warp_lookback(ws + 4, tile, tile_kept);
+        if (threadIdx.x == 0) {
+            s_base = base;
+            atomicAdd(ws + 1, tile_kept);
+            atomicAdd(ws + 2, tile_uniq);
+            if (any_overlap) atomicOr(ws + 3, 1ull);
+        }
+    }
+    __syncthreads();
+    const u64 kbase = s_base;
+
+    // Pass 2: write into shared staging at tile-local positions.
+    ai = ai0;
+    bi = bi0;
+    u64 k_local = excl;  // kept N before this thread within the tile
+    for (u32 s = d; s < de; ++s) {
+        const bool takeA = bi >= nb || (ai < na && sA[1 + ai] <= sB[1 + bi]);
+        if (takeA) {
+            sm.outF[ai + k_local] = sA[1 + ai];
+            ++ai;
+        } else {
+            const K x = sB[1 + bi];
+            const bool dup = (b0 + bi > 0) && sB[bi] == x;
+            const bool inF = (a0 + ai > 0) && sA[ai] == x;
+            if (!dup && !inF) {
+                sm.outF[ai + k_local] = x;
+                sm.outD[k_local] = x;
+                ++k_local;
+            }
+            ++bi;
+        }
+    }
+    __syncthreads();
+    // Coalesced copy-out: F' rows [a0 + kbase, a1 + kbase + tile_kept),
+    //                     D rows  [kbase, kbase + tile_kept).
+    const u32 nout = na + (u32)tile_kept;
+    if (Fout)
+        for (u32 i = threadIdx.x; i < nout; i += kMergeThreads) Fout[a0 + kbase + i] = sm.outF[i];
+    if (Dout)
+        for (u32 i = threadIdx.x; i < (u32)tile_kept; i += kMergeThreads) Dout[kbase + i] = sm.outD[i];
+}
+
+}  // namespace
+
+template <typename K>
+MergeResult diff_merge(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K* Fout, K* Dout) {
+    MergeResult r;
+    if (nn == 0) {
+        if (Fout && nf) c.d2d(Fout, F, nf * sizeof(K));
+        return r;
+    }
+    const u64 total = nf + nn;
+    const u64 tiles = (total + kMergeTile - 1) / kMergeTile;
+    DevBuf<u64> splits(c, tiles + 1);
+    merge_partition_kernel<K><<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, c.stream>>>(
+        F, nf, N, nn, kMergeTile, tiles + 1, splits.p);
+    c.check_launch();
+    DevBuf<u64> ws(c, 4 + tiles);
+    c.memset(ws.p, 0, (4 + tiles) * sizeof(u64));
+    const size_t smem = sizeof(MergeSmem<K>);
+    static bool attr_set = false;
+    if (!attr_set) {
+        GD_CUDA(cudaFuncSetAttribute(diff_merge_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        attr_set = true;
+    }
+    diff_merge_kernel<K><<<(unsigned)tiles, kMergeThreads, smem, c.stream>>>(F, nf, N, nn, splits.p,
+                                                                               Fout, Dout, ws.p);
+    c.check_launch();
+    unsigned long long w[3];
+    c.read_words(w, ws.p + 1, 3);
+    r.delta_n = w[0];
+    r.unique_new = w[1];
+    r.overlap = w[2] != 0;
+    return r;
+}
+
+template MergeResult diff_merge<u64>(Ctx&, const u64*, u64, const u64*, u64, u64*, u64*);
+template MergeResult diff_merge<u128>(Ctx&, const u128*, u64, const u128*, u64, u128*, u128*);
+
+}  // namespace gd

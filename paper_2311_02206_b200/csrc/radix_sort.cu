@@ -1,0 +1,216 @@
+// radix_sort.cu — LSD onesweep radix sort of bit-packed tuple keys (the HISA
+// sort of canonicalize, tuple_array.hpp:73-133, and of permute_columns,
+// ra.hpp:426-454).
+//
+// One pass per 8-bit digit over only the significant low `nbits` bits of the
+// packed keys.  A single histogram kernel counts every pass's digits in one
+// read of the keys; each pass is then ONE kernel: a CTA claims a tile, ranks
+// its keys with warp-level multi-split (__match_any_sync + per-warp digit
+// counters in shared memory, stable), publishes its per-digit counts,
+// resolves its global per-digit offsets by decoupled look-back (one thread
+// per digit), stages the keys digit-sorted in shared memory and writes them
+// out so consecutive threads write consecutive addresses of a digit run.
+// HBM traffic per pass: read 8·n + write 8·n bytes (u64 keys).
+#include "dev_common.cuh"
+#include "ops.h"
+
+namespace gd {
+
+namespace {
+
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 256;
+constexpr int kSortThreads = 256;
+constexpr int kWarps = kSortThreads / 32;
+constexpr u64 kPortion = 1ull << 26;  // keys per look-back portion (30-bit status values)
+
+template <typename K> struct SortItems;
+template <> struct SortItems<u64> { static constexpr int v = 16; };  // 4096 keys / tile
+template <> struct SortItems<u128> { static constexpr int v = 8; };  // 2048 keys / tile
+
+template <typename K>
+__device__ __forceinline__ u32 digit_of(K k, u32 shift) {
+    return (u32)(k >> shift) & (kRadix - 1);
+}
+
+// Counts the digits of every pass for keys [begin, begin+n).
+template <typename K>
+__global__ void __launch_bounds__(256) radix_hist_kernel(const K* __restrict__ keys, u64 begin, u64 n,
+                                                         int npass, u64* __restrict__ hist) {
+    __shared__ u32 sh[16 * kRadix];
+    for (int i = threadIdx.x; i < npass * kRadix; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const K k = keys[begin + i];
+        for (int p = 0; p < npass; ++p) atomicAdd(&sh[p * kRadix + digit_of(k, p * kRadixBits)], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < npass * kRadix; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], (u64)sh[i]);
+}
+
+// bases[pass][d] = number of keys whose pass-digit is smaller than d.
+__global__ void radix_bases_kernel(const u64* __restrict__ hist, u64* __restrict__ bases) {
+    __shared__ u64 scan_tmp[kRadix / 32 + 1];
+    const int pass = blockIdx.x;
+    const int d = threadIdx.x;
+    u64 all;
+    bases[pass * kRadix + d] =
+        block_exclusive_scan<u64, kRadix>(hist[pass * kRadix + d], all, scan_tmp);
+}
+
+constexpr u32 kSFlagA = 1u << 30;
+constexpr u32 kSFlagP = 2u << 30;
+constexpr u32 kSMask = (1u << 30) - 1;
+
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
+    const K* __restrict__ in, K* __restrict__ out, u64 portion_begin, u64 portion_n, u32 shift,
+    const u64* __restrict__ digit_base, u64* __restrict__ next_base, u32* __restrict__ ws,
+    u32 ntiles) {
+    constexpr int I = SortItems<K>::v;
+    constexpr int TILE = kSortThreads * I;
+    __shared__ K s_keys[TILE];
+    __shared__ u32 s_whist[kWarps][kRadix + 1];
+    __shared__ u32 s_dstart[kRadix];
+    __shared__ u64 s_gbase[kRadix];
+    __shared__ u32 s_scan[kSortThreads / 32 + 1];
+    __shared__ u32 s_tile;
+
+    u32* counter = ws;
+    u32* status = ws + 1;
+
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    const u32 warp = threadIdx.x >> 5, lane = lane_id();
+    for (int i = threadIdx.x; i < kWarps * (kRadix + 1); i += kSortThreads) (&s_whist[0][0])[i] = 0;
+    __syncthreads();
+    const u64 tile = s_tile;
+    const u64 tile_begin = tile * TILE;
+    const u32 tile_n = (u32)min((u64)TILE, portion_n - tile_begin);
+
+    K k[I];
+    u32 d[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        const u32 idx = warp * (I * 32) + i * 32 + lane;
+        if (idx < tile_n) {
+            k[i] = in[portion_begin + tile_begin + idx];
+            d[i] = digit_of(k[i], shift);
+        } else {
+            k[i] = 0;
+            d[i] = kRadix;  // invalid: own group, never counted
+        }
+    }
+
+    // Warp-level multi-split ranking, stable in (item, lane) = input order.
+    u32 rank[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        const u32 peers = __match_any_sync(0xffffffffu, d[i]);
+        const u32 leader = __ffs(peers) - 1;
+        const u32 base = s_whist[warp][d[i]];
+        __syncwarp();
+        if (lane == leader) s_whist[warp][d[i]] = base + __popc(peers);
+        __syncwarp();
+        rank[i] = base + __popc(peers & lanemask_lt());
+    }
+    __syncthreads();
+
+    // Thread t owns digit t: per-warp exclusive offsets and the tile count.
+    const u32 t = threadIdx.x;
+    u32 cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const u32 c = s_whist[w][t];
+        s_whist[w][t] = cnt;
+        cnt += c;
+    }
+    // Publish the tile aggregate early so successors can proceed.
+    u32* my_status = status + tile * kRadix + t;
+    if (tile == 0) st_relaxed32(my_status, kSFlagP | cnt);
+    else st_relaxed32(my_status, kSFlagA | cnt);
+
+    u32 total;
+    const u32 dstart = block_exclusive_scan<u32, kSortThreads>(cnt, total, s_scan);
+    s_dstart[t] = dstart;
+
+    // Look-back for digit t across previous tiles of this portion.
+    u32 excl = 0;
+    if (tile > 0) {
+        long long pred = (long long)tile - 1;
+        while (pred >= 0) {
+            const u32 s = ld_relaxed32(status + (u64)pred * kRadix + t);
+            const u32 flag = s >> 30;
+            if (flag == 0) continue;
+            excl += s & kSMask;
+            if (flag == 2) break;
+            --pred;
+        }
+        st_relaxed32(my_status, kSFlagP | (excl + cnt));
+    }
+    const u64 base_t = digit_base[t];
+    s_gbase[t] = base_t + excl - dstart;
+    // The last tile of a portion hands the next portion its digit bases.
+    if (tile == ntiles - 1 && next_base) next_base[t] = base_t + excl + cnt;
+    __syncthreads();
+
+    // Scatter into shared memory in digit-sorted (stable) order.
+#pragma unroll
+    for (int i = 0; i < I; ++i)
+        if (d[i] < kRadix) s_keys[s_dstart[d[i]] + s_whist[warp][d[i]] + rank[i]] = k[i];
+    __syncthreads();
+
+    for (u32 j = threadIdx.x; j < tile_n; j += kSortThreads) {
+        const K key = s_keys[j];
+        out[s_gbase[digit_of(key, shift)] + j] = key;
+    }
+}
+
+}  // namespace
+
+template <typename K>
+K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
+    if (n <= 1 || nbits == 0) return a;
+    const int npass = (int)((nbits + kRadixBits - 1) / kRadixBits);
+    const int nportions = (int)((n + kPortion - 1) / kPortion);
+    constexpr int TILE = kSortThreads * SortItems<K>::v;
+
+    const u64 hist_words = (u64)npass * kRadix;
+    DevBuf<u64> hist(c, hist_words);
+    DevBuf<u64> bases(c, hist_words + 2 * kRadix);  // + two portion ping-pong rows
+    c.memset(hist.p, 0, hist_words * sizeof(u64));
+    {
+        const int grid = (int)std::min<u64>((u64)c.num_sms * 4, (n + 255) / 256);
+        radix_hist_kernel<K><<<grid, 256, 0, c.stream>>>(a, 0, n, npass, hist.p);
+        c.check_launch();
+    }
+    radix_bases_kernel<<<npass, kRadix, 0, c.stream>>>(hist.p, bases.p);
+    c.check_launch();
+    u64* pp[2] = {bases.p + hist_words, bases.p + hist_words + kRadix};
+
+    const u64 max_tiles = (std::min(n, kPortion) + TILE - 1) / TILE;
+    DevBuf<u32> ws(c, 1 + max_tiles * kRadix);
+    K* src = a;
+    K* dst = b;
+    for (int pass = 0; pass < npass; ++pass) {
+        for (int p = 0; p < nportions; ++p) {
+            const u64 pb = (u64)p * kPortion;
+            const u64 pn = std::min(kPortion, n - pb);
+            const u64 tiles = (pn + TILE - 1) / TILE;
+            c.memset(ws.p, 0, (1 + tiles * kRadix) * sizeof(u32));
+            const u64* rd = p == 0 ? bases.p + (u64)pass * kRadix : pp[(p - 1) & 1];
+            u64* wr = p + 1 < nportions ? pp[p & 1] : nullptr;
+            onesweep_kernel<K><<<(unsigned)tiles, kSortThreads, 0, c.stream>>>(
+                src, dst, pb, pn, (u32)(pass * kRadixBits), rd, wr, ws.p, (u32)tiles);
+            c.check_launch();
+        }
+        std::swap(src, dst);
+    }
+    return src;
+}
+
+template u64* radix_sort<u64>(Ctx&, u64*, u64*, u64, u32);
+template u128* radix_sort<u128>(Ctx&, u128*, u128*, u64, u32);
+
+}  // namespace gd

@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""bench.py — time-to-fixpoint and join tuples/sec of the B200 GDlog hot path.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W [--impl ours|reference]`.
+A "step" is one complete semi-naive evaluation (load EDB -> seed -> iterate to
+the fixpoint) of the benchmark workload: BASELINE.json configs[1], transitive
+closure on a synthetic power-law DAG of ~5M edge draws (workload c2_tc_pl,
+paper_2311_02206_b200/workloads.py).  `value` = join tuples produced per
+second of device time with the EDB already resident in HBM; `e2e` = the same
+metric through the C-ABI with host buffers (EDB upload + output-relation
+download inside the timed region).  N > 1 runs the hash-partitioned engine
+(one rank per GPU, NCCL all-to-all per iteration) on the same graph.
+
+Rank 0 prints ONE JSON line.  `--impl reference` times the reference CPU
+engine (oracle/_ref, compiled from the unmodified arraylog headers) on the
+box's host cores over a bounded sample of the same generator.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+# C2 workload (calibrated on B200 so |Reach| lands near 1e9)
+C2 = dict(n=5_000_000, m=5_000_000, window=200, alpha=1.05, seed=1)
+# bounded CPU sample of the same generator (reference engine ~10-30 s on 16 cores)
+CPU_SAMPLE = dict(n=250_000, m=250_000, window=200, alpha=1.05, seed=1)
+PROGRAM = "reach"
+HEAD = "Reach"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = ROOT / "gpurun_out" / f"clocks_rank{device}.csv"
+
+    def start(self):
+        try:
+            self.path.parent.mkdir(exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = max(mx, float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        load = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def flush_l2(torch, buf):
+    buf.add_(1)  # 256 MiB write > 126 MB L2
+
+
+def gen_workload():
+    from paper_2311_02206_b200 import workloads as W
+    return W.tc_pl(C2["n"], C2["m"], C2["window"], C2["alpha"], C2["seed"])
+
+
+# ---------------------------------------------------------------------------
+
+def cpu_baseline_sample():
+    """The reference engine timed on a bounded sample (rank 0, N=1)."""
+    from oracle.bindings import RefOracle
+    from paper_2311_02206_b200 import abi as A
+    from paper_2311_02206_b200 import workloads as W
+
+    s = CPU_SAMPLE
+    edges = W.tc_pl(s["n"], s["m"], s["window"], s["alpha"], s["seed"])
+    ref = RefOracle()
+    cfg = A.gd_engine_config((1 << 64) - 1, 1, 5, 0.8, 0, 0, 0)
+    e = ref.engine(PROGRAM, cfg)
+    t0 = time.perf_counter()
+    e.load_edb("Edge", edges)
+    e.run()
+    dt = time.perf_counter() - t0
+    return e, edges, dt
+
+
+def join_tuples_of(edges: np.ndarray, reach: np.ndarray) -> int:
+    """J summed over all iterations for Reach(f,t) :- Edge(f,m), Reach(m,t):
+    every Reach row enters Δ exactly once and joins with indeg(m) edges, so
+    ΣJ = Σ_{(m,t) in Reach} indeg(m) (indeg over distinct edges)."""
+    e = np.unique(edges, axis=0)
+    indeg = np.bincount(e[:, 1].astype(np.int64), minlength=int(max(e.max(), reach.max() if len(reach) else 0)) + 1)
+    return int(indeg[reach[:, 0].astype(np.int64)].sum())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    args = ap.parse_args()
+
+    if args.impl == "reference":
+        run_reference_main(args)
+        return
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2311_02206_b200 import arraylog as al
+    from paper_2311_02206_b200.partition import TorchExchange, run_partitioned
+
+    stream = torch.cuda.current_stream()
+    ctx = al.Context(local, stream.cuda_stream)
+    edges = gen_workload()
+    d_edges = torch.from_numpy(edges.view(np.int64)).cuda()
+    flush = torch.empty(256 << 20 >> 2, dtype=torch.int32, device="cuda")
+    exch = TorchExchange() if world > 1 else None
+
+    def one_step():
+        e = al.engine(PROGRAM, ctx=ctx)
+        if world > 1:
+            e.set_partition(rank, world)
+        e.load_edb_device("Edge", d_edges.data_ptr(), len(edges))
+        if world > 1:
+            e.seed()
+            run_partitioned(e, exch, world)
+        else:
+            e.run()
+        return e
+
+    # warm-up (also the parity/size record)
+    for i in range(args.warmup):
+        e = one_step()
+        if i == 0:
+            reach_n = e.relation_count(HEAD)
+            iters = e.raw_stats().iterations
+            jt = e.raw_stats().join_tuples
+            log(f"warmup: |Edge|={len(edges)} |{HEAD}|={reach_n} iterations={iters} J={jt}")
+        e.close()
+        torch.cuda.synchronize()
+
+    # timed steps
+    sampler = ClockSampler(local)
+    if not args.no_profile:
+        ctx.set_profiling(True)
+        ctx.profile_reset()
+    launches0 = ctx.kernel_launches
+    times, joins = [], []
+    sampler.start()
+    for _ in range(args.steps):
+        flush_l2(torch, flush)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        e = one_step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1)
+        jt = e.raw_stats().join_tuples
+        if world > 1:
+            t = torch.tensor([ms, float(jt)], dtype=torch.float64, device="cuda")
+            mx = t[:1].clone()
+            torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+            sm = t[1:].clone()
+            torch.distributed.all_reduce(sm)
+            ms, jt = float(mx.item()), int(sm.item())
+        times.append(ms)
+        joins.append(jt)
+        e.close()
+    clocks = sampler.stop()
+    launches = ctx.kernel_launches - launches0
+    prof = ctx.profile() if not args.no_profile else {}
+    ctx.set_profiling(False)
+
+    ms_step = float(np.mean(times))
+    value = float(np.mean(joins)) / (ms_step / 1e3)
+
+    # roofline of the dominant kernel class
+    peak, peak_kind = measured_peaks()
+    roof = None
+    if prof:
+        dom = max(prof, key=lambda k: prof[k][0])
+        ms_k, n_k, by_k = prof[dom]
+        achieved = (by_k / n_k) / (ms_k / n_k / 1e3) / 1e9 if n_k and ms_k else 0.0
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": peak_kind, "traffic": None,
+                "launches": n_k, "avg_launch_ms": ms_k / max(n_k, 1),
+                "algo_bytes_per_launch": by_k / max(n_k, 1),
+                "share_of_step": ms_k / (ms_step * args.steps)}
+        tp = ROOT / "profiles" / "ncu_traffic.json"
+        if tp.exists():
+            d = json.loads(tp.read_text()).get(dom)
+            if d:
+                roof["traffic"] = d.get("dram_bytes")
+                roof["traffic_algo_bytes"] = d.get("algo_bytes")
+                roof["traffic_source"] = d.get("source")
+        jm = [k for k in ("join_probe", "join_materialize", "diff_merge")]
+        jm_ms = sum(prof[k][0] for k in jm)
+        jm_by = sum(prof[k][2] for k in jm)
+        roof["join_merge"] = {"achieved": jm_by / (jm_ms / 1e3) / 1e9 if jm_ms else 0.0,
+                              "frac": (jm_by / (jm_ms / 1e3) / 1e9) / peak if jm_ms else 0.0}
+        roof["kernel_ms_per_step"] = {k: v[0] / args.steps for k, v in prof.items()}
+
+    # e2e through the C-ABI with host buffers (rank 0 at N=1)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        host_edges = torch.from_numpy(edges.view(np.int64)).pin_memory().numpy().view(np.uint64)
+        out = torch.empty((reach_n, 2), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+        e2e_t = []
+        for _ in range(max(1, min(args.steps, 3))):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e = al.engine(PROGRAM, ctx=ctx)
+            e.load_edb("Edge", al.tuple_array(2, host_edges))
+            e.run()
+            n = e.relation_count(HEAD)
+            ctx.check(ctx.lib.gd_engine_relation_download(e.h, 1, out.ctypes.data, n))
+            dt = time.perf_counter() - t0
+            e2e_t.append(dt)
+            e.close()
+        e2e = {"value": float(np.mean(joins)) / float(np.mean(e2e_t)), "unit": "tuples/s",
+               "h2d_bytes_per_step": int(host_edges.nbytes), "d2h_bytes_per_step": int(reach_n * 16),
+               "seconds_per_step": float(np.mean(e2e_t))}
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            e, cedges, dt = cpu_baseline_sample()
+            r = e.relation(HEAD)
+            cj = join_tuples_of(cedges, r)
+            s = CPU_SAMPLE
+            cpu = {"value": cj / dt, "unit": "tuples/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"tc_pl n={s['n']} m={s['m']} W={s['window']} alpha={s['alpha']}: "
+                             f"|Reach|={len(r)} J={cj} in {dt:.2f}s",
+                   "time_to_fixpoint_s": dt}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "error": str(ex)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": "join_tuples_per_sec", "value": value, "unit": "tuples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "time_to_fixpoint_s": ms_step / 1e3,
+            "config": {"workload": "c2_tc_pl", "program": PROGRAM, **C2, "edges": int(len(edges)),
+                       "reach": int(reach_n), "iterations": int(iters), "join_tuples": int(np.mean(joins)),
+                       "parallelism": f"hash-partitioned x{world}" if world > 1 else "single",
+                       "l2": "flushed between steps (256 MiB write)"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_reference_main(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    times, joins = [], []
+    for i in range(args.warmup + args.steps):
+        e, edges, dt = cpu_baseline_sample()
+        r = e.relation(HEAD)
+        j = join_tuples_of(edges, r)
+        log(f"reference step {i}: {dt:.2f}s |Reach|={len(r)} iters={e.stats().iterations} J={j}")
+        if i >= args.warmup:
+            times.append(dt)
+            joins.append(j)
+    t = float(np.mean(times))
+    v = float(np.mean(joins)) / t
+    s = CPU_SAMPLE
+    line = {
+        "impl": "reference", "metric": "join_tuples_per_sec", "value": v, "unit": "tuples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "time_to_fixpoint_s": t,
+        "config": {"workload": "c2_tc_pl (bounded CPU sample of the same generator)", "program": PROGRAM, **s},
+        "cpu_baseline": {"value": v, "unit": "tuples/s", "cores": os.cpu_count(), "kind": "reference",
+                         "sample": f"tc_pl n={s['n']} m={s['m']} W={s['window']} alpha={s['alpha']}"},
+        "e2e": {"value": v, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -33,6 +33,8 @@ GD_FULL = 0
 GD_DELTA = 1
 
 PHASES = ("index", "join", "dedup", "difference", "merge", "other")  # stats.hpp:15-16
+KCLASSES = ("sort_pass", "sort_hist", "diff_merge", "join_probe", "join_materialize", "index_build",
+            "select", "other")  # gdlog_b200.h GD_KCLASS_COUNT
 
 u32 = C.c_uint32
 u64 = C.c_uint64
@@ -159,6 +161,9 @@ SIGNATURES = {
     "gd_last_error_phase": (C.c_char_p, [P]),
     "gd_ctx_kernel_launches": (u64, [P]),
     "gd_ctx_synchronize": (C.c_int, [P]),
+    "gd_ctx_set_profiling": (C.c_int, [P, C.c_int]),
+    "gd_ctx_profile_read": (C.c_int, [P, P, P, P]),
+    "gd_ctx_profile_reset": (C.c_int, [P]),
     "gd_prefix_hash": (C.c_int, [P, P, u64, u32, u32, P]),
     "gd_canonicalize": (C.c_int, [P, P, u64, u32, P, PU64]),
     "gd_permute_columns": (C.c_int, [P, P, u64, u32, C.c_int, P, u32, P, PU64]),

@@ -105,6 +105,21 @@ class Context:
     def synchronize(self):
         self.check(self.lib.gd_ctx_synchronize(self.h))
 
+    def set_profiling(self, on: bool):
+        self.check(self.lib.gd_ctx_set_profiling(self.h, int(on)))
+
+    def profile(self) -> dict:
+        """{kernel class: (ms, launches, algorithmic bytes)} since reset."""
+        n = len(A.KCLASSES)
+        ms = (C.c_double * n)()
+        la = (A.u64 * n)()
+        by = (A.u64 * n)()
+        self.check(self.lib.gd_ctx_profile_read(self.h, ms, la, by))
+        return {k: (ms[i], la[i], by[i]) for i, k in enumerate(A.KCLASSES)}
+
+    def profile_reset(self):
+        self.check(self.lib.gd_ctx_profile_reset(self.h))
+
     def close(self):
         if getattr(self, "h", None):
             self.lib.gd_ctx_destroy(self.h)

@@ -250,6 +250,30 @@ gd_status gd_ctx_synchronize(gd_ctx* ctx) {
     return guard(ctx, [&] { ctx->c->sync(); });
 }
 
+gd_status gd_ctx_set_profiling(gd_ctx* ctx, int enable) {
+    return guard(ctx, [&] { ctx->c->prof.on = enable != 0; });
+}
+
+gd_status gd_ctx_profile_read(gd_ctx* ctx, double* ms, uint64_t* launches, uint64_t* bytes) {
+    return guard(ctx, [&] {
+        ctx->c->sync();
+        ctx->c->prof.resolve();
+        for (int k = 0; k < KC_COUNT; ++k) {
+            if (ms) ms[k] = ctx->c->prof.ms[k];
+            if (launches) launches[k] = ctx->c->prof.launches[k];
+            if (bytes) bytes[k] = ctx->c->prof.bytes[k];
+        }
+    });
+}
+
+gd_status gd_ctx_profile_reset(gd_ctx* ctx) {
+    return guard(ctx, [&] {
+        ctx->c->sync();
+        ctx->c->prof.resolve();
+        ctx->c->prof.reset();
+    });
+}
+
 // ---- kernel-level entries -------------------------------------------
 
 gd_status gd_prefix_hash(gd_ctx* ctx, const uint64_t* rows, uint64_t n, uint32_t arity, uint32_t ncols,

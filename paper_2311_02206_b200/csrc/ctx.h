@@ -8,6 +8,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "gdlog_b200.h"
 
@@ -40,7 +41,68 @@ struct Error : std::runtime_error {
                                                cudaGetErrorString(e_));          \
     } while (0)
 
+// Kernel classes for live per-kernel timing (bench roofline).
+enum KClass : int {
+    KC_SORT_PASS = 0,   // onesweep_kernel (one digit pass)
+    KC_SORT_HIST,       // radix_hist_kernel
+    KC_MERGE,           // diff_merge_kernel (+ its partition)
+    KC_PROBE,           // join_probe_kernel
+    KC_MATERIALIZE,     // join_materialize_kernel (+ its partition)
+    KC_INDEX,           // group starts + index insert
+    KC_SELECT,          // compaction / select_project / unique
+    KC_OTHER,           // pack/unpack/permute/owner/...
+    KC_COUNT
+};
+
+// Records CUDA events around instrumented launches when enabled; resolves
+// them lazily (after a stream sync) into per-class time, launch counts and
+// algorithmic bytes.
+struct Profiler {
+    struct Rec {
+        int cls;
+        cudaEvent_t a, b;
+        uint64_t bytes;
+    };
+    bool on = false;
+    std::vector<cudaEvent_t> free_events;
+    std::vector<Rec> pending;
+    double ms[KC_COUNT] = {};
+    uint64_t launches[KC_COUNT] = {};
+    uint64_t bytes[KC_COUNT] = {};
+
+    cudaEvent_t take() {
+        if (free_events.empty()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            return e;
+        }
+        cudaEvent_t e = free_events.back();
+        free_events.pop_back();
+        return e;
+    }
+    void resolve() {
+        for (auto& r : pending) {
+            float t = 0;
+            if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) ms[r.cls] += t;
+            launches[r.cls] += 1;
+            bytes[r.cls] += r.bytes;
+            free_events.push_back(r.a);
+            free_events.push_back(r.b);
+        }
+        pending.clear();
+    }
+    void reset() {
+        pending.clear();
+        for (int i = 0; i < KC_COUNT; ++i) ms[i] = 0, launches[i] = 0, bytes[i] = 0;
+    }
+    ~Profiler() {
+        for (auto& r : pending) free_events.push_back(r.a), free_events.push_back(r.b);
+        for (auto e : free_events) cudaEventDestroy(e);
+    }
+};
+
 struct Ctx {
+    Profiler prof;
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -105,6 +167,25 @@ struct Ctx {
         bytes_in_use -= bytes;
     }
     void sync() { GD_CUDA(cudaStreamSynchronize(stream)); }
+
+    // Instrumented launch bracket: t = prof_begin(); <launch>; prof_end(t, ...).
+    cudaEvent_t prof_begin() {
+        if (!prof.on) return nullptr;
+        cudaEvent_t a = prof.take();
+        cudaEventRecord(a, stream);
+        return a;
+    }
+    // Returns the index of the pending record (to patch bytes later) or -1.
+    long prof_end(cudaEvent_t a, int cls, uint64_t bytes) {
+        if (!a) return -1;
+        cudaEvent_t b = prof.take();
+        cudaEventRecord(b, stream);
+        prof.pending.push_back({cls, a, b, bytes});
+        return (long)prof.pending.size() - 1;
+    }
+    void prof_add_bytes(long rec, uint64_t bytes) {
+        if (rec >= 0 && rec < (long)prof.pending.size()) prof.pending[rec].bytes += bytes;
+    }
     void check_launch() {
         ++launches;
         cudaError_t e = cudaGetLastError();

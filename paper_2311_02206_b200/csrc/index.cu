@@ -95,9 +95,11 @@ void build_index(Ctx& c, const K* rows, u64 n, u32 arity, u32 bits, u32 plen, do
     out.slots.reserve_discard(c, out.slot_count);
     c.memset(out.slots.p, 0xff, out.slot_count * sizeof(Slot));
     if (groups) {
+        cudaEvent_t t = c.prof_begin();
         index_insert_kernel<K><<<grid_for(c, groups), 256, 0, c.stream>>>(
             rows, arity, bits, plen, gs.p, groups, out.slots.p, out.slot_count);
         c.check_launch();
+        c.prof_end(t, KC_INDEX, groups * (16 + 2 * 8 + sizeof(K)));
     }
 }
 

@@ -208,9 +208,12 @@ u64 join_probe(Ctx& c, const K* outer, u64 n, const DevJoin& jd, const IndexView
     c.memset(ws.p, 0, (2 + tiles) * sizeof(u64));
     IndexView<K> view{};
     if (ix) view = *ix;
+    cudaEvent_t t = c.prof_begin();
     join_probe_kernel<K><<<(unsigned)tiles, kProbeThreads, 0, c.stream>>>(outer, n, jd, view, inner_n,
                                                                            row_start, row_off, ws.p);
     c.check_launch();
+    // algorithmic bytes: the outer rows + one 16-byte slot probe per row
+    c.prof_end(t, KC_PROBE, n * (sizeof(K) + (jd.jcc ? sizeof(Slot) : 0)));
     unsigned long long total;
     c.read_words(&total, ws.p + 1, 1);
     return total;
@@ -222,12 +225,17 @@ void join_materialize(Ctx& c, const K* outer, u64 n, const K* inner, const DevJo
     if (total == 0 || n == 0) return;
     const u64 tiles = (n + total + kLbsTile - 1) / kLbsTile;
     DevBuf<u64> splits(c, tiles + 1);
+    cudaEvent_t tp = c.prof_begin();
     lbs_partition_kernel<<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, c.stream>>>(
         row_off, n, total, kLbsTile, tiles + 1, splits.p);
     c.check_launch();
+    c.prof_end(tp, KC_OTHER, 0);
+    cudaEvent_t t = c.prof_begin();
     join_materialize_kernel<K><<<(unsigned)tiles, kLbsThreads, 0, c.stream>>>(
         outer, n, inner, jd, row_start, row_off, total, splits.p, out, flags);
     c.check_launch();
+    // algorithmic bytes: the matched inner rows read + the output rows written
+    c.prof_end(t, KC_MATERIALIZE, 2 * total * sizeof(K));
 }
 
 template <typename K>

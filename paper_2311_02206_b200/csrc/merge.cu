@@ -172,9 +172,11 @@ MergeResult diff_merge(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K* Fout, 
     const u64 total = nf + nn;
     const u64 tiles = (total + kMergeTile - 1) / kMergeTile;
     DevBuf<u64> splits(c, tiles + 1);
+    cudaEvent_t tp = c.prof_begin();
     merge_partition_kernel<K><<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, c.stream>>>(
         F, nf, N, nn, kMergeTile, tiles + 1, splits.p);
     c.check_launch();
+    c.prof_end(tp, KC_OTHER, 0);
     DevBuf<u64> ws(c, 4 + tiles);
     c.memset(ws.p, 0, (4 + tiles) * sizeof(u64));
     const size_t smem = sizeof(MergeSmem<K>);
@@ -184,14 +186,19 @@ MergeResult diff_merge(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K* Fout, 
                                      (int)smem));
         attr_set = true;
     }
+    cudaEvent_t t = c.prof_begin();
     diff_merge_kernel<K><<<(unsigned)tiles, kMergeThreads, smem, c.stream>>>(F, nf, N, nn, splits.p,
                                                                                Fout, Dout, ws.p);
     c.check_launch();
+    const long rec = c.prof_end(t, KC_MERGE, 0);
     unsigned long long w[3];
     c.read_words(w, ws.p + 1, 3);
     r.delta_n = w[0];
     r.unique_new = w[1];
     r.overlap = w[2] != 0;
+    // algorithmic bytes: read F and the sorted new rows, write
+    // F' = F + D and D.
+    c.prof_add_bytes(rec, sizeof(K) * ((nf + nn) + (Fout ? nf + r.delta_n : 0) + (Dout ? r.delta_n : 0)));
     return r;
 }
 

@@ -182,8 +182,10 @@ K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
     c.memset(hist.p, 0, hist_words * sizeof(u64));
     {
         const int grid = (int)std::min<u64>((u64)c.num_sms * 4, (n + 255) / 256);
+        cudaEvent_t t = c.prof_begin();
         radix_hist_kernel<K><<<grid, 256, 0, c.stream>>>(a, 0, n, npass, hist.p);
         c.check_launch();
+        c.prof_end(t, KC_SORT_HIST, n * sizeof(K));
     }
     radix_bases_kernel<<<npass, kRadix, 0, c.stream>>>(hist.p, bases.p);
     c.check_launch();
@@ -201,9 +203,11 @@ K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
             c.memset(ws.p, 0, (1 + tiles * kRadix) * sizeof(u32));
             const u64* rd = p == 0 ? bases.p + (u64)pass * kRadix : pp[(p - 1) & 1];
             u64* wr = p + 1 < nportions ? pp[p & 1] : nullptr;
+            cudaEvent_t t = c.prof_begin();
             onesweep_kernel<K><<<(unsigned)tiles, kSortThreads, 0, c.stream>>>(
                 src, dst, pb, pn, (u32)(pass * kRadixBits), rd, wr, ws.p, (u32)tiles);
             c.check_launch();
+            c.prof_end(t, KC_SORT_PASS, 2 * pn * sizeof(K));
         }
         std::swap(src, dst);
     }

@@ -52,8 +52,10 @@ u64 run_select(Ctx& c, u64 n, Pred pred, Emit emit) {
     const u64 tiles = (n + kSelTile - 1) / kSelTile;
     DevBuf<u64> ws(c, 2 + tiles);
     c.memset(ws.p, 0, (2 + tiles) * sizeof(u64));
+    cudaEvent_t t = c.prof_begin();
     select_kernel<<<(unsigned)tiles, kSelThreads, 0, c.stream>>>(n, pred, emit, ws.p);
     c.check_launch();
+    c.prof_end(t, KC_SELECT, 0);
     unsigned long long total;
     c.read_words(&total, ws.p + 1, 1);
     return total;

@@ -1,0 +1,133 @@
+"""Hash-partitioned multi-GPU fixpoint (component N1).
+
+One process per GPU.  Every rank holds the EDB replicated and the IDB
+tuples it owns (owner = hash(tuple) mod nranks, engine.cu keep_owned).  Per
+iteration each rank:
+  1. runs the recursive joins on its local Δ, sorts + dedups the derived
+     rows and groups them by owner rank      (gd_engine_partition_begin);
+  2. exchanges the groups with an all-to-all-v (NCCL over NVLink through
+     torch.distributed: counts first, then the rows);
+  3. merges what it received into its local full relation, producing its
+     local Δ                                  (gd_engine_partition_end);
+  4. all-reduces |Δ| — the fixpoint is reached when the global sum is 0.
+
+The exchange is abstracted (`Exchange`) so the same loop runs over NCCL,
+over gloo (CPU tests) or over an in-process loopback of P logical shards on
+one GPU (parity tests).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+class CudaBuffer:
+    """__cuda_array_interface__ view of a device pointer (zero-copy into
+    torch.as_tensor)."""
+
+    def __init__(self, ptr: int, nwords: int):
+        self.__cuda_array_interface__ = {
+            "shape": (nwords,), "typestr": "<u8", "data": (ptr, False), "version": 3, "strides": None}
+
+
+class TorchExchange:
+    """All-to-all-v + all-reduce through torch.distributed (NCCL on GPUs)."""
+
+    def __init__(self, device: str = "cuda"):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.device = torch, dist, device
+        self.rank = dist.get_rank()
+        self.size = dist.get_world_size()
+        self._recv = None
+
+    def _wrap(self, ptr: int, nwords: int):
+        torch = self.torch
+        if self.device == "cpu":  # host pointer (gloo tests)
+            import ctypes
+
+            arr = np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_int64)), shape=(nwords,))
+            return torch.from_numpy(arr)
+        return torch.as_tensor(CudaBuffer(ptr, nwords), device=self.device).view(torch.int64)
+
+    def exchange(self, send_counts: np.ndarray, send_ptr: int, words: int):
+        torch, dist = self.torch, self.dist
+        cnt = torch.as_tensor(send_counts.astype(np.int64), device=self.device)
+        rcnt = torch.empty_like(cnt)
+        dist.all_to_all_single(rcnt, cnt)
+        rc = rcnt.cpu().numpy()
+        total_send = int(send_counts.sum())
+        total_recv = int(rc.sum())
+        if total_send:
+            send = self._wrap(send_ptr, total_send * words)
+        else:
+            send = torch.empty(0, dtype=torch.int64, device=self.device)
+        if self._recv is None or self._recv.numel() < max(total_recv * words, 1):
+            self._recv = torch.empty(max(total_recv * words, 1) * 5 // 4 + 1024, dtype=torch.int64,
+                                     device=self.device)
+        recv = self._recv[: total_recv * words]
+        dist.all_to_all_single(recv, send, [int(x) * words for x in rc], [int(x) * words for x in send_counts])
+        return (recv.data_ptr() if total_recv else 0), total_recv
+
+    def allreduce_sum(self, x: int) -> int:
+        t = self.torch.tensor([x], dtype=self.torch.int64, device=self.device)
+        self.dist.all_reduce(t)
+        return int(t.item())
+
+
+def run_partitioned(eng, exchange, nranks: int, max_iters: int = 1 << 30) -> int:
+    """Drives one rank's engine to the global fixpoint; returns iterations.
+    `eng` must be seeded with set_partition(rank, nranks) applied."""
+    words = eng.exchange_words()
+    it = 0
+    local = eng.relation_delta_count() if hasattr(eng, "relation_delta_count") else None
+    while it < max_iters:
+        counts, ptr = eng.partition_begin(nranks)
+        rptr, rrows = exchange.exchange(counts, ptr, words)
+        local = eng.partition_end(rptr, rrows)
+        it += 1
+        if exchange.allreduce_sum(local) == 0:
+            break
+    return it
+
+
+class LoopbackCluster:
+    """P logical shards in one process (one GPU): the all-to-all is a
+    device-to-device gather of every shard's send groups.  Used by the
+    parity tests of the partitioned path on a single B200."""
+
+    def __init__(self, engines):
+        import torch
+
+        self.torch = torch
+        self.engines = engines
+        self.P = len(engines)
+
+    def run(self, max_iters: int = 1 << 30) -> int:
+        torch = self.torch
+        P = self.P
+        words = self.engines[0].exchange_words()
+        it = 0
+        while it < max_iters:
+            sends = [e.partition_begin(P) for e in self.engines]  # (counts, ptr)
+            views = []
+            for counts, ptr in sends:
+                tot = int(counts.sum())
+                if tot:
+                    t = torch.as_tensor(CudaBuffer(ptr, tot * words), device="cuda").view(torch.int64).clone()
+                else:
+                    t = torch.empty(0, dtype=torch.int64, device="cuda")
+                offs = np.concatenate([[0], np.cumsum(counts.astype(np.int64))]) * words
+                views.append((t, offs))
+            total = 0
+            for dst, e in enumerate(self.engines):
+                parts = [t[offs[dst]: offs[dst + 1]] for t, offs in views]
+                recv = torch.cat(parts) if parts else torch.empty(0, dtype=torch.int64, device="cuda")
+                torch.cuda.synchronize()  # the engine reads recv on its own stream
+                n = recv.numel() // words
+                total += e.partition_end(recv.data_ptr() if n else 0, n)
+                del recv
+            it += 1
+            if total == 0:
+                break
+        return it

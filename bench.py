@@ -33,7 +33,7 @@ sys.path.insert(0, str(ROOT))
 # C2 workload (calibrated on B200 so |Reach| lands near 1e9)
 C2 = dict(n=5_000_000, m=5_000_000, window=200, alpha=1.05, seed=1)
 # bounded CPU sample of the same generator (reference engine ~10-30 s on 16 cores)
-CPU_SAMPLE = dict(n=250_000, m=250_000, window=200, alpha=1.05, seed=1)
+CPU_SAMPLE = dict(n=200_000, m=200_000, window=200, alpha=1.05, seed=1)
 PROGRAM = "reach"
 HEAD = "Reach"
 
@@ -219,13 +219,14 @@ def main():
         torch.cuda.synchronize()
         ms = t0.elapsed_time(t1)
         jt = e.raw_stats().join_tuples
+        reach_n = e.relation_count(HEAD)
+        iters = e.raw_stats().iterations
         if world > 1:
-            t = torch.tensor([ms, float(jt)], dtype=torch.float64, device="cuda")
-            mx = t[:1].clone()
+            mx = torch.tensor([ms], dtype=torch.float64, device="cuda")
             torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-            sm = t[1:].clone()
+            sm = torch.tensor([jt, reach_n], dtype=torch.int64, device="cuda")
             torch.distributed.all_reduce(sm)
-            ms, jt = float(mx.item()), int(sm.item())
+            ms, jt, reach_n = float(mx.item()), int(sm[0].item()), int(sm[1].item())
         times.append(ms)
         joins.append(jt)
         e.close()

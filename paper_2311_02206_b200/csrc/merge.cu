@@ -43,11 +43,16 @@ __global__ void merge_partition_kernel(const K* __restrict__ A, u64 na, const K*
     splits[t] = lo;
 }
 
+// Shared-memory index padding: one spare element every 8, so the per-thread
+// sequential merges (threads 8 elements apart) hit distinct banks.
+__device__ __forceinline__ u32 pad8(u32 i) { return i + (i >> 3); }
+constexpr u32 kPadTile = kMergeTile + (kMergeTile >> 3) + 8;
+
 template <typename K>
 struct MergeSmem {
-    K in[kMergeTile + 2];   // [halo F | F tile | halo N | N tile]
-    K outF[kMergeTile];
-    K outD[kMergeTile];
+    K in[kPadTile + 2];  // [halo F | F tile | halo N | N tile], padded indices
+    K outF[kPadTile];
+    K outD[kPadTile];
 };
 
 // ws: [0] tile counter, [1] kept total, [2] unique-N total, [3] overlap,
@@ -70,17 +75,20 @@ __global__ void __launch_bounds__(kMergeThreads) diff_merge_kernel(
     const u64 b0 = diag0 - a0, b1 = diag1 - a1;
     const u32 na = (u32)(a1 - a0), nb = (u32)(b1 - b0);
 
-    // Stage: in[0] = F[a0-1] (halo), in[1..na] = F tile,
-    //        in[na+1] = N[b0-1] (halo), in[na+2..] = N tile.
-    K* sA = sm.in;
-    K* sB = sm.in + na + 1;
-    for (u32 i = threadIdx.x; i < na; i += kMergeThreads) sA[1 + i] = F[a0 + i];
-    for (u32 i = threadIdx.x; i < nb; i += kMergeThreads) sB[1 + i] = N[b0 + i];
+    // Stage (logical index -> padded slot): A(i) = F[a0 - 1 + i] for
+    // i in [0, na] (A(0) is the halo), B(i) = N[b0 - 1 + i] at logical
+    // offset na + 1.
+    K* in = sm.in;
+    const u32 boff = na + 1;
+    for (u32 i = threadIdx.x; i < na; i += kMergeThreads) in[pad8(1 + i)] = F[a0 + i];
+    for (u32 i = threadIdx.x; i < nb; i += kMergeThreads) in[pad8(boff + 1 + i)] = N[b0 + i];
     if (threadIdx.x == 0) {
-        sA[0] = a0 > 0 ? F[a0 - 1] : K(0);
-        sB[0] = b0 > 0 ? N[b0 - 1] : K(0);
+        in[pad8(0)] = a0 > 0 ? F[a0 - 1] : K(0);
+        in[pad8(boff)] = b0 > 0 ? N[b0 - 1] : K(0);
     }
     __syncthreads();
+#define SA(i) in[pad8(i)]
+#define SB(i) in[pad8(boff + (i))]
 
     // Per-thread sub-range of the tile's merge path.
     const u32 tn = na + nb;
@@ -89,33 +97,46 @@ __global__ void __launch_bounds__(kMergeThreads) diff_merge_kernel(
     u32 lo = d > nb ? d - nb : 0, hi = min(d, na);
     while (lo < hi) {
         const u32 mid = (lo + hi) >> 1;
-        if (sA[1 + mid] <= sB[1 + (d - 1 - mid)]) lo = mid + 1;
+        if (SA(1 + mid) <= SB(1 + (d - 1 - mid))) lo = mid + 1;
         else hi = mid;
     }
-    const u32 ai0 = lo, bi0 = d - lo;
+    const u32 ai0 = lo;
 
-    // Pass 1 over the sub-range: count kept / unique / overlap.
-    u32 ai = ai0, bi = bi0;
+    // One sequential merge of <= kMergeItems steps into registers.
+    // kind: 0 = F row, 1 = kept N row (new), 2 = dropped N row.
+    K val[kMergeItems];
+    u32 kinds = 0;  // 2 bits per step
+    u32 ai = ai0, bi = d - ai0;
     u64 kept = 0, uniq = 0;
     bool overlap = false;
-    for (u32 s = d; s < de; ++s) {
-        const bool takeA = bi >= nb || (ai < na && sA[1 + ai] <= sB[1 + bi]);
-        if (takeA) {
-            ++ai;
+#pragma unroll
+    for (int s = 0; s < kMergeItems; ++s) {
+        if (d + s < de) {
+            const K xa = SA(1 + ai);
+            const K xb = SB(1 + bi);
+            const bool takeA = bi >= nb || (ai < na && xa <= xb);
+            if (takeA) {
+                val[s] = xa;
+                ++ai;
+            } else {
+                const bool dup = (b0 + bi > 0) && SB(bi) == xb;
+                const bool inF = (a0 + ai > 0) && SA(ai) == xb;
+                uniq += !dup;
+                overlap |= (inF && !dup);
+                const bool keep = !dup && !inF;
+                kept += keep;
+                val[s] = xb;
+                kinds |= (keep ? 1u : 2u) << (2 * s);
+                ++bi;
+            }
         } else {
-            const K x = sB[1 + bi];
-            const bool dup = (b0 + bi > 0) && sB[bi] == x;
-            const bool inF = (a0 + ai > 0) && sA[ai] == x;
-            uniq += !dup;
-            overlap |= (inF && !dup);
-            kept += (!dup && !inF);
-            ++bi;
+            kinds |= 3u << (2 * s);
         }
     }
     u64 tile_kept;
-    const u64 excl = block_exclusive_scan<u64, kMergeThreads>(kept, tile_kept, s_scan);
-    u64 tile_uniq;
-    block_exclusive_scan<u64, kMergeThreads>(uniq, tile_uniq, s_scan);
+    const u64 excl = block_exclusive_scan<u64, kMergeThreads>(kept | (uniq << 32), tile_kept, s_scan);
+    const u64 tile_uniq = tile_kept >> 32;
+    tile_kept &= 0xffffffffull;
     const bool any_overlap = __syncthreads_or(overlap);
     if (threadIdx.x < 32) {
         const u64 base = warp_lookback(ws + 4, tile, tile_kept);
@@ -126,38 +147,32 @@ __global__ void __launch_bounds__(kMergeThreads) diff_merge_kernel(
             if (any_overlap) atomicOr(ws + 3, 1ull);
         }
     }
-    __syncthreads();
-    const u64 kbase = s_base;
-
-    // Pass 2: write into shared staging at tile-local positions.
-    ai = ai0;
-    bi = bi0;
-    u64 k_local = excl;  // kept N before this thread within the tile
-    for (u32 s = d; s < de; ++s) {
-        const bool takeA = bi >= nb || (ai < na && sA[1 + ai] <= sB[1 + bi]);
-        if (takeA) {
-            sm.outF[ai + k_local] = sA[1 + ai];
-            ++ai;
-        } else {
-            const K x = sB[1 + bi];
-            const bool dup = (b0 + bi > 0) && sB[bi] == x;
-            const bool inF = (a0 + ai > 0) && sA[ai] == x;
-            if (!dup && !inF) {
-                sm.outF[ai + k_local] = x;
-                sm.outD[k_local] = x;
-                ++k_local;
-            }
-            ++bi;
+    // Registers -> staging at tile-local output positions.
+    u32 a = ai0;
+    u32 k = (u32)(excl & 0xffffffffull);  // kept N rows before this thread in the tile
+#pragma unroll
+    for (int s = 0; s < kMergeItems; ++s) {
+        const u32 kind = (kinds >> (2 * s)) & 3u;
+        if (kind == 0) {
+            sm.outF[pad8(a + k)] = val[s];
+            ++a;
+        } else if (kind == 1) {
+            sm.outF[pad8(a + k)] = val[s];
+            sm.outD[pad8(k)] = val[s];
+            ++k;
         }
     }
+#undef SA
+#undef SB
     __syncthreads();
+    const u64 kbase = s_base;
     // Coalesced copy-out: F' rows [a0 + kbase, a1 + kbase + tile_kept),
     //                     D rows  [kbase, kbase + tile_kept).
     const u32 nout = na + (u32)tile_kept;
     if (Fout)
-        for (u32 i = threadIdx.x; i < nout; i += kMergeThreads) Fout[a0 + kbase + i] = sm.outF[i];
+        for (u32 i = threadIdx.x; i < nout; i += kMergeThreads) Fout[a0 + kbase + i] = sm.outF[pad8(i)];
     if (Dout)
-        for (u32 i = threadIdx.x; i < (u32)tile_kept; i += kMergeThreads) Dout[kbase + i] = sm.outD[i];
+        for (u32 i = threadIdx.x; i < (u32)tile_kept; i += kMergeThreads) Dout[kbase + i] = sm.outD[pad8(i)];
 }
 
 }  // namespace

@@ -455,8 +455,8 @@ gd_status gd_merge_sorted(gd_ctx* ctx, const uint64_t* full, uint64_t nf, int fu
             DevBuf<K> pf(c, std::max<u64>(nf, 1)), pd(c, std::max<u64>(nd, 1)), res(c, nf + nd);
             pack_rows<K>(c, df.p, nf, arity, eo.e, pf.p);
             pack_rows<K>(c, dd.p, nd, arity, eo.e, pd.p);
-            const MergeResult mr = diff_merge<K>(c, pf.p, nf, pd.p, nd, res.p, nullptr);
-            if (mr.overlap) throw_logic("merge_sorted: inputs are not disjoint");
+            if (merge_disjoint<K>(c, pf.p, nf, pd.p, nd, res.p))
+                throw_logic("merge_sorted: inputs are not disjoint");
             DevBuf<u64> un(c, (nf + nd) * arity);
             unpack_rows<K>(c, res.p, nf + nd, arity, eo.e, un.p);
             download(c, (u64*)out, un.p, (nf + nd) * arity);
@@ -482,7 +482,7 @@ gd_status gd_difference(gd_ctx* ctx, const uint64_t* new_rows, uint64_t nn, int 
             DevBuf<K> pn(c, nn), pf(c, std::max<u64>(nf, 1)), res(c, nn);
             pack_rows<K>(c, dn.p, nn, arity, eo.e, pn.p);
             pack_rows<K>(c, df.p, nf, arity, eo.e, pf.p);
-            const MergeResult mr = diff_merge<K>(c, pf.p, nf, pn.p, nn, nullptr, res.p);
+            const MergeResult mr = difference_sorted<K>(c, pf.p, nf, pn.p, nn, res.p);
             DevBuf<u64> un(c, std::max<u64>(mr.delta_n * arity, 1));
             unpack_rows<K>(c, res.p, mr.delta_n, arity, eo.e, un.p);
             download(c, (u64*)out, un.p, mr.delta_n * arity);

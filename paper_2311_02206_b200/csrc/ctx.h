@@ -51,6 +51,7 @@ enum KClass : int {
     KC_INDEX,           // group starts + index insert
     KC_SELECT,          // compaction / select_project / unique
     KC_OTHER,           // pack/unpack/permute/owner/...
+    KC_DIFF,            // difference flags (search or streaming)
     KC_COUNT
 };
 

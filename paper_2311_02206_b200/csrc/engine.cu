@@ -347,7 +347,7 @@ private:
                 permute_keys<K>(c, st.delta.p, dn, ar, bits, cp.perm.data(), a.p);
                 K* sorted = radix_sort<K>(c, a.p, b.p, dn, ar * bits);
                 ensure_discard(c, cp.alt, cp.n + dn);
-                diff_merge<K>(c, cp.rows.p, cp.n, sorted, dn, cp.alt.p, nullptr);
+                merge_disjoint<K>(c, cp.rows.p, cp.n, sorted, dn, cp.alt.p);
                 cp.rows.swap(cp.alt);
                 cp.n += dn;
                 data = cp.rows.p;
@@ -533,8 +533,7 @@ private:
         DevBuf<K> gained(c, m);
         {
             PhaseTimer t(E, "difference");
-            ensure_discard(c, head.full_alt, head.full_n + m);
-            mr = diff_merge<K>(c, head.full.p, head.full_n, sorted, m, head.full_alt.p, gained.p);
+            mr = difference_sorted<K>(c, head.full.p, head.full_n, sorted, m, gained.p);
         }
         {
             Tracked scratch(E.acct, Accountant::kTemp, m * 8 + rb(m, ar), "dedup");
@@ -547,6 +546,8 @@ private:
         {
             PhaseTimer t(E, "merge");
             merge_accounting(h, head.full_n, mr.delta_n, "merge");
+            ensure_discard(c, head.full_alt, head.full_n + mr.delta_n);
+            merge_disjoint<K>(c, head.full.p, head.full_n, gained.p, mr.delta_n, head.full_alt.p);
         }
         head.full.swap(head.full_alt);
         head.full_n += mr.delta_n;
@@ -568,10 +569,9 @@ private:
                 PhaseTimer t(E, "dedup");
                 sorted = sort_rows(st.new_acc, m, ar);
             }
-            PhaseTimer t(E, "merge");
-            ensure_discard(c, st.full_alt, st.full_n + m);
+            PhaseTimer t(E, "difference");
             ensure_discard(c, st.delta_alt, m);
-            mr = diff_merge<K>(c, st.full.p, st.full_n, sorted, m, st.full_alt.p, st.delta_alt.p);
+            mr = difference_sorted<K>(c, st.full.p, st.full_n, sorted, m, st.delta_alt.p);
             Tracked scratch(E.acct, Accountant::kTemp, m * 8 + rb(m, ar), "dedup");
         }
         Tracked fresh_charge(E.acct, Accountant::kTemp, rb(mr.unique_new, ar), "dedup");
@@ -586,6 +586,8 @@ private:
         if (mr.delta_n > 0) {
             PhaseTimer t(E, "merge");
             merge_accounting(r, st.full_n, mr.delta_n, "merge");
+            ensure_discard(c, st.full_alt, st.full_n + mr.delta_n);
+            merge_disjoint<K>(c, st.full.p, st.full_n, st.delta.p, mr.delta_n, st.full_alt.p);
             st.full.swap(st.full_alt);
             st.full_n += mr.delta_n;
             ++st.merge_gen;
@@ -672,14 +674,16 @@ void Impl<K>::partition_end(const void* d_recv, u64 recv_rows, u64* local_delta)
             PhaseTimer t(E, "dedup");
             sorted = sort_rows(buf, recv_rows, ar);
         }
-        PhaseTimer t(E, "merge");
-        ensure_discard(c, st.full_alt, st.full_n + recv_rows);
+        PhaseTimer t(E, "difference");
         ensure_discard(c, st.delta_alt, recv_rows);
-        mr = diff_merge<K>(c, st.full.p, st.full_n, sorted, recv_rows, st.full_alt.p, st.delta_alt.p);
+        mr = difference_sorted<K>(c, st.full.p, st.full_n, sorted, recv_rows, st.delta_alt.p);
     }
     st.delta.swap(st.delta_alt);
     st.delta_n = mr.delta_n;
     if (mr.delta_n) {
+        PhaseTimer t(E, "merge");
+        ensure_discard(c, st.full_alt, st.full_n + mr.delta_n);
+        merge_disjoint<K>(c, st.full.p, st.full_n, st.delta.p, mr.delta_n, st.full_alt.p);
         st.full.swap(st.full_alt);
         st.full_n += mr.delta_n;
     }

@@ -1,21 +1,24 @@
-// merge.cu — the fused difference + merge of one iteration
-// (difference, ra.hpp:386-422, then merge_sorted, ra.hpp:299-381, and the
-// adjacent-dedup tail of canonicalize, tuple_array.hpp:124-131).
+// merge.cu — difference (ra.hpp:386-422) and merge_sorted (ra.hpp:299-381)
+// of one iteration, with the adjacent-dedup tail of canonicalize
+// (tuple_array.hpp:124-131) folded into the difference.
 //
 // Inputs: F canonical (sorted, unique) and N sorted with duplicates (the
-// radix-sorted join output).  One merge-path pass emits
-//     F' = F U N   and   D = unique(N) \ F
-// in a single read of F and N and a single write of F' and D.
+// radix-sorted join output).
 //
-// Merge order breaks ties F-first, so an N element x is in F iff the F
-// element immediately before it in merge order equals x, and is a
-// duplicate iff the N element before it equals x.  Each tile of
-// kMergeThreads * kMergeItems merged positions is delimited by a global
-// merge-path search (partition kernel), staged in shared memory, merged by
-// per-thread sequential merges, and its output offsets come from a block
-// scan of kept-N counts plus a decoupled look-back across tiles.
+// difference_sorted:  D = unique(N) \ F.  One flag per N row: "first of its
+//   run and absent from F", then an order-preserving compaction.  Membership
+//   is a binary search of F when N is small next to F (the long tail: reads
+//   O(|N| log |F|) sectors instead of streaming F), else a merge-path pass
+//   that stages each tile's F and N segments in shared memory.
+// merge_disjoint:  F' = F U D for disjoint canonical inputs.  A merge-path
+//   partition fixes every tile's output range up front (output position =
+//   merge-path diagonal), so there is no cross-tile dependency: tiles that
+//   receive no D row are straight coalesced copies of F, the others merge in
+//   bank-conflict-free padded shared memory.  HBM traffic: read F + D, write
+//   F' — the roofline of the step.
 #include "dev_common.cuh"
 #include "ops.h"
+#include "select.cuh"
 
 namespace gd {
 
@@ -25,8 +28,8 @@ constexpr int kMergeThreads = 256;
 constexpr int kMergeItems = 8;
 constexpr u64 kMergeTile = (u64)kMergeThreads * kMergeItems;
 
-// splits[t] = number of F elements among the first min(t*tile, nf+nn)
-// positions of the merged order (ties: F first).
+// splits[t] = number of A rows among the first min(t*tile, na+nb) positions
+// of the merged order (ties: A first).
 template <typename K>
 __global__ void merge_partition_kernel(const K* __restrict__ A, u64 na, const K* __restrict__ B,
                                        u64 nb, u64 tile, u64 nsplits, u64* __restrict__ splits) {
@@ -43,181 +46,256 @@ __global__ void merge_partition_kernel(const K* __restrict__ A, u64 na, const K*
     splits[t] = lo;
 }
 
-// Shared-memory index padding: one spare element every 8, so the per-thread
+// Shared-memory index padding: one spare element every 8, so per-thread
 // sequential merges (threads 8 elements apart) hit distinct banks.
 __device__ __forceinline__ u32 pad8(u32 i) { return i + (i >> 3); }
 constexpr u32 kPadTile = kMergeTile + (kMergeTile >> 3) + 8;
 
+// ---- difference: flags ---------------------------------------------------
+
+// Binary-search membership (|N| << |F|): keep[j] = first-of-run && not in F.
+template <typename K>
+__global__ void diff_flags_search_kernel(const K* __restrict__ F, u64 nf, const K* __restrict__ N, u64 nn,
+                                         uint8_t* __restrict__ keep, u64* counters) {
+    u64 uniq = 0;
+    for (u64 j = (u64)blockIdx.x * blockDim.x + threadIdx.x; j < nn; j += (u64)gridDim.x * blockDim.x) {
+        const K x = N[j];
+        const bool first = j == 0 || N[j - 1] != x;
+        bool in_f = false;
+        if (first && nf) {
+            u64 lo = 0, hi = nf;
+            while (lo < hi) {
+                const u64 mid = (lo + hi) >> 1;
+                if (F[mid] < x) lo = mid + 1;
+                else hi = mid;
+            }
+            in_f = lo < nf && F[lo] == x;
+        }
+        keep[j] = (first && !in_f) ? 1 : 0;
+        uniq += first;
+    }
+    uniq = warp_sum(uniq);
+    if (lane_id() == 0 && uniq) atomicAdd(counters, uniq);
+}
+
+// Streaming membership (|N| comparable to |F|): merge-path tiles over
+// (F, N); for each N row the largest F row <= it (merge order, F first)
+// decides membership.
+template <typename K>
+__global__ void __launch_bounds__(kMergeThreads) diff_flags_stream_kernel(
+    const K* __restrict__ F, u64 nf, const K* __restrict__ N, u64 nn, const u64* __restrict__ splits,
+    uint8_t* __restrict__ keep, u64* counters) {
+    __shared__ K sA[kMergeTile + 1];
+    const u64 tile = blockIdx.x;
+    const u64 diag0 = tile * kMergeTile;
+    const u64 diag1 = min(diag0 + kMergeTile, nf + nn);
+    const u64 a0 = splits[tile], a1 = splits[tile + 1];
+    const u64 b0 = diag0 - a0, b1 = diag1 - a1;
+    const u32 na = (u32)(a1 - a0);
+    if (b1 == b0) return;
+    for (u32 i = threadIdx.x; i < na; i += kMergeThreads) sA[1 + i] = F[a0 + i];
+    if (threadIdx.x == 0) sA[0] = a0 > 0 ? F[a0 - 1] : K(0);
+    __syncthreads();
+    const bool has_halo = a0 > 0;
+    u64 uniq = 0;
+    for (u64 j = b0 + threadIdx.x; j < b1; j += kMergeThreads) {
+        const K x = N[j];
+        const bool first = j == 0 || N[j - 1] != x;
+        // count of tile F rows <= x (upper bound over sA[1..na])
+        u32 lo = 0, hi = na;
+        while (lo < hi) {
+            const u32 mid = (lo + hi) >> 1;
+            if (sA[1 + mid] <= x) lo = mid + 1;
+            else hi = mid;
+        }
+        const bool in_f = lo > 0 ? sA[lo] == x : (has_halo && sA[0] == x);
+        keep[j] = (first && !in_f) ? 1 : 0;
+        uniq += first;
+    }
+    uniq = warp_sum(uniq);
+    if (lane_id() == 0 && uniq) atomicAdd(counters, uniq);
+}
+
+// ---- merge of disjoint canonical arrays -----------------------------------
+
 template <typename K>
 struct MergeSmem {
-    K in[kPadTile + 2];  // [halo F | F tile | halo N | N tile], padded indices
-    K outF[kPadTile];
-    K outD[kPadTile];
+    K in[kPadTile + 2];
+    K out[kPadTile];
 };
 
-// ws: [0] tile counter, [1] kept total, [2] unique-N total, [3] overlap,
-//     [4..] tile statuses.
 template <typename K>
-__global__ void __launch_bounds__(kMergeThreads) diff_merge_kernel(
-    const K* __restrict__ F, u64 nf, const K* __restrict__ N, u64 nn,
-    const u64* __restrict__ splits, K* __restrict__ Fout, K* __restrict__ Dout, u64* ws) {
+__global__ void __launch_bounds__(kMergeThreads) merge_disjoint_kernel(
+    const K* __restrict__ A, u64 na_all, const K* __restrict__ B, u64 nb_all, const u64* __restrict__ splits,
+    K* __restrict__ out, u64* overlap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    MergeSmem<K>& sm = *reinterpret_cast<MergeSmem<K>*>(smem_raw);
-    __shared__ u64 s_tile;
-    __shared__ u64 s_scan[kMergeThreads / 32 + 1];
-    __shared__ u64 s_base;
-
-    const u64 tile = claim_tile(ws, &s_tile);
-    const u64 total = nf + nn;
+    const u64 tile = blockIdx.x;
     const u64 diag0 = tile * kMergeTile;
-    const u64 diag1 = min(diag0 + kMergeTile, total);
+    const u64 diag1 = min(diag0 + kMergeTile, na_all + nb_all);
     const u64 a0 = splits[tile], a1 = splits[tile + 1];
     const u64 b0 = diag0 - a0, b1 = diag1 - a1;
     const u32 na = (u32)(a1 - a0), nb = (u32)(b1 - b0);
 
-    // Stage (logical index -> padded slot): A(i) = F[a0 - 1 + i] for
-    // i in [0, na] (A(0) is the halo), B(i) = N[b0 - 1 + i] at logical
-    // offset na + 1.
-    K* in = sm.in;
-    const u32 boff = na + 1;
-    for (u32 i = threadIdx.x; i < na; i += kMergeThreads) in[pad8(1 + i)] = F[a0 + i];
-    for (u32 i = threadIdx.x; i < nb; i += kMergeThreads) in[pad8(boff + 1 + i)] = N[b0 + i];
-    if (threadIdx.x == 0) {
-        in[pad8(0)] = a0 > 0 ? F[a0 - 1] : K(0);
-        in[pad8(boff)] = b0 > 0 ? N[b0 - 1] : K(0);
+    if (nb == 0) {
+        // Pure copy of A[a0, a1) to out[diag0, ...): unrolled, coalesced.
+        const K* __restrict__ src = A + a0;
+        K* __restrict__ dst = out + diag0;
+        K v[kMergeItems];
+#pragma unroll
+        for (int s = 0; s < kMergeItems; ++s) {
+            const u32 i = threadIdx.x + s * kMergeThreads;
+            if (i < na) v[s] = src[i];
+        }
+#pragma unroll
+        for (int s = 0; s < kMergeItems; ++s) {
+            const u32 i = threadIdx.x + s * kMergeThreads;
+            if (i < na) dst[i] = v[s];
+        }
+        return;
     }
+
+    MergeSmem<K>& sm = *reinterpret_cast<MergeSmem<K>*>(smem_raw);
+    K* in = sm.in;
+    const u32 boff = na;
+    for (u32 i = threadIdx.x; i < na; i += kMergeThreads) in[pad8(i)] = A[a0 + i];
+    for (u32 i = threadIdx.x; i < nb; i += kMergeThreads) in[pad8(boff + i)] = B[b0 + i];
     __syncthreads();
 #define SA(i) in[pad8(i)]
 #define SB(i) in[pad8(boff + (i))]
-
-    // Per-thread sub-range of the tile's merge path.
     const u32 tn = na + nb;
     const u32 d = min((u32)threadIdx.x * kMergeItems, tn);
     const u32 de = min(d + kMergeItems, tn);
     u32 lo = d > nb ? d - nb : 0, hi = min(d, na);
     while (lo < hi) {
         const u32 mid = (lo + hi) >> 1;
-        if (SA(1 + mid) <= SB(1 + (d - 1 - mid))) lo = mid + 1;
+        if (SA(mid) <= SB(d - 1 - mid)) lo = mid + 1;
         else hi = mid;
     }
-    const u32 ai0 = lo;
-
-    // One sequential merge of <= kMergeItems steps into registers.
-    // kind: 0 = F row, 1 = kept N row (new), 2 = dropped N row.
-    K val[kMergeItems];
-    u32 kinds = 0;  // 2 bits per step
-    u32 ai = ai0, bi = d - ai0;
-    u64 kept = 0, uniq = 0;
-    bool overlap = false;
+    u32 ai = lo, bi = d - lo;
+    // an equal pair split by the tile boundary: A[a0-1] (end of the
+    // previous tile, A first on ties) against this tile's first B row
+    bool ov = threadIdx.x == 0 && a0 > 0 && A[a0 - 1] == SB(0);
 #pragma unroll
     for (int s = 0; s < kMergeItems; ++s) {
         if (d + s < de) {
-            const K xa = SA(1 + ai);
-            const K xb = SB(1 + bi);
+            const K xa = SA(ai);
+            const K xb = SB(bi);
             const bool takeA = bi >= nb || (ai < na && xa <= xb);
-            if (takeA) {
-                val[s] = xa;
-                ++ai;
-            } else {
-                const bool dup = (b0 + bi > 0) && SB(bi) == xb;
-                const bool inF = (a0 + ai > 0) && SA(ai) == xb;
-                uniq += !dup;
-                overlap |= (inF && !dup);
-                const bool keep = !dup && !inF;
-                kept += keep;
-                val[s] = xb;
-                kinds |= (keep ? 1u : 2u) << (2 * s);
-                ++bi;
-            }
-        } else {
-            kinds |= 3u << (2 * s);
-        }
-    }
-    u64 tile_kept;
-    const u64 excl = block_exclusive_scan<u64, kMergeThreads>(kept | (uniq << 32), tile_kept, s_scan);
-    const u64 tile_uniq = tile_kept >> 32;
-    tile_kept &= 0xffffffffull;
-    const bool any_overlap = __syncthreads_or(overlap);
-    if (threadIdx.x < 32) {
-        const u64 base = warp_lookback(ws + 4, tile, tile_kept);
-        if (threadIdx.x == 0) {
-            s_base = base;
-            atomicAdd(ws + 1, tile_kept);
-            atomicAdd(ws + 2, tile_uniq);
-            if (any_overlap) atomicOr(ws + 3, 1ull);
-        }
-    }
-    // Registers -> staging at tile-local output positions.
-    u32 a = ai0;
-    u32 k = (u32)(excl & 0xffffffffull);  // kept N rows before this thread in the tile
-#pragma unroll
-    for (int s = 0; s < kMergeItems; ++s) {
-        const u32 kind = (kinds >> (2 * s)) & 3u;
-        if (kind == 0) {
-            sm.outF[pad8(a + k)] = val[s];
-            ++a;
-        } else if (kind == 1) {
-            sm.outF[pad8(a + k)] = val[s];
-            sm.outD[pad8(k)] = val[s];
-            ++k;
+            ov |= (ai < na && bi < nb && xa == xb);
+            sm.out[pad8(d + s)] = takeA ? xa : xb;
+            ai += takeA;
+            bi += !takeA;
         }
     }
 #undef SA
 #undef SB
-    __syncthreads();
-    const u64 kbase = s_base;
-    // Coalesced copy-out: F' rows [a0 + kbase, a1 + kbase + tile_kept),
-    //                     D rows  [kbase, kbase + tile_kept).
-    const u32 nout = na + (u32)tile_kept;
-    if (Fout)
-        for (u32 i = threadIdx.x; i < nout; i += kMergeThreads) Fout[a0 + kbase + i] = sm.outF[pad8(i)];
-    if (Dout)
-        for (u32 i = threadIdx.x; i < (u32)tile_kept; i += kMergeThreads) Dout[kbase + i] = sm.outD[pad8(i)];
+    if (__syncthreads_or(ov) && threadIdx.x == 0) atomicOr(overlap, 1ull);
+    for (u32 i = threadIdx.x; i < tn; i += kMergeThreads) out[diag0 + i] = sm.out[pad8(i)];
+}
+
+struct FlagKeep {
+    const uint8_t* f;
+    __device__ bool operator()(u64 i) const { return f[i] != 0; }
+};
+template <typename K>
+struct CopyRow {
+    const K* in;
+    K* out;
+    __device__ void operator()(u64 i, u64 pos) const { out[pos] = in[i]; }
+};
+
+template <typename K>
+u64* partition(Ctx& c, const K* A, u64 na, const K* B, u64 nb, DevBuf<u64>& splits, u64& tiles) {
+    tiles = (na + nb + kMergeTile - 1) / kMergeTile;
+    splits.reserve_discard(c, tiles + 1);
+    cudaEvent_t tp = c.prof_begin();
+    merge_partition_kernel<K><<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, c.stream>>>(
+        A, na, B, nb, kMergeTile, tiles + 1, splits.p);
+    c.check_launch();
+    c.prof_end(tp, KC_OTHER, 0);
+    return splits.p;
 }
 
 }  // namespace
 
 template <typename K>
-MergeResult diff_merge(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K* Fout, K* Dout) {
+MergeResult difference_sorted(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K* Dout) {
     MergeResult r;
-    if (nn == 0) {
-        if (Fout && nf) c.d2d(Fout, F, nf * sizeof(K));
-        return r;
+    if (nn == 0) return r;
+    DevBuf<uint8_t> keep(c, nn);
+    DevBuf<u64> counters(c, 1);
+    c.memset(counters.p, 0, sizeof(u64));
+    // binary search when N is small next to F, else stream F once
+    const bool search = nf == 0 || nn * 24 < nf;
+    cudaEvent_t t;
+    if (search) {
+        const int grid = (int)std::max<u64>(1, std::min<u64>((nn + 255) / 256, (u64)c.num_sms * 16));
+        t = c.prof_begin();
+        diff_flags_search_kernel<K><<<grid, 256, 0, c.stream>>>(F, nf, N, nn, keep.p, counters.p);
+        c.check_launch();
+    } else {
+        DevBuf<u64> splits;
+        u64 tiles = 0;
+        partition<K>(c, F, nf, N, nn, splits, tiles);
+        t = c.prof_begin();
+        diff_flags_stream_kernel<K><<<(unsigned)tiles, kMergeThreads, 0, c.stream>>>(F, nf, N, nn, splits.p,
+                                                                                     keep.p, counters.p);
+        c.check_launch();
     }
-    const u64 total = nf + nn;
-    const u64 tiles = (total + kMergeTile - 1) / kMergeTile;
-    DevBuf<u64> splits(c, tiles + 1);
-    cudaEvent_t tp = c.prof_begin();
-    merge_partition_kernel<K><<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, c.stream>>>(
-        F, nf, N, nn, kMergeTile, tiles + 1, splits.p);
-    c.check_launch();
-    c.prof_end(tp, KC_OTHER, 0);
-    DevBuf<u64> ws(c, 4 + tiles);
-    c.memset(ws.p, 0, (4 + tiles) * sizeof(u64));
-    const size_t smem = sizeof(MergeSmem<K>);
-    static bool attr_set = false;
-    if (!attr_set) {
-        GD_CUDA(cudaFuncSetAttribute(diff_merge_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        attr_set = true;
-    }
-    cudaEvent_t t = c.prof_begin();
-    diff_merge_kernel<K><<<(unsigned)tiles, kMergeThreads, smem, c.stream>>>(F, nf, N, nn, splits.p,
-                                                                               Fout, Dout, ws.p);
-    c.check_launch();
-    const long rec = c.prof_end(t, KC_MERGE, 0);
-    unsigned long long w[3];
-    c.read_words(w, ws.p + 1, 3);
-    r.delta_n = w[0];
-    r.unique_new = w[1];
-    r.overlap = w[2] != 0;
-    // algorithmic bytes: read F and the sorted new rows, write
-    // F' = F + D and D.
-    c.prof_add_bytes(rec, sizeof(K) * ((nf + nn) + (Fout ? nf + r.delta_n : 0) + (Dout ? r.delta_n : 0)));
+    // algorithmic bytes: N read + flags written (+ F streamed when streaming)
+    c.prof_end(t, KC_DIFF, nn * (sizeof(K) + 1) + (search ? 0 : nf * sizeof(K)));
+    r.delta_n = run_select(c, nn, FlagKeep{keep.p}, CopyRow<K>{N, Dout});
+    unsigned long long u;
+    c.read_words(&u, counters.p, 1);
+    r.unique_new = u;
     return r;
 }
 
-template MergeResult diff_merge<u64>(Ctx&, const u64*, u64, const u64*, u64, u64*, u64*);
-template MergeResult diff_merge<u128>(Ctx&, const u128*, u64, const u128*, u64, u128*, u128*);
+template <typename K>
+bool merge_disjoint(Ctx& c, const K* A, u64 na, const K* B, u64 nb, K* out) {
+    if (nb == 0) {
+        if (na) c.d2d(out, A, na * sizeof(K));
+        return false;
+    }
+    if (na == 0) {
+        c.d2d(out, B, nb * sizeof(K));
+        return false;
+    }
+    DevBuf<u64> splits;
+    u64 tiles = 0;
+    partition<K>(c, A, na, B, nb, splits, tiles);
+    DevBuf<u64> ov(c, 1);
+    c.memset(ov.p, 0, sizeof(u64));
+    const size_t smem = sizeof(MergeSmem<K>);
+    GD_CUDA(cudaFuncSetAttribute(merge_disjoint_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaEvent_t t = c.prof_begin();
+    merge_disjoint_kernel<K><<<(unsigned)tiles, kMergeThreads, smem, c.stream>>>(A, na, B, nb, splits.p, out, ov.p);
+    c.check_launch();
+    // algorithmic bytes: read A and B, write A + B
+    c.prof_end(t, KC_MERGE, 2 * (na + nb) * sizeof(K));
+    unsigned long long o;
+    c.read_words(&o, ov.p, 1);
+    return o != 0;
+}
+
+template <typename K>
+MergeResult diff_merge(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K* Fout, K* Dout) {
+    DevBuf<K> dtmp;
+    if (!Dout) {
+        dtmp = DevBuf<K>(c, std::max<u64>(nn, 1));
+        Dout = dtmp.p;
+    }
+    MergeResult r = difference_sorted<K>(c, F, nf, N, nn, Dout);
+    if (Fout) r.overlap = merge_disjoint<K>(c, F, nf, Dout, r.delta_n, Fout);
+    return r;
+}
+
+#define GD_INST(K)                                                                         \
+    template MergeResult difference_sorted<K>(Ctx&, const K*, u64, const K*, u64, K*);     \
+    template bool merge_disjoint<K>(Ctx&, const K*, u64, const K*, u64, K*);               \
+    template MergeResult diff_merge<K>(Ctx&, const K*, u64, const K*, u64, K*, K*);
+GD_INST(u64)
+GD_INST(u128)
+#undef GD_INST
 
 }  // namespace gd

@@ -95,6 +95,12 @@ struct MergeResult {
 // Fout must hold nf + nn rows, Dout nn rows.
 template <typename K>
 MergeResult diff_merge(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K* Fout, K* Dout);
+// D = unique(N) \ F (difference + adjacent dedup); Dout holds nn rows.
+template <typename K>
+MergeResult difference_sorted(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K* Dout);
+// out = A U B for canonical inputs; returns true if they overlap.
+template <typename K>
+bool merge_disjoint(Ctx& c, const K* A, u64 na, const K* B, u64 nb, K* out);
 
 // ---- index.cu -------------------------------------------------------
 struct Slot {

@@ -64,9 +64,23 @@ struct CopyState {
 };
 
 template <typename K>
+struct Run {
+    DevBuf<K> buf;
+    u64 n = 0;
+};
+
+// Tier ratio of the tiered (LSM) full relation: every run holds at least
+// kTierRatio times the rows of the next smaller one.
+constexpr u64 kTierRatio = 4;
+
+template <typename K>
 struct RelDev {
+    // full relation = `full` (the base run) U every run of `tail`; all
+    // sorted and pairwise disjoint.  `tail` stays empty unless `lsm`.
     DevBuf<K> full, full_alt;
     u64 full_n = 0;
+    std::vector<Run<K>> tail;
+    bool lsm = false;
     DevBuf<K> delta, delta_alt;
     u64 delta_n = 0;
     DevBuf<K> new_acc;
@@ -97,6 +111,12 @@ public:
                     cp.prefix = key.second;
                     cp.identity = is_identity(st.inner_perm, ar);
                 }
+        // Relations that are never a join inner (no indexed copy) keep their
+        // full version tiered: Δ is appended as a small sorted run and runs
+        // are merged (merge-path) only when a run reaches 1/kTierRatio of its
+        // larger neighbour — the per-iteration O(|F|) merge of the reference
+        // becomes O(|F| log |F|) over the whole fixpoint.
+        for (u32 r = 0; r < nrels; ++r) rels[r].lsm = !E.info_[r].is_edb && rels[r].copies.empty();
         // EDB rows: pack under the engine encoding; order is preserved, so
         // canonical raw rows stay canonical (no re-sort).
         for (u32 r = 0; r < nrels; ++r) {
@@ -141,6 +161,7 @@ public:
         for (u32 r = 0; r < rels.size(); ++r) {
             if (E.info_[r].is_edb) continue;
             auto& st = rels[r];
+            compact(st);
             ensure_discard(c, st.delta, st.full_n);
             if (st.full_n) c.d2d(st.delta.p, st.full.p, st.full_n * sizeof(K));
             assign_delta(r, st.full_n, "other");
@@ -156,6 +177,7 @@ public:
         for (u32 r = 0; r < rels.size(); ++r) {
             if (E.info_[r].is_edb) continue;
             auto& st = rels[r];
+            compact(st);
             if (st.full_n == 0) continue;
             DevBuf<u32> own(c, st.full_n);
             DevBuf<uint8_t> flags(c, st.full_n);
@@ -217,12 +239,15 @@ public:
                 E.info_[r].log.push_back(log);
             }
         }
+        // the fixpoint's canonical output: one sorted array per relation
+        for (auto& st : rels) compact(st);
     }
 
-    u64 count(u32 r) override { return rels[r].full_n; }
+    u64 count(u32 r) override { return total_n(rels[r]); }
 
     void download(u32 r, u64* out, bool device) override {
         auto& st = rels[r];
+        compact(st);
         const u32 ar = E.info_[r].arity;
         if (st.full_n == 0) return;
         if (device) {
@@ -237,7 +262,88 @@ public:
     }
 
     u64 digest(u32 r) override {
+        compact(rels[r]);
         return digest_rows<K>(c, rels[r].full.p, rels[r].full_n, E.info_[r].arity, E.enc.e);
+    }
+
+    // ---- tiered full relation ---------------------------------------------
+    static u64 total_n(const RelDev<K>& st) {
+        u64 t = st.full_n;
+        for (const auto& r : st.tail) t += r.n;
+        return t;
+    }
+
+    // Merges the tail runs (smallest first) and then into the base run.
+    void compact(RelDev<K>& st) {
+        while (st.tail.size() > 1) {
+            Run<K> b = std::move(st.tail.back());
+            st.tail.pop_back();
+            Run<K>& a = st.tail.back();
+            Run<K> m;
+            m.buf = DevBuf<K>(c, a.n + b.n);
+            merge_disjoint<K>(c, a.buf.p, a.n, b.buf.p, b.n, m.buf.p);
+            m.n = a.n + b.n;
+            a = std::move(m);
+        }
+        if (!st.tail.empty()) {
+            Run<K> b = std::move(st.tail.back());
+            st.tail.pop_back();
+            ensure_discard(c, st.full_alt, st.full_n + b.n);
+            merge_disjoint<K>(c, st.full.p, st.full_n, b.buf.p, b.n, st.full_alt.p);
+            st.full.swap(st.full_alt);
+            st.full_n += b.n;
+        }
+    }
+
+    // D = unique(N) \ full (N sorted, duplicates allowed).
+    MergeResult difference_full(RelDev<K>& st, const K* N, u64 nn, K* Dout) {
+        if (!st.tail.empty() && nn * 24 >= total_n(st)) compact(st);
+        if (st.tail.empty()) return difference_sorted<K>(c, st.full.p, st.full_n, N, nn, Dout);
+        std::vector<const K*> ptr{st.full.p};
+        std::vector<u64> ns{st.full_n};
+        for (const auto& r : st.tail) {
+            ptr.push_back(r.buf.p);
+            ns.push_back(r.n);
+        }
+        return difference_runs<K>(c, ptr.data(), ns.data(), (u32)ptr.size(), N, nn, Dout);
+    }
+
+    // full <- full U D (D disjoint from full, canonical).
+    void add_to_full(RelDev<K>& st, const K* D, u64 nd) {
+        if (nd == 0) return;
+        if (!st.lsm) {
+            ensure_discard(c, st.full_alt, st.full_n + nd);
+            merge_disjoint<K>(c, st.full.p, st.full_n, D, nd, st.full_alt.p);
+            st.full.swap(st.full_alt);
+            st.full_n += nd;
+            return;
+        }
+        Run<K> run;
+        run.buf = DevBuf<K>(c, nd);
+        c.d2d(run.buf.p, D, nd * sizeof(K));
+        run.n = nd;
+        st.tail.push_back(std::move(run));
+        // restore the tier invariant (each run >= kTierRatio x the next one)
+        while (!st.tail.empty()) {
+            const size_t k = st.tail.size();
+            const u64 prev = k >= 2 ? st.tail[k - 2].n : st.full_n;
+            if (prev >= kTierRatio * st.tail[k - 1].n) break;
+            Run<K> b = std::move(st.tail.back());
+            st.tail.pop_back();
+            if (k >= 2) {
+                Run<K>& a = st.tail.back();
+                Run<K> m;
+                m.buf = DevBuf<K>(c, a.n + b.n);
+                merge_disjoint<K>(c, a.buf.p, a.n, b.buf.p, b.n, m.buf.p);
+                m.n = a.n + b.n;
+                a = std::move(m);
+            } else {
+                ensure_discard(c, st.full_alt, st.full_n + b.n);
+                merge_disjoint<K>(c, st.full.p, st.full_n, b.buf.p, b.n, st.full_alt.p);
+                st.full.swap(st.full_alt);
+                st.full_n += b.n;
+            }
+        }
     }
 
     // ---- hash-partitioned mode -----------------------------
@@ -331,6 +437,7 @@ private:
     void refresh_copies(u32 r) {
         PhaseTimer t(E, "index");
         auto& st = rels[r];
+        if (!st.copies.empty()) compact(st);
         const u32 ar = E.info_[r].arity;
         for (auto& kv : st.copies) {
             CopyState<K>& cp = kv.second;
@@ -379,6 +486,7 @@ private:
         auto& src = rels[v.src_rel];
         const u32 ar = E.info_[v.src_rel].arity;
         const bool use_delta = v.src_version == GD_DELTA;
+        if (!use_delta) compact(src);
         const K* cur = use_delta ? src.delta.p : src.full.p;
         u64 cur_n = use_delta ? src.delta_n : src.full_n;
         u32 cur_ar = ar;
@@ -533,7 +641,7 @@ private:
         DevBuf<K> gained(c, m);
         {
             PhaseTimer t(E, "difference");
-            mr = difference_sorted<K>(c, head.full.p, head.full_n, sorted, m, gained.p);
+            mr = difference_full(head, sorted, m, gained.p);
         }
         {
             Tracked scratch(E.acct, Accountant::kTemp, m * 8 + rb(m, ar), "dedup");
@@ -545,12 +653,9 @@ private:
         fresh_charge.reset();
         {
             PhaseTimer t(E, "merge");
-            merge_accounting(h, head.full_n, mr.delta_n, "merge");
-            ensure_discard(c, head.full_alt, head.full_n + mr.delta_n);
-            merge_disjoint<K>(c, head.full.p, head.full_n, gained.p, mr.delta_n, head.full_alt.p);
+            merge_accounting(h, total_n(head), mr.delta_n, "merge");
+            add_to_full(head, gained.p, mr.delta_n);
         }
-        head.full.swap(head.full_alt);
-        head.full_n += mr.delta_n;
         ++head.merge_gen;
         head.last_merge_was_delta = false;
         head.dirty = true;
@@ -571,7 +676,7 @@ private:
             }
             PhaseTimer t(E, "difference");
             ensure_discard(c, st.delta_alt, m);
-            mr = difference_sorted<K>(c, st.full.p, st.full_n, sorted, m, st.delta_alt.p);
+            mr = difference_full(st, sorted, m, st.delta_alt.p);
             Tracked scratch(E.acct, Accountant::kTemp, m * 8 + rb(m, ar), "dedup");
         }
         Tracked fresh_charge(E.acct, Accountant::kTemp, rb(mr.unique_new, ar), "dedup");
@@ -585,18 +690,15 @@ private:
         st.delta_n = mr.delta_n;
         if (mr.delta_n > 0) {
             PhaseTimer t(E, "merge");
-            merge_accounting(r, st.full_n, mr.delta_n, "merge");
-            ensure_discard(c, st.full_alt, st.full_n + mr.delta_n);
-            merge_disjoint<K>(c, st.full.p, st.full_n, st.delta.p, mr.delta_n, st.full_alt.p);
-            st.full.swap(st.full_alt);
-            st.full_n += mr.delta_n;
+            merge_accounting(r, total_n(st), mr.delta_n, "merge");
+            add_to_full(st, st.delta.p, mr.delta_n);
             ++st.merge_gen;
             st.last_merge_was_delta = true;
             st.dirty = true;
         }
         log.new_unique = mr.unique_new;
         log.delta_out = mr.delta_n;
-        log.full_after = st.full_n;
+        log.full_after = total_n(st);
     }
 };
 
@@ -676,20 +778,17 @@ void Impl<K>::partition_end(const void* d_recv, u64 recv_rows, u64* local_delta)
         }
         PhaseTimer t(E, "difference");
         ensure_discard(c, st.delta_alt, recv_rows);
-        mr = difference_sorted<K>(c, st.full.p, st.full_n, sorted, recv_rows, st.delta_alt.p);
+        mr = difference_full(st, sorted, recv_rows, st.delta_alt.p);
     }
     st.delta.swap(st.delta_alt);
     st.delta_n = mr.delta_n;
     if (mr.delta_n) {
         PhaseTimer t(E, "merge");
-        ensure_discard(c, st.full_alt, st.full_n + mr.delta_n);
-        merge_disjoint<K>(c, st.full.p, st.full_n, st.delta.p, mr.delta_n, st.full_alt.p);
-        st.full.swap(st.full_alt);
-        st.full_n += mr.delta_n;
+        add_to_full(st, st.delta.p, mr.delta_n);
     }
     log.new_unique = mr.unique_new;
     log.delta_out = mr.delta_n;
-    log.full_after = st.full_n;
+    log.full_after = total_n(st);
     E.info_[rec_rel].log.push_back(log);
     *local_delta = mr.delta_n;
 }

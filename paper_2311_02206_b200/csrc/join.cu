@@ -61,50 +61,111 @@ __device__ __forceinline__ K outer_prefix(const DevJoin& jd, K o) {
     return p;
 }
 
-// ws: [0] tile counter, [1] candidate total, [2..] statuses.
+// Pass 1a: one probe per outer row, kProbeItems independent rows per thread
+// (row = tile base + item * threads + tid: coalesced, and the items' slot
+// loads are issued together for memory-level parallelism).  Writes the
+// match start and count of every row and the tile's count sum; no
+// cross-tile dependency.
 template <typename K>
 __global__ void __launch_bounds__(kProbeThreads) join_probe_kernel(
     const K* __restrict__ outer, u64 n, DevJoin jd, IndexView<K> ix, u64 inner_n,
-    u64* __restrict__ row_start, u64* __restrict__ row_off, u64* ws) {
-    __shared__ u64 s_tile;
+    u64* __restrict__ row_start, u64* __restrict__ row_cnt, u64* __restrict__ tile_sum) {
+    __shared__ u64 s_red[kProbeThreads / 32];
+    const u64 base = (u64)blockIdx.x * kProbeTile + threadIdx.x;
+    u64 sum = 0;
+    if (jd.jcc == 0) {
+#pragma unroll
+        for (int j = 0; j < kProbeItems; ++j) {
+            const u64 r = base + (u64)j * kProbeThreads;
+            if (r < n) {
+                row_start[r] = 0;
+                row_cnt[r] = inner_n;
+                sum += inner_n;
+            }
+        }
+    } else {
+        K pre[kProbeItems];
+        u64 tag[kProbeItems], pos[kProbeItems];
+        Slot s[kProbeItems];
+#pragma unroll
+        for (int j = 0; j < kProbeItems; ++j) {
+            const u64 r = base + (u64)j * kProbeThreads;
+            pre[j] = r < n ? outer_prefix(jd, outer[r]) : K(0);
+        }
+#pragma unroll
+        for (int j = 0; j < kProbeItems; ++j) {
+            tag[j] = index_tag<K>(pre[j]);
+            pos[j] = slot_home(tag[j], ix.slot_count);
+            s[j] = ix.slots[pos[j]];
+        }
+#pragma unroll
+        for (int j = 0; j < kProbeItems; ++j) {
+            const u64 r = base + (u64)j * kProbeThreads;
+            if (r >= n) continue;
+            u64 st = 0, ln = 0;
+            if (s[j].tag == tag[j] && (sizeof(K) == 8 ||
+                                       prefix_of(ix.rows[s[j].val & kStartMask], ix.arity, ix.bits, ix.plen) == pre[j])) {
+                st = s[j].val & kStartMask;
+                const u64 l = s[j].val >> 40;
+                ln = l == kLenSat ? run_end(ix, pre[j], st) - st : l;
+            } else if (s[j].tag != kEmptySlot) {
+                index_probe(ix, pre[j], st, ln);  // collision chain (rare)
+            }
+            row_start[r] = st;
+            row_cnt[r] = ln;
+            sum += ln;
+        }
+    }
+    sum = warp_sum(sum);
+    if (lane_id() == 0) s_red[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u64 t = 0;
+        for (int w = 0; w < kProbeThreads / 32; ++w) t += s_red[w];
+        tile_sum[blockIdx.x] = t;
+    }
+}
+
+// Pass 1b: exclusive scan of the per-tile sums (one block); total at [ntiles].
+__global__ void __launch_bounds__(1024) scan_tiles_kernel(u64* __restrict__ tile_sum, u64 ntiles) {
+    __shared__ u64 s_scan[1024 / 32 + 1];
+    __shared__ u64 s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (u64 b = 0; b < ntiles; b += 1024) {
+        const u64 i = b + threadIdx.x;
+        const u64 v = i < ntiles ? tile_sum[i] : 0;
+        u64 tot;
+        const u64 ex = block_exclusive_scan<u64, 1024>(v, tot, s_scan);
+        if (i < ntiles) tile_sum[i] = s_carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) tile_sum[ntiles] = s_carry;
+}
+
+// Pass 1c: row offsets = tile prefix + in-tile exclusive scan of counts
+// (in place over the counts); row_off[n] = total.
+__global__ void __launch_bounds__(kProbeThreads) apply_offsets_kernel(u64* __restrict__ row_off, u64 n,
+                                                                      const u64* __restrict__ tile_prefix) {
     __shared__ u64 s_scan[kProbeThreads / 32 + 1];
-    __shared__ u64 s_base;
-    const u64 tile = claim_tile(ws, &s_tile);
-    const u64 begin = tile * kProbeTile + (u64)threadIdx.x * kProbeItems;
-    u64 st[kProbeItems], ln[kProbeItems];
+    const u64 begin = (u64)blockIdx.x * kProbeTile + (u64)threadIdx.x * kProbeItems;
+    u64 c[kProbeItems];
     u64 sum = 0;
 #pragma unroll
     for (int j = 0; j < kProbeItems; ++j) {
-        st[j] = 0;
-        ln[j] = 0;
-        const u64 r = begin + j;
-        if (r < n) {
-            if (jd.jcc == 0) {
-                ln[j] = inner_n;
-            } else {
-                index_probe(ix, outer_prefix(jd, outer[r]), st[j], ln[j]);
-            }
-        }
-        sum += ln[j];
+        c[j] = begin + j < n ? row_off[begin + j] : 0;
+        sum += c[j];
     }
-    u64 tile_total;
-    const u64 excl = block_exclusive_scan<u64, kProbeThreads>(sum, tile_total, s_scan);
-    if (threadIdx.x < 32) {
-        const u64 base = warp_lookback(ws + 2, tile, tile_total);
-        if (threadIdx.x == 0) {
-            s_base = base;
-            atomicAdd(ws + 1, tile_total);
-        }
-    }
-    __syncthreads();
-    u64 off = s_base + excl;
+    u64 tot;
+    u64 off = tile_prefix[blockIdx.x] + block_exclusive_scan<u64, kProbeThreads>(sum, tot, s_scan);
 #pragma unroll
     for (int j = 0; j < kProbeItems; ++j) {
         const u64 r = begin + j;
         if (r < n) {
-            row_start[r] = st[j];
             row_off[r] = off;
-            off += ln[j];
+            off += c[j];
             if (r == n - 1) row_off[n] = off;
         }
     }
@@ -204,18 +265,23 @@ u64 join_probe(Ctx& c, const K* outer, u64 n, const DevJoin& jd, const IndexView
         return 0;
     }
     const u64 tiles = (n + kProbeTile - 1) / kProbeTile;
-    DevBuf<u64> ws(c, 2 + tiles);
-    c.memset(ws.p, 0, (2 + tiles) * sizeof(u64));
+    DevBuf<u64> tile_sum(c, tiles + 1);
     IndexView<K> view{};
     if (ix) view = *ix;
     cudaEvent_t t = c.prof_begin();
     join_probe_kernel<K><<<(unsigned)tiles, kProbeThreads, 0, c.stream>>>(outer, n, jd, view, inner_n,
-                                                                           row_start, row_off, ws.p);
+                                                                           row_start, row_off, tile_sum.p);
     c.check_launch();
     // algorithmic bytes: the outer rows + one 16-byte slot probe per row
     c.prof_end(t, KC_PROBE, n * (sizeof(K) + (jd.jcc ? sizeof(Slot) : 0)));
+    cudaEvent_t t2 = c.prof_begin();
+    scan_tiles_kernel<<<1, 1024, 0, c.stream>>>(tile_sum.p, tiles);
+    c.check_launch();
+    apply_offsets_kernel<<<(unsigned)tiles, kProbeThreads, 0, c.stream>>>(row_off, n, tile_sum.p);
+    c.check_launch();
+    c.prof_end(t2, KC_SELECT, 0);
     unsigned long long total;
-    c.read_words(&total, ws.p + 1, 1);
+    c.read_words(&total, row_off + n, 1);
     return total;
 }
 

@@ -78,6 +78,43 @@ __global__ void diff_flags_search_kernel(const K* __restrict__ F, u64 nf, const 
     if (lane_id() == 0 && uniq) atomicAdd(counters, uniq);
 }
 
+// Binary-search membership against a tiered full relation (several sorted
+// disjoint runs, engine.cu LSM mode).
+constexpr int kMaxRuns = 24;
+struct RunSet {
+    const void* ptr[kMaxRuns];
+    u64 n[kMaxRuns];
+    u32 count;
+};
+
+template <typename K>
+__global__ void diff_flags_search_runs_kernel(RunSet rs, const K* __restrict__ N, u64 nn,
+                                              uint8_t* __restrict__ keep, u64* counters) {
+    u64 uniq = 0;
+    for (u64 j = (u64)blockIdx.x * blockDim.x + threadIdx.x; j < nn; j += (u64)gridDim.x * blockDim.x) {
+        const K x = N[j];
+        const bool first = j == 0 || N[j - 1] != x;
+        bool in_f = false;
+        if (first) {
+            for (u32 r = 0; r < rs.count && !in_f; ++r) {
+                const K* __restrict__ F = static_cast<const K*>(rs.ptr[r]);
+                const u64 nf = rs.n[r];
+                u64 lo = 0, hi = nf;
+                while (lo < hi) {
+                    const u64 mid = (lo + hi) >> 1;
+                    if (F[mid] < x) lo = mid + 1;
+                    else hi = mid;
+                }
+                in_f = lo < nf && F[lo] == x;
+            }
+        }
+        keep[j] = (first && !in_f) ? 1 : 0;
+        uniq += first;
+    }
+    uniq = warp_sum(uniq);
+    if (lane_id() == 0 && uniq) atomicAdd(counters, uniq);
+}
+
 // Streaming membership (|N| comparable to |F|): merge-path tiles over
 // (F, N); for each N row the largest F row <= it (merge order, F first)
 // decides membership.
@@ -252,6 +289,37 @@ MergeResult difference_sorted(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K*
 }
 
 template <typename K>
+MergeResult difference_runs(Ctx& c, const K* const* runs, const u64* ns, u32 nruns, const K* N, u64 nn,
+                            K* Dout) {
+    if (nruns <= 1) return difference_sorted<K>(c, nruns ? runs[0] : nullptr, nruns ? ns[0] : 0, N, nn, Dout);
+    if (nruns > (u32)kMaxRuns) throw_logic("difference_runs: too many runs");
+    MergeResult r;
+    if (nn == 0) return r;
+    RunSet rs{};
+    u64 total = 0;
+    for (u32 i = 0; i < nruns; ++i) {
+        rs.ptr[i] = runs[i];
+        rs.n[i] = ns[i];
+        total += ns[i];
+    }
+    rs.count = nruns;
+    DevBuf<uint8_t> keep(c, nn);
+    DevBuf<u64> counters(c, 1);
+    c.memset(counters.p, 0, sizeof(u64));
+    const int grid = (int)std::max<u64>(1, std::min<u64>((nn + 255) / 256, (u64)c.num_sms * 16));
+    cudaEvent_t t = c.prof_begin();
+    diff_flags_search_runs_kernel<K><<<grid, 256, 0, c.stream>>>(rs, N, nn, keep.p, counters.p);
+    c.check_launch();
+    c.prof_end(t, KC_DIFF, nn * (sizeof(K) + 1));
+    r.delta_n = run_select(c, nn, FlagKeep{keep.p}, CopyRow<K>{N, Dout});
+    unsigned long long u;
+    c.read_words(&u, counters.p, 1);
+    r.unique_new = u;
+    (void)total;
+    return r;
+}
+
+template <typename K>
 bool merge_disjoint(Ctx& c, const K* A, u64 na, const K* B, u64 nb, K* out) {
     if (nb == 0) {
         if (na) c.d2d(out, A, na * sizeof(K));
@@ -293,6 +361,7 @@ MergeResult diff_merge(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K* Fout, 
 #define GD_INST(K)                                                                         \
     template MergeResult difference_sorted<K>(Ctx&, const K*, u64, const K*, u64, K*);     \
     template bool merge_disjoint<K>(Ctx&, const K*, u64, const K*, u64, K*);               \
+    template MergeResult difference_runs<K>(Ctx&, const K* const*, const u64*, u32, const K*, u64, K*); \
     template MergeResult diff_merge<K>(Ctx&, const K*, u64, const K*, u64, K*, K*);
 GD_INST(u64)
 GD_INST(u128)

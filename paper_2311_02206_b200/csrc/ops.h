@@ -98,6 +98,10 @@ MergeResult diff_merge(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K* Fout, 
 // D = unique(N) \ F (difference + adjacent dedup); Dout holds nn rows.
 template <typename K>
 MergeResult difference_sorted(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K* Dout);
+// D = unique(N) \ (R_0 U ... U R_k) for sorted disjoint runs R_i.
+template <typename K>
+MergeResult difference_runs(Ctx& c, const K* const* runs, const u64* ns, u32 nruns, const K* N, u64 nn,
+                            K* Dout);
 // out = A U B for canonical inputs; returns true if they overlap.
 template <typename K>
 bool merge_disjoint(Ctx& c, const K* A, u64 na, const K* B, u64 nb, K* out);

@@ -376,7 +376,7 @@ gd_status gd_index_lookup(gd_ctx* ctx, const uint64_t* rows, uint64_t n, uint32_
             pack_rows<K>(c, d.p, n, arity, eo.e, pk.p);
             DevIndex<K> idx;
             build_index<K>(c, pk.p, n, arity, eo.e.bits, prefix_len, load_factor, idx);
-            *out_slot_count = idx.slot_count;
+            *out_slot_count = idx.logical_slots;
             *out_occupied = idx.groups;
             if (nkeys) {
                 DevBuf<K> pkeys(c, nkeys);
@@ -455,7 +455,7 @@ gd_status gd_merge_sorted(gd_ctx* ctx, const uint64_t* full, uint64_t nf, int fu
             DevBuf<K> pf(c, std::max<u64>(nf, 1)), pd(c, std::max<u64>(nd, 1)), res(c, nf + nd);
             pack_rows<K>(c, df.p, nf, arity, eo.e, pf.p);
             pack_rows<K>(c, dd.p, nd, arity, eo.e, pd.p);
-            if (merge_disjoint<K>(c, pf.p, nf, pd.p, nd, res.p))
+            if (merge_disjoint<K>(c, pf.p, nf, pd.p, nd, res.p, true))
                 throw_logic("merge_sorted: inputs are not disjoint");
             DevBuf<u64> un(c, (nf + nd) * arity);
             unpack_rows<K>(c, res.p, nf + nd, arity, eo.e, un.p);

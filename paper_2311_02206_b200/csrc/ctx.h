@@ -210,6 +210,14 @@ struct Ctx {
         sync();
         for (int i = 0; i < n; ++i) out[i] = pinned[i];
     }
+    // Two scattered device words with one synchronization.
+    void read2(unsigned long long* a, const void* da, unsigned long long* b, const void* db) {
+        d2h(pinned, da, sizeof(unsigned long long));
+        d2h(pinned + 1, db, sizeof(unsigned long long));
+        sync();
+        *a = pinned[0];
+        *b = pinned[1];
+    }
 };
 
 // RAII device buffer of T elements from the context pool.

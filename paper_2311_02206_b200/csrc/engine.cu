@@ -472,7 +472,7 @@ private:
             cp.synced_gen = st.merge_gen;
             if (cp.prefix > 0) build_index<K>(c, data, cp.n, ar, bits, cp.prefix, E.cfg.load_factor, cp.index);
             scratch.reset();
-            const u64 bytes = rb(cp.n, ar) + (cp.prefix > 0 ? cp.index.slot_count * 16ull : 0);
+            const u64 bytes = rb(cp.n, ar) + (cp.prefix > 0 ? cp.index.logical_slots * 16ull : 0);
             E.acct.charge(Accountant::kContainer, bytes, "index");
             E.acct.release(Accountant::kContainer, cp.bytes);
             cp.bytes = bytes;

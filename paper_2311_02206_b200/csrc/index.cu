@@ -91,7 +91,11 @@ void build_index(Ctx& c, const K* rows, u64 n, u32 arity, u32 bits, u32 plen, do
     const u64 groups = group_starts<K>(c, rows, n, arity, bits, plen, gs);
     out.groups = groups;
     out.plen = plen;
-    out.slot_count = slot_count_for(groups, lf);
+    // The reference's sizing (and accounted bytes) use the configured load
+    // factor; the device table is allocated at <= 0.5 so linear-probe chains
+    // stay short (expected ~1.5 probes per hit, ~2.5 per miss).
+    out.logical_slots = slot_count_for(groups, lf);
+    out.slot_count = slot_count_for(groups, std::min(lf, 0.5));
     out.slots.reserve_discard(c, out.slot_count);
     c.memset(out.slots.p, 0xff, out.slot_count * sizeof(Slot));
     if (groups) {

@@ -18,7 +18,7 @@ namespace gd {
 namespace {
 
 constexpr int kProbeThreads = 256;
-constexpr int kProbeItems = 8;
+constexpr int kProbeItems = 4;
 constexpr u64 kProbeTile = (u64)kProbeThreads * kProbeItems;
 constexpr int kLbsThreads = 256;
 constexpr u64 kLbsTile = 1024;

@@ -281,9 +281,11 @@ MergeResult difference_sorted(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K*
     }
     // algorithmic bytes: N read + flags written (+ F streamed when streaming)
     c.prof_end(t, KC_DIFF, nn * (sizeof(K) + 1) + (search ? 0 : nf * sizeof(K)));
-    r.delta_n = run_select(c, nn, FlagKeep{keep.p}, CopyRow<K>{N, Dout});
-    unsigned long long u;
-    c.read_words(&u, counters.p, 1);
+    DevBuf<u64> ws;
+    run_select_async(c, nn, FlagKeep{keep.p}, CopyRow<K>{N, Dout}, ws);
+    unsigned long long d, u;
+    c.read2(&d, ws.p + 1, &u, counters.p);
+    r.delta_n = d;
     r.unique_new = u;
     return r;
 }
@@ -311,16 +313,18 @@ MergeResult difference_runs(Ctx& c, const K* const* runs, const u64* ns, u32 nru
     diff_flags_search_runs_kernel<K><<<grid, 256, 0, c.stream>>>(rs, N, nn, keep.p, counters.p);
     c.check_launch();
     c.prof_end(t, KC_DIFF, nn * (sizeof(K) + 1));
-    r.delta_n = run_select(c, nn, FlagKeep{keep.p}, CopyRow<K>{N, Dout});
-    unsigned long long u;
-    c.read_words(&u, counters.p, 1);
+    DevBuf<u64> ws;
+    run_select_async(c, nn, FlagKeep{keep.p}, CopyRow<K>{N, Dout}, ws);
+    unsigned long long d, u;
+    c.read2(&d, ws.p + 1, &u, counters.p);
+    r.delta_n = d;
     r.unique_new = u;
     (void)total;
     return r;
 }
 
 template <typename K>
-bool merge_disjoint(Ctx& c, const K* A, u64 na, const K* B, u64 nb, K* out) {
+bool merge_disjoint(Ctx& c, const K* A, u64 na, const K* B, u64 nb, K* out, bool check_overlap) {
     if (nb == 0) {
         if (na) c.d2d(out, A, na * sizeof(K));
         return false;
@@ -335,12 +339,18 @@ bool merge_disjoint(Ctx& c, const K* A, u64 na, const K* B, u64 nb, K* out) {
     DevBuf<u64> ov(c, 1);
     c.memset(ov.p, 0, sizeof(u64));
     const size_t smem = sizeof(MergeSmem<K>);
-    GD_CUDA(cudaFuncSetAttribute(merge_disjoint_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    static int attr_device = -1;  // one process drives one device
+    if (attr_device != c.device) {
+        GD_CUDA(cudaFuncSetAttribute(merge_disjoint_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        attr_device = c.device;
+    }
     cudaEvent_t t = c.prof_begin();
     merge_disjoint_kernel<K><<<(unsigned)tiles, kMergeThreads, smem, c.stream>>>(A, na, B, nb, splits.p, out, ov.p);
     c.check_launch();
     // algorithmic bytes: read A and B, write A + B
     c.prof_end(t, KC_MERGE, 2 * (na + nb) * sizeof(K));
+    if (!check_overlap) return false;
     unsigned long long o;
     c.read_words(&o, ov.p, 1);
     return o != 0;
@@ -354,13 +364,13 @@ MergeResult diff_merge(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K* Fout, 
         Dout = dtmp.p;
     }
     MergeResult r = difference_sorted<K>(c, F, nf, N, nn, Dout);
-    if (Fout) r.overlap = merge_disjoint<K>(c, F, nf, Dout, r.delta_n, Fout);
+    if (Fout) r.overlap = merge_disjoint<K>(c, F, nf, Dout, r.delta_n, Fout, true);
     return r;
 }
 
 #define GD_INST(K)                                                                         \
     template MergeResult difference_sorted<K>(Ctx&, const K*, u64, const K*, u64, K*);     \
-    template bool merge_disjoint<K>(Ctx&, const K*, u64, const K*, u64, K*);               \
+    template bool merge_disjoint<K>(Ctx&, const K*, u64, const K*, u64, K*, bool);         \
     template MergeResult difference_runs<K>(Ctx&, const K* const*, const u64*, u32, const K*, u64, K*); \
     template MergeResult diff_merge<K>(Ctx&, const K*, u64, const K*, u64, K*, K*);
 GD_INST(u64)

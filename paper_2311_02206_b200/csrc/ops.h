@@ -102,9 +102,10 @@ MergeResult difference_sorted(Ctx& c, const K* F, u64 nf, const K* N, u64 nn, K*
 template <typename K>
 MergeResult difference_runs(Ctx& c, const K* const* runs, const u64* ns, u32 nruns, const K* N, u64 nn,
                             K* Dout);
-// out = A U B for canonical inputs; returns true if they overlap.
+// out = A U B for canonical inputs; returns true if they overlap (only
+// checked — one extra synchronization — when check_overlap is set).
 template <typename K>
-bool merge_disjoint(Ctx& c, const K* A, u64 na, const K* B, u64 nb, K* out);
+bool merge_disjoint(Ctx& c, const K* A, u64 na, const K* B, u64 nb, K* out, bool check_overlap = false);
 
 // ---- index.cu -------------------------------------------------------
 struct Slot {
@@ -117,7 +118,8 @@ constexpr u64 kLenSat = (1ull << 24) - 1;
 template <typename K>
 struct DevIndex {
     DevBuf<Slot> slots;
-    u64 slot_count = 0;
+    u64 slot_count = 0;     // physical slots (probe table)
+    u64 logical_slots = 0;  // index_map::slot_count() of the reference sizing rule
     u64 groups = 0;
     u32 plen = 0;
 };

@@ -192,7 +192,13 @@ K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
     u64* pp[2] = {bases.p + hist_words, bases.p + hist_words + kRadix};
 
     const u64 max_tiles = (std::min(n, kPortion) + TILE - 1) / TILE;
-    DevBuf<u32> ws(c, 1 + max_tiles * kRadix);
+    const u64 ws_words = 1 + max_tiles * kRadix;
+    // One look-back workspace per pass, cleared by a single memset, when
+    // the keys fit one portion (the common case); larger sorts reuse one
+    // workspace and clear it before every launch.
+    const bool single = nportions == 1;
+    DevBuf<u32> ws(c, single ? ws_words * npass : ws_words);
+    if (single) c.memset(ws.p, 0, ws_words * npass * sizeof(u32));
     K* src = a;
     K* dst = b;
     for (int pass = 0; pass < npass; ++pass) {
@@ -200,12 +206,13 @@ K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
             const u64 pb = (u64)p * kPortion;
             const u64 pn = std::min(kPortion, n - pb);
             const u64 tiles = (pn + TILE - 1) / TILE;
-            c.memset(ws.p, 0, (1 + tiles * kRadix) * sizeof(u32));
+            u32* w = single ? ws.p + (u64)pass * ws_words : ws.p;
+            if (!single) c.memset(w, 0, (1 + tiles * kRadix) * sizeof(u32));
             const u64* rd = p == 0 ? bases.p + (u64)pass * kRadix : pp[(p - 1) & 1];
             u64* wr = p + 1 < nportions ? pp[p & 1] : nullptr;
             cudaEvent_t t = c.prof_begin();
             onesweep_kernel<K><<<(unsigned)tiles, kSortThreads, 0, c.stream>>>(
-                src, dst, pb, pn, (u32)(pass * kRadixBits), rd, wr, ws.p, (u32)tiles);
+                src, dst, pb, pn, (u32)(pass * kRadixBits), rd, wr, w, (u32)tiles);
             c.check_launch();
             c.prof_end(t, KC_SORT_PASS, 2 * pn * sizeof(K));
         }

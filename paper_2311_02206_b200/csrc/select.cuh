@@ -45,17 +45,26 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(u64 n, Pred pred, E
         if (f[j]) emit(begin + j, pos++);
 }
 
-// Launches the compaction; returns the number of selected items (syncs).
+// Launches the compaction without reading the count back; the selected
+// total lands in ws.p[1] (n == 0: ws holds a zero).
 template <typename Pred, typename Emit>
-u64 run_select(Ctx& c, u64 n, Pred pred, Emit emit) {
-    if (n == 0) return 0;
+void run_select_async(Ctx& c, u64 n, Pred pred, Emit emit, DevBuf<u64>& ws) {
     const u64 tiles = (n + kSelTile - 1) / kSelTile;
-    DevBuf<u64> ws(c, 2 + tiles);
+    ws.reserve_discard(c, 2 + tiles);
     c.memset(ws.p, 0, (2 + tiles) * sizeof(u64));
+    if (n == 0) return;
     cudaEvent_t t = c.prof_begin();
     select_kernel<<<(unsigned)tiles, kSelThreads, 0, c.stream>>>(n, pred, emit, ws.p);
     c.check_launch();
     c.prof_end(t, KC_SELECT, 0);
+}
+
+// Launches the compaction; returns the number of selected items (syncs).
+template <typename Pred, typename Emit>
+u64 run_select(Ctx& c, u64 n, Pred pred, Emit emit) {
+    if (n == 0) return 0;
+    DevBuf<u64> ws;
+    run_select_async(c, n, pred, emit, ws);
     unsigned long long total;
     c.read_words(&total, ws.p + 1, 1);
     return total;

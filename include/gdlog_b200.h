@@ -85,6 +85,12 @@ gd_status gd_ctx_set_profiling(gd_ctx* ctx, int enable);
 gd_status gd_ctx_profile_read(gd_ctx* ctx, double* ms, uint64_t* launches,
                               uint64_t* bytes);
 gd_status gd_ctx_profile_reset(gd_ctx* ctx);
+/* Host-side counters since context creation: seconds spent inside the
+ * stream-ordered allocator and in stream synchronizations, and their
+ * counts (diagnostics for launch/sync-bound long tails). */
+gd_status gd_ctx_host_counters(gd_ctx* ctx, double* alloc_seconds,
+                               uint64_t* allocs, double* sync_seconds,
+                               uint64_t* syncs);
 
 /* ------------------------------------------------------------------ */
 /* Join-spec and plan data (ra.hpp:18-66, plan.hpp:18-58)              */

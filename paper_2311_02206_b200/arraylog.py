@@ -120,6 +120,12 @@ class Context:
     def profile_reset(self):
         self.check(self.lib.gd_ctx_profile_reset(self.h))
 
+    def host_counters(self) -> dict:
+        a, s = C.c_double(), C.c_double()
+        na, ns = A.u64(), A.u64()
+        self.check(self.lib.gd_ctx_host_counters(self.h, C.byref(a), C.byref(na), C.byref(s), C.byref(ns)))
+        return {"alloc_s": a.value, "allocs": na.value, "sync_s": s.value, "syncs": ns.value}
+
     def close(self):
         if getattr(self, "h", None):
             self.lib.gd_ctx_destroy(self.h)

@@ -266,6 +266,16 @@ gd_status gd_ctx_profile_read(gd_ctx* ctx, double* ms, uint64_t* launches, uint6
     });
 }
 
+gd_status gd_ctx_host_counters(gd_ctx* ctx, double* alloc_seconds, uint64_t* allocs, double* sync_seconds,
+                               uint64_t* syncs) {
+    return guard(ctx, [&] {
+        if (alloc_seconds) *alloc_seconds = ctx->c->alloc_seconds;
+        if (allocs) *allocs = ctx->c->alloc_count;
+        if (sync_seconds) *sync_seconds = ctx->c->sync_seconds;
+        if (syncs) *syncs = ctx->c->sync_count;
+    });
+}
+
 gd_status gd_ctx_profile_reset(gd_ctx* ctx) {
     return guard(ctx, [&] {
         ctx->c->sync();

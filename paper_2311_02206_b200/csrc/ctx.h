@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <time.h>
+
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -141,33 +144,109 @@ struct Ctx {
         GD_CUDA(cudaMallocHost(&pinned, kPinnedWords * sizeof(unsigned long long)));
     }
     ~Ctx() {
+        flush_cache();
+        for (auto& kv : live_) cudaFreeAsync(kv.first, stream);
+        live_.clear();
+        cudaStreamSynchronize(stream);
         if (pinned) cudaFreeHost(pinned);
         if (own_stream && stream) cudaStreamDestroy(stream);
     }
     Ctx(const Ctx&) = delete;
     Ctx& operator=(const Ctx&) = delete;
 
+    // host-side counters (gd_ctx_host_counters): time spent in the
+    // allocator and in stream synchronizations
+    double alloc_seconds = 0, sync_seconds = 0;
+    uint64_t alloc_count = 0, sync_count = 0;
+
+    static double now_s() {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        return ts.tv_sec + ts.tv_nsec * 1e-9;
+    }
+
+    // Stream-ordered caching allocator.  All work of a context is on one
+    // stream, so a block released here may be handed out again at once:
+    // any later use is ordered after the earlier one.  Sizes are rounded to
+    // size classes (powers of two below 1 MiB, 1/8-octave steps above) and
+    // reused from a per-class free list; cudaMallocAsync is only reached on
+    // a miss, and the cache is flushed back to the pool before an
+    // allocation is declared out of memory.
+    std::multimap<size_t, void*> cache_;     // size class -> free blocks
+    std::map<void*, size_t> live_;           // block -> size class
+    uint64_t cached_bytes = 0;
+
+    static size_t size_class(size_t bytes) {
+        if (bytes <= 256) return 256;
+        if (bytes <= (1u << 20)) {
+            size_t c = 256;
+            while (c < bytes) c <<= 1;
+            return c;
+        }
+        size_t top = 1u << 20;
+        while (top * 2 <= bytes) top <<= 1;
+        const size_t step = top / 8;
+        return (bytes + step - 1) / step * step;
+    }
+
+    void flush_cache() {
+        for (auto& kv : cache_) cudaFreeAsync(kv.second, stream);
+        cache_.clear();
+        cached_bytes = 0;
+    }
+
     void* alloc(size_t bytes) {
         if (bytes == 0) bytes = 16;
+        const size_t cls = size_class(bytes);
+        const double t0 = now_s();
+        ++alloc_count;
         void* p = nullptr;
-        cudaError_t e = cudaMallocAsync(&p, bytes, stream);
-        if (e == cudaErrorMemoryAllocation) {
-            cudaGetLastError();
-            throw_budget(cur_phase, "device allocation of " + std::to_string(bytes) +
-                                        " bytes failed (HBM exhausted)");
+        auto it = cache_.find(cls);
+        if (it != cache_.end()) {
+            p = it->second;
+            cache_.erase(it);
+            cached_bytes -= cls;
+        } else {
+            cudaError_t e = cudaMallocAsync(&p, cls, stream);
+            if (e == cudaErrorMemoryAllocation) {
+                cudaGetLastError();
+                flush_cache();
+                e = cudaMallocAsync(&p, cls, stream);
+            }
+            if (e == cudaErrorMemoryAllocation) {
+                cudaGetLastError();
+                alloc_seconds += now_s() - t0;
+                throw_budget(cur_phase, "device allocation of " + std::to_string(bytes) +
+                                            " bytes failed (HBM exhausted)");
+            }
+            if (e != cudaSuccess)
+                throw Error(GD_ERR_CUDA, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
         }
-        if (e != cudaSuccess) throw Error(GD_ERR_CUDA, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
-        bytes_in_use += bytes;
+        alloc_seconds += now_s() - t0;
+        live_[p] = cls;
+        bytes_in_use += cls;
         if (bytes_in_use > bytes_peak) bytes_peak = bytes_in_use;
         return p;
     }
-    void free(void* p, size_t bytes) {
+    void free(void* p, size_t /*bytes*/) {
         if (!p) return;
-        if (bytes == 0) bytes = 16;
-        cudaFreeAsync(p, stream);
-        bytes_in_use -= bytes;
+        auto it = live_.find(p);
+        if (it == live_.end()) {
+            cudaFreeAsync(p, stream);
+            return;
+        }
+        const size_t cls = it->second;
+        live_.erase(it);
+        bytes_in_use -= cls;
+        cache_.emplace(cls, p);
+        cached_bytes += cls;
     }
-    void sync() { GD_CUDA(cudaStreamSynchronize(stream)); }
+    void sync() {
+        const double t0 = now_s();
+        GD_CUDA(cudaStreamSynchronize(stream));
+        sync_seconds += now_s() - t0;
+        ++sync_count;
+    }
 
     // Instrumented launch bracket: t = prof_begin(); <launch>; prof_end(t, ...).
     cudaEvent_t prof_begin() {

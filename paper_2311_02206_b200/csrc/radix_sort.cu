@@ -24,10 +24,6 @@ constexpr int kSortThreads = 256;
 constexpr int kWarps = kSortThreads / 32;
 constexpr u64 kPortion = 1ull << 26;  // keys per look-back portion (30-bit status values)
 
-template <typename K> struct SortItems;
-template <> struct SortItems<u64> { static constexpr int v = 16; };  // 4096 keys / tile
-template <> struct SortItems<u128> { static constexpr int v = 8; };  // 2048 keys / tile
-
 template <typename K>
 __device__ __forceinline__ u32 digit_of(K k, u32 shift) {
     return (u32)(k >> shift) & (kRadix - 1);
@@ -64,12 +60,11 @@ constexpr u32 kSFlagA = 1u << 30;
 constexpr u32 kSFlagP = 2u << 30;
 constexpr u32 kSMask = (1u << 30) - 1;
 
-template <typename K>
+template <typename K, int I>
 __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
     const K* __restrict__ in, K* __restrict__ out, u64 portion_begin, u64 portion_n, u32 shift,
     const u64* __restrict__ digit_base, u64* __restrict__ next_base, u32* __restrict__ ws,
     u32 ntiles) {
-    constexpr int I = SortItems<K>::v;
     constexpr int TILE = kSortThreads * I;
     __shared__ K s_keys[TILE];
     __shared__ u32 s_whist[kWarps][kRadix + 1];
@@ -89,31 +84,39 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
     const u64 tile_begin = tile * TILE;
     const u32 tile_n = (u32)min((u64)TILE, portion_n - tile_begin);
 
+    // Digits are recomputed from the keys where needed (fewer registers);
+    // invalid (past-the-end) items use digit kRadix, a group never counted.
     K k[I];
-    u32 d[I];
 #pragma unroll
     for (int i = 0; i < I; ++i) {
         const u32 idx = warp * (I * 32) + i * 32 + lane;
-        if (idx < tile_n) {
-            k[i] = in[portion_begin + tile_begin + idx];
-            d[i] = digit_of(k[i], shift);
-        } else {
-            k[i] = 0;
-            d[i] = kRadix;  // invalid: own group, never counted
-        }
+        k[i] = idx < tile_n ? in[portion_begin + tile_begin + idx] : K(0);
     }
+    auto dig = [&](int i) -> u32 {
+        const u32 idx = warp * (I * 32) + i * 32 + lane;
+        return idx < tile_n ? digit_of(k[i], shift) : (u32)kRadix;
+    };
 
-    // Warp-level multi-split ranking, stable in (item, lane) = input order.
-    u32 rank[I];
+    // Warp-level multi-split ranking, stable in (item, lane) = input order:
+    // peers share a digit; the group leader bumps the warp's digit counter
+    // with one shared atomic and broadcasts the old value.  Ranks (< 2^16)
+    // are packed two per register.
+    u32 rank2[(I + 1) / 2];
+    // all match masks first: independent MATCH instructions pipeline
+    u32 pm[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) pm[i] = __match_any_sync(0xffffffffu, dig(i));
 #pragma unroll
     for (int i = 0; i < I; ++i) {
-        const u32 peers = __match_any_sync(0xffffffffu, d[i]);
-        const u32 leader = __ffs(peers) - 1;
-        const u32 base = s_whist[warp][d[i]];
-        __syncwarp();
-        if (lane == leader) s_whist[warp][d[i]] = base + __popc(peers);
-        __syncwarp();
-        rank[i] = base + __popc(peers & lanemask_lt());
+        const u32 d = dig(i);
+        const u32 peers = pm[i];
+        const u32 leader = 31 - __clz(peers);  // highest lane: no bit reversal
+        u32 base = 0;
+        if (lane == leader) base = atomicAdd(&s_whist[warp][d], (u32)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        const u32 r = base + __popc(peers & lanemask_lt());
+        if (i & 1) rank2[i >> 1] |= r << 16;
+        else rank2[i >> 1] = r;
     }
     __syncthreads();
 
@@ -135,17 +138,38 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
     const u32 dstart = block_exclusive_scan<u32, kSortThreads>(cnt, total, s_scan);
     s_dstart[t] = dstart;
 
-    // Look-back for digit t across previous tiles of this portion.
+    // Look-back for digit t across previous tiles of this portion, a window
+    // of kLookWindow predecessors per step (independent loads), so the walk
+    // back to the nearest inclusive prefix takes ~tiles/kLookWindow round
+    // trips instead of one per tile.
     u32 excl = 0;
     if (tile > 0) {
+        constexpr int kLookWindow = 16;
         long long pred = (long long)tile - 1;
-        while (pred >= 0) {
-            const u32 s = ld_relaxed32(status + (u64)pred * kRadix + t);
-            const u32 flag = s >> 30;
-            if (flag == 0) continue;
-            excl += s & kSMask;
-            if (flag == 2) break;
-            --pred;
+        while (true) {
+            u32 s[kLookWindow];
+#pragma unroll
+            for (int w = 0; w < kLookWindow; ++w)
+                s[w] = pred - w >= 0 ? ld_relaxed32(status + (u64)(pred - w) * kRadix + t) : kSFlagP;
+            int first_inv = kLookWindow, first_p = kLookWindow;
+#pragma unroll
+            for (int w = kLookWindow - 1; w >= 0; --w) {
+                const u32 f = s[w] >> 30;
+                if (f == 0) first_inv = w;
+                if (f == 2) first_p = w;
+            }
+            if (first_inv < first_p) {  // an unpublished tile before any prefix: wait on it
+#pragma unroll
+                for (int w = 0; w < kLookWindow; ++w)
+                    if (w < first_inv) excl += s[w] & kSMask;
+                pred -= first_inv;
+                continue;
+            }
+#pragma unroll
+            for (int w = 0; w < kLookWindow; ++w)
+                if (w <= first_p) excl += s[w] & kSMask;
+            if (first_p < kLookWindow) break;
+            pred -= kLookWindow;
         }
         st_relaxed32(my_status, kSFlagP | (excl + cnt));
     }
@@ -157,8 +181,11 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
 
     // Scatter into shared memory in digit-sorted (stable) order.
 #pragma unroll
-    for (int i = 0; i < I; ++i)
-        if (d[i] < kRadix) s_keys[s_dstart[d[i]] + s_whist[warp][d[i]] + rank[i]] = k[i];
+    for (int i = 0; i < I; ++i) {
+        const u32 d = dig(i);
+        const u32 r = (rank2[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
+        if (d < kRadix) s_keys[s_dstart[d] + s_whist[warp][d] + r] = k[i];
+    }
     __syncthreads();
 
     for (u32 j = threadIdx.x; j < tile_n; j += kSortThreads) {
@@ -169,12 +196,34 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
 
 }  // namespace
 
+// Keys per thread of a onesweep tile (4/8/16 are compiled; GD_SORT_ITEMS
+// overrides for experiments, scripts/sortbench.py).
+template <typename K>
+int sort_items(u64 n) {
+    static const int forced = [] {
+        const char* e = getenv("GD_SORT_ITEMS");
+        return e ? atoi(e) : 0;
+    }();
+    (void)n;  // measured on B200: 16 keys/thread is fastest from 64K to 16M keys
+    int i = forced ? forced : 16;
+    if (sizeof(K) > 8) i = std::min(i, 8);
+    return i == 16 || i == 8 ? i : 4;
+}
+
+template <typename K, int I>
+void launch_onesweep(const Ctx& c, u64 tiles, const K* src, K* dst, u64 pb, u64 pn, u32 shift, const u64* rd,
+                     u64* wr, u32* w) {
+    onesweep_kernel<K, I><<<(unsigned)tiles, kSortThreads, 0, c.stream>>>(src, dst, pb, pn, shift, rd, wr, w,
+                                                                          (u32)tiles);
+}
+
 template <typename K>
 K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
     if (n <= 1 || nbits == 0) return a;
     const int npass = (int)((nbits + kRadixBits - 1) / kRadixBits);
     const int nportions = (int)((n + kPortion - 1) / kPortion);
-    constexpr int TILE = kSortThreads * SortItems<K>::v;
+    const int items = sort_items<K>(n);
+    const u64 TILE = (u64)kSortThreads * items;
 
     const u64 hist_words = (u64)npass * kRadix;
     DevBuf<u64> hist(c, hist_words);
@@ -211,8 +260,10 @@ K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
             const u64* rd = p == 0 ? bases.p + (u64)pass * kRadix : pp[(p - 1) & 1];
             u64* wr = p + 1 < nportions ? pp[p & 1] : nullptr;
             cudaEvent_t t = c.prof_begin();
-            onesweep_kernel<K><<<(unsigned)tiles, kSortThreads, 0, c.stream>>>(
-                src, dst, pb, pn, (u32)(pass * kRadixBits), rd, wr, w, (u32)tiles);
+            const u32 shift = (u32)(pass * kRadixBits);
+            if (items == 16) launch_onesweep<K, (sizeof(K) > 8 ? 8 : 16)>(c, tiles, src, dst, pb, pn, shift, rd, wr, w);
+            else if (items == 8) launch_onesweep<K, 8>(c, tiles, src, dst, pb, pn, shift, rd, wr, w);
+            else launch_onesweep<K, 4>(c, tiles, src, dst, pb, pn, shift, rd, wr, w);
             c.check_launch();
             c.prof_end(t, KC_SORT_PASS, 2 * pn * sizeof(K));
         }

@@ -198,11 +198,8 @@ def main():
         e.close()
         torch.cuda.synchronize()
 
-    # timed steps
+    # timed steps (no per-kernel events inside: they would perturb the step)
     sampler = ClockSampler(local)
-    if not args.no_profile:
-        ctx.set_profiling(True)
-        ctx.profile_reset()
     launches0 = ctx.kernel_launches
     times, joins = [], []
     sampler.start()
@@ -232,8 +229,26 @@ def main():
         e.close()
     clocks = sampler.stop()
     launches = ctx.kernel_launches - launches0
-    prof = ctx.profile() if not args.no_profile else {}
-    ctx.set_profiling(False)
+
+    # one more identical step with CUDA events around every instrumented
+    # launch (on the launching stream): per-kernel durations and their
+    # algorithmic bytes for the roofline
+    prof, prof_ms = {}, None
+    if not args.no_profile:
+        flush_l2(torch, flush)
+        torch.cuda.synchronize()
+        ctx.set_profiling(True)
+        ctx.profile_reset()
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        e = one_step()
+        p1.record(stream)
+        torch.cuda.synchronize()
+        prof_ms = p0.elapsed_time(p1)
+        prof = ctx.profile()
+        ctx.set_profiling(False)
+        e.close()
 
     ms_step = float(np.mean(times))
     value = float(np.mean(joins)) / (ms_step / 1e3)
@@ -249,7 +264,7 @@ def main():
                 "frac": achieved / peak, "peak_source": peak_kind, "traffic": None,
                 "launches": n_k, "avg_launch_ms": ms_k / max(n_k, 1),
                 "algo_bytes_per_launch": by_k / max(n_k, 1),
-                "share_of_step": ms_k / (ms_step * args.steps)}
+                "share_of_step": ms_k / prof_ms, "profiled_step_ms": prof_ms}
         tp = ROOT / "profiles" / "ncu_traffic.json"
         if tp.exists():
             d = json.loads(tp.read_text()).get(dom)
@@ -262,7 +277,8 @@ def main():
         jm_by = sum(prof[k][2] for k in jm)
         roof["join_merge"] = {"achieved": jm_by / (jm_ms / 1e3) / 1e9 if jm_ms else 0.0,
                               "frac": (jm_by / (jm_ms / 1e3) / 1e9) / peak if jm_ms else 0.0}
-        roof["kernel_ms_per_step"] = {k: v[0] / args.steps for k, v in prof.items()}
+        roof["kernel_ms_per_step"] = {k: round(v[0], 3) for k, v in prof.items()}
+        roof["kernel_gbs"] = {k: round(v[2] / (v[0] / 1e3) / 1e9, 1) for k, v in prof.items() if v[0] and v[2]}
 
     # e2e through the C-ABI with host buffers (rank 0 at N=1)
     e2e = None

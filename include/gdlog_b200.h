@@ -78,9 +78,10 @@ gd_status gd_ctx_synchronize(gd_ctx* ctx);
 /* Live per-kernel timing with CUDA events on the context stream (used by
  * bench.py for the roofline).  Classes: 0 sort pass, 1 sort histogram,
  * 2 diff+merge, 3 join probe, 4 join materialize, 5 index build,
- * 6 compaction/select, 7 other, 8 difference.  read() synchronizes and reports, per
- * class, total milliseconds, launches and algorithmic bytes. */
-#define GD_KCLASS_COUNT 9
+ * 6 compaction/select, 7 other, 8 difference, 9 fused join+insert of the
+ * resident loop, 10 loop control (gate/end).  read() synchronizes and
+ * reports, per class, total milliseconds, launches and algorithmic bytes. */
+#define GD_KCLASS_COUNT 11
 gd_status gd_ctx_set_profiling(gd_ctx* ctx, int enable);
 gd_status gd_ctx_profile_read(gd_ctx* ctx, double* ms, uint64_t* launches,
                               uint64_t* bytes);

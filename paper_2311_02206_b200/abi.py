@@ -34,7 +34,7 @@ GD_DELTA = 1
 
 PHASES = ("index", "join", "dedup", "difference", "merge", "other")  # stats.hpp:15-16
 KCLASSES = ("sort_pass", "sort_hist", "diff_merge", "join_probe", "join_materialize", "index_build",
-            "select", "other", "difference")  # gdlog_b200.h GD_KCLASS_COUNT
+            "select", "other", "difference", "join_insert", "loop_ctl")  # gdlog_b200.h GD_KCLASS_COUNT
 
 u32 = C.c_uint32
 u64 = C.c_uint64

@@ -55,6 +55,8 @@ enum KClass : int {
     KC_SELECT,          // compaction / select_project / unique
     KC_OTHER,           // pack/unpack/permute/owner/...
     KC_DIFF,            // difference flags (search or streaming)
+    KC_INSERT,          // loop_materialize_insert / loop_select_insert
+    KC_LOOP_CTL,        // loop_gate / loop_end / loop_select_cand
     KC_COUNT
 };
 
@@ -119,6 +121,12 @@ struct Ctx {
     const char* cur_phase = "other";  // for device-OOM -> budget_error(phase)
     unsigned long long* pinned = nullptr;  // small pinned readback area
     static constexpr int kPinnedWords = 64;
+    void* pinned_big = nullptr;  // lazily allocated pinned area (loop control block)
+    static constexpr size_t kPinnedBig = 64 << 10;
+    void* pinned_area() {
+        if (!pinned_big) GD_CUDA(cudaMallocHost(&pinned_big, kPinnedBig));
+        return pinned_big;
+    }
 
     Ctx(int dev, void* s) : device(dev) {
         int n = 0;
@@ -149,6 +157,7 @@ struct Ctx {
         live_.clear();
         cudaStreamSynchronize(stream);
         if (pinned) cudaFreeHost(pinned);
+        if (pinned_big) cudaFreeHost(pinned_big);
         if (own_stream && stream) cudaStreamDestroy(stream);
     }
     Ctx(const Ctx&) = delete;

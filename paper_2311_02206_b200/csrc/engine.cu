@@ -14,10 +14,13 @@
 // and their HISA index rebuilt; identity copies alias the full relation.
 // The logical-byte accountant and EBM bookkeeping replay the reference's
 // charges in the same order (accounting.h).
+#include <cstdlib>
 #include <cstring>
 #include <set>
+#include <type_traits>
 
 #include "engine.h"
+#include "loop.h"
 #include "ops.h"
 
 namespace gd {
@@ -202,6 +205,12 @@ public:
         for (u32 i = 0; i < by_name.size(); ++i) by_name[i] = i;
         std::sort(by_name.begin(), by_name.end(),
                   [&](u32 a, u32 b) { return E.info_[a].name < E.info_[b].name; });
+        if constexpr (std::is_same_v<K, u64>) {
+            if (loop_eligible(rec)) {
+                iterate_loop(rec, by_name);
+                return;
+            }
+        }
 
         for (;;) {
             bool active = false;
@@ -344,6 +353,534 @@ public:
                 st.full_n += b.n;
             }
         }
+    }
+
+    // ---- resident device loop (loop.h) ---------------------
+    // Eligible when every recursive head is never a join inner (so its full
+    // version is only probed for membership and read back at the end), keys
+    // are u64, one rank, no finite budget (budget_error must surface at the
+    // reference's charge: those runs keep the host-driven loop), and Δ = full
+    // (the state seed() leaves).
+    bool loop_eligible(const std::vector<u32>& rec) {
+        if (E.nranks > 1 || E.cfg.memory_budget_bytes != Accountant::kUnlimited) return false;
+        if (const char* e = getenv("GD_LOOP")) if (e[0] == '0') return false;
+        if (rec.empty() || rec.size() > kLoopMaxHeads) return false;
+        u32 nsteps = 0;
+        for (u32 r : rec) {
+            const auto& st = rels[r];
+            if (!st.lsm || st.delta_n != total_n(st)) return false;
+        }
+        auto is_head = [&](u32 r) { return std::find(rec.begin(), rec.end(), r) != rec.end(); };
+        for (const auto& p : E.plans_) {
+            if (!p.recursive) continue;
+            for (u32 v = 0; v < p.nvariants; ++v) {
+                const gd_variant& var = p.variants[v];
+                if (var.src_version == GD_DELTA && !is_head(var.src_rel)) return false;
+                nsteps += std::max<u32>(1, var.nsteps);
+                for (u32 s = 0; s < var.nsteps; ++s)
+                    if (is_head(var.steps[s].inner_rel)) return false;
+            }
+        }
+        return nsteps <= kLoopMaxSteps;
+    }
+
+    struct LStep {
+        u32 plan = 0, var = 0;
+        bool final = false, select = false;
+        u32 head = 0;            // loop-head index (final steps)
+        u32 kind = LO_STATIC;    // outer source
+        u32 src_head = 0, src_step = 0;
+        const u64* static_ptr = nullptr;
+        u64 static_n = 0;
+        DevJoin jd{};
+        bool has_iv = false;
+        IndexView<u64> iv{};
+        const u64* inner = nullptr;
+        u64 inner_n = 0;
+        u32 proj_arity = 0;
+        DevBuf<u64> row_start, row_off, splits, temp;
+        u64 rows_cap = 0, splits_cap = 0, temp_cap = 0;
+        LoopStepBufs bufs() const { return LoopStepBufs{row_start.p, row_off.p, rows_cap, splits.p, splits_cap}; }
+    };
+    struct LHead {
+        u32 rel = 0;
+        DevBuf<u64> log;
+        DevBuf<u64> tab;  // tab_cap slots of loop_slot_bytes(sbits)
+        u64 log_cap = 0, tab_cap = 0, tab_limit = 0;
+        u32 sbits = 0;
+        void alloc_tab(Ctx& c, u64 cap) {
+            tab.release();
+            tab_cap = cap;
+            tab_limit = tab_limit_of(cap);
+            tab = DevBuf<u64>(c, cap * loop_slot_bytes(sbits) / 8);
+            loop_table_clear(c, tab.p, cap, sbits);
+        }
+    };
+    // Linear probing stays short (~1.5 slot reads per new key with the
+    // sector scan) at load <= 1/2; tables grow to load 1/3.
+    static u64 tab_limit_of(u64 cap) { return cap / 2; }
+
+    void iterate_loop(const std::vector<u32>& rec, const std::vector<u32>& by_name) {
+        bool active = false;
+        for (u32 r : rec) active |= rels[r].delta_n > 0;
+        if (!active) return;
+        loop_prepare();
+        // iteration 1, step (1): refresh the (static) indexed copies
+        for (u32 r : by_name)
+            if (rels[r].dirty) refresh_copies(r);
+
+        // GD_LOOP_TINY=1 starts every capacity at its minimum so tests walk
+        // the overflow -> rollback -> grow -> re-run path on small inputs.
+        const bool tiny = getenv("GD_LOOP_TINY") && getenv("GD_LOOP_TINY")[0] == '1';
+        const u32 nh = (u32)rec.size();
+        std::vector<LHead> heads(nh);
+        auto head_of = [&](u32 r) -> u32 {
+            return (u32)(std::find(rec.begin(), rec.end(), r) - rec.begin());
+        };
+        for (u32 h = 0; h < nh; ++h) {
+            auto& st = rels[rec[h]];
+            compact(st);
+            heads[h].rel = rec[h];
+            const u64 f0 = st.full_n;
+            heads[h].log_cap = tiny ? std::max<u64>(f0, 1) : std::max<u64>(2 * f0, 1 << 16);
+            heads[h].log = DevBuf<u64>(c, heads[h].log_cap);
+            if (f0) c.d2d(heads[h].log.p, st.full.p, f0 * sizeof(u64));
+            heads[h].sbits = loop_stamp_bits(E.info_[rec[h]].arity * bits);
+            heads[h].alloc_tab(c, tiny ? 2 * f0 + 16 : std::max<u64>(4 * f0, 1 << 16));
+            loop_table_fill(c, heads[h].tab.p, heads[h].tab_cap, heads[h].sbits, heads[h].log.p, f0);
+        }
+
+        // variant-steps in execution order (plan order, variant order)
+        std::vector<LStep> steps;
+        for (u32 pi = 0; pi < E.plans_.size(); ++pi) {
+            const gd_rule_plan& p = E.plans_[pi];
+            if (!p.recursive) continue;
+            for (u32 v = 0; v < p.nvariants; ++v) {
+                const gd_variant& var = p.variants[v];
+                const u32 ar = E.info_[var.src_rel].arity;
+                u32 cur_ar = ar;
+                u32 cur_perm[kMaxArity];
+                for (u32 i = 0; i < kMaxArity; ++i) cur_perm[i] = i < ar ? var.src_perm[i] : i;
+                const u32 first = (u32)steps.size();
+                const u32 n = std::max<u32>(1, var.nsteps);
+                for (u32 s = 0; s < n; ++s) {
+                    steps.emplace_back();
+                    LStep& L = steps.back();
+                    L.plan = pi;
+                    L.var = v;
+                    L.final = s + 1 == n;
+                    L.head = head_of(p.head_rel);
+                    if (s == 0) {
+                        auto it = std::find(rec.begin(), rec.end(), var.src_rel);
+                        if (it != rec.end()) {
+                            L.kind = var.src_version == GD_DELTA ? LO_DELTA : LO_FULL;
+                            L.src_head = (u32)(it - rec.begin());
+                        } else {
+                            auto& src = rels[var.src_rel];
+                            compact(src);
+                            L.kind = LO_STATIC;
+                            L.static_ptr = reinterpret_cast<const u64*>(src.full.p);
+                            L.static_n = src.full_n;
+                        }
+                    } else {
+                        L.kind = LO_TEMP;
+                        L.src_step = first + s - 1;
+                    }
+                    if (var.nsteps == 0) {
+                        L.select = true;
+                        L.jd = make_desc(0, cur_ar, cur_perm, 0, var.sel_arity, var.sel_proj, var.nsel_filters,
+                                         var.sel_filters);
+                        continue;
+                    }
+                    const gd_join_step& st = var.steps[s];
+                    auto& in = rels[st.inner_rel];
+                    const u32 iar = E.info_[st.inner_rel].arity;
+                    CopyState<K>& cp = in.copies.at(CopyKey{std::vector<u32>(st.inner_perm, st.inner_perm + iar),
+                                                            st.join_column_count});
+                    L.inner = reinterpret_cast<const u64*>(cp.identity ? in.full.p : cp.rows.p);
+                    L.inner_n = cp.identity ? in.full_n : cp.n;
+                    L.jd = make_desc(st.join_column_count, cur_ar, cur_perm, iar, st.proj_arity, st.proj,
+                                     st.nfilters, st.filters);
+                    L.proj_arity = st.proj_arity;
+                    if (st.join_column_count > 0 && L.inner_n > 0) {
+                        L.has_iv = true;
+                        L.iv = IndexView<u64>{cp.index.slots.p, cp.index.slot_count, L.inner, L.inner_n, iar, bits,
+                                              st.join_column_count};
+                    }
+                    cur_ar = st.proj_arity;
+                    for (u32 i = 0; i < kMaxArity; ++i) cur_perm[i] = i;
+                }
+            }
+        }
+        const u32 ns = (u32)steps.size();
+        const u64 d0 = rels[rec[0]].delta_n;
+        for (auto& L : steps) {
+            L.rows_cap = tiny ? 2 : std::max<u64>(d0 + 1, 1 << 12);
+            L.splits_cap = tiny ? 2 : std::max<u64>(2 * d0 / kLoopMatTile + 2, 1 << 12);
+            if (!L.select) {
+                L.row_start = DevBuf<u64>(c, L.rows_cap);
+                L.row_off = DevBuf<u64>(c, L.rows_cap);
+                L.splits = DevBuf<u64>(c, L.splits_cap);
+            }
+            if (!L.final) {
+                L.temp_cap = tiny ? 1 : std::max<u64>(4 * d0, 1 << 16);
+                L.temp = DevBuf<u64>(c, L.temp_cap);
+            }
+        }
+        DevBuf<u64> block_sums(c, (u64)loop_grid(c));
+        u64 hist_cap = tiny ? 1 : 1024;
+        DevBuf<gd_iter_record> hist_rec(c, hist_cap * nh);
+        DevBuf<u64> hist_steps(c, hist_cap * ns);
+
+        // control block
+        DevBuf<LoopCtl> ctl(c, 1);
+        LoopCtl* hc = static_cast<LoopCtl*>(c.pinned_area());
+        std::memset(hc, 0, sizeof(LoopCtl));
+        hc->nheads = nh;
+        hc->hist_cap = hist_cap;
+        for (u32 h = 0; h < nh; ++h) {
+            const auto& st = rels[rec[h]];
+            hc->h[h].log_n = st.full_n;
+            hc->h[h].dlo = st.full_n - st.delta_n;
+            hc->h[h].dhi = st.full_n;
+        }
+        c.h2d(ctl.p, hc, sizeof(LoopCtl));
+
+        auto outer_of = [&](const LStep& L) {
+            LoopOuter o{};
+            o.kind = L.kind;
+            o.head = L.src_head;
+            o.src_step = L.src_step;
+            if (L.kind == LO_STATIC) {
+                o.ptr = L.static_ptr;
+                o.n = L.static_n;
+            } else if (L.kind == LO_TEMP) {
+                o.ptr = steps[L.src_step].temp.p;
+            } else {
+                o.ptr = heads[L.src_head].log.p;
+            }
+            return o;
+        };
+        auto bufs_of = [&](u32 h) {
+            return LoopHeadBufs{heads[h].log.p, heads[h].log_cap, heads[h].tab.p, heads[h].tab_cap,
+                                heads[h].tab_limit, heads[h].sbits, 0};
+        };
+        // One iteration's kernel sequence (captured into the graph, or
+        // launched eagerly when profiling).  The gate runs in the last CTA
+        // of the last scan and loop_end in the last CTA of the last insert
+        // when the sequence allows it.
+        auto record_iteration = [&](cudaStream_t s, bool use_cond, unsigned long long cond) {
+            auto br = [&]() { return c.prof_begin(); };
+            LoopGateDesc g{};
+            g.stamp_max = 0xfffffffeu;
+            for (u32 i = 0; i < ns; ++i)
+                if (steps[i].final) {
+                    g.final_step[g.nfinal] = i;
+                    g.final_head[g.nfinal] = steps[i].head;
+                    ++g.nfinal;
+                }
+            for (u32 h = 0; h < nh; ++h) {
+                g.log_cap[h] = heads[h].log_cap;
+                g.tab_limit[h] = heads[h].tab_limit;
+                if (heads[h].sbits) g.stamp_max = std::min<u32>(g.stamp_max, (1u << heads[h].sbits) - 1);
+            }
+            const bool fuse_gate = !steps[ns - 1].select;
+            for (u32 i = 0; i < ns; ++i) {
+                LStep& L = steps[i];
+                const LoopOuter o = outer_of(L);
+                if (L.select) {
+                    cudaEvent_t t = br();
+                    loop_select_cand(c, s, ctl.p, i, o);
+                    c.prof_end(t, KC_LOOP_CTL, 0);
+                    continue;
+                }
+                cudaEvent_t t = br();
+                loop_probe(c, s, ctl.p, i, o, L.jd, L.has_iv ? &L.iv : nullptr, L.inner_n, L.bufs(), block_sums.p);
+                c.prof_end(t, KC_PROBE, 0);
+                t = br();
+                loop_scan(c, s, ctl.p, i, o, L.bufs(), block_sums.p, fuse_gate && i + 1 == ns ? &g : nullptr);
+                c.prof_end(t, KC_SELECT, 0);
+                if (!L.final) {
+                    t = br();
+                    loop_materialize_temp(c, s, ctl.p, i, o, L.inner, L.jd, L.bufs(), L.temp.p, L.temp_cap);
+                    c.prof_end(t, KC_MATERIALIZE, 0);
+                }
+            }
+            if (!fuse_gate) {
+                cudaEvent_t t = br();
+                loop_gate(c, s, ctl.p, g);
+                c.prof_end(t, KC_LOOP_CTL, 0);
+            }
+            const LoopEndDesc end{LoopHist{hist_rec.p, hist_steps.p, ns}, cond, use_cond ? 1 : 0};
+            u32 last_final = 0;
+            for (u32 i = 0; i < ns; ++i)
+                if (steps[i].final) last_final = i;
+            for (u32 i = 0; i < ns; ++i) {
+                LStep& L = steps[i];
+                if (!L.final) continue;
+                const LoopOuter o = outer_of(L);
+                const LoopEndDesc* e = i == last_final ? &end : nullptr;
+                cudaEvent_t t = br();
+                if (L.select)
+                    loop_select_insert(c, s, ctl.p, i, L.head, o, L.jd, bufs_of(L.head), e);
+                else
+                    loop_materialize_insert(c, s, ctl.p, i, L.head, o, L.inner, L.jd, L.bufs(), bufs_of(L.head), e);
+                c.prof_end(t, KC_INSERT, 0);
+            }
+        };
+
+        // CUDA graph: while (some Δ non-empty) { iteration }
+        // Modes: "graph" (default) one launch of a graph whose conditional
+        // while node repeats the iteration until loop_end clears it;
+        // "batch" a plain graph of one iteration launched GD_LOOP_BATCH
+        // times per host check; "eager" direct launches, one check per
+        // iteration (used when per-kernel profiling is on).
+        const char* mode = getenv("GD_LOOP_MODE");
+        const bool eager = c.prof.on || (mode && std::string(mode) == "eager");
+        const bool batch = !eager && mode && std::string(mode) == "batch";
+        const int batch_n = getenv("GD_LOOP_BATCH") ? std::max(1, atoi(getenv("GD_LOOP_BATCH"))) : 16;
+        cudaGraphExec_t exec = nullptr;
+        cudaGraph_t graph = nullptr;
+        cudaStream_t cap_stream = nullptr;
+        u64 kernels_per_iter = 0;
+        auto destroy_graph = [&]() {
+            if (exec) cudaGraphExecDestroy(exec);
+            if (graph) cudaGraphDestroy(graph);
+            exec = nullptr;
+            graph = nullptr;
+        };
+        auto build_graph = [&]() {
+            destroy_graph();
+            if (!cap_stream) GD_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+            if (batch) {
+                GD_CUDA(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
+                const u64 l0 = c.launches;
+                try {
+                    record_iteration(cap_stream, false, 0);
+                } catch (...) {
+                    cudaStreamEndCapture(cap_stream, &graph);
+                    throw;
+                }
+                kernels_per_iter = c.launches - l0;
+                c.launches = l0;
+                GD_CUDA(cudaStreamEndCapture(cap_stream, &graph));
+                GD_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+                return;
+            }
+            GD_CUDA(cudaGraphCreate(&graph, 0));
+            cudaGraphConditionalHandle hdl;
+            GD_CUDA(cudaGraphConditionalHandleCreate(&hdl, graph, 1, cudaGraphCondAssignDefault));
+            cudaGraphNodeParams np{};
+            np.type = cudaGraphNodeTypeConditional;
+            np.conditional.handle = hdl;
+            np.conditional.type = cudaGraphCondTypeWhile;
+            np.conditional.size = 1;
+            cudaGraphNode_t node;
+            GD_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
+            cudaGraph_t body = np.conditional.phGraph_out[0];
+            GD_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0,
+                                                  cudaStreamCaptureModeThreadLocal));
+            const u64 l0 = c.launches;
+            try {
+                record_iteration(cap_stream, true, (unsigned long long)hdl);
+            } catch (...) {
+                cudaStreamEndCapture(cap_stream, &body);
+                throw;
+            }
+            kernels_per_iter = c.launches - l0;
+            c.launches = l0;
+            GD_CUDA(cudaStreamEndCapture(cap_stream, &body));
+            GD_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        };
+
+        u64 rollbacks = 0;
+        u32 done_iters = 0;
+        {
+            PhaseTimer t(E, "join");
+            for (;;) {
+                if (eager) {
+                    record_iteration(c.stream, false, 0);
+                } else {
+                    if (!exec) build_graph();
+                    for (int b = 0; b < (batch ? batch_n : 1); ++b) GD_CUDA(cudaGraphLaunch(exec, c.stream));
+                }
+                c.d2h(hc, ctl.p, sizeof(LoopCtl));
+                c.sync();
+                if (!eager)  // kernels that did work (batch: the early-exiting tail too)
+                    c.launches += kernels_per_iter * (batch ? (u64)batch_n
+                                                            : hc->iter - done_iters + (hc->overflow ? 1 : 0));
+                done_iters = hc->iter;
+                if (c.prof.on) c.prof.resolve();
+                if (hc->overflow) {
+                    ++rollbacks;
+                    for (u32 i = 0; i < ns; ++i) {
+                        LStep& L = steps[i];
+                        if (hc->need_rows[i] > L.rows_cap) {
+                            L.rows_cap = hc->need_rows[i] + hc->need_rows[i] / 2;
+                            L.row_start = DevBuf<u64>(c, L.rows_cap);
+                            L.row_off = DevBuf<u64>(c, L.rows_cap);
+                        }
+                        if (hc->need_splits[i] > L.splits_cap) {
+                            L.splits_cap = hc->need_splits[i] + hc->need_splits[i] / 2;
+                            L.splits = DevBuf<u64>(c, L.splits_cap);
+                        }
+                        if (hc->need_temp[i] > L.temp_cap) {
+                            L.temp_cap = hc->need_temp[i] + hc->need_temp[i] / 2;
+                            L.temp = DevBuf<u64>(c, L.temp_cap);
+                        }
+                        hc->need_rows[i] = hc->need_splits[i] = hc->need_temp[i] = 0;
+                    }
+                    for (u32 h = 0; h < nh; ++h) {
+                        LHead& H = heads[h];
+                        const u64 ln = hc->h[h].log_n;
+                        if (hc->need_log[h] > H.log_cap) {
+                            const u64 cap = hc->need_log[h] + hc->need_log[h] / 2;
+                            DevBuf<u64> nl(c, cap);
+                            if (ln) c.d2d(nl.p, H.log.p, ln * sizeof(u64));
+                            H.log = std::move(nl);
+                            H.log_cap = cap;
+                        }
+                        if (hc->need_tab[h] > H.tab_limit || hc->need_restamp) {
+                            // grow and/or restart the stamp epoch: rebuild from the log
+                            H.alloc_tab(c, hc->need_tab[h] > H.tab_limit ? 3 * hc->need_tab[h] : H.tab_cap);
+                            loop_table_fill(c, H.tab.p, H.tab_cap, H.sbits, H.log.p, ln);
+                        }
+                        hc->need_log[h] = hc->need_tab[h] = 0;
+                    }
+                    if (hc->need_hist > hist_cap) {
+                        const u64 cap = hc->need_hist;
+                        DevBuf<gd_iter_record> r2(c, cap * nh);
+                        DevBuf<u64> s2(c, cap * ns);
+                        c.d2d(r2.p, hist_rec.p, hist_cap * nh * sizeof(gd_iter_record));
+                        c.d2d(s2.p, hist_steps.p, hist_cap * ns * sizeof(u64));
+                        hist_rec = std::move(r2);
+                        hist_steps = std::move(s2);
+                        hist_cap = cap;
+                        hc->hist_cap = cap;
+                    }
+                    hc->need_hist = 0;
+                    if (hc->need_restamp) hc->epoch_base = hc->iter;
+                    hc->need_restamp = 0;
+                    hc->overflow = 0;
+                    c.h2d(ctl.p, hc, sizeof(LoopCtl));
+                    destroy_graph();
+                    continue;
+                }
+                if (hc->done) break;
+            }
+        }
+        destroy_graph();
+        if (cap_stream) cudaStreamDestroy(cap_stream);
+        (void)rollbacks;
+
+        // replay the reference's bookkeeping from the device history
+        const u64 iters = hc->iter;
+        std::vector<gd_iter_record> recs(iters * nh);
+        std::vector<u64> totals(iters * ns);
+        if (iters) {
+            c.d2h(recs.data(), hist_rec.p, recs.size() * sizeof(gd_iter_record));
+            c.d2h(totals.data(), hist_steps.p, totals.size() * sizeof(u64));
+            c.sync();
+        }
+        for (u64 i = 0; i < iters; ++i) replay_iteration(rec, &recs[i * nh], &totals[i * ns], steps);
+
+        // the fixpoint's canonical output: sort each head's log once
+        PhaseTimer t(E, "dedup");
+        for (u32 h = 0; h < nh; ++h) {
+            auto& st = rels[rec[h]];
+            LHead& H = heads[h];
+            H.tab.release();
+            const u64 f = hc->h[h].log_n;
+            const u32 ar = E.info_[rec[h]].arity;
+            DevBuf<u64> scratch(c, std::max<u64>(f, 1));
+            u64* sorted = radix_sort<u64>(c, H.log.p, scratch.p, f, ar * bits);
+            DevBuf<u64>& res = sorted == H.log.p ? H.log : scratch;
+            st.full.release();
+            st.full.ctx = res.ctx;
+            st.full.p = reinterpret_cast<K*>(res.p);
+            st.full.cap = res.cap;
+            res.p = nullptr;
+            res.cap = 0;
+            st.full_n = f;
+            st.tail.clear();
+            st.delta_n = 0;
+            st.new_n = 0;
+        }
+    }
+
+    // The reference's per-iteration bookkeeping (engine.hpp:196-251) from the
+    // device history: Δ history, iteration records, join tuples and the
+    // accountant / EBM charges in the reference's order.
+    void replay_iteration(const std::vector<u32>& rec, const gd_iter_record* r, const u64* totals,
+                          const std::vector<LStep>& steps) {
+        ++E.iterations;
+        auto head_of = [&](u32 rel) -> int {
+            auto it = std::find(rec.begin(), rec.end(), rel);
+            return it == rec.end() ? -1 : (int)(it - rec.begin());
+        };
+        for (size_t i = 0; i < rec.size(); ++i) E.info_[rec[i]].history.push_back(r[i].delta_in);
+        std::vector<u64> joined(rels.size(), 0);
+        size_t g = 0;
+        for (const auto& p : E.plans_) {
+            if (!p.recursive) continue;
+            for (u32 v = 0; v < p.nvariants; ++v) {
+                const gd_variant& var = p.variants[v];
+                const u32 n = std::max<u32>(1, var.nsteps);
+                const int sh = head_of(var.src_rel);
+                const bool use_delta = var.src_version == GD_DELTA;
+                u64 cur_n;
+                if (sh >= 0) cur_n = use_delta ? r[sh].delta_in : r[sh].full_after - r[sh].delta_out;
+                else cur_n = rels[var.src_rel].full_n;
+                if (!(use_delta && cur_n == 0)) {
+                    const u64 m = replay_chain(var, cur_n, totals + g);
+                    joined[p.head_rel] += m;
+                    append_new(p.head_rel, m);
+                }
+                g += n;
+            }
+        }
+        for (size_t i = 0; i < rec.size(); ++i) {
+            const u32 rr = rec[i];
+            RelInfo& ri = E.info_[rr];
+            const u32 ar = ri.arity;
+            if (joined[rr] != r[i].join) throw_logic("device loop: join count mismatch in the iteration record");
+            const u64 m = r[i].join;
+            if (m > 0) Tracked scratch(E.acct, Accountant::kTemp, m * 8 + rb(m, ar), "dedup");
+            Tracked fresh_charge(E.acct, Accountant::kTemp, rb(r[i].new_unique, ar), "dedup");
+            E.acct.release(Accountant::kContainer, ri.new_bytes);
+            ri.new_bytes = 0;
+            fresh_charge.reset();
+            assign_delta(rr, r[i].delta_out, "difference");
+            if (r[i].delta_out > 0) {
+                merge_accounting(rr, r[i].full_after - r[i].delta_out, r[i].delta_out, "merge");
+                ++rels[rr].merge_gen;
+                rels[rr].last_merge_was_delta = true;
+                rels[rr].dirty = true;
+            }
+            ri.log.push_back(r[i]);
+        }
+    }
+
+    // execute_chain's charges (engine.hpp:401-484) for known step totals.
+    u64 replay_chain(const gd_variant& v, u64 cur_n, const u64* totals) {
+        const u32 ar = E.info_[v.src_rel].arity;
+        Tracked permuted_charge;
+        if (!is_identity(v.src_perm, ar)) {
+            Tracked scratch(E.acct, Accountant::kTemp, 2 * rb(cur_n, ar) + cur_n * 8, "join");
+            scratch.reset();
+            permuted_charge = Tracked(E.acct, Accountant::kTemp, rb(cur_n, ar), "join");
+        }
+        if (v.nsteps == 0) return totals[0];
+        Tracked chained_charge;
+        for (u32 s = 0; s < v.nsteps; ++s) {
+            const u64 total = totals[s];
+            Tracked out_charge(E.acct, Accountant::kTemp, total * v.steps[s].proj_arity * 8ull, "join");
+            E.join_tuples += total;
+            if (s + 1 == v.nsteps) return total;
+            chained_charge = std::move(out_charge);
+            permuted_charge.reset();
+        }
+        return 0;
     }
 
     // ---- hash-partitioned mode -----------------------------

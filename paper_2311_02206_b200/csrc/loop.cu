@@ -1,0 +1,770 @@
+// loop.cu — kernels of the resident fixpoint loop (loop.h): one iteration of
+// engine::iterate_to_fixpoint (engine.hpp:181-257) for loop heads as a fixed
+// kernel sequence whose sizes live in device memory (LoopCtl), so the
+// sequence can be captured once into a CUDA graph and repeated on the
+// device.
+//
+// Per variant-step:  loop_probe   one HISA probe per outer row (join_count,
+//                                 ra.hpp:141-182) + per-CTA count sums;
+//                    loop_scan    exclusive scan of the counts (the
+//                                 sequential prefix sum of join_materialize,
+//                                 ra.hpp:235-238), CTA prefixes from the sums;
+//                    loop_materialize_temp  intermediate chain steps
+//                                 (execute_chain temps, engine.hpp:401-484).
+// Then loop_gate (capacity check of every insertion before any side effect),
+// loop_materialize_insert — the final step's load-balanced expansion fused
+// with canonicalize's dedup, difference and the append of Δ
+// (tuple_array.hpp:73-133, ra.hpp:386-422): every join row probes the
+// head's full-tuple hash index once — and loop_end (records the iteration,
+// advances Δ, detects the fixpoint, sets the graph's while condition).
+//
+// Grids are fixed at capture (multiples of the SM count); every kernel
+// reads its sizes from LoopCtl and returns at once when the loop is done or
+// an overflow rolled the iteration back.
+#include "index.cuh"
+#include "join.cuh"
+#include "loop.h"
+
+namespace gd {
+
+namespace {
+
+constexpr int kLT = 256;              // threads per CTA
+constexpr int kLItems = 4;            // probe rows per thread per tile
+constexpr u64 kLTile = (u64)kLT * kLItems;
+constexpr u64 kHashSeed = 0x9e3779b97f4a7c15ull;
+constexpr int kScan = 4;  // slots read per collision step (one 32-byte sector when aligned)
+
+__device__ __forceinline__ bool loop_stopped(const LoopCtl* ctl) {
+    return (ctl->overflow | ctl->done) != 0;
+}
+
+__device__ __forceinline__ void resolve(const LoopOuter& o, const LoopCtl* ctl, const u64*& p, u64& n) {
+    switch (o.kind) {
+        case LO_DELTA:
+            p = o.ptr + ctl->h[o.head].dlo;
+            n = ctl->h[o.head].dhi - ctl->h[o.head].dlo;
+            break;
+        case LO_FULL:
+            p = o.ptr;
+            n = ctl->h[o.head].dhi;
+            break;
+        case LO_TEMP:
+            p = o.ptr;
+            n = ctl->step_total[o.src_step];
+            break;
+        default:
+            p = o.ptr;
+            n = o.n;
+    }
+}
+
+__device__ __forceinline__ u64 hs_home(u64 key, u64 cap) { return __umul64hi(fmix64(key ^ kHashSeed), cap); }
+
+// Membership + insertion of PER keys in the head's full-tuple index, the
+// first CAS of every key issued together (independent L2 round trips in
+// flight).  fresh[k]: the key is new (appended to the log by the caller);
+// first[k]: first occurrence of the key in this iteration (stamp `st`) —
+// the distinct count of the join output.
+template <int PER>
+__device__ __forceinline__ void hs_insert_packed(u64* __restrict__ tab, u64 cap, u32 sb, u64 st, const u64 (&key)[PER],
+                                                 const bool (&ok)[PER], bool (&fresh)[PER], bool (&first)[PER]) {
+    const u64 smask = (1ull << sb) - 1;
+    u64 pos[PER], old[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        fresh[k] = first[k] = false;
+        if (ok[k]) {
+            pos[k] = hs_home(key[k], cap);
+            old[k] = atomicCAS(&tab[pos[k]], kEmptySlot, key[k] << sb | st);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        if (!ok[k]) continue;
+        const u64 want = key[k] << sb | st;
+        u64 o = old[k];
+        u64 p = pos[k];
+        while (true) {
+            if (o == kEmptySlot) {
+                fresh[k] = first[k] = true;
+                break;
+            }
+            if ((o >> sb) == key[k]) {
+                while ((o & smask) != st) {  // seen before, not yet this iteration
+                    const u64 o2 = atomicCAS(&tab[p], o, want);
+                    if (o2 == o) {
+                        first[k] = true;
+                        break;
+                    }
+                    o = o2;
+                }
+                break;
+            }
+            // collision: read the next kScan slots together (one round trip,
+            // mostly one sector) and CAS only the first candidate
+            u64 w[kScan];
+#pragma unroll
+            for (int q = 0; q < kScan; ++q) {
+                u64 pq = p + 1 + q;
+                pq = pq >= cap ? pq - cap : pq;
+                w[q] = __ldcg(&tab[pq]);
+            }
+            int hit = kScan;
+#pragma unroll
+            for (int q = kScan - 1; q >= 0; --q)
+                if (w[q] == kEmptySlot || (w[q] >> sb) == key[k]) hit = q;
+            p = p + 1 + (hit == kScan ? kScan - 1 : hit);
+            p = p >= cap ? p - cap : p;
+            if (hit == kScan) {  // all kScan occupied by other keys: continue after them
+                o = w[kScan - 1];
+                continue;
+            }
+            o = w[hit] == kEmptySlot ? atomicCAS(&tab[p], kEmptySlot, want) : w[hit];
+        }
+    }
+}
+
+template <int PER>
+__device__ __forceinline__ void hs_insert_wide(HSlot* __restrict__ tab, u64 cap, u32 st, const u64 (&key)[PER],
+                                               const bool (&ok)[PER], bool (&fresh)[PER], bool (&first)[PER]) {
+    u64 pos[PER], old[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        fresh[k] = first[k] = false;
+        if (ok[k]) {
+            pos[k] = hs_home(key[k], cap);
+            old[k] = atomicCAS(&tab[pos[k]].key, kEmptySlot, key[k]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        if (!ok[k]) continue;
+        u64 o = old[k];
+        u64 p = pos[k];
+        while (o != kEmptySlot && o != key[k]) {
+            p = p + 1 == cap ? 0 : p + 1;
+            o = atomicCAS(&tab[p].key, kEmptySlot, key[k]);
+        }
+        fresh[k] = o == kEmptySlot;
+        first[k] = __ldcg(&tab[p].stamp) != st && atomicExch(&tab[p].stamp, st) != st;
+    }
+}
+
+template <int PER>
+__device__ __forceinline__ void hs_insert(const LoopHeadBufs& hb, u32 st, const u64 (&key)[PER],
+                                          const bool (&ok)[PER], bool (&fresh)[PER], bool (&first)[PER]) {
+    if (hb.sbits)
+        hs_insert_packed<PER>(static_cast<u64*>(hb.tab), hb.tab_cap, hb.sbits, st, key, ok, fresh, first);
+    else
+        hs_insert_wide<PER>(static_cast<HSlot*>(hb.tab), hb.tab_cap, st, key, ok, fresh, first);
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {
+    v = warp_sum(v);
+    if (lane_id() == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    T t = 0;
+#pragma unroll
+    for (int w = 0; w < kLT / 32; ++w) t += red[w];
+    __syncthreads();
+    return t;
+}
+
+// Uniform per-CTA view of the stop flags (another CTA may raise overflow
+// while this one starts).
+__device__ __forceinline__ bool cta_stopped(const LoopCtl* ctl, u32* s) {
+    if (threadIdx.x == 0) {
+        const volatile LoopCtl* v = ctl;
+        *s = (v->overflow | v->done) != 0;
+    }
+    __syncthreads();
+    return *s != 0;
+}
+
+// True in every thread of the grid's last CTA to get here; that CTA sees
+// every other CTA's writes (fence before the count).
+__device__ __forceinline__ bool last_cta(LoopCtl* ctl, u32* s) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const u32 t = atomicAdd(&ctl->ctas_done, 1u);
+        *s = t == gridDim.x - 1;
+        if (*s) {
+            ctl->ctas_done = 0;
+            __threadfence();
+        }
+    }
+    __syncthreads();
+    return *s != 0;
+}
+
+// Each CTA of a fixed grid owns a contiguous chunk of outer rows (a whole
+// number of tiles), so per-CTA sums + the scan give row offsets without
+// look-back or workspace resets.
+__device__ __forceinline__ void chunk_of(u64 n, u64& begin, u64& end) {
+    const u64 tiles = (n + kLTile - 1) / kLTile;
+    const u64 per = (tiles + gridDim.x - 1) / gridDim.x;
+    begin = min(n, (u64)blockIdx.x * per * kLTile);
+    end = min(n, begin + per * kLTile);
+}
+
+// ---- gate / end bodies (one thread) --------------------------------------
+
+// One thread; every control-block load is issued up front (__ldcg: L2,
+// coherent after the caller's fence) so the body costs a few round trips.
+__device__ void gate_body(LoopCtl* ctl, const LoopGateDesc& g) {
+    const u32 overflow = __ldcg(&ctl->overflow), done = __ldcg(&ctl->done), iter = __ldcg(&ctl->iter);
+    const u32 nh = __ldcg(&ctl->nheads), epoch = __ldcg(&ctl->epoch_base);
+    const u64 hist_cap = __ldcg(&ctl->hist_cap);
+    u64 cand[kLoopMaxSteps];
+    for (u32 f = 0; f < g.nfinal; ++f) cand[f] = __ldcg(&ctl->step_cand[g.final_step[f]]);
+    u64 log_n[kLoopMaxHeads];
+    for (u32 h = 0; h < nh; ++h) log_n[h] = __ldcg(&ctl->h[h].log_n);
+    if (overflow | done) return;
+    if (iter >= hist_cap) {
+        ctl->need_hist = hist_cap * 2;
+        ctl->overflow = 1;
+        return;
+    }
+    if (iter + 1 - epoch > g.stamp_max) {
+        ctl->need_restamp = 1;
+        ctl->overflow = 1;
+        return;
+    }
+    u64 add[kLoopMaxHeads];
+    for (u32 h = 0; h < kLoopMaxHeads; ++h) add[h] = 0;
+    for (u32 f = 0; f < g.nfinal; ++f) add[g.final_head[f]] += cand[f];
+    bool over = false;
+    for (u32 h = 0; h < nh; ++h) {
+        ctl->h[h].cand = add[h];
+        const u64 need = log_n[h] + add[h];
+        if (need > g.log_cap[h]) {
+            ctl->need_log[h] = need;
+            over = true;
+        }
+        if (need > g.tab_limit[h]) {
+            ctl->need_tab[h] = need;
+            over = true;
+        }
+    }
+    if (over) ctl->overflow = 1;
+}
+
+__device__ void end_body(LoopCtl* ctl, const LoopEndDesc& e) {
+    const cudaGraphConditionalHandle cond = (cudaGraphConditionalHandle)e.cond;
+    const u32 overflow = __ldcg(&ctl->overflow), done = __ldcg(&ctl->done), iter = __ldcg(&ctl->iter);
+    const u32 nh = __ldcg(&ctl->nheads);
+    const u32 ns = e.hist.nsteps;
+    if (done) {
+        if (e.use_cond) cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    if (overflow) {  // roll back: nothing was inserted (gate)
+        for (u32 h = 0; h < nh; ++h) ctl->h[h].cand = ctl->h[h].J = ctl->h[h].N = ctl->h[h].D = 0;
+        for (u32 s = 0; s < ns; ++s) ctl->step_total[s] = 0;
+        if (e.use_cond) cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    u64 dlo[kLoopMaxHeads], dhi[kLoopMaxHeads], J[kLoopMaxHeads], N[kLoopMaxHeads], D[kLoopMaxHeads],
+        ln[kLoopMaxHeads], tot[kLoopMaxSteps];
+    for (u32 h = 0; h < nh; ++h) {
+        dlo[h] = __ldcg(&ctl->h[h].dlo);
+        dhi[h] = __ldcg(&ctl->h[h].dhi);
+        J[h] = __ldcg(&ctl->h[h].J);
+        N[h] = __ldcg(&ctl->h[h].N);
+        D[h] = __ldcg(&ctl->h[h].D);
+        ln[h] = __ldcg(&ctl->h[h].log_n);
+    }
+    for (u32 s = 0; s < ns; ++s) tot[s] = __ldcg(&ctl->step_total[s]);
+    const u64 i = iter;
+    bool active = false;
+    for (u32 h = 0; h < nh; ++h) {
+        gd_iter_record r;
+        r.delta_in = dhi[h] - dlo[h];
+        r.join = J[h];
+        r.new_unique = N[h];
+        r.delta_out = D[h];
+        r.full_after = ln[h];
+        e.hist.rec[i * nh + h] = r;
+        LoopHeadState& st = ctl->h[h];
+        st.dlo = dhi[h];
+        st.dhi = ln[h];
+        active |= ln[h] > dhi[h];
+        st.cand = st.J = st.N = st.D = 0;
+    }
+    for (u32 s = 0; s < ns; ++s) {
+        e.hist.steps[i * ns + s] = tot[s];
+        ctl->step_total[s] = 0;
+    }
+    ctl->iter = iter + 1;
+    ctl->done = active ? 0 : 1;
+    __threadfence();
+    if (e.use_cond) cudaGraphSetConditional(cond, active ? 1 : 0);
+}
+
+// ---- kernels ----------------------------------------------------------------
+
+__global__ void __launch_bounds__(kLT) loop_probe_kernel(LoopCtl* ctl, u32 step, LoopOuter o, DevJoin jd,
+                                                         IndexView<u64> ix, u64 inner_n, LoopStepBufs sb,
+                                                         u64* __restrict__ block_sums) {
+    __shared__ u64 red[kLT / 32];
+    __shared__ u32 s_flag;
+    if (cta_stopped(ctl, &s_flag)) return;
+    const u64* outer;
+    u64 n;
+    resolve(o, ctl, outer, n);
+    if (n + 1 > sb.rows_cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctl->need_rows[step] = n + 1;
+            ctl->overflow = 1;
+        }
+        return;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->step_n[step] = n;
+    u64* __restrict__ row_start = sb.row_start;
+    u64* __restrict__ row_cnt = sb.row_off;
+    u64 begin, end;
+    chunk_of(n, begin, end);
+    u64 sum = 0;
+    for (u64 t0 = begin; t0 < end; t0 += kLTile) {
+        const u64 base = t0 + threadIdx.x;
+        if (jd.jcc == 0 || inner_n == 0) {  // Cartesian step / empty inner
+#pragma unroll
+            for (int j = 0; j < kLItems; ++j) {
+                const u64 r = base + (u64)j * kLT;
+                if (r < end) {
+                    const u64 c = jd.jcc == 0 ? inner_n : 0;
+                    row_start[r] = 0;
+                    row_cnt[r] = c;
+                    sum += c;
+                }
+            }
+            continue;
+        }
+        u64 pre[kLItems];
+        Slot s[kLItems];
+#pragma unroll
+        for (int j = 0; j < kLItems; ++j) {
+            const u64 r = base + (u64)j * kLT;
+            pre[j] = r < end ? outer_prefix(jd, outer[r]) : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < kLItems; ++j) s[j] = ix.slots[slot_home(pre[j], ix.slot_count)];
+#pragma unroll
+        for (int j = 0; j < kLItems; ++j) {
+            const u64 r = base + (u64)j * kLT;
+            if (r >= end) continue;
+            u64 st = 0, ln = 0;
+            if (s[j].tag == pre[j]) {
+                st = s[j].val & kStartMask;
+                const u64 l = s[j].val >> 40;
+                ln = l == kLenSat ? run_end(ix, pre[j], st) - st : l;
+            } else if (s[j].tag != kEmptySlot) {
+                index_probe(ix, pre[j], st, ln);  // collision chain (rare)
+            }
+            row_start[r] = st;
+            row_cnt[r] = ln;
+            sum += ln;
+        }
+    }
+    sum = block_sum(sum, red);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = sum;
+}
+
+// Row r's outputs occupy merge-path items [off_r + r, off_r + c_r + r]
+// (outputs, then its row end E_r = off_{r+1} + r); the split of a tile
+// boundary D (number of row ends before D) is r for E_{r-1} < D <= E_r.
+__global__ void __launch_bounds__(kLT) loop_scan_kernel(LoopCtl* ctl, u32 step, LoopOuter o, LoopStepBufs sb,
+                                                        const u64* __restrict__ block_sums, LoopGateDesc g,
+                                                        int do_gate) {
+    __shared__ u64 red[kLT / 32];
+    __shared__ u64 s_scan[kLT / 32 + 1];
+    __shared__ u32 s_flag;
+    if (!cta_stopped(ctl, &s_flag)) {
+        const u64* outer;
+        u64 n;
+        resolve(o, ctl, outer, n);
+        u64 pre = 0, all = 0;
+        for (u32 b = threadIdx.x; b < gridDim.x; b += kLT) {
+            const u64 v = block_sums[b];
+            all += v;
+            if (b < blockIdx.x) pre += v;
+        }
+        pre = block_sum(pre, red);
+        all = block_sum(all, red);
+        const u64 ntiles = all ? (n + all + kLoopMatTile - 1) / kLoopMatTile : 0;
+        const bool fits = ntiles + 1 <= sb.splits_cap;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            sb.row_off[n] = all;
+            ctl->step_cand[step] = all;
+            if (!fits) {
+                ctl->need_splits[step] = ntiles + 1;
+                ctl->overflow = 1;
+            } else if (ntiles) {
+                sb.splits[ntiles] = n;
+            }
+        }
+        u64* __restrict__ row_off = sb.row_off;
+        u64 begin, end;
+        chunk_of(n, begin, end);
+        u64 carry = pre;
+        for (u64 t0 = begin; t0 < end; t0 += kLTile) {
+            const u64 first = t0 + (u64)threadIdx.x * kLItems;
+            u64 c[kLItems];
+            u64 sum = 0;
+#pragma unroll
+            for (int j = 0; j < kLItems; ++j) {
+                c[j] = first + j < end ? row_off[first + j] : 0;
+                sum += c[j];
+            }
+            u64 tot;
+            u64 off = carry + block_exclusive_scan<u64, kLT>(sum, tot, s_scan);
+#pragma unroll
+            for (int j = 0; j < kLItems; ++j) {
+                const u64 r = first + j;
+                if (r < end) {
+                    row_off[r] = off;
+                    if (fits) {
+                        const u64 e_r = off + c[j] + r;
+                        for (u64 d = (off + r + kLoopMatTile - 1) / kLoopMatTile * kLoopMatTile; d <= e_r;
+                             d += kLoopMatTile)
+                            sb.splits[d / kLoopMatTile] = r;
+                    }
+                }
+                off += c[j];
+            }
+            carry += tot;
+        }
+    }
+    if (do_gate && last_cta(ctl, &s_flag) && threadIdx.x == 0) gate_body(ctl, g);
+}
+
+struct MatSmem {
+    u64 off[kLoopMatTile + 1];
+    u64 start[kLoopMatTile + 1];
+    u64 outer[kLoopMatTile + 1];
+};
+
+// Stages tile `tile`'s rows; returns false when the tile has no output.
+__device__ __forceinline__ bool stage_tile(MatSmem& sm, u64 tile, const u64* outer, u64 n, u64 total,
+                                           const LoopStepBufs& sb, u64& b0, u64& b1, u32& rcount) {
+    const u64 diag0 = tile * kLoopMatTile;
+    const u64 diag1 = min(diag0 + kLoopMatTile, n + total);
+    const u64 a0 = sb.splits[tile], a1 = sb.splits[tile + 1];
+    b0 = diag0 - a0;
+    b1 = diag1 - a1;
+    __syncthreads();  // previous tile's readers are done with sm
+    if (b1 <= b0) return false;
+    const u64 rlast = min(a1, n - 1);
+    rcount = (u32)(rlast - a0 + 1);
+    for (u32 i = threadIdx.x; i < rcount; i += kLT) {
+        sm.off[i] = sb.row_off[a0 + i];
+        sm.start[i] = sb.row_start[a0 + i];
+        sm.outer[i] = outer[a0 + i];
+    }
+    __syncthreads();
+    return true;
+}
+
+__device__ __forceinline__ u32 row_of(const MatSmem& sm, u32 rcount, u64 j) {
+    u32 lo = 0, hi = rcount;
+    while (hi - lo > 1) {
+        const u32 mid = (lo + hi) >> 1;
+        if (sm.off[mid] <= j) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+constexpr int kPer = (int)(kLoopMatTile / kLT);  // outputs per thread per tile
+
+__global__ void __launch_bounds__(kLT) loop_materialize_temp_kernel(LoopCtl* ctl, u32 step, LoopOuter o,
+                                                                    const u64* __restrict__ inner, DevJoin jd,
+                                                                    LoopStepBufs sb, u64* __restrict__ temp,
+                                                                    u64 temp_cap) {
+    __shared__ MatSmem sm;
+    __shared__ u64 s_scan[kLT / 32 + 1];
+    __shared__ u64 s_base;
+    __shared__ u32 s_flag;
+    if (cta_stopped(ctl, &s_flag)) return;
+    const u64* outer;
+    u64 n;
+    resolve(o, ctl, outer, n);
+    const u64 total = ctl->step_cand[step];
+    if (total > temp_cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctl->need_temp[step] = total;
+            ctl->overflow = 1;
+        }
+        return;
+    }
+    if (jd.nfilters == 0 && blockIdx.x == 0 && threadIdx.x == 0) ctl->step_total[step] = total;
+    if (total == 0) return;
+    const u64 ntiles = (n + total + kLoopMatTile - 1) / kLoopMatTile;
+    for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        u64 b0, b1;
+        u32 rcount;
+        if (!stage_tile(sm, tile, outer, n, total, sb, b0, b1, rcount)) continue;
+        if (jd.nfilters == 0) {
+            for (u64 j = b0 + threadIdx.x; j < b1; j += kLT) {
+                const u32 r = row_of(sm, rcount, j);
+                const u64 i = inner[sm.start[r] + (j - sm.off[r])];
+                temp[j] = project(jd, sm.outer[r], i);
+            }
+            continue;
+        }
+        // filtered: survivors compacted through one atomic per tile
+        u64 key[kPer];
+        bool keep[kPer];
+        u64 cnt = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const u64 j = b0 + threadIdx.x + (u64)k * kLT;
+            keep[k] = false;
+            if (j < b1) {
+                const u32 r = row_of(sm, rcount, j);
+                const u64 ov = sm.outer[r];
+                const u64 i = inner[sm.start[r] + (j - sm.off[r])];
+                keep[k] = passes(jd, ov, i);
+                key[k] = project(jd, ov, i);
+                cnt += keep[k];
+            }
+        }
+        u64 tot;
+        const u64 ex = block_exclusive_scan<u64, kLT>(cnt, tot, s_scan);
+        if (threadIdx.x == 0) s_base = tot ? atomicAdd(&ctl->step_total[step], tot) : 0;
+        __syncthreads();
+        u64 p = s_base + ex;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if (keep[k]) temp[p++] = key[k];
+    }
+}
+
+__global__ void loop_gate_kernel(LoopCtl* ctl, LoopGateDesc g) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) gate_body(ctl, g);
+}
+
+__global__ void loop_end_kernel(LoopCtl* ctl, LoopEndDesc e) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) end_body(ctl, e);
+}
+
+__global__ void loop_select_cand_kernel(LoopCtl* ctl, u32 step, LoopOuter o) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (loop_stopped(ctl)) return;
+    const u64* p;
+    u64 n;
+    resolve(o, ctl, p, n);
+    ctl->step_n[step] = n;
+    ctl->step_cand[step] = n;
+}
+
+// Appends this thread's new keys to the head's log (one atomic per CTA).
+template <int PER>
+__device__ __forceinline__ void append_block(LoopCtl* ctl, u32 head, u64* __restrict__ log, const u64 (&keys)[PER],
+                                             const bool (&fresh)[PER], u64 cnt, u64 J, u64 N, u32 step,
+                                             u64* s_scan, u64* s_base, u64* red) {
+    u64 tot;
+    const u64 ex = block_exclusive_scan<u64, kLT>(cnt, tot, s_scan);
+    const u64 j = block_sum(J, red);
+    const u64 nn = block_sum(N, red);
+    if (threadIdx.x == 0) {
+        *s_base = tot ? atomicAdd(&ctl->h[head].log_n, tot) : 0;
+        if (tot) atomicAdd(&ctl->h[head].D, tot);
+        if (j) {
+            atomicAdd(&ctl->h[head].J, j);
+            atomicAdd(&ctl->step_total[step], j);
+        }
+        if (nn) atomicAdd(&ctl->h[head].N, nn);
+    }
+    __syncthreads();
+    u64 p = *s_base + ex;
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+        if (fresh[k]) log[p++] = keys[k];
+}
+
+__global__ void __launch_bounds__(kLT) loop_materialize_insert_kernel(
+    LoopCtl* ctl, u32 step, u32 head, LoopOuter o, const u64* __restrict__ inner, DevJoin jd, LoopStepBufs sb,
+    LoopHeadBufs hb, LoopEndDesc e, int do_end) {
+    __shared__ MatSmem sm;
+    __shared__ u64 s_scan[kLT / 32 + 1];
+    __shared__ u64 red[kLT / 32];
+    __shared__ u64 s_base;
+    __shared__ u32 s_flag;
+    if (!cta_stopped(ctl, &s_flag)) {
+        const u64* outer;
+        u64 n;
+        resolve(o, ctl, outer, n);
+        const u64 total = ctl->step_cand[step];
+        const u32 it = ctl->iter + 1 - ctl->epoch_base;
+        const u64 ntiles = total ? (n + total + kLoopMatTile - 1) / kLoopMatTile : 0;
+        for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            u64 b0, b1;
+            u32 rcount;
+            if (!stage_tile(sm, tile, outer, n, total, sb, b0, b1, rcount)) continue;
+            u64 key[kPer];
+            bool ok[kPer];
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const u64 j = b0 + threadIdx.x + (u64)k * kLT;
+                ok[k] = j < b1;
+                key[k] = 0;
+                if (ok[k]) {
+                    const u32 r = row_of(sm, rcount, j);
+                    const u64 ov = sm.outer[r];
+                    const u64 i = inner[sm.start[r] + (j - sm.off[r])];
+                    ok[k] = passes(jd, ov, i);
+                    key[k] = project(jd, ov, i);
+                }
+            }
+            bool fresh[kPer], first[kPer];
+            hs_insert<kPer>(hb, it, key, ok, fresh, first);
+            u64 cnt = 0, J = 0, N = 0;
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                J += ok[k];
+                cnt += fresh[k];
+                N += first[k];
+            }
+            append_block<kPer>(ctl, head, hb.log, key, fresh, cnt, J, N, step, s_scan, &s_base, red);
+        }
+    }
+    if (do_end && last_cta(ctl, &s_flag) && threadIdx.x == 0) end_body(ctl, e);
+}
+
+__global__ void __launch_bounds__(kLT) loop_select_insert_kernel(LoopCtl* ctl, u32 step, u32 head, LoopOuter o,
+                                                                 DevJoin jd, LoopHeadBufs hb, LoopEndDesc e,
+                                                                 int do_end) {
+    __shared__ u64 s_scan[kLT / 32 + 1];
+    __shared__ u64 red[kLT / 32];
+    __shared__ u64 s_base;
+    __shared__ u32 s_flag;
+    if (!cta_stopped(ctl, &s_flag)) {
+        const u64* outer;
+        u64 n;
+        resolve(o, ctl, outer, n);
+        const u32 it = ctl->iter + 1 - ctl->epoch_base;
+        const u64 ntiles = (n + kLT - 1) / kLT;
+        for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const u64 r = tile * kLT + threadIdx.x;
+            u64 key[1] = {0};
+            bool ok[1] = {r < n && passes(jd, outer[r], 0ull)};
+            if (ok[0]) key[0] = project(jd, outer[r], 0ull);
+            bool fresh[1], first[1];
+            hs_insert<1>(hb, it, key, ok, fresh, first);
+            const u64 cnt = fresh[0], J = ok[0], N = first[0];
+            append_block<1>(ctl, head, hb.log, key, fresh, cnt, J, N, step, s_scan, &s_base, red);
+        }
+    }
+    if (do_end && last_cta(ctl, &s_flag) && threadIdx.x == 0) end_body(ctl, e);
+}
+
+// Rebuild of a table from the log (keys unique): stamp 0 = "before the
+// current epoch".
+__global__ void table_fill_kernel(void* tab, u64 cap, u32 sb, const u64* __restrict__ keys, u64 n) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 key = keys[i];
+        u64 pos = hs_home(key, cap);
+        while (true) {
+            u64* w = sb ? static_cast<u64*>(tab) + pos : &static_cast<HSlot*>(tab)[pos].key;
+            const u64 want = sb ? key << sb : key;
+            const u64 old = atomicCAS(w, kEmptySlot, want);
+            if (old == kEmptySlot) {
+                if (!sb) static_cast<HSlot*>(tab)[pos].stamp = 0;
+                break;
+            }
+            pos = pos + 1 == cap ? 0 : pos + 1;
+        }
+    }
+}
+
+template <typename Kern>
+int occupancy(Kern k, size_t smem = 0) {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kLT, smem);
+    return b > 0 ? b : 1;
+}
+
+int g_occ_temp = 0, g_occ_insert = 0, g_occ_select = 0;
+
+}  // namespace
+
+int loop_grid(const Ctx& c) { return c.num_sms * 4; }
+
+void loop_prepare() {
+    if (g_occ_temp) return;
+    g_occ_temp = occupancy(loop_materialize_temp_kernel);
+    g_occ_insert = occupancy(loop_materialize_insert_kernel);
+    g_occ_select = occupancy(loop_select_insert_kernel);
+}
+
+void loop_table_clear(Ctx& c, void* tab, u64 cap, u32 sbits) { c.memset(tab, 0xff, cap * loop_slot_bytes(sbits)); }
+
+void loop_table_fill(Ctx& c, void* tab, u64 cap, u32 sbits, const u64* keys, u64 n) {
+    if (n == 0) return;
+    const int grid = (int)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)c.num_sms * 16));
+    table_fill_kernel<<<grid, 256, 0, c.stream>>>(tab, cap, sbits, keys, n);
+    c.check_launch();
+}
+
+void loop_probe(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const DevJoin& jd,
+                const IndexView<u64>* ix, u64 inner_n, const LoopStepBufs& sb, u64* block_sums) {
+    IndexView<u64> v{};
+    if (ix) v = *ix;
+    loop_probe_kernel<<<loop_grid(c), kLT, 0, s>>>(ctl, step, o, jd, v, inner_n, sb, block_sums);
+    c.check_launch();
+}
+
+void loop_scan(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const LoopStepBufs& sb,
+               const u64* block_sums, const LoopGateDesc* gate) {
+    LoopGateDesc g{};
+    if (gate) g = *gate;
+    loop_scan_kernel<<<loop_grid(c), kLT, 0, s>>>(ctl, step, o, sb, block_sums, g, gate ? 1 : 0);
+    c.check_launch();
+}
+
+void loop_gate(Ctx& c, cudaStream_t s, LoopCtl* ctl, const LoopGateDesc& g) {
+    loop_gate_kernel<<<1, 32, 0, s>>>(ctl, g);
+    c.check_launch();
+}
+
+void loop_materialize_temp(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const u64* inner,
+                           const DevJoin& jd, const LoopStepBufs& sb, u64* temp, u64 temp_cap) {
+    loop_materialize_temp_kernel<<<c.num_sms * g_occ_temp, kLT, 0, s>>>(ctl, step, o, inner, jd, sb, temp,
+                                                                         temp_cap);
+    c.check_launch();
+}
+
+void loop_select_cand(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o) {
+    loop_select_cand_kernel<<<1, 32, 0, s>>>(ctl, step, o);
+    c.check_launch();
+}
+
+void loop_materialize_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
+                             const u64* inner, const DevJoin& jd, const LoopStepBufs& sb,
+                             const LoopHeadBufs& hb, const LoopEndDesc* end) {
+    LoopEndDesc e{};
+    if (end) e = *end;
+    loop_materialize_insert_kernel<<<c.num_sms * g_occ_insert, kLT, 0, s>>>(ctl, step, head, o, inner, jd, sb, hb,
+                                                                             e, end ? 1 : 0);
+    c.check_launch();
+}
+
+void loop_select_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
+                        const DevJoin& jd, const LoopHeadBufs& hb, const LoopEndDesc* end) {
+    LoopEndDesc e{};
+    if (end) e = *end;
+    loop_select_insert_kernel<<<c.num_sms * g_occ_select, kLT, 0, s>>>(ctl, step, head, o, jd, hb, e,
+                                                                        end ? 1 : 0);
+    c.check_launch();
+}
+
+void loop_end(Ctx& c, cudaStream_t s, LoopCtl* ctl, const LoopEndDesc& end) {
+    loop_end_kernel<<<1, 32, 0, s>>>(ctl, end);
+    c.check_launch();
+}
+
+}  // namespace gd

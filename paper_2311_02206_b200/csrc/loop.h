@@ -1,0 +1,170 @@
+// loop.h — the resident device loop of the semi-naive fixpoint (engine.hpp:
+// 181-257) for relations that are never a join inner (TC's Reach, SG's SG,
+// …): the whole iteration runs on the device with every size read from
+// device memory, so one iteration is a fixed kernel sequence that is
+// captured once into a CUDA graph and repeated under a device-side `while`
+// condition (termination = every Δ empty, detected on the device).
+//
+// Relation store of a loop head h:
+//   log_h   append-only array of packed keys; log[0, dhi) is the full
+//           relation, log[dlo, dhi) the current Δ (delta ⊆ full,
+//           SPEC.md:306), new rows are appended at log_n;
+//   tab_h   HISA index over the whole tuple (prefix_len = arity): open
+//           addressing; membership of a join output in full is one slot
+//           CAS, and a per-slot stamp (last iteration that produced the key)
+//           gives the distinct count of the iteration's join output
+//           (canonicalize's unique) in the same pass.
+// Dedup + difference + append are fused into the join's materialize:
+// the join output J is never written to HBM.  The canonical (sorted) full
+// relation is produced once, by the onesweep radix sort, when the loop ends.
+#pragma once
+
+#include "ops.h"
+
+namespace gd {
+
+constexpr u32 kLoopMaxHeads = 8;
+constexpr u32 kLoopMaxSteps = 32;  // variant-steps per iteration
+constexpr u64 kLoopMatTile = 1024; // merge-path items (rows + outputs) per materialize tile
+
+// Wide slot (keys of more than 56 bits): the key and the stamp of the last
+// iteration that produced it.
+struct HSlot {
+    u64 key;    // kEmptySlot when free
+    u32 stamp;  // iteration - epoch_base that last produced the key
+    u32 pad;
+};
+// Packed slot (keys of at most 64 - sbits bits, sbits >= 8): one u64 word
+// key << sbits | stamp, so insertion and the stamp update are one CAS.
+
+// Where a step's outer rows come from (resolved on the device).
+enum LoopOuterKind : u32 {
+    LO_STATIC = 0,  // (ptr, n) fixed at capture
+    LO_DELTA = 1,   // log of head `head`, [dlo, dhi)
+    LO_FULL = 2,    // log of head `head`, [0, dhi)
+    LO_TEMP = 3,    // ptr = temp buffer, n = ctl.step_total[src_step]
+};
+
+struct LoopOuter {
+    u32 kind;
+    u32 head;
+    u32 src_step;
+    u32 pad;
+    const u64* ptr;
+    u64 n;
+};
+
+struct LoopHeadState {
+    u64 log_n;  // rows in the log (= |full| after the iteration)
+    u64 dlo, dhi;
+    u64 cand;   // candidate upper bound of this iteration's insertions
+    u64 J, N, D;  // join rows (post-filter), distinct join rows, new rows
+};
+
+// Device control block of one engine's loop.
+struct LoopCtl {
+    u32 iter;      // completed iterations
+    u32 done;      // every Δ empty
+    u32 overflow;  // a capacity was exceeded: iteration rolled back, host grows
+    u32 nheads;
+    u64 hist_cap;
+    u32 epoch_base;    // stamps are iter + 1 - epoch_base
+    u32 need_restamp;  // stamp range exhausted: host rebuilds the tables
+    u32 ctas_done;     // last-CTA detection of the fused gate / end epilogues
+    u32 pad;
+    LoopHeadState h[kLoopMaxHeads];
+    u64 step_cand[kLoopMaxSteps];   // candidates (pre-filter) of each step
+    u64 step_total[kLoopMaxSteps];  // rows produced (post-filter) of each step
+    u64 step_n[kLoopMaxSteps];      // outer rows of each step
+    // capacities the host must provide after an overflow
+    u64 need_rows[kLoopMaxSteps];
+    u64 need_splits[kLoopMaxSteps];
+    u64 need_temp[kLoopMaxSteps];
+    u64 need_log[kLoopMaxHeads];
+    u64 need_tab[kLoopMaxHeads];
+    u64 need_hist;
+};
+
+// Per-iteration history written by loop_end: rec[i * nheads + h] and the
+// post-filter totals of every step, steps[i * nsteps + s].
+struct LoopHist {
+    gd_iter_record* rec;
+    u64* steps;
+    u32 nsteps;
+};
+
+// Storage of one head (captured into the graph).
+struct LoopHeadBufs {
+    u64* log;
+    u64 log_cap;
+    void* tab;      // u64[tab_cap] (packed, sbits > 0) or HSlot[tab_cap]
+    u64 tab_cap;
+    u64 tab_limit;  // max keys before the table must grow
+    u32 sbits;      // stamp bits of packed slots; 0 = wide HSlot
+    u32 pad;
+};
+inline u64 loop_slot_bytes(u32 sbits) { return sbits ? 8 : sizeof(HSlot); }
+// Stamp bits for keys of `key_bits` bits (0: wide slots).
+inline u32 loop_stamp_bits(u32 key_bits) {
+    const u32 spare = key_bits >= 64 ? 0 : 64 - key_bits;
+    return spare >= 8 ? (spare > 24 ? 24 : spare) : 0;
+}
+
+// Per-step buffers: row_start / row_off hold rows_cap entries, splits the
+// merge-path split of every materialize tile (splits_cap entries).
+struct LoopStepBufs {
+    u64* row_start;
+    u64* row_off;
+    u64 rows_cap;
+    u64* splits;
+    u64 splits_cap;
+};
+
+// Candidate bound of the final steps -> overflow check of every head.
+struct LoopGateDesc {
+    u32 nfinal;
+    u32 final_step[kLoopMaxSteps];
+    u32 final_head[kLoopMaxSteps];
+    u64 log_cap[kLoopMaxHeads];
+    u64 tab_limit[kLoopMaxHeads];
+    u32 stamp_max;  // largest stamp every head's slots can hold
+};
+
+struct LoopEndDesc {
+    LoopHist hist;
+    unsigned long long cond;  // cudaGraphConditionalHandle
+    int use_cond;
+};
+
+// ---- launchers (loop.cu); all stream-ordered on `s`, no host sync ----
+int loop_grid(const Ctx& c);
+// Kernel occupancies (called once before the first launch or capture).
+void loop_prepare();
+void loop_table_clear(Ctx& c, void* tab, u64 cap, u32 sbits);
+// Inserts keys (unique) into an empty table (stamp 0).
+void loop_table_fill(Ctx& c, void* tab, u64 cap, u32 sbits, const u64* keys, u64 n);
+
+// One HISA probe per outer row: row_start, counts (into row_off), per-CTA sums.
+void loop_probe(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const DevJoin& jd,
+                const IndexView<u64>* ix, u64 inner_n, const LoopStepBufs& sb, u64* block_sums);
+// Exclusive scan of the counts + the materialize splits; when `gate` is
+// non-null the last CTA also runs the gate (it must be the iteration's last
+// candidate-producing launch).
+void loop_scan(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const LoopStepBufs& sb,
+               const u64* block_sums, const LoopGateDesc* gate);
+void loop_gate(Ctx& c, cudaStream_t s, LoopCtl* ctl, const LoopGateDesc& g);
+void loop_materialize_temp(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o,
+                           const u64* inner, const DevJoin& jd, const LoopStepBufs& sb, u64* temp, u64 temp_cap);
+// Candidate bound of a select (nsteps == 0) final step = its outer rows.
+void loop_select_cand(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o);
+// Final steps; when `end` is non-null the last CTA records the iteration.
+void loop_materialize_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
+                             const u64* inner, const DevJoin& jd, const LoopStepBufs& sb,
+                             const LoopHeadBufs& hb, const LoopEndDesc* end);
+void loop_select_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
+                        const DevJoin& jd, const LoopHeadBufs& hb, const LoopEndDesc* end);
+// Records the iteration (or rolls it back on overflow) and sets the graph's
+// while-condition (cond ignored unless use_cond).
+void loop_end(Ctx& c, cudaStream_t s, LoopCtl* ctl, const LoopEndDesc& end);
+
+}  // namespace gd

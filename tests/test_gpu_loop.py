@@ -1,0 +1,112 @@
+"""The resident device loop (csrc/loop.cu) against the
+host-driven loop and the reference engine: graph (device-side `while`),
+eager and host-driven modes give byte-identical relations, identical Δ
+histories, iteration records and accountant statistics; GD_LOOP_TINY=1
+starts every capacity at its minimum so every overflow -> rollback ->
+grow -> re-run path runs.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2311_02206_b200 import arraylog as al
+from tests.helpers import chain_edges, program_from_ref, rows
+from tests.test_gpu_engine import CUSTOM, assert_same, corpus, run_gpu, run_ref
+
+pytestmark = pytest.mark.gpu
+
+MODES = {
+    "graph": {},
+    "eager": {"GD_LOOP_MODE": "eager"},
+    "tiny": {"GD_LOOP_TINY": "1"},
+    "tiny_eager": {"GD_LOOP_TINY": "1", "GD_LOOP_MODE": "eager"},
+    "host": {"GD_LOOP": "0"},
+}
+
+
+class env:
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update(self.kv)
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def run_mode(mode, program, db):
+    with env(**MODES[mode]):
+        return run_gpu(program, db)
+
+
+def c1_edges(ref):
+    import ctypes as C
+    raw = np.zeros((10000, 2), dtype=np.uint64)
+    assert ref.lib.ref_gen_tc_rand(C.c_uint64(10000), C.c_uint64(10000), C.c_uint64(1),
+                                   raw.ctypes.data_as(C.c_void_p)) == 0
+    return raw
+
+
+@pytest.mark.parametrize("mode", sorted(MODES))
+def test_c1_all_modes(ref, mode):
+    raw = c1_edges(ref)
+    g = run_mode(mode, "reach", {"Edge": raw})
+    assert g.relation("Reach").count() == 198733
+    assert g.stats().iterations == 46
+    assert g.iter_log("Reach")[:3] == [(9999, 10018, 10017, 10008, 20007), (10008, 9999, 9998, 9996, 30003),
+                                       (9996, 10013, 10012, 10004, 40007)]
+    assert_same(g, run_ref(ref, "reach", {"Edge": raw}), ["Reach"])
+    assert g.raw_stats().join_tuples == 190496  # SURVEY §6 probe: ΣJ over 46 iterations
+
+
+@pytest.mark.parametrize("mode", ["graph", "tiny", "eager"])
+@pytest.mark.parametrize("idx", [0, 17, 55])
+def test_sg_corpus_modes(ref, mode, idx):
+    g, _ = corpus(ref, 1, idx)
+    assert_same(run_mode(mode, "sg", {"Edge": g}), run_ref(ref, "sg", {"Edge": g}), ["SG"])
+
+
+@pytest.mark.parametrize("mode", ["graph", "tiny"])
+@pytest.mark.parametrize("case", sorted(CUSTOM))
+def test_custom_programs_modes(ref, mode, case):
+    src, db = CUSTOM[case]
+    r = run_ref(ref, src, db)
+    prog = program_from_ref(r)
+    assert_same(run_mode(mode, prog, db), r, prog.idbs)
+
+
+@pytest.mark.parametrize("mode", ["graph", "tiny"])
+def test_long_chain_many_iterations(ref, mode):
+    """1200-node path: 1199 iterations (> the initial history capacity)."""
+    e = chain_edges(1200)
+    g = run_mode(mode, "reach", {"Edge": e})
+    assert g.stats().iterations == 1199
+    assert g.relation("Reach").count() == 1199 * 1200 // 2
+    assert_same(g, run_ref(ref, "reach", {"Edge": e}), ["Reach"])
+
+
+def test_modes_agree_on_power_law(ref):
+    from paper_2311_02206_b200 import workloads as W
+    e = W.tc_pl(20000, 20000, 100, 1.05, 3)
+    outs = {m: run_mode(m, "reach", {"Edge": e}) for m in ("graph", "host", "tiny")}
+    base = outs["host"]
+    for m, g in outs.items():
+        assert np.array_equal(g.relation("Reach").data, base.relation("Reach").data), m
+        assert g.iter_log("Reach") == base.iter_log("Reach"), m
+        assert g.raw_stats().charge_events == base.raw_stats().charge_events, m
+        assert g.raw_stats().peak_tracked_bytes == base.raw_stats().peak_tracked_bytes, m
+    assert_same(base, run_ref(ref, "reach", {"Edge": e}), ["Reach"])
+
+
+def test_repeated_engines_reuse_context(ref):
+    e = rows([1, 2, 2, 3, 3, 4, 4, 1], 2)
+    for _ in range(3):
+        g = run_gpu("reach", {"Edge": e})
+        assert g.relation("Reach").count() == 16

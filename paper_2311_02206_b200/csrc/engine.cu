@@ -417,7 +417,8 @@ public:
         }
     };
     // Linear probing stays short (~1.5 slot reads per new key with the
-    // sector scan) at load <= 1/2; tables grow to load 1/3.
+    // sector scan) at load <= 1/2; a full table grows 3x (to load 1/6), so
+    // the re-spreads move about half the final key count in total.
     static u64 tab_limit_of(u64 cap) { return cap / 2; }
 
     void iterate_loop(const std::vector<u32>& rec, const std::vector<u32>& by_name) {
@@ -695,6 +696,8 @@ public:
 
         u64 rollbacks = 0;
         u32 done_iters = 0;
+        const bool trace = getenv("GD_LOOP_TRACE") && getenv("GD_LOOP_TRACE")[0] == '1';
+        double tlast = 0;
         {
             PhaseTimer t(E, "join");
             for (;;) {
@@ -712,6 +715,8 @@ public:
                 done_iters = hc->iter;
                 if (c.prof.on) c.prof.resolve();
                 if (hc->overflow) {
+                    // growth / restamp time is index (HISA) build time
+                    PhaseTimer tg(E, "index");
                     ++rollbacks;
                     for (u32 i = 0; i < ns; ++i) {
                         LStep& L = steps[i];
@@ -733,17 +738,32 @@ public:
                     for (u32 h = 0; h < nh; ++h) {
                         LHead& H = heads[h];
                         const u64 ln = hc->h[h].log_n;
+                        auto tr = [&](const char* what, u64 a, u64 b2) {
+                            if (!trace) return;
+                            c.sync();
+                            const double t1 = Ctx::now_s();
+                            fprintf(stderr, "[loop] iter %u %s %llu -> %llu: %.3f ms\n", hc->iter, what,
+                                    (unsigned long long)a, (unsigned long long)b2, (t1 - tlast) * 1e3);
+                            tlast = t1;
+                        };
+                        if (trace) { c.sync(); tlast = Ctx::now_s(); }
                         if (hc->need_log[h] > H.log_cap) {
-                            const u64 cap = hc->need_log[h] + hc->need_log[h] / 2;
+                            const u64 cap = 2 * hc->need_log[h];
                             DevBuf<u64> nl(c, cap);
                             if (ln) c.d2d(nl.p, H.log.p, ln * sizeof(u64));
                             H.log = std::move(nl);
+                            tr("log", H.log_cap, cap);
                             H.log_cap = cap;
                         }
-                        if (hc->need_tab[h] > H.tab_limit || hc->need_restamp) {
-                            // grow and/or restart the stamp epoch: rebuild from the log
-                            H.alloc_tab(c, hc->need_tab[h] > H.tab_limit ? 3 * hc->need_tab[h] : H.tab_cap);
-                            loop_table_fill(c, H.tab.p, H.tab_cap, H.sbits, H.log.p, ln);
+                        if (hc->need_tab[h] > H.tab_limit) {  // grow: stream the old table into the new
+                            DevBuf<u64> old = std::move(H.tab);
+                            const u64 old_cap = H.tab_cap;
+                            H.alloc_tab(c, 6 * hc->need_tab[h]);  // load 1/6 after growth
+                            tr("tab-alloc+clear", old_cap, H.tab_cap);
+                            loop_table_rehash(c, old.p, old_cap, H.tab.p, H.tab_cap, H.sbits);
+                            tr("tab-rehash", old_cap, H.tab_cap);
+                        } else if (hc->need_restamp) {
+                            loop_table_restamp(c, H.tab.p, H.tab_cap, H.sbits);
                         }
                         hc->need_log[h] = hc->need_tab[h] = 0;
                     }
@@ -763,6 +783,7 @@ public:
                     hc->need_restamp = 0;
                     hc->overflow = 0;
                     c.h2d(ctl.p, hc, sizeof(LoopCtl));
+                    c.sync();
                     destroy_graph();
                     continue;
                 }

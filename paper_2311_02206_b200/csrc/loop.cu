@@ -681,6 +681,64 @@ __global__ void table_fill_kernel(void* tab, u64 cap, u32 sb, const u64* __restr
     }
 }
 
+// Growth: re-spread the old table into a larger one.  Home positions are
+// umul64hi(hash, cap), monotone in the hash, and linear probing keeps each
+// run in home order, so a contiguous run of old slots lands on a nearly
+// contiguous run of new slots.  Each thread moves its own run of kRun old
+// slots, so the CASes of a warp do not pile onto the same lines and every
+// thread streams through both tables.  Stamps restart at 0 (growth happens
+// between iterations).
+constexpr u64 kRun = 32;
+__global__ void table_rehash_kernel(const void* old_tab, u64 old_cap, void* tab, u64 cap, u32 sb) {
+    const u64 runs = (old_cap + kRun - 1) / kRun;
+    for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < runs; r += (u64)gridDim.x * blockDim.x) {
+        const u64 end = min(old_cap, (r + 1) * kRun);
+        // [blk, pos) is a range of slots known to be occupied (this thread's
+        // placements and the occupied slots its probes stepped over): a key
+        // whose home falls inside it may start probing at pos — no empty
+        // slot lies between its home and its placement, so lookups find it.
+        u64 blk = 0, pos = 0;
+        for (u64 i = r * kRun; i < end; ++i) {
+            const u64 w = sb ? __ldcs(static_cast<const u64*>(old_tab) + i)
+                             : __ldcs(&static_cast<const HSlot*>(old_tab)[i].key);
+            if (w == kEmptySlot) continue;
+            const u64 key = sb ? w >> sb : w;
+            const u64 home = hs_home(key, cap);
+            const bool inside = blk <= home && home < pos;
+            const u64 start = inside ? pos : home;
+            u64 p = start;
+            while (true) {
+                u64* t = sb ? static_cast<u64*>(tab) + p : &static_cast<HSlot*>(tab)[p].key;
+                if (atomicCAS(t, kEmptySlot, sb ? key << sb : key) == kEmptySlot) {
+                    if (!sb) static_cast<HSlot*>(tab)[p].stamp = 0;
+                    break;
+                }
+                p = p + 1 == cap ? 0 : p + 1;
+            }
+            if (p + 1 == cap || p < start) {  // wrapped: forget the range
+                blk = pos = 0;
+            } else {
+                if (!inside) blk = home;  // [home, p] occupied now
+                pos = p + 1;
+            }
+        }
+    }
+}
+
+// New stamp epoch in place: every stamp back to 0.
+__global__ void table_restamp_kernel(void* tab, u64 cap, u32 sb) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (u64)gridDim.x * blockDim.x) {
+        if (sb) {
+            u64* t = static_cast<u64*>(tab) + i;
+            const u64 w = *t;
+            if (w != kEmptySlot) *t = w >> sb << sb;
+        } else {
+            HSlot& h = static_cast<HSlot*>(tab)[i];
+            if (h.key != kEmptySlot) h.stamp = 0;
+        }
+    }
+}
+
 template <typename Kern>
 int occupancy(Kern k, size_t smem = 0) {
     int b = 0;
@@ -707,6 +765,20 @@ void loop_table_fill(Ctx& c, void* tab, u64 cap, u32 sbits, const u64* keys, u64
     if (n == 0) return;
     const int grid = (int)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)c.num_sms * 16));
     table_fill_kernel<<<grid, 256, 0, c.stream>>>(tab, cap, sbits, keys, n);
+    c.check_launch();
+}
+
+void loop_table_rehash(Ctx& c, const void* old_tab, u64 old_cap, void* tab, u64 cap, u32 sbits) {
+    if (old_cap == 0) return;
+    const u64 runs = (old_cap + kRun - 1) / kRun;
+    const int grid = (int)std::max<u64>(1, std::min<u64>((runs + 255) / 256, (u64)c.num_sms * 16));
+    table_rehash_kernel<<<grid, 256, 0, c.stream>>>(old_tab, old_cap, tab, cap, sbits);
+    c.check_launch();
+}
+
+void loop_table_restamp(Ctx& c, void* tab, u64 cap, u32 sbits) {
+    const int grid = (int)std::max<u64>(1, std::min<u64>((cap + 255) / 256, (u64)c.num_sms * 16));
+    table_restamp_kernel<<<grid, 256, 0, c.stream>>>(tab, cap, sbits);
     c.check_launch();
 }
 

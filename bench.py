@@ -272,7 +272,7 @@ def main():
                 roof["traffic"] = d.get("dram_bytes")
                 roof["traffic_algo_bytes"] = d.get("algo_bytes")
                 roof["traffic_source"] = d.get("source")
-        jm = [k for k in ("join_probe", "join_materialize", "diff_merge", "difference")]
+        jm = [k for k in ("join_probe", "join_materialize", "join_insert", "diff_merge", "difference")]
         jm_ms = sum(prof[k][0] for k in jm)
         jm_by = sum(prof[k][2] for k in jm)
         roof["join_merge"] = {"achieved": jm_by / (jm_ms / 1e3) / 1e9 if jm_ms else 0.0,

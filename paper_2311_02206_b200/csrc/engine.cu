@@ -395,6 +395,8 @@ public:
         DevJoin jd{};
         bool has_iv = false;
         IndexView<u64> iv{};
+        DevBuf<u32> dense;  // dense (CSR) form of the inner's index, if built
+        LoopDense dv{nullptr, 0, 0};
         const u64* inner = nullptr;
         u64 inner_n = 0;
         u32 proj_arity = 0;
@@ -507,6 +509,9 @@ public:
                         L.has_iv = true;
                         L.iv = IndexView<u64>{cp.index.slots.p, cp.index.slot_count, L.inner, L.inner_n, iar, bits,
                                               st.join_column_count};
+                        if (st.join_column_count == 1 && !(getenv("GD_DENSE") && getenv("GD_DENSE")[0] == '0') &&
+                            loop_dense_build(c, L.inner, L.inner_n, iar, bits, L.dense, L.dv.lo, L.dv.span))
+                            L.dv.off = L.dense.p;
                     }
                     cur_ar = st.proj_arity;
                     for (u32 i = 0; i < kMaxArity; ++i) cur_perm[i] = i;
@@ -570,6 +575,14 @@ public:
         // launched eagerly when profiling).  The gate runs in the last CTA
         // of the last scan and loop_end in the last CTA of the last insert
         // when the sequence allows it.
+        // (profiler record, kind, step): algorithmic bytes are patched in
+        // after the iteration, once its sizes are known (eager mode only)
+        struct ProfRec {
+            long rec;
+            int kind;  // 0 probe, 1 temp, 2 insert, 3 select insert
+            u32 step;
+        };
+        std::vector<ProfRec> prof_recs;
         auto record_iteration = [&](cudaStream_t s, bool use_cond, unsigned long long cond) {
             auto br = [&]() { return c.prof_begin(); };
             LoopGateDesc g{};
@@ -596,15 +609,16 @@ public:
                     continue;
                 }
                 cudaEvent_t t = br();
-                loop_probe(c, s, ctl.p, i, o, L.jd, L.has_iv ? &L.iv : nullptr, L.inner_n, L.bufs(), block_sums.p);
-                c.prof_end(t, KC_PROBE, 0);
+                loop_probe(c, s, ctl.p, i, o, L.jd, L.has_iv ? &L.iv : nullptr, L.dv, L.inner_n, L.bufs(),
+                           block_sums.p);
+                prof_recs.push_back({c.prof_end(t, KC_PROBE, 0), 0, i});
                 t = br();
                 loop_scan(c, s, ctl.p, i, o, L.bufs(), block_sums.p, fuse_gate && i + 1 == ns ? &g : nullptr);
                 c.prof_end(t, KC_SELECT, 0);
                 if (!L.final) {
                     t = br();
                     loop_materialize_temp(c, s, ctl.p, i, o, L.inner, L.jd, L.bufs(), L.temp.p, L.temp_cap);
-                    c.prof_end(t, KC_MATERIALIZE, 0);
+                    prof_recs.push_back({c.prof_end(t, KC_MATERIALIZE, 0), 1, i});
                 }
             }
             if (!fuse_gate) {
@@ -626,7 +640,7 @@ public:
                     loop_select_insert(c, s, ctl.p, i, L.head, o, L.jd, bufs_of(L.head), e);
                 else
                     loop_materialize_insert(c, s, ctl.p, i, L.head, o, L.inner, L.jd, L.bufs(), bufs_of(L.head), e);
-                c.prof_end(t, KC_INSERT, 0);
+                prof_recs.push_back({c.prof_end(t, KC_INSERT, 0), L.select ? 3 : 2, i});
             }
         };
 
@@ -697,11 +711,14 @@ public:
         u64 rollbacks = 0;
         u32 done_iters = 0;
         const bool trace = getenv("GD_LOOP_TRACE") && getenv("GD_LOOP_TRACE")[0] == '1';
+        std::vector<u64> prev_log_n(nh);
+        for (u32 h = 0; h < nh; ++h) prev_log_n[h] = hc->h[h].log_n;
         double tlast = 0;
         {
             PhaseTimer t(E, "join");
             for (;;) {
                 if (eager) {
+                    prof_recs.clear();
                     record_iteration(c.stream, false, 0);
                 } else {
                     if (!exec) build_graph();
@@ -713,7 +730,30 @@ public:
                     c.launches += kernels_per_iter * (batch ? (u64)batch_n
                                                             : hc->iter - done_iters + (hc->overflow ? 1 : 0));
                 done_iters = hc->iter;
-                if (c.prof.on) c.prof.resolve();
+                if (c.prof.on) {
+                    // algorithmic bytes: probe = outer key + one
+                    // index slot per row; temp = inner row read + row written;
+                    // insert = inner row + one membership slot per candidate,
+                    // plus the new rows appended (charged to the head's first
+                    // final step)
+                    std::vector<bool> charged(nh, false);
+                    for (const ProfRec& pr : prof_recs) {
+                        const LStep& L = steps[pr.step];
+                        u64 by = 0;
+                        if (pr.kind == 0) by = hc->step_n[pr.step] * (8 + (L.has_iv ? sizeof(Slot) : 0));
+                        else if (pr.kind == 1) by = hc->step_cand[pr.step] * 16;
+                        else {
+                            by = hc->step_cand[pr.step] * (pr.kind == 2 ? 16 : 16);
+                            if (!charged[L.head]) {
+                                charged[L.head] = true;
+                                by += (hc->h[L.head].log_n - prev_log_n[L.head]) * 8;
+                            }
+                        }
+                        c.prof_add_bytes(pr.rec, by);
+                    }
+                    for (u32 h = 0; h < nh; ++h) prev_log_n[h] = hc->h[h].log_n;
+                    c.prof.resolve();
+                }
                 if (hc->overflow) {
                     // growth / restamp time is index (HISA) build time
                     PhaseTimer tg(E, "index");

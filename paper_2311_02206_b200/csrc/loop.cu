@@ -307,8 +307,8 @@ __device__ void end_body(LoopCtl* ctl, const LoopEndDesc& e) {
 // ---- kernels ----------------------------------------------------------------
 
 __global__ void __launch_bounds__(kLT) loop_probe_kernel(LoopCtl* ctl, u32 step, LoopOuter o, DevJoin jd,
-                                                         IndexView<u64> ix, u64 inner_n, LoopStepBufs sb,
-                                                         u64* __restrict__ block_sums) {
+                                                         IndexView<u64> ix, LoopDense dense, u64 inner_n,
+                                                         LoopStepBufs sb, u64* __restrict__ block_sums) {
     __shared__ u64 red[kLT / 32];
     __shared__ u32 s_flag;
     if (cta_stopped(ctl, &s_flag)) return;
@@ -344,12 +344,31 @@ __global__ void __launch_bounds__(kLT) loop_probe_kernel(LoopCtl* ctl, u32 step,
             continue;
         }
         u64 pre[kLItems];
-        Slot s[kLItems];
 #pragma unroll
         for (int j = 0; j < kLItems; ++j) {
             const u64 r = base + (u64)j * kLT;
             pre[j] = r < end ? outer_prefix(jd, outer[r]) : 0ull;
         }
+        if (dense.off) {
+            u32 a[kLItems], b[kLItems];
+#pragma unroll
+            for (int j = 0; j < kLItems; ++j) {
+                const u64 q = pre[j] - dense.lo;
+                const bool in = q < dense.span;
+                a[j] = in ? __ldg(dense.off + q) : 0u;
+                b[j] = in ? __ldg(dense.off + q + 1) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < kLItems; ++j) {
+                const u64 r = base + (u64)j * kLT;
+                if (r >= end) continue;
+                row_start[r] = a[j];
+                row_cnt[r] = b[j] - a[j];
+                sum += b[j] - a[j];
+            }
+            continue;
+        }
+        Slot s[kLItems];
 #pragma unroll
         for (int j = 0; j < kLItems; ++j) s[j] = ix.slots[slot_home(pre[j], ix.slot_count)];
 #pragma unroll
@@ -783,11 +802,44 @@ void loop_table_restamp(Ctx& c, void* tab, u64 cap, u32 sbits) {
 }
 
 void loop_probe(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const DevJoin& jd,
-                const IndexView<u64>* ix, u64 inner_n, const LoopStepBufs& sb, u64* block_sums) {
+                const IndexView<u64>* ix, const LoopDense& dense, u64 inner_n, const LoopStepBufs& sb,
+                u64* block_sums) {
     IndexView<u64> v{};
     if (ix) v = *ix;
-    loop_probe_kernel<<<loop_grid(c), kLT, 0, s>>>(ctl, step, o, jd, v, inner_n, sb, block_sums);
+    loop_probe_kernel<<<loop_grid(c), kLT, 0, s>>>(ctl, step, o, jd, v, dense, inner_n, sb, block_sums);
     c.check_launch();
+}
+
+namespace {
+// off[q] = lower_bound of prefix lo + q among the sorted rows (q in [0, span]).
+__global__ void dense_offsets_kernel(const u64* __restrict__ rows, u64 n, u32 arity, u32 bits, u64 lo, u64 span,
+                                     u32* __restrict__ off) {
+    for (u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x; q <= span; q += (u64)gridDim.x * blockDim.x) {
+        const u64 p = lo + q;
+        u64 a = 0, b = n;
+        while (a < b) {
+            const u64 m = (a + b) >> 1;
+            if (prefix_of(rows[m], arity, bits, 1) < p) a = m + 1;
+            else b = m;
+        }
+        off[q] = (u32)a;
+    }
+}
+}  // namespace
+
+bool loop_dense_build(Ctx& c, const u64* rows, u64 n, u32 arity, u32 bits, DevBuf<u32>& off, u64& lo, u64& span) {
+    if (n == 0 || n >= (1ull << 32)) return false;
+    unsigned long long first = 0, last = 0;
+    c.read2(&first, rows, &last, rows + (n - 1));
+    lo = prefix_of(first, arity, bits, 1);
+    const u64 hi = prefix_of(last, arity, bits, 1);
+    span = hi - lo + 1;
+    if (span > 4 * n + 4096) return false;
+    off = DevBuf<u32>(c, span + 1);
+    const int grid = (int)std::max<u64>(1, std::min<u64>((span + 256) / 256, (u64)c.num_sms * 16));
+    dense_offsets_kernel<<<grid, 256, 0, c.stream>>>(rows, n, arity, bits, lo, span, off.p);
+    c.check_launch();
+    return true;
 }
 
 void loop_scan(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const LoopStepBufs& sb,

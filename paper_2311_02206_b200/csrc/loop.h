@@ -110,6 +110,20 @@ inline u32 loop_stamp_bits(u32 key_bits) {
     return spare >= 8 ? (spare > 24 ? 24 : spare) : 0;
 }
 
+// Dense form of a static inner's HISA index (join prefix of one column whose
+// values span at most a few times the row count): off[p - lo] = first row
+// with prefix p, off[span] = n.  A probe is one 8-byte L2-resident read
+// instead of a random slot of the hash table; ranges equal range_lookup's.
+struct LoopDense {
+    const u32* off;  // nullptr: use the hash index
+    u64 lo;
+    u64 span;
+};
+// Builds the dense form when worthwhile (span <= 4n + 4096, n < 2^32);
+// returns false otherwise.
+bool loop_dense_build(Ctx& c, const u64* rows, u64 n, u32 arity, u32 bits, DevBuf<u32>& off, u64& lo,
+                      u64& span);
+
 // Per-step buffers: row_start / row_off hold rows_cap entries, splits the
 // merge-path split of every materialize tile (splits_cap entries).
 struct LoopStepBufs {
@@ -150,7 +164,8 @@ void loop_table_restamp(Ctx& c, void* tab, u64 cap, u32 sbits);
 
 // One HISA probe per outer row: row_start, counts (into row_off), per-CTA sums.
 void loop_probe(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const DevJoin& jd,
-                const IndexView<u64>* ix, u64 inner_n, const LoopStepBufs& sb, u64* block_sums);
+                const IndexView<u64>* ix, const LoopDense& dense, u64 inner_n, const LoopStepBufs& sb,
+                u64* block_sums);
 // Exclusive scan of the counts + the materialize splits; when `gate` is
 // non-null the last CTA also runs the gate (it must be the iteration's last
 // candidate-producing launch).

@@ -22,6 +22,7 @@ MODES = {
     "tiny": {"GD_LOOP_TINY": "1"},
     "tiny_eager": {"GD_LOOP_TINY": "1", "GD_LOOP_MODE": "eager"},
     "host": {"GD_LOOP": "0"},
+    "hashindex": {"GD_DENSE": "0"},
 }
 
 
@@ -66,7 +67,7 @@ def test_c1_all_modes(ref, mode):
     assert g.raw_stats().join_tuples == 190496  # SURVEY §6 probe: ΣJ over 46 iterations
 
 
-@pytest.mark.parametrize("mode", ["graph", "tiny", "eager"])
+@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "hashindex"])
 @pytest.mark.parametrize("idx", [0, 17, 55])
 def test_sg_corpus_modes(ref, mode, idx):
     g, _ = corpus(ref, 1, idx)
@@ -95,7 +96,7 @@ def test_long_chain_many_iterations(ref, mode):
 def test_modes_agree_on_power_law(ref):
     from paper_2311_02206_b200 import workloads as W
     e = W.tc_pl(20000, 20000, 100, 1.05, 3)
-    outs = {m: run_mode(m, "reach", {"Edge": e}) for m in ("graph", "host", "tiny")}
+    outs = {m: run_mode(m, "reach", {"Edge": e}) for m in ("graph", "host", "tiny", "hashindex")}
     base = outs["host"]
     for m, g in outs.items():
         assert np.array_equal(g.relation("Reach").data, base.relation("Reach").data), m

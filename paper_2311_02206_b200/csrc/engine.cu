@@ -387,6 +387,9 @@ public:
     struct LStep {
         u32 plan = 0, var = 0;
         bool final = false, select = false;
+        // GD_LOOP_SPLIT=1: materialize the final step's rows, then insert
+        // them (comparison mode; the fused kernel moves fewer bytes)
+        bool split_insert = false;
         u32 head = 0;            // loop-head index (final steps)
         u32 kind = LO_STATIC;    // outer source
         u32 src_head = 0, src_step = 0;
@@ -472,6 +475,7 @@ public:
                     L.plan = pi;
                     L.var = v;
                     L.final = s + 1 == n;
+                    L.split_insert = getenv("GD_LOOP_SPLIT") && getenv("GD_LOOP_SPLIT")[0] == '1';
                     L.head = head_of(p.head_rel);
                     if (s == 0) {
                         auto it = std::find(rec.begin(), rec.end(), var.src_rel);
@@ -528,7 +532,7 @@ public:
                 L.row_off = DevBuf<u64>(c, L.rows_cap);
                 L.splits = DevBuf<u64>(c, L.splits_cap);
             }
-            if (!L.final) {
+            if (!L.final || (L.split_insert && !L.select)) {  // chain temps / split-insert input
                 L.temp_cap = tiny ? 1 : std::max<u64>(4 * d0, 1 << 16);
                 L.temp = DevBuf<u64>(c, L.temp_cap);
             }
@@ -615,7 +619,7 @@ public:
                 t = br();
                 loop_scan(c, s, ctl.p, i, o, L.bufs(), block_sums.p, fuse_gate && i + 1 == ns ? &g : nullptr);
                 c.prof_end(t, KC_SELECT, 0);
-                if (!L.final) {
+                if (!L.final || L.split_insert) {
                     t = br();
                     loop_materialize_temp(c, s, ctl.p, i, o, L.inner, L.jd, L.bufs(), L.temp.p, L.temp_cap);
                     prof_recs.push_back({c.prof_end(t, KC_MATERIALIZE, 0), 1, i});
@@ -638,6 +642,8 @@ public:
                 cudaEvent_t t = br();
                 if (L.select)
                     loop_select_insert(c, s, ctl.p, i, L.head, o, L.jd, bufs_of(L.head), e);
+                else if (L.split_insert)
+                    loop_insert_keys(c, s, ctl.p, i, L.head, L.temp.p, bufs_of(L.head), e);
                 else
                     loop_materialize_insert(c, s, ctl.p, i, L.head, o, L.inner, L.jd, L.bufs(), bufs_of(L.head), e);
                 prof_recs.push_back({c.prof_end(t, KC_INSERT, 0), L.select ? 3 : 2, i});
@@ -743,7 +749,8 @@ public:
                         if (pr.kind == 0) by = hc->step_n[pr.step] * (8 + (L.has_iv ? sizeof(Slot) : 0));
                         else if (pr.kind == 1) by = hc->step_cand[pr.step] * 16;
                         else {
-                            by = hc->step_cand[pr.step] * (pr.kind == 2 ? 16 : 16);
+                            // one key read (kind 2: materialized row; 3: outer row) + one slot
+                            by = hc->step_cand[pr.step] * 16;
                             if (!charged[L.head]) {
                                 charged[L.head] = true;
                                 by += (hc->h[L.head].log_n - prev_log_n[L.head]) * 8;

@@ -61,103 +61,101 @@ __device__ __forceinline__ void resolve(const LoopOuter& o, const LoopCtl* ctl, 
 
 __device__ __forceinline__ u64 hs_home(u64 key, u64 cap) { return __umul64hi(fmix64(key ^ kHashSeed), cap); }
 
-// Membership + insertion of PER keys in the head's full-tuple index, the
-// first CAS of every key issued together (independent L2 round trips in
-// flight).  fresh[k]: the key is new (appended to the log by the caller);
-// first[k]: first occurrence of the key in this iteration (stamp `st`) —
-// the distinct count of the join output.
-template <int PER>
-__device__ __forceinline__ void hs_insert_packed(u64* __restrict__ tab, u64 cap, u32 sb, u64 st, const u64 (&key)[PER],
-                                                 const bool (&ok)[PER], bool (&fresh)[PER], bool (&first)[PER]) {
+// Rare paths of a packed-slot insertion, out of line (register pressure of
+// the batched fast path): the key was seen in an earlier iteration (stamp
+// update), or its home slot holds another key (linear probing, kScan slots
+// read per round trip).  o = the value the home-slot CAS returned.
+// Returns bit 0 = new key, bit 1 = first occurrence this iteration.
+__device__ __noinline__ u32 insert_slow_packed(u64* __restrict__ tab, u64 cap, u32 sb, u64 st, u64 key, u64 o) {
     const u64 smask = (1ull << sb) - 1;
-    u64 pos[PER], old[PER];
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-        fresh[k] = first[k] = false;
-        if (ok[k]) {
-            pos[k] = hs_home(key[k], cap);
-            old[k] = atomicCAS(&tab[pos[k]], kEmptySlot, key[k] << sb | st);
+    const u64 want = key << sb | st;
+    u64 p = hs_home(key, cap);
+    while (true) {
+        if (o == kEmptySlot) return 3;
+        if ((o >> sb) == key) {
+            while ((o & smask) != st) {  // seen before, not yet this iteration
+                const u64 o2 = atomicCAS(&tab[p], o, want);
+                if (o2 == o) return 2;
+                o = o2;
+            }
+            return 0;
         }
-    }
+        // collision: read the next kScan slots together (one round trip,
+        // mostly one sector) and CAS only the first candidate
+        u64 w[kScan];
 #pragma unroll
-    for (int k = 0; k < PER; ++k) {
-        if (!ok[k]) continue;
-        const u64 want = key[k] << sb | st;
-        u64 o = old[k];
-        u64 p = pos[k];
-        while (true) {
-            if (o == kEmptySlot) {
-                fresh[k] = first[k] = true;
-                break;
-            }
-            if ((o >> sb) == key[k]) {
-                while ((o & smask) != st) {  // seen before, not yet this iteration
-                    const u64 o2 = atomicCAS(&tab[p], o, want);
-                    if (o2 == o) {
-                        first[k] = true;
-                        break;
-                    }
-                    o = o2;
-                }
-                break;
-            }
-            // collision: read the next kScan slots together (one round trip,
-            // mostly one sector) and CAS only the first candidate
-            u64 w[kScan];
-#pragma unroll
-            for (int q = 0; q < kScan; ++q) {
-                u64 pq = p + 1 + q;
-                pq = pq >= cap ? pq - cap : pq;
-                w[q] = __ldcg(&tab[pq]);
-            }
-            int hit = kScan;
-#pragma unroll
-            for (int q = kScan - 1; q >= 0; --q)
-                if (w[q] == kEmptySlot || (w[q] >> sb) == key[k]) hit = q;
-            p = p + 1 + (hit == kScan ? kScan - 1 : hit);
-            p = p >= cap ? p - cap : p;
-            if (hit == kScan) {  // all kScan occupied by other keys: continue after them
-                o = w[kScan - 1];
-                continue;
-            }
-            o = w[hit] == kEmptySlot ? atomicCAS(&tab[p], kEmptySlot, want) : w[hit];
+        for (int q = 0; q < kScan; ++q) {
+            u64 pq = p + 1 + q;
+            pq = pq >= cap ? pq - cap : pq;
+            w[q] = __ldcg(&tab[pq]);
         }
+        int hit = kScan;
+        u64 wv = w[kScan - 1];
+#pragma unroll
+        for (int q = kScan - 1; q >= 0; --q)
+            if (w[q] == kEmptySlot || (w[q] >> sb) == key) {
+                hit = q;
+                wv = w[q];
+            }
+        p = p + 1 + (hit == kScan ? kScan - 1 : hit);
+        p = p >= cap ? p - cap : p;
+        o = (hit < kScan && wv == kEmptySlot) ? atomicCAS(&tab[p], kEmptySlot, want) : wv;
     }
 }
 
-template <int PER>
-__device__ __forceinline__ void hs_insert_wide(HSlot* __restrict__ tab, u64 cap, u32 st, const u64 (&key)[PER],
-                                               const bool (&ok)[PER], bool (&fresh)[PER], bool (&first)[PER]) {
-    u64 pos[PER], old[PER];
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-        fresh[k] = first[k] = false;
-        if (ok[k]) {
-            pos[k] = hs_home(key[k], cap);
-            old[k] = atomicCAS(&tab[pos[k]].key, kEmptySlot, key[k]);
-        }
+__device__ __noinline__ u32 insert_slow_wide(HSlot* __restrict__ tab, u64 cap, u32 st, u64 key, u64 o) {
+    u64 p = hs_home(key, cap);
+    while (o != kEmptySlot && o != key) {
+        p = p + 1 == cap ? 0 : p + 1;
+        o = atomicCAS(&tab[p].key, kEmptySlot, key);
     }
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-        if (!ok[k]) continue;
-        u64 o = old[k];
-        u64 p = pos[k];
-        while (o != kEmptySlot && o != key[k]) {
-            p = p + 1 == cap ? 0 : p + 1;
-            o = atomicCAS(&tab[p].key, kEmptySlot, key[k]);
-        }
-        fresh[k] = o == kEmptySlot;
-        first[k] = __ldcg(&tab[p].stamp) != st && atomicExch(&tab[p].stamp, st) != st;
-    }
+    const u32 fresh = o == kEmptySlot;
+    const u32 first = __ldcg(&tab[p].stamp) != st && atomicExch(&tab[p].stamp, st) != st;
+    return fresh | first << 1;
 }
 
+// Membership + insertion of PER keys in the head's full-tuple index: the
+// home-slot CAS of every key is issued together (independent L2 round trips
+// in flight); a CAS that finds an empty slot (new key) or this key already
+// stamped with this iteration settles it; anything else takes the slow path.
+// fresh: bit k = key k is new (appended by the caller); first: bit k = first
+// occurrence of key k in this iteration (stamp st) — the distinct count of
+// the join output.
 template <int PER>
-__device__ __forceinline__ void hs_insert(const LoopHeadBufs& hb, u32 st, const u64 (&key)[PER],
-                                          const bool (&ok)[PER], bool (&fresh)[PER], bool (&first)[PER]) {
-    if (hb.sbits)
-        hs_insert_packed<PER>(static_cast<u64*>(hb.tab), hb.tab_cap, hb.sbits, st, key, ok, fresh, first);
-    else
-        hs_insert_wide<PER>(static_cast<HSlot*>(hb.tab), hb.tab_cap, st, key, ok, fresh, first);
+__device__ __forceinline__ void hs_insert(const LoopHeadBufs& hb, u32 st, const u64 (&key)[PER], u32 ok,
+                                          u32& fresh, u32& first) {
+    fresh = first = 0;
+    u64 old[PER];
+    if (hb.sbits) {
+        u64* tab = static_cast<u64*>(hb.tab);
+        const u32 sb = hb.sbits;
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+            old[k] = (ok >> k & 1) ? atomicCAS(&tab[hs_home(key[k], hb.tab_cap)], kEmptySlot, key[k] << sb | st)
+                                   : 0ull;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            if (!(ok >> k & 1)) continue;
+            u32 r;
+            if (old[k] == kEmptySlot) r = 3;
+            else if (old[k] == (key[k] << sb | st)) r = 0;
+            else r = insert_slow_packed(tab, hb.tab_cap, sb, st, key[k], old[k]);
+            fresh |= (r & 1u) << k;
+            first |= (r >> 1) << k;
+        }
+    } else {
+        HSlot* tab = static_cast<HSlot*>(hb.tab);
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+            old[k] = (ok >> k & 1) ? atomicCAS(&tab[hs_home(key[k], hb.tab_cap)].key, kEmptySlot, key[k]) : 0ull;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            if (!(ok >> k & 1)) continue;
+            const u32 r = insert_slow_wide(tab, hb.tab_cap, st, key[k], old[k]);
+            fresh |= (r & 1u) << k;
+            first |= (r >> 1) << k;
+        }
+    }
 }
 
 template <typename T>
@@ -218,10 +216,7 @@ __device__ void gate_body(LoopCtl* ctl, const LoopGateDesc& g) {
     const u32 overflow = __ldcg(&ctl->overflow), done = __ldcg(&ctl->done), iter = __ldcg(&ctl->iter);
     const u32 nh = __ldcg(&ctl->nheads), epoch = __ldcg(&ctl->epoch_base);
     const u64 hist_cap = __ldcg(&ctl->hist_cap);
-    u64 cand[kLoopMaxSteps];
-    for (u32 f = 0; f < g.nfinal; ++f) cand[f] = __ldcg(&ctl->step_cand[g.final_step[f]]);
-    u64 log_n[kLoopMaxHeads];
-    for (u32 h = 0; h < nh; ++h) log_n[h] = __ldcg(&ctl->h[h].log_n);
+    u64 log_n0 = nh ? __ldcg(&ctl->h[0].log_n) : 0;
     if (overflow | done) return;
     if (iter >= hist_cap) {
         ctl->need_hist = hist_cap * 2;
@@ -233,13 +228,13 @@ __device__ void gate_body(LoopCtl* ctl, const LoopGateDesc& g) {
         ctl->overflow = 1;
         return;
     }
-    u64 add[kLoopMaxHeads];
-    for (u32 h = 0; h < kLoopMaxHeads; ++h) add[h] = 0;
-    for (u32 f = 0; f < g.nfinal; ++f) add[g.final_head[f]] += cand[f];
     bool over = false;
     for (u32 h = 0; h < nh; ++h) {
-        ctl->h[h].cand = add[h];
-        const u64 need = log_n[h] + add[h];
+        u64 add = 0;
+        for (u32 f = 0; f < g.nfinal; ++f)
+            if (g.final_head[f] == h) add += __ldcg(&ctl->step_cand[g.final_step[f]]);
+        ctl->h[h].cand = add;
+        const u64 need = (h ? __ldcg(&ctl->h[h].log_n) : log_n0) + add;
         if (need > g.log_cap[h]) {
             ctl->need_log[h] = need;
             over = true;
@@ -267,35 +262,26 @@ __device__ void end_body(LoopCtl* ctl, const LoopEndDesc& e) {
         if (e.use_cond) cudaGraphSetConditional(cond, 0);
         return;
     }
-    u64 dlo[kLoopMaxHeads], dhi[kLoopMaxHeads], J[kLoopMaxHeads], N[kLoopMaxHeads], D[kLoopMaxHeads],
-        ln[kLoopMaxHeads], tot[kLoopMaxSteps];
-    for (u32 h = 0; h < nh; ++h) {
-        dlo[h] = __ldcg(&ctl->h[h].dlo);
-        dhi[h] = __ldcg(&ctl->h[h].dhi);
-        J[h] = __ldcg(&ctl->h[h].J);
-        N[h] = __ldcg(&ctl->h[h].N);
-        D[h] = __ldcg(&ctl->h[h].D);
-        ln[h] = __ldcg(&ctl->h[h].log_n);
-    }
-    for (u32 s = 0; s < ns; ++s) tot[s] = __ldcg(&ctl->step_total[s]);
     const u64 i = iter;
     bool active = false;
-    for (u32 h = 0; h < nh; ++h) {
-        gd_iter_record r;
-        r.delta_in = dhi[h] - dlo[h];
-        r.join = J[h];
-        r.new_unique = N[h];
-        r.delta_out = D[h];
-        r.full_after = ln[h];
-        e.hist.rec[i * nh + h] = r;
+    for (u32 h = 0; h < nh; ++h) {  // a head's fields are loaded together
         LoopHeadState& st = ctl->h[h];
-        st.dlo = dhi[h];
-        st.dhi = ln[h];
-        active |= ln[h] > dhi[h];
+        const u64 dlo = __ldcg(&st.dlo), dhi = __ldcg(&st.dhi), J = __ldcg(&st.J), N = __ldcg(&st.N),
+                  D = __ldcg(&st.D), ln = __ldcg(&st.log_n);
+        gd_iter_record r;
+        r.delta_in = dhi - dlo;
+        r.join = J;
+        r.new_unique = N;
+        r.delta_out = D;
+        r.full_after = ln;
+        e.hist.rec[i * nh + h] = r;
+        st.dlo = dhi;
+        st.dhi = ln;
+        active |= ln > dhi;
         st.cand = st.J = st.N = st.D = 0;
     }
     for (u32 s = 0; s < ns; ++s) {
-        e.hist.steps[i * ns + s] = tot[s];
+        e.hist.steps[i * ns + s] = __ldcg(&ctl->step_total[s]);
         ctl->step_total[s] = 0;
     }
     ctl->iter = iter + 1;
@@ -580,37 +566,69 @@ __global__ void loop_select_cand_kernel(LoopCtl* ctl, u32 step, LoopOuter o) {
     ctl->step_cand[step] = n;
 }
 
-// Appends this thread's new keys to the head's log (one atomic per CTA).
+// Appends the CTA's new keys of one tile to the log: one atomic per CTA and
+// tile on the shared counter (per-warp atomics contend on it), warp ballots
+// + an 8-entry scan for the positions.
 template <int PER>
-__device__ __forceinline__ void append_block(LoopCtl* ctl, u32 head, u64* __restrict__ log, const u64 (&keys)[PER],
-                                             const bool (&fresh)[PER], u64 cnt, u64 J, u64 N, u32 step,
-                                             u64* s_scan, u64* s_base, u64* red) {
-    u64 tot;
-    const u64 ex = block_exclusive_scan<u64, kLT>(cnt, tot, s_scan);
-    const u64 j = block_sum(J, red);
-    const u64 nn = block_sum(N, red);
+__device__ __forceinline__ void append_cta(u64* __restrict__ log, unsigned long long* log_n, const u64 (&key)[PER],
+                                           u32 fresh, u32* s_warp, u64* s_base) {
+    constexpr int W = kLT / 32;
+    u32 m[PER];
+    u32 tot = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        m[k] = __ballot_sync(0xffffffffu, fresh >> k & 1);
+        tot += __popc(m[k]);
+    }
+    const u32 warp = threadIdx.x >> 5;
+    if (lane_id() == 0) s_warp[warp] = tot;
+    __syncthreads();
     if (threadIdx.x == 0) {
-        *s_base = tot ? atomicAdd(&ctl->h[head].log_n, tot) : 0;
-        if (tot) atomicAdd(&ctl->h[head].D, tot);
-        if (j) {
-            atomicAdd(&ctl->h[head].J, j);
-            atomicAdd(&ctl->step_total[step], j);
+        u32 all = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const u32 c = s_warp[w];
+            s_warp[w] = all;
+            all += c;
         }
-        if (nn) atomicAdd(&ctl->h[head].N, nn);
+        *s_base = all ? atomicAdd(log_n, (unsigned long long)all) : 0;
     }
     __syncthreads();
-    u64 p = *s_base + ex;
+    u64 base = *s_base + s_warp[warp];
+    const u32 lt = lanemask_lt();
 #pragma unroll
-    for (int k = 0; k < PER; ++k)
-        if (fresh[k]) log[p++] = keys[k];
+    for (int k = 0; k < PER; ++k) {
+        if (fresh >> k & 1) log[base + __popc(m[k] & lt)] = key[k];
+        base += __popc(m[k]);
+    }
 }
 
+// Flushes per-thread J / N / D counts of a CTA (once, at exit).
+__device__ __forceinline__ void flush_counts(LoopCtl* ctl, u32 head, u32 step, u64 J, u64 N, u64 D, u64* red,
+                                             bool step_total = true) {
+    const u64 j = block_sum(J, red);
+    const u64 nn = block_sum(N, red);
+    const u64 d = block_sum(D, red);
+    if (threadIdx.x == 0) {
+        if (j) {
+            atomicAdd(&ctl->h[head].J, j);
+            if (step_total) atomicAdd(&ctl->step_total[step], j);
+        }
+        if (nn) atomicAdd(&ctl->h[head].N, nn);
+        if (d) atomicAdd(&ctl->h[head].D, d);
+    }
+}
+
+// Final step: load-balanced expansion fused with dedup + difference + append
+// (the join rows are never written to HBM).  Each random slot CAS costs a
+// 64-byte line read and write-back, so this kernel runs at the random
+// read-modify-write rate of HBM.
 __global__ void __launch_bounds__(kLT) loop_materialize_insert_kernel(
     LoopCtl* ctl, u32 step, u32 head, LoopOuter o, const u64* __restrict__ inner, DevJoin jd, LoopStepBufs sb,
     LoopHeadBufs hb, LoopEndDesc e, int do_end) {
     __shared__ MatSmem sm;
-    __shared__ u64 s_scan[kLT / 32 + 1];
     __shared__ u64 red[kLT / 32];
+    __shared__ u32 s_warp[kLT / 32];
     __shared__ u64 s_base;
     __shared__ u32 s_flag;
     if (!cta_stopped(ctl, &s_flag)) {
@@ -620,36 +638,71 @@ __global__ void __launch_bounds__(kLT) loop_materialize_insert_kernel(
         const u64 total = ctl->step_cand[step];
         const u32 it = ctl->iter + 1 - ctl->epoch_base;
         const u64 ntiles = total ? (n + total + kLoopMatTile - 1) / kLoopMatTile : 0;
+        u64 J = 0, N = 0, D = 0;
         for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             u64 b0, b1;
             u32 rcount;
             if (!stage_tile(sm, tile, outer, n, total, sb, b0, b1, rcount)) continue;
             u64 key[kPer];
-            bool ok[kPer];
+            u32 ok = 0;
 #pragma unroll
             for (int k = 0; k < kPer; ++k) {
                 const u64 j = b0 + threadIdx.x + (u64)k * kLT;
-                ok[k] = j < b1;
                 key[k] = 0;
-                if (ok[k]) {
+                if (j < b1) {
                     const u32 r = row_of(sm, rcount, j);
                     const u64 ov = sm.outer[r];
                     const u64 i = inner[sm.start[r] + (j - sm.off[r])];
-                    ok[k] = passes(jd, ov, i);
+                    if (passes(jd, ov, i)) ok |= 1u << k;
                     key[k] = project(jd, ov, i);
                 }
             }
-            bool fresh[kPer], first[kPer];
+            u32 fresh, first;
             hs_insert<kPer>(hb, it, key, ok, fresh, first);
-            u64 cnt = 0, J = 0, N = 0;
-#pragma unroll
-            for (int k = 0; k < kPer; ++k) {
-                J += ok[k];
-                cnt += fresh[k];
-                N += first[k];
-            }
-            append_block<kPer>(ctl, head, hb.log, key, fresh, cnt, J, N, step, s_scan, &s_base, red);
+            J += __popc(ok);
+            N += __popc(first);
+            D += __popc(fresh);
+            append_cta<kPer>(hb.log, &ctl->h[head].log_n, key, fresh, s_warp, &s_base);
         }
+        flush_counts(ctl, head, step, J, N, D, red);
+    }
+    if (do_end && last_cta(ctl, &s_flag) && threadIdx.x == 0) end_body(ctl, e);
+}
+
+// Dedup + difference + append of a final step's join rows (materialized in
+// `keys` by loop_materialize_temp): each thread keeps kInsPer CASes in flight
+// (the random-CAS rate needs ~8 K in flight per SM; a fused materialize
+// kernel holds too many registers to get there).
+constexpr int kInsPer = 8;
+__global__ void __launch_bounds__(kLT, 4) loop_insert_keys_kernel(LoopCtl* ctl, u32 step, u32 head,
+                                                                  const u64* __restrict__ keys, LoopHeadBufs hb,
+                                                                  LoopEndDesc e, int do_end) {
+    __shared__ u64 red[kLT / 32];
+    __shared__ u32 s_warp[kLT / 32];
+    __shared__ u64 s_base;
+    __shared__ u32 s_flag;
+    if (!cta_stopped(ctl, &s_flag)) {
+        const u64 n = ctl->step_total[step];
+        const u32 it = ctl->iter + 1 - ctl->epoch_base;
+        constexpr u64 kChunk = (u64)kLT * kInsPer;
+        u64 J = 0, N = 0, D = 0;
+        for (u64 base = (u64)blockIdx.x * kChunk; base < n; base += (u64)gridDim.x * kChunk) {
+            u64 key[kInsPer];
+            u32 ok = 0;
+#pragma unroll
+            for (int k = 0; k < kInsPer; ++k) {
+                const u64 j = base + (u64)k * kLT + threadIdx.x;
+                key[k] = j < n ? __ldcs(keys + j) : 0ull;
+                ok |= (u32)(j < n) << k;
+            }
+            u32 fresh, first;
+            hs_insert<kInsPer>(hb, it, key, ok, fresh, first);
+            J += __popc(ok);
+            N += __popc(first);
+            D += __popc(fresh);
+            append_cta<kInsPer>(hb.log, &ctl->h[head].log_n, key, fresh, s_warp, &s_base);
+        }
+        flush_counts(ctl, head, step, J, N, D, red, false);
     }
     if (do_end && last_cta(ctl, &s_flag) && threadIdx.x == 0) end_body(ctl, e);
 }
@@ -657,8 +710,8 @@ __global__ void __launch_bounds__(kLT) loop_materialize_insert_kernel(
 __global__ void __launch_bounds__(kLT) loop_select_insert_kernel(LoopCtl* ctl, u32 step, u32 head, LoopOuter o,
                                                                  DevJoin jd, LoopHeadBufs hb, LoopEndDesc e,
                                                                  int do_end) {
-    __shared__ u64 s_scan[kLT / 32 + 1];
     __shared__ u64 red[kLT / 32];
+    __shared__ u32 s_warp[kLT / 32];
     __shared__ u64 s_base;
     __shared__ u32 s_flag;
     if (!cta_stopped(ctl, &s_flag)) {
@@ -667,16 +720,20 @@ __global__ void __launch_bounds__(kLT) loop_select_insert_kernel(LoopCtl* ctl, u
         resolve(o, ctl, outer, n);
         const u32 it = ctl->iter + 1 - ctl->epoch_base;
         const u64 ntiles = (n + kLT - 1) / kLT;
+        u64 J = 0, N = 0, D = 0;
         for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const u64 r = tile * kLT + threadIdx.x;
             u64 key[1] = {0};
-            bool ok[1] = {r < n && passes(jd, outer[r], 0ull)};
-            if (ok[0]) key[0] = project(jd, outer[r], 0ull);
-            bool fresh[1], first[1];
+            const u32 ok = r < n && passes(jd, outer[r], 0ull) ? 1u : 0u;
+            if (ok) key[0] = project(jd, outer[r], 0ull);
+            u32 fresh, first;
             hs_insert<1>(hb, it, key, ok, fresh, first);
-            const u64 cnt = fresh[0], J = ok[0], N = first[0];
-            append_block<1>(ctl, head, hb.log, key, fresh, cnt, J, N, step, s_scan, &s_base, red);
+            J += ok;
+            N += first;
+            D += fresh;
+            append_cta<1>(hb.log, &ctl->h[head].log_n, key, fresh, s_warp, &s_base);
         }
+        flush_counts(ctl, head, step, J, N, D, red);
     }
     if (do_end && last_cta(ctl, &s_flag) && threadIdx.x == 0) end_body(ctl, e);
 }
@@ -765,7 +822,7 @@ int occupancy(Kern k, size_t smem = 0) {
     return b > 0 ? b : 1;
 }
 
-int g_occ_temp = 0, g_occ_insert = 0, g_occ_select = 0;
+int g_occ_temp = 0, g_occ_insert = 0, g_occ_select = 0, g_occ_keys = 0;
 
 }  // namespace
 
@@ -775,6 +832,7 @@ void loop_prepare() {
     if (g_occ_temp) return;
     g_occ_temp = occupancy(loop_materialize_temp_kernel);
     g_occ_insert = occupancy(loop_materialize_insert_kernel);
+    g_occ_keys = occupancy(loop_insert_keys_kernel);
     g_occ_select = occupancy(loop_select_insert_kernel);
 }
 
@@ -864,6 +922,14 @@ void loop_materialize_temp(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const
 
 void loop_select_cand(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o) {
     loop_select_cand_kernel<<<1, 32, 0, s>>>(ctl, step, o);
+    c.check_launch();
+}
+
+void loop_insert_keys(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const u64* keys,
+                      const LoopHeadBufs& hb, const LoopEndDesc* end) {
+    LoopEndDesc e{};
+    if (end) e = *end;
+    loop_insert_keys_kernel<<<c.num_sms * g_occ_keys, kLT, 0, s>>>(ctl, step, head, keys, hb, e, end ? 1 : 0);
     c.check_launch();
 }
 

@@ -177,9 +177,14 @@ void loop_materialize_temp(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const
 // Candidate bound of a select (nsteps == 0) final step = its outer rows.
 void loop_select_cand(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o);
 // Final steps; when `end` is non-null the last CTA records the iteration.
+// Final step fused: expansion + insertion + append (the product path).
 void loop_materialize_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
                              const u64* inner, const DevJoin& jd, const LoopStepBufs& sb,
                              const LoopHeadBufs& hb, const LoopEndDesc* end);
+// Inserts the step's materialized join rows (ctl.step_total of them) into
+// the head's full-tuple index and appends the new ones to its log.
+void loop_insert_keys(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const u64* keys,
+                      const LoopHeadBufs& hb, const LoopEndDesc* end);
 void loop_select_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
                         const DevJoin& jd, const LoopHeadBufs& hb, const LoopEndDesc* end);
 // Records the iteration (or rolls it back on overflow) and sets the graph's

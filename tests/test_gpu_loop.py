@@ -23,6 +23,8 @@ MODES = {
     "tiny_eager": {"GD_LOOP_TINY": "1", "GD_LOOP_MODE": "eager"},
     "host": {"GD_LOOP": "0"},
     "hashindex": {"GD_DENSE": "0"},
+    "split": {"GD_LOOP_SPLIT": "1"},
+    "tiny_split": {"GD_LOOP_TINY": "1", "GD_LOOP_SPLIT": "1"},
 }
 
 
@@ -67,14 +69,14 @@ def test_c1_all_modes(ref, mode):
     assert g.raw_stats().join_tuples == 190496  # SURVEY §6 probe: ΣJ over 46 iterations
 
 
-@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "hashindex"])
+@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "hashindex", "split"])
 @pytest.mark.parametrize("idx", [0, 17, 55])
 def test_sg_corpus_modes(ref, mode, idx):
     g, _ = corpus(ref, 1, idx)
     assert_same(run_mode(mode, "sg", {"Edge": g}), run_ref(ref, "sg", {"Edge": g}), ["SG"])
 
 
-@pytest.mark.parametrize("mode", ["graph", "tiny"])
+@pytest.mark.parametrize("mode", ["graph", "tiny", "tiny_split"])
 @pytest.mark.parametrize("case", sorted(CUSTOM))
 def test_custom_programs_modes(ref, mode, case):
     src, db = CUSTOM[case]

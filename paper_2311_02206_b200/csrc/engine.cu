@@ -807,7 +807,7 @@ public:
                             const u64 old_cap = H.tab_cap;
                             H.alloc_tab(c, 6 * hc->need_tab[h]);  // load 1/6 after growth
                             tr("tab-alloc+clear", old_cap, H.tab_cap);
-                            loop_table_rehash(c, old.p, old_cap, H.tab.p, H.tab_cap, H.sbits);
+                            loop_table_rehash(c, old.p, old_cap, H.tab.p, H.tab_cap, H.sbits, ln);
                             tr("tab-rehash", old_cap, H.tab_cap);
                         } else if (hc->need_restamp) {
                             loop_table_restamp(c, H.tab.p, H.tab_cap, H.sbits);

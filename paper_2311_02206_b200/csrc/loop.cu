@@ -801,6 +801,80 @@ __global__ void table_rehash_kernel(const void* old_tab, u64 old_cap, void* tab,
     }
 }
 
+// Atomic-free growth (the CAS re-spread runs at the L2 atomic rate even
+// though its addresses stream).  Thread t owns old slots [32t, 32t+32) and
+// the new-table zone [32t·g, 32(t+1)·g) (g = new/old capacity, zones
+// partition the new table).  It places each of its keys whose new home lies
+// in its zone at the first free zone slot at or after the home (a 256-bit
+// occupancy map in registers) with a plain store: every slot between a
+// key's home and its position holds a key, the linear-probing invariant.
+// Keys whose home falls outside the zone, or that overflow it, are spilled
+// and CAS-inserted afterwards (table_fill over the spill list).
+constexpr u64 kPlaceMaxZone = 256;
+__global__ void table_place_kernel(const void* old_tab, u64 old_cap, void* tab, u64 cap, u32 sb,
+                                   u64* __restrict__ spill, unsigned long long* nspill) {
+    const u64 runs = (old_cap + kRun - 1) / kRun;
+    for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < runs; r += (u64)gridDim.x * blockDim.x) {
+        const u64 i0 = r * kRun, i1 = min(old_cap, i0 + kRun);
+        const u64 zlo = (u64)((u128)i0 * cap / old_cap);
+        const u64 zhi = i1 == old_cap ? cap : (u64)((u128)i1 * cap / old_cap);
+        const u64 width = zhi - zlo;  // <= kPlaceMaxZone (host checks the growth ratio)
+        u64 bm0 = 0, bm1 = 0, bm2 = 0, bm3 = 0;
+        for (u64 i = i0; i < i1; ++i) {
+            const u64 w = sb ? static_cast<const u64*>(old_tab)[i] : static_cast<const HSlot*>(old_tab)[i].key;
+            if (w == kEmptySlot) continue;
+            const u64 key = sb ? w >> sb : w;
+            const u64 h = hs_home(key, cap);
+            u64 q = kPlaceMaxZone;
+            if (h >= zlo && h < zhi) {
+                const u32 off = (u32)(h - zlo);
+                // first zero bit >= off over the four words
+                const u64 m0 = off < 64 ? ~bm0 & (~0ull << off) : 0;
+                const u64 m1 = off < 128 ? ~bm1 & (off > 64 ? ~0ull << (off - 64) : ~0ull) : 0;
+                const u64 m2 = off < 192 ? ~bm2 & (off > 128 ? ~0ull << (off - 128) : ~0ull) : 0;
+                const u64 m3 = ~bm3 & (off > 192 ? ~0ull << (off - 192) : ~0ull);
+                if (m0) q = __ffsll((long long)m0) - 1;
+                else if (m1) q = 64 + __ffsll((long long)m1) - 1;
+                else if (m2) q = 128 + __ffsll((long long)m2) - 1;
+                else if (m3) q = 192 + __ffsll((long long)m3) - 1;
+            }
+            if (q < width) {
+                if (q < 64) bm0 |= 1ull << q;
+                else if (q < 128) bm1 |= 1ull << (q - 64);
+                else if (q < 192) bm2 |= 1ull << (q - 128);
+                else bm3 |= 1ull << (q - 192);
+                if (sb) {
+                    static_cast<u64*>(tab)[zlo + q] = key << sb;
+                } else {
+                    HSlot& d = static_cast<HSlot*>(tab)[zlo + q];
+                    d.key = key;
+                    d.stamp = 0;
+                }
+            } else {
+                spill[atomicAdd(nspill, 1ull)] = key;
+            }
+        }
+    }
+}
+
+// CAS insertion of the spilled keys (count in device memory).
+__global__ void table_fill_dev_kernel(void* tab, u64 cap, u32 sb, const u64* __restrict__ keys,
+                                      const unsigned long long* n_ptr) {
+    const u64 n = *n_ptr;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 key = keys[i];
+        u64 pos = hs_home(key, cap);
+        while (true) {
+            u64* w = sb ? static_cast<u64*>(tab) + pos : &static_cast<HSlot*>(tab)[pos].key;
+            if (atomicCAS(w, kEmptySlot, sb ? key << sb : key) == kEmptySlot) {
+                if (!sb) static_cast<HSlot*>(tab)[pos].stamp = 0;
+                break;
+            }
+            pos = pos + 1 == cap ? 0 : pos + 1;
+        }
+    }
+}
+
 // New stamp epoch in place: every stamp back to 0.
 __global__ void table_restamp_kernel(void* tab, u64 cap, u32 sb) {
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (u64)gridDim.x * blockDim.x) {
@@ -845,8 +919,22 @@ void loop_table_fill(Ctx& c, void* tab, u64 cap, u32 sbits, const u64* keys, u64
     c.check_launch();
 }
 
-void loop_table_rehash(Ctx& c, const void* old_tab, u64 old_cap, void* tab, u64 cap, u32 sbits) {
+void loop_table_rehash(Ctx& c, const void* old_tab, u64 old_cap, void* tab, u64 cap, u32 sbits, u64 nkeys) {
     if (old_cap == 0) return;
+    // zones of at most kPlaceMaxZone slots: growth ratio below 8
+    if (cap < old_cap * (kPlaceMaxZone / kRun) - kPlaceMaxZone && !(getenv("GD_REHASH_CAS") &&
+                                                                   getenv("GD_REHASH_CAS")[0] == '1')) {
+        DevBuf<u64> spill(c, std::max<u64>(nkeys, 1));
+        DevBuf<unsigned long long> ns(c, 1);
+        c.memset(ns.p, 0, sizeof(unsigned long long));
+        const u64 runs = (old_cap + kRun - 1) / kRun;
+        const int grid = (int)std::max<u64>(1, std::min<u64>((runs + 255) / 256, (u64)c.num_sms * 16));
+        table_place_kernel<<<grid, 256, 0, c.stream>>>(old_tab, old_cap, tab, cap, sbits, spill.p, ns.p);
+        c.check_launch();
+        table_fill_dev_kernel<<<c.num_sms * 4, 256, 0, c.stream>>>(tab, cap, sbits, spill.p, ns.p);
+        c.check_launch();
+        return;
+    }
     const u64 runs = (old_cap + kRun - 1) / kRun;
     const int grid = (int)std::max<u64>(1, std::min<u64>((runs + 255) / 256, (u64)c.num_sms * 16));
     table_rehash_kernel<<<grid, 256, 0, c.stream>>>(old_tab, old_cap, tab, cap, sbits);

@@ -157,8 +157,9 @@ void loop_prepare();
 void loop_table_clear(Ctx& c, void* tab, u64 cap, u32 sbits);
 // Inserts keys (unique) into an empty table (stamp 0).
 void loop_table_fill(Ctx& c, void* tab, u64 cap, u32 sbits, const u64* keys, u64 n);
-// Moves every key of old_tab into the (cleared, larger) tab, stamps 0.
-void loop_table_rehash(Ctx& c, const void* old_tab, u64 old_cap, void* tab, u64 cap, u32 sbits);
+// Moves every key (nkeys of them) of old_tab into the (cleared, larger)
+// tab, stamps 0.
+void loop_table_rehash(Ctx& c, const void* old_tab, u64 old_cap, void* tab, u64 cap, u32 sbits, u64 nkeys);
 // Resets every stamp to 0 in place (new stamp epoch).
 void loop_table_restamp(Ctx& c, void* tab, u64 cap, u32 sbits);
 

@@ -25,6 +25,7 @@ MODES = {
     "hashindex": {"GD_DENSE": "0"},
     "split": {"GD_LOOP_SPLIT": "1"},
     "tiny_split": {"GD_LOOP_TINY": "1", "GD_LOOP_SPLIT": "1"},
+    "tiny_casrehash": {"GD_LOOP_TINY": "1", "GD_REHASH_CAS": "1"},
 }
 
 
@@ -98,7 +99,7 @@ def test_long_chain_many_iterations(ref, mode):
 def test_modes_agree_on_power_law(ref):
     from paper_2311_02206_b200 import workloads as W
     e = W.tc_pl(20000, 20000, 100, 1.05, 3)
-    outs = {m: run_mode(m, "reach", {"Edge": e}) for m in ("graph", "host", "tiny", "hashindex")}
+    outs = {m: run_mode(m, "reach", {"Edge": e}) for m in ("graph", "host", "tiny", "hashindex", "tiny_casrehash")}
     base = outs["host"]
     for m, g in outs.items():
         assert np.array_equal(g.relation("Reach").data, base.relation("Reach").data), m

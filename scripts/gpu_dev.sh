@@ -1,3 +1,4 @@
 #!/bin/bash
-timeout 600 python scripts/run_configs.py c1_tc_rand c3_sg_tree c4_cspa > gpurun_out/configs.log 2>&1
-GD_LOOP_MODE=eager timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-profile > gpurun_out/bench_ncu.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_loop.py -x -q > gpurun_out/pytest_loop.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_loop.log
+timeout 300 python scripts/diag.py 5e6 1.05 1 > gpurun_out/diag.log 2>&1
+timeout 300 python scripts/loop_modes.py > gpurun_out/loop_modes.log 2>&1

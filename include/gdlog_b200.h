@@ -92,6 +92,10 @@ gd_status gd_ctx_profile_reset(gd_ctx* ctx);
 gd_status gd_ctx_host_counters(gd_ctx* ctx, double* alloc_seconds,
                                uint64_t* allocs, double* sync_seconds,
                                uint64_t* syncs);
+/* Bytes copied host->device and device->host by this context since its
+ * creation (the e2e bench reports the bytes that actually cross PCIe:
+ * relation downloads move packed keys when the encoding allows). */
+gd_status gd_ctx_transfer_bytes(gd_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 
 /* ------------------------------------------------------------------ */
 /* Join-spec and plan data (ra.hpp:18-66, plan.hpp:18-58)              */

@@ -165,6 +165,7 @@ SIGNATURES = {
     "gd_ctx_profile_read": (C.c_int, [P, P, P, P]),
     "gd_ctx_profile_reset": (C.c_int, [P]),
     "gd_ctx_host_counters": (C.c_int, [P, P, P, P, P]),
+    "gd_ctx_transfer_bytes": (C.c_int, [P, P, P]),
     "gd_prefix_hash": (C.c_int, [P, P, u64, u32, u32, P]),
     "gd_canonicalize": (C.c_int, [P, P, u64, u32, P, PU64]),
     "gd_permute_columns": (C.c_int, [P, P, u64, u32, C.c_int, P, u32, P, PU64]),

@@ -120,6 +120,12 @@ class Context:
     def profile_reset(self):
         self.check(self.lib.gd_ctx_profile_reset(self.h))
 
+    def transfer_bytes(self) -> tuple[int, int]:
+        """(host->device, device->host) bytes copied by this context."""
+        h, d = A.u64(), A.u64()
+        self.check(self.lib.gd_ctx_transfer_bytes(self.h, C.byref(h), C.byref(d)))
+        return int(h.value), int(d.value)
+
     def host_counters(self) -> dict:
         a, s = C.c_double(), C.c_double()
         na, ns = A.u64(), A.u64()

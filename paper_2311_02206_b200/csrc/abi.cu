@@ -266,6 +266,13 @@ gd_status gd_ctx_profile_read(gd_ctx* ctx, double* ms, uint64_t* launches, uint6
     });
 }
 
+gd_status gd_ctx_transfer_bytes(gd_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {
+    return guard(ctx, [&] {
+        if (h2d) *h2d = ctx->c->h2d_bytes;
+        if (d2h) *d2h = ctx->c->d2h_bytes;
+    });
+}
+
 gd_status gd_ctx_host_counters(gd_ctx* ctx, double* alloc_seconds, uint64_t* allocs, double* sync_seconds,
                                uint64_t* syncs) {
     return guard(ctx, [&] {

@@ -127,6 +127,18 @@ struct Ctx {
         if (!pinned_big) GD_CUDA(cudaMallocHost(&pinned_big, kPinnedBig));
         return pinned_big;
     }
+    // Pinned staging for chunked host downloads (kept for the context's life).
+    void* staging = nullptr;
+    size_t staging_bytes = 0;
+    void* pinned_staging(size_t bytes) {
+        if (staging_bytes < bytes) {
+            if (staging) cudaFreeHost(staging);
+            staging = nullptr;
+            GD_CUDA(cudaMallocHost(&staging, bytes));
+            staging_bytes = bytes;
+        }
+        return staging;
+    }
 
     Ctx(int dev, void* s) : device(dev) {
         int n = 0;
@@ -158,6 +170,7 @@ struct Ctx {
         cudaStreamSynchronize(stream);
         if (pinned) cudaFreeHost(pinned);
         if (pinned_big) cudaFreeHost(pinned_big);
+        if (staging) cudaFreeHost(staging);
         if (own_stream && stream) cudaStreamDestroy(stream);
     }
     Ctx(const Ctx&) = delete;
@@ -283,11 +296,14 @@ struct Ctx {
     void memset(void* p, int v, size_t bytes) {
         if (bytes) GD_CUDA(cudaMemsetAsync(p, v, bytes, stream));
     }
+    uint64_t h2d_bytes = 0, d2h_bytes = 0;  // gd_ctx_transfer_bytes
     void h2d(void* d, const void* h, size_t bytes) {
         if (bytes) GD_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, stream));
+        h2d_bytes += bytes;
     }
     void d2h(void* h, const void* d, size_t bytes) {
         if (bytes) GD_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, stream));
+        d2h_bytes += bytes;
     }
     void d2d(void* d, const void* s, size_t bytes) {
         if (bytes) GD_CUDA(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, stream));

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <set>
+#include <thread>
 #include <type_traits>
 
 #include "engine.h"
@@ -264,10 +265,71 @@ public:
             c.sync();
             return;
         }
+        if constexpr (std::is_same_v<K, u64>) {
+            if (!E.enc.e.dict && ar > 1 && st.full_n >= (1u << 20) &&
+                !(getenv("GD_HOST_UNPACK") && getenv("GD_HOST_UNPACK")[0] == '0')) {
+                download_packed(st.full.p, st.full_n, ar, out);
+                return;
+            }
+        }
         DevBuf<u64> tmp(c, st.full_n * ar);
         unpack_rows<K>(c, st.full.p, st.full_n, ar, E.enc.e, tmp.p);
         c.d2h(out, tmp.p, st.full_n * ar * sizeof(u64));
         c.sync();
+    }
+
+    // Host download of identity-encoded u64 keys: the packed keys cross PCIe
+    // (8 B per row instead of 8·arity) into two pinned staging buffers, and
+    // host threads unpack chunk k into the caller's rows while chunk k+1 is
+    // in flight.  Bytes equal unpack_rows + copy.
+    void download_packed(const u64* keys, u64 n, u32 ar, u64* out) {
+        constexpr u64 kChunk = 16u << 20;  // rows per chunk (128 MB of keys)
+        u64* stage[2];
+        void* area = c.pinned_staging(2 * kChunk * sizeof(u64));
+        stage[0] = static_cast<u64*>(area);
+        stage[1] = stage[0] + kChunk;
+        cudaEvent_t ev[2];
+        GD_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+        GD_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+        const u32 bits = E.enc.e.bits;
+        const u64 mask = bits >= 64 ? ~0ull : (1ull << bits) - 1;
+        const unsigned hw = std::thread::hardware_concurrency();
+        const unsigned nt = std::max(1u, std::min(hw ? hw : 8u, 32u));
+        const u64 nchunks = (n + kChunk - 1) / kChunk;
+        auto issue = [&](u64 k) {
+            const u64 b = k * kChunk, m = std::min(kChunk, n - b);
+            c.d2h(stage[k & 1], keys + b, m * sizeof(u64));
+            GD_CUDA(cudaEventRecord(ev[k & 1], c.stream));
+        };
+        issue(0);
+        for (u64 k = 0; k < nchunks; ++k) {
+            GD_CUDA(cudaEventSynchronize(ev[k & 1]));
+            if (k + 1 < nchunks) issue(k + 1);  // staging[(k+1)&1] was unpacked at step k-1
+            const u64 b = k * kChunk, m = std::min(kChunk, n - b);
+            const u64* src = stage[k & 1];
+            u64* dst = out + b * ar;
+            auto work = [&](unsigned t) {
+                const u64 lo = m * t / nt, hi = m * (t + 1) / nt;
+                if (ar == 2) {
+                    for (u64 i = lo; i < hi; ++i) {
+                        const u64 key = src[i];
+                        dst[2 * i] = (key >> bits) & mask;
+                        dst[2 * i + 1] = key & mask;
+                    }
+                } else {
+                    for (u64 i = lo; i < hi; ++i) {
+                        const u64 key = src[i];
+                        for (u32 col = 0; col < ar; ++col) dst[i * ar + col] = (key >> ((ar - 1 - col) * bits)) & mask;
+                    }
+                }
+            };
+            std::vector<std::thread> pool;
+            for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work, t);
+            work(0);
+            for (auto& th : pool) th.join();
+        }
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
     }
 
     u64 digest(u32 r) override {

@@ -1,0 +1,40 @@
+"""Host download of large relations (engine.relation): packed keys cross
+PCIe and host threads unpack them (engine.cu download_packed); the rows
+must equal the device-unpack path and the numpy canonical form."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2311_02206_b200 import arraylog as al
+from tests.helpers import program_from_ref
+
+pytestmark = pytest.mark.gpu
+
+COPY2 = ".decl E(2)\nC(x, y) :- E(x, y).\n"
+COPY3 = ".decl E(3)\nC(x, y, z) :- E(x, y, z).\n"
+
+
+def canonical(a):
+    return np.unique(a, axis=0)
+
+
+@pytest.mark.parametrize("arity,n,hi", [(2, 3_000_000, 1 << 20), (3, 2_100_000, 1 << 14), (2, 40_000_000, 1 << 30)])
+def test_host_unpack_matches(ref, arity, n, hi):
+    src = COPY2 if arity == 2 else COPY3
+    r = ref.engine(src)
+    prog = program_from_ref(r)
+    rng = np.random.default_rng(arity * 7 + n)
+    e = rng.integers(0, hi, size=(n, arity), dtype=np.uint64)
+    outs = {}
+    for mode in ("1", "0"):
+        os.environ["GD_HOST_UNPACK"] = mode
+        try:
+            g = al.engine(prog)
+            g.load_edb("E", al.tuple_array(arity, e))
+            g.run()
+            outs[mode] = g.relation("C").data.copy()
+        finally:
+            os.environ.pop("GD_HOST_UNPACK", None)
+    assert np.array_equal(outs["1"], outs["0"])
+    assert np.array_equal(outs["1"].reshape(-1, arity), canonical(e))

@@ -19,6 +19,9 @@
 #include <set>
 #include <thread>
 #include <type_traits>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 #include "engine.h"
 #include "loop.h"
@@ -301,9 +304,14 @@ public:
             c.d2h(stage[k & 1], keys + b, m * sizeof(u64));
             GD_CUDA(cudaEventRecord(ev[k & 1], c.stream));
         };
+        const bool trace = getenv("GD_DL_TRACE") && getenv("GD_DL_TRACE")[0] == '1';
+        double t_wait = 0, t_unpack = 0;
         issue(0);
         for (u64 k = 0; k < nchunks; ++k) {
+            const double tw = Ctx::now_s();
             GD_CUDA(cudaEventSynchronize(ev[k & 1]));
+            t_wait += Ctx::now_s() - tw;
+            const double tu = Ctx::now_s();
             if (k + 1 < nchunks) issue(k + 1);  // staging[(k+1)&1] was unpacked at step k-1
             const u64 b = k * kChunk, m = std::min(kChunk, n - b);
             const u64* src = stage[k & 1];
@@ -311,11 +319,23 @@ public:
             auto work = [&](unsigned t) {
                 const u64 lo = m * t / nt, hi = m * (t + 1) / nt;
                 if (ar == 2) {
+#if defined(__x86_64__)
+                    // non-temporal stores: the rows are written once and not
+                    // read back here, so skip the read-for-ownership of each line
+                    long long* d = reinterpret_cast<long long*>(dst);
+                    for (u64 i = lo; i < hi; ++i) {
+                        const u64 key = src[i];
+                        _mm_stream_si64(d + 2 * i, (long long)((key >> bits) & mask));
+                        _mm_stream_si64(d + 2 * i + 1, (long long)(key & mask));
+                    }
+                    _mm_sfence();
+#else
                     for (u64 i = lo; i < hi; ++i) {
                         const u64 key = src[i];
                         dst[2 * i] = (key >> bits) & mask;
                         dst[2 * i + 1] = key & mask;
                     }
+#endif
                 } else {
                     for (u64 i = lo; i < hi; ++i) {
                         const u64 key = src[i];
@@ -327,7 +347,11 @@ public:
             for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work, t);
             work(0);
             for (auto& th : pool) th.join();
+            t_unpack += Ctx::now_s() - tu;
         }
+        if (trace)
+            fprintf(stderr, "[download] %llu rows, %u threads: waiting on PCIe %.1f ms, unpacking %.1f ms\n",
+                    (unsigned long long)n, nt, t_wait * 1e3, t_unpack * 1e3);
         cudaEventDestroy(ev[0]);
         cudaEventDestroy(ev[1]);
     }

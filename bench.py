@@ -272,6 +272,15 @@ def main():
                 roof["traffic"] = d.get("dram_bytes")
                 roof["traffic_algo_bytes"] = d.get("algo_bytes")
                 roof["traffic_source"] = d.get("source")
+        # The fused insert is bound by random 8-byte slot CASes, each of which
+        # moves a ~111-byte line of DRAM traffic on B200: report its measured
+        # DRAM traffic (ncu) against the measured random-CAS ceiling too.
+        rc = ROOT / "profiles" / "random_access_ceiling.json"
+        if dom == "join_insert" and roof.get("traffic") and rc.exists():
+            ceil = json.loads(rc.read_text())
+            gbs = roof["traffic"] / (roof["avg_launch_ms"] / 1e3) / 1e9
+            roof["random_access"] = {"dram_gbs": gbs, "ceiling_gbs": ceil["cas_dram_tbps"] * 1e3,
+                                     "frac": gbs / (ceil["cas_dram_tbps"] * 1e3), "ceiling_source": ceil["source"]}
         jm = [k for k in ("join_probe", "join_materialize", "join_insert", "diff_merge", "difference")]
         jm_ms = sum(prof[k][0] for k in jm)
         jm_by = sum(prof[k][2] for k in jm)

@@ -292,6 +292,28 @@ typedef struct gd_iter_record {
     uint64_t full_after;
 } gd_iter_record;
 
+/* ---- fact ingestion and canonical TSV output ------
+ * The text is parsed / produced on the device.  Numeric files only: the
+ * reference's dictionary mode (io.hpp:19-41) interns tokens on the host
+ * (arraylog.py) before the rows reach the device. */
+
+/* read_facts(path, arity) (io.hpp:64-114): `text` holds the file bytes,
+ * `name` (nullable) stands for the path in messages.  Writes the canonical
+ * rows (sorted, duplicates collapsed) to out[count * arity]; GD_ERR_LOAD
+ * with the reference's message on the first bad line ("<name>:<line>:
+ * expected N columns, got M" / "'tok' is not an unsigned integer" / "value
+ * is reserved"); GD_ERR_INVALID_ARG (count set) when capacity_rows is too
+ * small. */
+gd_status gd_parse_facts(gd_ctx* ctx, const char* name, const char* text, uint64_t len, uint32_t arity,
+                         uint64_t* out, uint64_t capacity_rows, uint64_t* count);
+/* file_is_all_integers (io.hpp:145-170): *result = 1 when every data token
+ * is an unsigned decimal below the sentinel. */
+gd_status gd_facts_all_integers(gd_ctx* ctx, const char* text, uint64_t len, int* result);
+/* to_tsv(rel) (io.hpp:118-133) of n canonical rows: the bytes into
+ * out[capacity] (out == NULL: *len only). */
+gd_status gd_rows_to_tsv(gd_ctx* ctx, const uint64_t* rows, uint64_t n, uint32_t arity, char* out,
+                         uint64_t capacity, uint64_t* len);
+
 typedef struct gd_engine gd_engine;
 
 /* engine(program, engine_config) (engine.hpp:66-88).  Relations are ids
@@ -318,6 +340,13 @@ gd_status gd_engine_load_edb_device(gd_engine* eng, uint32_t rel,
                                     int canonical);
 
 /* seed / iterate_to_fixpoint / run (engine.hpp:130-257). */
+/* load_edb(name, read_facts(path, arity)) with the text parsed on the
+ * device straight into the relation (no host rows). */
+gd_status gd_engine_load_edb_tsv(gd_engine* eng, uint32_t rel, const char* name, const char* text,
+                                 uint64_t len);
+/* write_relation / to_tsv of relation(rel) (io.hpp:118-143): the canonical
+ * TSV bytes into out[capacity] (out == NULL: *len only). */
+gd_status gd_engine_relation_tsv(gd_engine* eng, uint32_t rel, char* out, uint64_t capacity, uint64_t* len);
 gd_status gd_engine_seed(gd_engine* eng);
 gd_status gd_engine_iterate(gd_engine* eng);
 gd_status gd_engine_run(gd_engine* eng);

@@ -245,6 +245,42 @@ class RefOracle(_Base):
     def _err(self):
         return self.lib.ref_last_error().decode()
 
+    # ---- fact files / TSV (io.hpp) ----
+    def read_facts(self, path, arity, use_dict=False):
+        """(status, rows or error message) of the reference read_facts."""
+        import numpy as np
+        cap = max(1, Path(path).stat().st_size // 2 + 1) if Path(path).exists() else 1
+        out = np.zeros((cap, arity), dtype=np.uint64)
+        n = C.c_uint64()
+        rc = self.lib.ref_read_facts(str(path).encode(), C.c_uint32(arity), C.c_int(int(use_dict)),
+                                     out.ctypes.data_as(C.c_void_p), C.c_uint64(cap), C.byref(n))
+        return (rc, out[: n.value]) if rc == 0 else (rc, self._err())
+
+    def to_tsv(self, rows, arity) -> bytes:
+        import numpy as np
+        rows = np.ascontiguousarray(rows, dtype=np.uint64).reshape(-1, arity)
+        cap = max(1, rows.shape[0] * arity * 21 + 16)
+        buf = C.create_string_buffer(cap)
+        n = C.c_uint64()
+        rc = self.lib.ref_to_tsv(rows.ctypes.data_as(C.c_void_p), C.c_uint64(rows.shape[0]), C.c_uint32(arity), buf,
+                                 C.c_uint64(cap), C.byref(n))
+        assert rc == 0, self._err()
+        return buf.raw[: n.value]
+
+    def dict_roundtrip(self, path, arity) -> bytes:
+        cap = Path(path).stat().st_size * 2 + 16
+        buf = C.create_string_buffer(cap)
+        n = C.c_uint64()
+        rc = self.lib.ref_dict_roundtrip(str(path).encode(), C.c_uint32(arity), buf, C.c_uint64(cap), C.byref(n))
+        assert rc == 0, self._err()
+        return buf.raw[: n.value]
+
+    def file_is_all_integers(self, path) -> bool:
+        r = C.c_int()
+        rc = self.lib.ref_file_is_all_integers(str(path).encode(), C.byref(r))
+        assert rc == 0, self._err()
+        return bool(r.value)
+
     def _phase(self):
         return self.lib.ref_last_error_phase().decode()
 

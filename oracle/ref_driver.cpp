@@ -510,4 +510,45 @@ int ref_acceptance_corpus(int kind, uint32_t idx, uint64_t* out, uint64_t cap_ro
     });
 }
 
+// ---- fact files / TSV (io.hpp) ----------------------------------------
+// read_facts(path, arity[, dictionary]): canonical rows into out.
+int ref_read_facts(const char* path, uint32_t arity, int use_dict, uint64_t* out, uint64_t cap_rows,
+                   uint64_t* count) {
+    return guard([&] {
+        dictionary d;
+        tuple_array t = read_facts(path, arity, use_dict ? &d : nullptr);
+        *count = t.count();
+        if (t.count() > cap_rows) throw std::logic_error("read_facts: capacity");
+        if (!t.data.empty()) std::memcpy(out, t.data.data(), t.data.size() * sizeof(uint64_t));
+    });
+}
+
+// to_tsv of rows (canonicalized first, like a relation) -> bytes.
+int ref_to_tsv(const uint64_t* rows, uint64_t n, uint32_t arity, char* out, uint64_t cap, uint64_t* len) {
+    return guard([&] {
+        tuple_array t = canonicalize(make_rows(rows, n, arity, false));
+        const std::string s = to_tsv(t);
+        *len = s.size();
+        if (s.size() > cap) throw std::logic_error("to_tsv: capacity");
+        std::memcpy(out, s.data(), s.size());
+    });
+}
+
+// read_facts with a dictionary, then write_relation with it: the decoded
+// canonical TSV bytes.
+int ref_dict_roundtrip(const char* path, uint32_t arity, char* out, uint64_t cap, uint64_t* len) {
+    return guard([&] {
+        dictionary d;
+        tuple_array t = read_facts(path, arity, &d);
+        const std::string s = to_tsv(t, &d);
+        *len = s.size();
+        if (s.size() > cap) throw std::logic_error("to_tsv: capacity");
+        std::memcpy(out, s.data(), s.size());
+    });
+}
+
+int ref_file_is_all_integers(const char* path, int* result) {
+    return guard([&] { *result = file_is_all_integers(path) ? 1 : 0; });
+}
+
 }  // extern "C"

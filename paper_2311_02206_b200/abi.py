@@ -184,6 +184,11 @@ SIGNATURES = {
     "gd_engine_destroy": (C.c_int, [P]),
     "gd_engine_set_plans": (C.c_int, [P, C.POINTER(gd_rule_plan), u32]),
     "gd_engine_load_edb": (C.c_int, [P, u32, P, u64, C.c_int]),
+    "gd_engine_load_edb_tsv": (C.c_int, [P, u32, C.c_char_p, P, u64]),
+    "gd_engine_relation_tsv": (C.c_int, [P, u32, P, u64, P]),
+    "gd_parse_facts": (C.c_int, [P, C.c_char_p, P, u64, u32, P, u64, P]),
+    "gd_facts_all_integers": (C.c_int, [P, P, u64, P]),
+    "gd_rows_to_tsv": (C.c_int, [P, P, u64, u32, P, u64, P]),
     "gd_engine_load_edb_device": (C.c_int, [P, u32, P, u64, C.c_int]),
     "gd_engine_seed": (C.c_int, [P]),
     "gd_engine_iterate": (C.c_int, [P]),

@@ -76,6 +76,114 @@ _ERRORS = {
 
 
 # ---------------------------------------------------------------------------
+# Fact files and TSV output (io.hpp:17-170).  Numeric files are parsed and
+# formatted on the device (tsv.cu); the dictionary mode interns tokens here,
+# on the host, exactly as io.hpp's dictionary does (first-appearance ids).
+
+class dictionary:
+    """Symbol table, tokens -> dense ids in first-appearance order (io.hpp:19-41)."""
+
+    def __init__(self):
+        self._fwd: dict[str, int] = {}
+        self._rev: list[str] = []
+
+    def intern(self, token: str) -> int:
+        i = self._fwd.get(token)
+        if i is None:
+            i = len(self._rev)
+            self._fwd[token] = i
+            self._rev.append(token)
+        return i
+
+    def symbol(self, i: int) -> str:
+        if i < 0 or i >= len(self._rev):
+            raise logic_error("dictionary: id out of range")
+        return self._rev[i]
+
+    def size(self) -> int:
+        return len(self._rev)
+
+
+def _read_bytes(path) -> bytes:
+    try:
+        with open(path, "rb") as f:
+            return f.read()
+    except OSError:
+        raise load_error(f"cannot open fact file '{path}'") from None
+
+
+def _dict_rows(text: bytes, arity: int, d: dictionary, name: str) -> np.ndarray:
+    """read_facts with a dictionary (io.hpp:80-99): same line rules, tokens interned."""
+    vals = []
+    for ln, raw in enumerate(text.decode().split("\n") if text else [], 1):
+        line = raw[:-1] if raw.endswith("\r") else raw
+        stripped = line.strip(" \t")
+        if not stripped or stripped[0] == "#":
+            continue
+        cols = [t for t in line.replace("\t", " ").split(" ") if t]
+        if len(cols) != arity:
+            raise load_error(f"{name}:{ln}: expected {arity} columns, got {len(cols)}")
+        vals.extend(d.intern(t) for t in cols)
+    return np.asarray(vals, dtype=np.uint64).reshape(-1, arity)
+
+
+def read_facts(path, arity: int, dict_: dictionary | None = None, workers: int = 1,
+               ctx: Context | None = None) -> tuple_array:
+    """read_facts (io.hpp:64-114): canonical rows of a fact file.  Numeric
+    files are parsed on the device; with a dictionary, tokens are interned on
+    the host and the rows canonicalized on the device."""
+    if arity <= 0:
+        raise load_error("read_facts: arity must be positive")
+    text = _read_bytes(path)
+    ctx = ctx or default_context()
+    if dict_ is not None:
+        return canonicalize(tuple_array(arity, _dict_rows(text, arity, dict_, str(path))), ctx=ctx)
+    cap = text.count(b"\n") + 1
+    out = np.empty((cap, arity), dtype=np.uint64)
+    n = A.u64()
+    ctx.check(ctx.lib.gd_parse_facts(ctx.h, str(path).encode(), text, len(text), arity, _ptr(out), cap,
+                                     C.byref(n)))
+    return tuple_array(arity, out[: n.value], canonical=True)
+
+
+def file_is_all_integers(path, ctx: Context | None = None) -> bool:
+    """file_is_all_integers (io.hpp:145-170)."""
+    text = _read_bytes(path)
+    ctx = ctx or default_context()
+    r = C.c_int()
+    ctx.check(ctx.lib.gd_facts_all_integers(ctx.h, text, len(text), C.byref(r)))
+    return bool(r.value)
+
+
+def to_tsv(rel, dict_: dictionary | None = None, ctx: Context | None = None) -> str:
+    """to_tsv: of a run_stats (stats.hpp:50-64), or of a relation (io.hpp:118-133):
+    tab-separated rows, decimal or decoded tokens."""
+    if not isinstance(rel, tuple_array):
+        return _stats_to_tsv(rel)
+    if dict_ is not None:
+        return "".join("\t".join(dict_.symbol(int(v)) for v in r) + "\n" for r in rel.data)
+    ctx = ctx or default_context()
+    d = np.ascontiguousarray(rel.data)
+    n = A.u64()
+    ctx.check(ctx.lib.gd_rows_to_tsv(ctx.h, _ptr(d), rel.count(), rel.arity, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(max(n.value, 1))
+    ctx.check(ctx.lib.gd_rows_to_tsv(ctx.h, _ptr(d), rel.count(), rel.arity, buf, n.value, C.byref(n)))
+    return buf.raw[: n.value].decode()
+
+
+def write_relation(rel: tuple_array, path, dict_: dictionary | None = None, ctx: Context | None = None):
+    """write_relation (io.hpp:135-143): canonical relations only."""
+    if not rel.canonical:
+        raise logic_error("write_relation: relation must be canonical")
+    text = to_tsv(rel, dict_, ctx)
+    try:
+        with open(path, "wb") as f:
+            f.write(text.encode())
+    except OSError:
+        raise load_error(f"cannot open '{path}' for writing") from None
+
+
+# ---------------------------------------------------------------------------
 # Device context
 
 class Context:
@@ -518,7 +626,7 @@ class run_stats:
         return max(self.total_seconds - cat, 0.0)
 
 
-def to_tsv(s: run_stats) -> str:
+def _stats_to_tsv(s: run_stats) -> str:
     """to_tsv(run_stats) (stats.hpp:50-64)."""
     out = ["phase\tseconds"]
     for p in A.PHASES:
@@ -584,6 +692,22 @@ class engine:
             raise load_error(f"load_edb: '{name}' expects arity {ar}, got {facts.arity}")
         d = np.ascontiguousarray(facts.data)
         self.ctx.check(self.ctx.lib.gd_engine_load_edb(self.h, rid, _ptr(d), facts.count(), int(facts.canonical)))
+
+    def load_edb_tsv(self, name: str, path):
+        """load_edb(name, read_facts(path, arity)) with the file parsed on the
+        device straight into the relation."""
+        rid = self._rid(name, edb=True)
+        text = _read_bytes(path)
+        self.ctx.check(self.ctx.lib.gd_engine_load_edb_tsv(self.h, rid, str(path).encode(), text, len(text)))
+
+    def relation_tsv(self, name: str) -> bytes:
+        """to_tsv(relation(name)) (io.hpp:118-133), formatted on the device."""
+        rid = self._rid(name)
+        n = A.u64()
+        self.ctx.check(self.ctx.lib.gd_engine_relation_tsv(self.h, rid, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(max(n.value, 1))
+        self.ctx.check(self.ctx.lib.gd_engine_relation_tsv(self.h, rid, buf, n.value, C.byref(n)))
+        return buf.raw[: n.value]
 
     def load_edb_device(self, name: str, d_ptr: int, count: int, canonical: bool = False):
         """load_edb from device-resident rows (count x arity uint64 at d_ptr)."""

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "engine.h"
+#include "tsv.h"
 #include "gdlog_b200.h"
 #include "ops.h"
 
@@ -263,6 +264,38 @@ gd_status gd_ctx_profile_read(gd_ctx* ctx, double* ms, uint64_t* launches, uint6
             if (launches) launches[k] = ctx->c->prof.launches[k];
             if (bytes) bytes[k] = ctx->c->prof.bytes[k];
         }
+    });
+}
+
+gd_status gd_parse_facts(gd_ctx* ctx, const char* name, const char* text, uint64_t len, uint32_t arity,
+                         uint64_t* out, uint64_t capacity_rows, uint64_t* count) {
+    return guard(ctx, [&] {
+        if ((!text && len) || !count) throw Error(GD_ERR_INVALID_ARG, "null argument");
+        Ctx& c = *ctx->c;
+        DevBuf<u64> rows;
+        const u64 n = parse_facts_device(c, text, len, arity, name ? name : "<facts>", rows);
+        *count = n;
+        if (n > capacity_rows || (n && !out)) throw Error(GD_ERR_INVALID_ARG, "read_facts: output buffer too small");
+        c.d2h(out, rows.p, n * arity * sizeof(u64));
+        c.sync();
+    });
+}
+
+gd_status gd_facts_all_integers(gd_ctx* ctx, const char* text, uint64_t len, int* result) {
+    return guard(ctx, [&] {
+        if ((!text && len) || !result) throw Error(GD_ERR_INVALID_ARG, "null argument");
+        *result = facts_all_integers_device(*ctx->c, text, len) ? 1 : 0;
+    });
+}
+
+gd_status gd_rows_to_tsv(gd_ctx* ctx, const uint64_t* rows, uint64_t n, uint32_t arity, char* out, uint64_t capacity,
+                         uint64_t* len) {
+    return guard(ctx, [&] {
+        if ((!rows && n) || !len || arity == 0) throw Error(GD_ERR_INVALID_ARG, "bad argument");
+        Ctx& c = *ctx->c;
+        DevBuf<u64> d(c, std::max<u64>(n * arity, 1));
+        c.h2d(d.p, rows, n * arity * sizeof(u64));
+        *len = rows_to_tsv_device(c, d.p, n, arity, out, capacity);
     });
 }
 
@@ -546,6 +579,28 @@ gd_status gd_engine_load_edb(gd_engine* eng, uint32_t rel, const uint64_t* rows,
 gd_status gd_engine_load_edb_device(gd_engine* eng, uint32_t rel, const uint64_t* d_rows, uint64_t n,
                                     int canonical) {
     ENG_GUARD(eng->e->load_edb(rel, (const u64*)d_rows, n, canonical != 0, true));
+}
+gd_status gd_engine_load_edb_tsv(gd_engine* eng, uint32_t rel, const char* name, const char* text, uint64_t len) {
+    ENG_GUARD({
+        if (!text && len) throw Error(GD_ERR_INVALID_ARG, "null text");
+        Engine& E = *eng->e;
+        E.check_rel(rel);
+        if (!E.info_[rel].is_edb)
+            throw_load("load_edb: '" + E.info_[rel].name + "' is not a declared EDB relation");
+        DevBuf<u64> rows;
+        const u64 n = parse_facts_device(E.c, text, len, E.info_[rel].arity, name ? name : E.info_[rel].name, rows);
+        E.load_edb(rel, rows.p, n, true, true);
+    });
+}
+gd_status gd_engine_relation_tsv(gd_engine* eng, uint32_t rel, char* out, uint64_t capacity, uint64_t* len) {
+    ENG_GUARD({
+        Engine& E = *eng->e;
+        const u64 n = E.relation_count(rel);
+        const u32 ar = E.rel(rel).arity;
+        DevBuf<u64> rows(E.c, std::max<u64>(n * ar, 1));
+        if (n) E.relation_download(rel, rows.p, n, true);
+        *len = rows_to_tsv_device(E.c, rows.p, n, ar, out, capacity);
+    });
 }
 gd_status gd_engine_seed(gd_engine* eng) { ENG_GUARD(eng->e->seed()); }
 gd_status gd_engine_iterate(gd_engine* eng) { ENG_GUARD(eng->e->iterate()); }

@@ -68,6 +68,10 @@ CONFIGS = {
                      desc="TC on a power-law DAG, 5e6 edge draws (n=2e6, W=40, alpha=2)"),
     "c3_sg_tree": dict(program="sg", gen=lambda: {"Edge": sg_tree(1_000_001, 40, 1)},
                        desc="SG on a random tree, 1e6 edges (W=40)"),
+    "c3_sg_tree_w1000": dict(program="sg", gen=lambda: {"Edge": sg_tree(1_000_001, 1000, 1)},
+                             desc="SG on a random tree, 1e6 edges (W=1000)"),
+    "c3_sg_tree_w4000": dict(program="sg", gen=lambda: {"Edge": sg_tree(1_000_001, 4000, 1)},
+                             desc="SG on a random tree, 1e6 edges (W=4000)"),
     "c4_cspa": dict(program="cspa", gen=lambda: dict(zip(("assign", "dereference"),
                                                         cspa_local(1_500_000, 362_000, 1_140_000, 256, 1))),
                     desc="CSPA, httpd-sized EDB (assign 3.62e5, dereference 1.14e6, modules of 256)"),

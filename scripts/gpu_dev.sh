@@ -1,5 +1,4 @@
 #!/bin/bash
-timeout 600 python -m pytest tests/test_gpu_download.py -x -q > gpurun_out/pytest_dl.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_dl.log
-timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-profile > gpurun_out/bench_quick.json 2> gpurun_out/bench_quick.err
-GD_HOST_UNPACK=0 timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-profile > gpurun_out/bench_quick0.json 2>> gpurun_out/bench_quick.err
-nproc > gpurun_out/nproc.txt; lscpu | head -20 >> gpurun_out/nproc.txt
+timeout 600 python -m pytest tests/test_gpu_loop.py -x -q > gpurun_out/pytest_loop.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_loop.log
+timeout 300 python scripts/diag.py 5e6 1.05 1 > gpurun_out/diag.log 2>&1
+timeout 300 python scripts/loop_modes.py > gpurun_out/loop_modes.log 2>&1

@@ -211,6 +211,14 @@ struct Ctx {
         return (bytes + step - 1) / step * step;
     }
 
+    // Bytes a new allocation could get: free device memory plus the blocks
+    // cached here (alloc() returns them to the pool before giving up).
+    uint64_t available_bytes() const {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 0;
+        return (uint64_t)fr + cached_bytes;
+    }
+
     void flush_cache() {
         for (auto& kv : cache_) cudaFreeAsync(kv.second, stream);
         cache_.clear();

@@ -499,10 +499,10 @@ public:
         DevBuf<u64> tab;  // tab_cap slots of loop_slot_bytes(sbits)
         u64 log_cap = 0, tab_cap = 0, tab_limit = 0;
         u32 sbits = 0;
-        void alloc_tab(Ctx& c, u64 cap) {
+        void alloc_tab(Ctx& c, u64 cap, bool dense = false) {
             tab.release();
             tab_cap = cap;
-            tab_limit = tab_limit_of(cap);
+            tab_limit = dense ? cap / 4 * 3 : tab_limit_of(cap);
             tab = DevBuf<u64>(c, cap * loop_slot_bytes(sbits) / 8);
             loop_table_clear(c, tab.p, cap, sbits);
         }
@@ -880,8 +880,15 @@ public:
                             tlast = t1;
                         };
                         if (trace) { c.sync(); tlast = Ctx::now_s(); }
+                        // Growth is sized against free HBM (C5-scale runs): 2x
+                        // for the log and 3x for the index when they fit, else
+                        // the largest size that does (index load up to 3/4).
+                        const u64 reserve = 1ull << 30;
                         if (hc->need_log[h] > H.log_cap) {
-                            const u64 cap = 2 * hc->need_log[h];
+                            const u64 need = hc->need_log[h];
+                            const u64 avail = c.available_bytes();
+                            const u64 fit = avail > reserve ? (avail - reserve) / sizeof(u64) : 0;
+                            const u64 cap = std::max(need + need / 16 + 1024, std::min(2 * need, fit));
                             DevBuf<u64> nl(c, cap);
                             if (ln) c.d2d(nl.p, H.log.p, ln * sizeof(u64));
                             H.log = std::move(nl);
@@ -889,9 +896,18 @@ public:
                             H.log_cap = cap;
                         }
                         if (hc->need_tab[h] > H.tab_limit) {  // grow: stream the old table into the new
+                            const u64 need = hc->need_tab[h];
+                            const u64 sb = loop_slot_bytes(H.sbits);
+                            const u64 avail = c.available_bytes();
+                            const u64 spill = (ln / 16 + (1u << 20)) * sizeof(u64);  // re-spread spill list
+                            const u64 fit = avail > reserve + spill ? (avail - reserve - spill) / sb : 0;
+                            const u64 cap = std::min(6 * need, fit);  // load 1/6 after growth when it fits
+                            if (cap < need / 3 * 4 + 16)
+                                throw_budget("index", "device memory cannot hold the full-tuple index of " +
+                                                          std::to_string(need) + " keys");
                             DevBuf<u64> old = std::move(H.tab);
                             const u64 old_cap = H.tab_cap;
-                            H.alloc_tab(c, 6 * hc->need_tab[h]);  // load 1/6 after growth
+                            H.alloc_tab(c, cap, cap < 2 * need);
                             tr("tab-alloc+clear", old_cap, H.tab_cap);
                             loop_table_rehash(c, old.p, old_cap, H.tab.p, H.tab_cap, H.sbits, ln);
                             tr("tab-rehash", old_cap, H.tab_cap);

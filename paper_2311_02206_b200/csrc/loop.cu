@@ -814,7 +814,7 @@ __global__ void table_rehash_kernel(const void* old_tab, u64 old_cap, void* tab,
 // and CAS-inserted afterwards (table_fill over the spill list).
 constexpr u64 kPlaceMaxZone = 256;
 __global__ void table_place_kernel(const void* old_tab, u64 old_cap, void* tab, u64 cap, u32 sb,
-                                   u64* __restrict__ spill, unsigned long long* nspill) {
+                                   u64* __restrict__ spill, unsigned long long* nspill, u64 spill_cap) {
     const u64 runs = (old_cap + kRun - 1) / kRun;
     for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < runs; r += (u64)gridDim.x * blockDim.x) {
         const u64 i0 = r * kRun, i1 = min(old_cap, i0 + kRun);
@@ -853,7 +853,8 @@ __global__ void table_place_kernel(const void* old_tab, u64 old_cap, void* tab, 
                     d.stamp = 0;
                 }
             } else {
-                spill[atomicAdd(nspill, 1ull)] = key;
+                const u64 at = atomicAdd(nspill, 1ull);
+                if (at < spill_cap) spill[at] = key;  // else: the host redoes the growth with CAS
             }
         }
     }
@@ -926,16 +927,22 @@ void loop_table_rehash(Ctx& c, const void* old_tab, u64 old_cap, void* tab, u64 
     // zones of at most kPlaceMaxZone slots: growth ratio below 8
     if (cap < old_cap * (kPlaceMaxZone / kRun) - kPlaceMaxZone && !(getenv("GD_REHASH_CAS") &&
                                                                    getenv("GD_REHASH_CAS")[0] == '1')) {
-        DevBuf<u64> spill(c, std::max<u64>(nkeys, 1));
+        const u64 spill_cap = nkeys / 16 + (1u << 20);
+        DevBuf<u64> spill(c, spill_cap);
         DevBuf<unsigned long long> ns(c, 1);
         c.memset(ns.p, 0, sizeof(unsigned long long));
         const u64 runs = (old_cap + kRun - 1) / kRun;
         const int grid = (int)std::max<u64>(1, std::min<u64>((runs + 255) / 256, (u64)c.num_sms * 16));
-        table_place_kernel<<<grid, 256, 0, c.stream>>>(old_tab, old_cap, tab, cap, sbits, spill.p, ns.p);
+        table_place_kernel<<<grid, 256, 0, c.stream>>>(old_tab, old_cap, tab, cap, sbits, spill.p, ns.p, spill_cap);
         c.check_launch();
-        table_fill_dev_kernel<<<c.num_sms * 4, 256, 0, c.stream>>>(tab, cap, sbits, spill.p, ns.p);
-        c.check_launch();
-        return;
+        unsigned long long spilled;
+        c.read_words(&spilled, ns.p, 1);
+        if (spilled <= spill_cap) {
+            table_fill_dev_kernel<<<c.num_sms * 4, 256, 0, c.stream>>>(tab, cap, sbits, spill.p, ns.p);
+            c.check_launch();
+            return;
+        }
+        loop_table_clear(c, tab, cap, sbits);  // spill list overflowed: CAS re-spread below
     }
     const u64 runs = (old_cap + kRun - 1) / kRun;
     const int grid = (int)std::max<u64>(1, std::min<u64>((runs + 255) / 256, (u64)c.num_sms * 16));

@@ -92,6 +92,7 @@ struct RelDev {
     u64 delta_n = 0;
     DevBuf<K> new_acc;
     u64 new_n = 0;
+    u64 last_unique = 0;  // distinct join rows of the last iteration (hash pre-dedup sizing)
     std::map<CopyKey, CopyState<K>> copies;
     bool dirty = true;
     u64 merge_gen = 0;
@@ -1377,13 +1378,38 @@ private:
         MergeResult mr;
         if (m > 0) {
             K* sorted;
+            u64 ms = m;  // rows that reach the sort
             {
                 PhaseTimer t(E, "dedup");
-                sorted = sort_rows(st.new_acc, m, ar);
+                bool done = false;
+                if constexpr (std::is_same_v<K, u64>) {
+                    // mostly-duplicate join output: hash pre-dedup, then sort
+                    // only the distinct rows (dedup.cu); the set is sized from
+                    // the previous iteration's distinct count
+                    const u64 expect = std::max<u64>(2 * st.last_unique + 4096, m / 64);
+                    if (m >= (1u << 20) && 4 * expect < m && !(getenv("GD_HASH_DEDUP") &&
+                                                               getenv("GD_HASH_DEDUP")[0] == '0')) {
+                        DevBuf<u64> uniq(c, std::min<u64>(m, 2 * expect + 1));
+                        const u64 u = hash_dedup(c, reinterpret_cast<const u64*>(st.new_acc.p), m, expect, uniq.p,
+                                                 uniq.cap);
+                        if (u != ~0ull) {
+                            DevBuf<K> tmp(c, std::max<u64>(u, 1));
+                            sorted = reinterpret_cast<K*>(radix_sort<u64>(c, uniq.p, reinterpret_cast<u64*>(tmp.p), u,
+                                                                          ar * bits));
+                            // keep the sorted rows alive in new_acc
+                            if (u) c.d2d(st.new_acc.p, sorted, u * sizeof(K));
+                            sorted = st.new_acc.p;
+                            ms = u;
+                            done = true;
+                        }
+                    }
+                }
+                if (!done) sorted = sort_rows(st.new_acc, m, ar);
             }
             PhaseTimer t(E, "difference");
-            ensure_discard(c, st.delta_alt, m);
-            mr = difference_full(st, sorted, m, st.delta_alt.p);
+            ensure_discard(c, st.delta_alt, ms);
+            mr = difference_full(st, sorted, ms, st.delta_alt.p);
+            st.last_unique = mr.unique_new;
             Tracked scratch(E.acct, Accountant::kTemp, m * 8 + rb(m, ar), "dedup");
         }
         Tracked fresh_charge(E.acct, Accountant::kTemp, rb(mr.unique_new, ar), "dedup");

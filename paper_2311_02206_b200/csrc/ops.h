@@ -84,6 +84,12 @@ void pack_keys_checked(Ctx& c, const u64* keys, u64 n, u32 plen, const Encoding&
 template <typename K>
 void permute_keys(Ctx& c, const K* in, u64 n, u32 arity, u32 bits, const u32* perm, K* out);
 
+// ---- dedup.cu -------------------------------------------------------
+// Distinct keys of keys[0, m) (unordered) into out via a hash set sized for
+// expect_unique; returns their count, or ~0 when more than min(set load
+// 1/2, out_cap) distinct keys exist (the caller then sorts all m rows).
+u64 hash_dedup(Ctx& c, const u64* keys, u64 m, u64 expect_unique, u64* out, u64 out_cap);
+
 // ---- merge.cu -------------------------------------------------------
 struct MergeResult {
     u64 delta_n = 0;     // rows of N kept (not in F, first of their run)

@@ -1,4 +1,4 @@
 #!/bin/bash
-timeout 600 python -m pytest tests/test_gpu_loop.py -x -q > gpurun_out/pytest_loop.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_loop.log
-GD_LOOP_TRACE=1 timeout 900 python scripts/run_configs.py c5_tc_dag > gpurun_out/c5.log 2>&1
-nvidia-smi --query-gpu=memory.total,memory.used --format=csv >> gpurun_out/c5.log
+timeout 300 python -m pytest tests/test_gpu_loop.py -x -q -k "hash_predup or c1_all" > gpurun_out/pytest_loop.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_loop.log
+timeout 300 python scripts/run_configs.py c4_cspa > gpurun_out/c4.log 2>&1
+GD_HASH_DEDUP=0 timeout 300 python scripts/run_configs.py c4_cspa >> gpurun_out/c4.log 2>&1

@@ -99,7 +99,8 @@ def test_long_chain_many_iterations(ref, mode):
 def test_modes_agree_on_power_law(ref):
     from paper_2311_02206_b200 import workloads as W
     e = W.tc_pl(20000, 20000, 100, 1.05, 3)
-    outs = {m: run_mode(m, "reach", {"Edge": e}) for m in ("graph", "host", "tiny", "hashindex", "tiny_casrehash")}
+    outs = {m: run_mode(m, "reach", {"Edge": e}) for m in ("graph", "host", "tiny", "hashindex", "tiny_casrehash",
+                                                            "eager")}
     base = outs["host"]
     for m, g in outs.items():
         assert np.array_equal(g.relation("Reach").data, base.relation("Reach").data), m
@@ -135,3 +136,17 @@ def test_hash_predup_matches_sort_path():
     gs, hs = g.raw_stats(), h.raw_stats()
     assert (gs.charge_events, gs.peak_tracked_bytes, gs.join_tuples) == (hs.charge_events, hs.peak_tracked_bytes,
                                                                         hs.join_tuples)
+
+
+@pytest.mark.parametrize("mode", ["graph", "tiny", "eager"])
+def test_hub_rows(ref, mode):
+    """Hubs (in-degree 700, out-degree 300) give Δ rows with long match
+    ranges next to short ones: the load-balanced expansion must match the
+    reference's results, histories and stats."""
+    rng = np.random.default_rng(11)
+    e = rng.integers(0, 3000, size=(6000, 2), dtype=np.uint64)
+    hubs = np.stack([rng.integers(0, 3000, size=700, dtype=np.uint64), np.full(700, 17, dtype=np.uint64)], 1)
+    hub2 = np.stack([np.full(300, 5, dtype=np.uint64), rng.integers(0, 3000, size=300, dtype=np.uint64)], 1)
+    edges = np.vstack([e, hubs, hub2])
+    g = run_mode(mode, "reach", {"Edge": edges})
+    assert_same(g, run_ref(ref, "reach", {"Edge": edges}), ["Reach"])

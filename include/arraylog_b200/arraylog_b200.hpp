@@ -16,6 +16,9 @@
 
 #include <cstring>
 #include <map>
+#include <filesystem>
+#include <fstream>
+#include <iterator>
 #include <memory>
 #include <optional>
 #include <span>
@@ -244,6 +247,60 @@ inline tuple_array difference(const tuple_array& new_rel, const tuple_array& ful
 
 // ---- engine (engine.hpp:40-558) ---------------------------------------------
 
+// ---- fact files / TSV (io.hpp:64-170), parsed and formatted on the device.
+// Numeric files only; pass the reference's arraylog::dictionary to the
+// reference's own read_facts / to_tsv for token files.
+
+namespace detail {
+inline std::string slurp(const std::filesystem::path& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw load_error("cannot open fact file '" + path.string() + "'");
+    return std::string((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+}
+}  // namespace detail
+
+inline tuple_array read_facts(const std::filesystem::path& path, std::uint32_t arity, unsigned /*workers*/ = 1,
+                              context& ctx = context::default_context()) {
+    if (arity == 0) throw load_error("read_facts: arity must be positive");
+    const std::string text = detail::slurp(path);
+    std::uint64_t cap = 1;
+    for (char ch : text) cap += ch == '\n';
+    tuple_array out(arity);
+    out.data.resize(cap * arity);
+    std::uint64_t n = 0;
+    ctx.check(gd_parse_facts(ctx.get(), path.string().c_str(), text.data(), text.size(), arity, out.data.data(), cap,
+                             &n));
+    out.data.resize(n * arity);
+    out.canonical = true;
+    return out;
+}
+
+inline bool file_is_all_integers(const std::filesystem::path& path, context& ctx = context::default_context()) {
+    const std::string text = detail::slurp(path);
+    int r = 0;
+    ctx.check(gd_facts_all_integers(ctx.get(), text.data(), text.size(), &r));
+    return r != 0;
+}
+
+inline std::string to_tsv(const tuple_array& rel, context& ctx = context::default_context()) {
+    std::uint64_t len = 0;
+    ctx.check(gd_rows_to_tsv(ctx.get(), rel.data.data(), rel.count(), rel.arity, nullptr, 0, &len));
+    std::string out(len, '\0');
+    if (len) ctx.check(gd_rows_to_tsv(ctx.get(), rel.data.data(), rel.count(), rel.arity, out.data(), len, &len));
+    return out;
+}
+
+inline void write_relation(const tuple_array& rel, const std::filesystem::path& path,
+                           context& ctx = context::default_context()) {
+    if (!rel.canonical) throw std::logic_error("write_relation: relation must be canonical");
+    const std::string text = to_tsv(rel, ctx);
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw load_error("cannot open '" + path.string() + "' for writing");
+    out << text;
+    out.flush();
+    if (!out) throw load_error("failed while writing '" + path.string() + "'");
+}
+
 class engine {
 public:
     explicit engine(program p, engine_config cfg = {}, context& ctx = context::default_context())
@@ -285,6 +342,29 @@ public:
     }
     const std::vector<rule_plan>& plans() const { return plans_; }
     const program& source_program() const { return prog_; }
+
+    // load_edb(name, read_facts(path, arity)) with the file parsed on the
+    // device straight into the relation.
+    void load_edb_file(const std::string& name, const std::filesystem::path& path) {
+        if (seeded_) throw std::logic_error("load_edb: engine already running");
+        auto it = ids_.find(name);
+        if (it == ids_.end() || !rels_[it->second].is_edb)
+            throw load_error("load_edb: '" + name + "' is not a declared EDB relation");
+        const std::string text = detail::slurp(path);
+        ctx_->check(gd_engine_load_edb_tsv(eng_.get(), it->second, path.string().c_str(), text.data(), text.size()));
+    }
+    // write_relation(relation(name), path), formatted on the device.
+    void write_relation_file(const std::string& name, const std::filesystem::path& path) {
+        auto it = ids_.find(name);
+        if (it == ids_.end()) throw usage_error("relation: unknown relation '" + name + "'");
+        std::uint64_t len = 0;
+        ctx_->check(gd_engine_relation_tsv(eng_.get(), it->second, nullptr, 0, &len));
+        std::string text(len, '\0');
+        if (len) ctx_->check(gd_engine_relation_tsv(eng_.get(), it->second, text.data(), len, &len));
+        std::ofstream out(path, std::ios::binary);
+        if (!out) throw load_error("cannot open '" + path.string() + "' for writing");
+        out << text;
+    }
 
     void load_edb(const std::string& name, tuple_array facts) {
         if (seeded_) throw std::logic_error("load_edb: engine already running");

@@ -6,6 +6,9 @@
 // reference.  Built by tests/cpp/Makefile (needs /root/reference at build
 // time only); run by tests/test_gpu_dropin.py on a B200.
 #include <cstdio>
+#include <filesystem>
+#include <fstream>
+#include <unistd.h>
 #include <random>
 #include <string>
 
@@ -58,7 +61,53 @@ static void compare_engines(const std::string& what, const program& prog,
     CHECK(a.buffer_allocations == b.buffer_allocations, (what + ": buffer allocations").c_str());
 }
 
+// io.hpp restated: device read_facts / to_tsv / engine file load + write
+// against the reference's own functions, byte for byte.
+static void io_scenarios() {
+    namespace fs = std::filesystem;
+    const fs::path dir = fs::temp_directory_path() / ("gd_io_" + std::to_string(::getpid()));
+    fs::create_directories(dir);
+    auto write = [&](const std::string& name, const std::string& text) {
+        const fs::path p = dir / name;
+        std::ofstream(p, std::ios::binary) << text;
+        return p;
+    };
+    const std::vector<std::string> texts = {"1 2\n2 3\n1 2\n", "# h\n1\t2\n\n  3   4 \n\t5\t6\r\n", "1 2\n3 4 5\n",
+                                            "x 1\n", "1 18446744073709551615\n", "", "7 8"};
+    for (std::size_t i = 0; i < texts.size(); ++i) {
+        const fs::path p = write("f" + std::to_string(i) + ".tsv", texts[i]);
+        std::string ref_err, dev_err;
+        tuple_array r(2), d(2);
+        try { r = read_facts(p, 2); } catch (const load_error& e) { ref_err = e.what(); }
+        try { d = b200::read_facts(p, 2); } catch (const load_error& e) { dev_err = e.what(); }
+        CHECK(ref_err == dev_err, ("read_facts error " + std::to_string(i)).c_str());
+        CHECK(ref_err.empty() ? r == d : true, ("read_facts rows " + std::to_string(i)).c_str());
+        CHECK(file_is_all_integers(p) == b200::file_is_all_integers(p), "file_is_all_integers");
+    }
+    std::mt19937_64 rng(223);
+    for (int t = 0; t < 5; ++t) {
+        tuple_array rel = canonicalize(oracles::random_relation(rng, 3, 500, 1000));
+        CHECK(to_tsv(rel) == b200::to_tsv(rel), "to_tsv bytes");
+    }
+    // engine: load a fact file on the device, write the IDB as TSV
+    tuple_array edges = canonicalize(oracles::from_set(2, oracles::random_graph(rng, 200, 800)));
+    const fs::path ep = dir / "edge.tsv";
+    write_relation(edges, ep);
+    arraylog::engine re(builtin_program("reach"));
+    re.load_edb("Edge", read_facts(ep, 2));
+    re.run();
+    b200::engine ge(builtin_program("reach"));
+    ge.load_edb_file("Edge", ep);
+    ge.run();
+    ge.write_relation_file("Reach", dir / "reach.tsv");
+    std::ifstream in(dir / "reach.tsv", std::ios::binary);
+    const std::string got((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    CHECK(got == to_tsv(re.relation("Reach")), "engine TSV round trip");
+    fs::remove_all(dir);
+}
+
 int main() {
+    io_scenarios();
     // engine_test.cpp:42-52 (path5), :71-81 (SG tree), :83-93 (CSPA seed)
     compare_engines("reach path5", builtin_program("reach"), {{"Edge", chain_edges(5)}});
     {

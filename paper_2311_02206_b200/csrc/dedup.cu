@@ -29,9 +29,15 @@ __global__ void __launch_bounds__(kDT) dedup_insert_kernel(const u64* __restrict
             const u64 j = base + (u64)k * kDT + threadIdx.x;
             key[k] = j < m ? __ldcs(keys + j) : kEmptySlot;
         }
+        // load first, CAS only empty slots (duplicates — most rows here —
+        // never issue an atomic; the CAS hits the loaded line in L2)
 #pragma unroll
         for (int k = 0; k < kDPer; ++k)
-            old[k] = key[k] != kEmptySlot ? atomicCAS(&tab[fmix64(key[k]) & mask], kEmptySlot, key[k]) : key[k];
+            old[k] = key[k] != kEmptySlot ? __ldcg(&tab[fmix64(key[k]) & mask]) : key[k];
+#pragma unroll
+        for (int k = 0; k < kDPer; ++k)
+            if (key[k] != kEmptySlot && old[k] == kEmptySlot)
+                old[k] = atomicCAS(&tab[fmix64(key[k]) & mask], kEmptySlot, key[k]);
         u32 fresh = 0;
 #pragma unroll
         for (int k = 0; k < kDPer; ++k) {

@@ -129,10 +129,19 @@ __device__ __forceinline__ void hs_insert(const LoopHeadBufs& hb, u32 st, const 
     if (hb.sbits) {
         u64* tab = static_cast<u64*>(hb.tab);
         const u32 sb = hb.sbits;
+        // Load the home slots first, then CAS only the empty ones: the CAS
+        // hits the line the load brought into L2, and random inserts run at
+        // the random-load rate (37 G/s) instead of the CAS-miss rate (22 G/s)
+        // on B200 (profiles/r1_micro_random_access_loadcas_b200.txt).
+        u64 home[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            home[k] = hs_home(key[k], hb.tab_cap);
+            old[k] = (ok >> k & 1) ? __ldcg(&tab[home[k]]) : 0ull;
+        }
 #pragma unroll
         for (int k = 0; k < PER; ++k)
-            old[k] = (ok >> k & 1) ? atomicCAS(&tab[hs_home(key[k], hb.tab_cap)], kEmptySlot, key[k] << sb | st)
-                                   : 0ull;
+            if ((ok >> k & 1) && old[k] == kEmptySlot) old[k] = atomicCAS(&tab[home[k]], kEmptySlot, key[k] << sb | st);
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             if (!(ok >> k & 1)) continue;
@@ -900,6 +909,9 @@ int occupancy(Kern k, size_t smem = 0) {
 }
 
 int g_occ_temp = 0, g_occ_insert = 0, g_occ_select = 0, g_occ_keys = 0;
+// Insert grid = waves x resident CTAs: CTAs beyond the resident set start as
+// others finish, so the hardware balances the iteration's tiles.
+int g_ins_waves = 1;
 
 }  // namespace
 
@@ -1035,7 +1047,9 @@ void loop_materialize_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32
                              const LoopHeadBufs& hb, const LoopEndDesc* end) {
     LoopEndDesc e{};
     if (end) e = *end;
-    loop_materialize_insert_kernel<<<c.num_sms * g_occ_insert, kLT, 0, s>>>(ctl, step, head, o, inner, jd, sb, hb,
+    const char* w = getenv("GD_INSERT_WAVES");
+    g_ins_waves = w ? std::max(1, atoi(w)) : g_ins_waves;
+    loop_materialize_insert_kernel<<<c.num_sms * g_occ_insert * g_ins_waves, kLT, 0, s>>>(ctl, step, head, o, inner, jd, sb, hb,
                                                                              e, end ? 1 : 0);
     c.check_launch();
 }

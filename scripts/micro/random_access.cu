@@ -20,7 +20,13 @@ __global__ void kern(u64* t, u64 n, u64 ops, u64 win, u64* sink) {
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       if (MODE == 0) v[k] = __ldcg(t + p[k]);
-      else v[k] = atomicCAS(t + p[k], ~0ull, i + k);
+      else if (MODE == 1) v[k] = atomicCAS(t + p[k], ~0ull, i + k);
+      else v[k] = __ldcg(t + p[k]);
+    }
+    if (MODE == 2) {
+#pragma unroll
+      for (int k = 0; k < PER; ++k)
+        if (v[k] == ~0ull) v[k] = atomicCAS(t + p[k], ~0ull, i + k);
     }
 #pragma unroll
     for (int k = 0; k < PER; ++k) acc += v[k];
@@ -35,7 +41,7 @@ int main() {
   u64 ops = 1ull << 28;
   for (size_t bytes = 128ull << 20; bytes <= maxb; bytes *= 4) {
     u64 n = bytes / 8;
-    for (int mode = 0; mode < 2; ++mode) {
+    for (int mode = 0; mode < 3; ++mode) {
       for (u64 win : {0ull, 1ull << 20}) {  // win = 8 MB windows
         if (win && win >= n) continue;
         cudaMemset(t, 0xff, bytes);
@@ -43,11 +49,12 @@ int main() {
         for (int r = 0; r < 3; ++r) {
           cudaEventRecord(a);
           if (mode == 0) kern<0, 4><<<sms * 8, 256>>>(t, n, ops, win, sink);
-          else kern<1, 4><<<sms * 8, 256>>>(t, n, ops, win, sink);
+          else if (mode == 1) kern<1, 4><<<sms * 8, 256>>>(t, n, ops, win, sink);
+          else kern<2, 4><<<sms * 8, 256>>>(t, n, ops, win, sink);
           cudaEventRecord(b); cudaEventSynchronize(b);
           float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
         }
-        printf("%6zu MB  %-6s %-9s %7.2f Gops/s\n", bytes >> 20, mode ? "cas" : "load", win ? "win8MB" : "uniform", ops / (best * 1e6));
+        printf("%6zu MB  %-9s %-9s %7.2f Gops/s\n", bytes >> 20, mode == 0 ? "load" : mode == 1 ? "cas" : "load+cas", win ? "win8MB" : "uniform", ops / (best * 1e6));
       }
     }
   }

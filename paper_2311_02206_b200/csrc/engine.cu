@@ -257,9 +257,13 @@ public:
         for (auto& st : rels) compact(st);
     }
 
-    u64 count(u32 r) override { return total_n(rels[r]); }
+    u64 count(u32 r) override {
+        if (pl && pl->heads[0].rel == r) return pl->hc->h[0].log_n;
+        return total_n(rels[r]);
+    }
 
     void download(u32 r, u64* out, bool device) override {
+        if (pl) part_loop_finish();
         auto& st = rels[r];
         compact(st);
         const u32 ar = E.info_[r].arity;
@@ -358,6 +362,7 @@ public:
     }
 
     u64 digest(u32 r) override {
+        if (pl) part_loop_finish();
         compact(rels[r]);
         return digest_rows<K>(c, rels[r].full.p, rels[r].full_n, E.info_[r].arity, E.enc.e);
     }
@@ -513,6 +518,79 @@ public:
     // the re-spreads move about half the final key count in total.
     static u64 tab_limit_of(u64 cap) { return cap / 2; }
 
+    // The recursive variants as loop steps (plan order, variant order): outer
+    // source, join descriptor, inner copy and index (dense form when
+    // worthwhile) of every step.  Shared by iterate_loop and partition mode.
+    void build_loop_steps(const std::vector<u32>& rec, std::vector<LStep>& steps) {
+        auto head_of = [&](u32 r) -> u32 {
+            return (u32)(std::find(rec.begin(), rec.end(), r) - rec.begin());
+        };
+    for (u32 pi = 0; pi < E.plans_.size(); ++pi) {
+        const gd_rule_plan& p = E.plans_[pi];
+        if (!p.recursive) continue;
+        for (u32 v = 0; v < p.nvariants; ++v) {
+            const gd_variant& var = p.variants[v];
+            const u32 ar = E.info_[var.src_rel].arity;
+            u32 cur_ar = ar;
+            u32 cur_perm[kMaxArity];
+            for (u32 i = 0; i < kMaxArity; ++i) cur_perm[i] = i < ar ? var.src_perm[i] : i;
+            const u32 first = (u32)steps.size();
+            const u32 n = std::max<u32>(1, var.nsteps);
+            for (u32 s = 0; s < n; ++s) {
+                steps.emplace_back();
+                LStep& L = steps.back();
+                L.plan = pi;
+                L.var = v;
+                L.final = s + 1 == n;
+                L.split_insert = getenv("GD_LOOP_SPLIT") && getenv("GD_LOOP_SPLIT")[0] == '1';
+                L.head = head_of(p.head_rel);
+                if (s == 0) {
+                    auto it = std::find(rec.begin(), rec.end(), var.src_rel);
+                    if (it != rec.end()) {
+                        L.kind = var.src_version == GD_DELTA ? LO_DELTA : LO_FULL;
+                        L.src_head = (u32)(it - rec.begin());
+                    } else {
+                        auto& src = rels[var.src_rel];
+                        compact(src);
+                        L.kind = LO_STATIC;
+                        L.static_ptr = reinterpret_cast<const u64*>(src.full.p);
+                        L.static_n = src.full_n;
+                    }
+                } else {
+                    L.kind = LO_TEMP;
+                    L.src_step = first + s - 1;
+                }
+                if (var.nsteps == 0) {
+                    L.select = true;
+                    L.jd = make_desc(0, cur_ar, cur_perm, 0, var.sel_arity, var.sel_proj, var.nsel_filters,
+                                     var.sel_filters);
+                    continue;
+                }
+                const gd_join_step& st = var.steps[s];
+                auto& in = rels[st.inner_rel];
+                const u32 iar = E.info_[st.inner_rel].arity;
+                CopyState<K>& cp = in.copies.at(CopyKey{std::vector<u32>(st.inner_perm, st.inner_perm + iar),
+                                                        st.join_column_count});
+                L.inner = reinterpret_cast<const u64*>(cp.identity ? in.full.p : cp.rows.p);
+                L.inner_n = cp.identity ? in.full_n : cp.n;
+                L.jd = make_desc(st.join_column_count, cur_ar, cur_perm, iar, st.proj_arity, st.proj,
+                                 st.nfilters, st.filters);
+                L.proj_arity = st.proj_arity;
+                if (st.join_column_count > 0 && L.inner_n > 0) {
+                    L.has_iv = true;
+                    L.iv = IndexView<u64>{cp.index.slots.p, cp.index.slot_count, L.inner, L.inner_n, iar, bits,
+                                          st.join_column_count};
+                    if (st.join_column_count == 1 && !(getenv("GD_DENSE") && getenv("GD_DENSE")[0] == '0') &&
+                        loop_dense_build(c, L.inner, L.inner_n, iar, bits, L.dense, L.dv.lo, L.dv.span))
+                        L.dv.off = L.dense.p;
+                }
+                cur_ar = st.proj_arity;
+                for (u32 i = 0; i < kMaxArity; ++i) cur_perm[i] = i;
+            }
+        }
+    }
+    }
+
     void iterate_loop(const std::vector<u32>& rec, const std::vector<u32>& by_name) {
         bool active = false;
         for (u32 r : rec) active |= rels[r].delta_n > 0;
@@ -545,70 +623,7 @@ public:
 
         // variant-steps in execution order (plan order, variant order)
         std::vector<LStep> steps;
-        for (u32 pi = 0; pi < E.plans_.size(); ++pi) {
-            const gd_rule_plan& p = E.plans_[pi];
-            if (!p.recursive) continue;
-            for (u32 v = 0; v < p.nvariants; ++v) {
-                const gd_variant& var = p.variants[v];
-                const u32 ar = E.info_[var.src_rel].arity;
-                u32 cur_ar = ar;
-                u32 cur_perm[kMaxArity];
-                for (u32 i = 0; i < kMaxArity; ++i) cur_perm[i] = i < ar ? var.src_perm[i] : i;
-                const u32 first = (u32)steps.size();
-                const u32 n = std::max<u32>(1, var.nsteps);
-                for (u32 s = 0; s < n; ++s) {
-                    steps.emplace_back();
-                    LStep& L = steps.back();
-                    L.plan = pi;
-                    L.var = v;
-                    L.final = s + 1 == n;
-                    L.split_insert = getenv("GD_LOOP_SPLIT") && getenv("GD_LOOP_SPLIT")[0] == '1';
-                    L.head = head_of(p.head_rel);
-                    if (s == 0) {
-                        auto it = std::find(rec.begin(), rec.end(), var.src_rel);
-                        if (it != rec.end()) {
-                            L.kind = var.src_version == GD_DELTA ? LO_DELTA : LO_FULL;
-                            L.src_head = (u32)(it - rec.begin());
-                        } else {
-                            auto& src = rels[var.src_rel];
-                            compact(src);
-                            L.kind = LO_STATIC;
-                            L.static_ptr = reinterpret_cast<const u64*>(src.full.p);
-                            L.static_n = src.full_n;
-                        }
-                    } else {
-                        L.kind = LO_TEMP;
-                        L.src_step = first + s - 1;
-                    }
-                    if (var.nsteps == 0) {
-                        L.select = true;
-                        L.jd = make_desc(0, cur_ar, cur_perm, 0, var.sel_arity, var.sel_proj, var.nsel_filters,
-                                         var.sel_filters);
-                        continue;
-                    }
-                    const gd_join_step& st = var.steps[s];
-                    auto& in = rels[st.inner_rel];
-                    const u32 iar = E.info_[st.inner_rel].arity;
-                    CopyState<K>& cp = in.copies.at(CopyKey{std::vector<u32>(st.inner_perm, st.inner_perm + iar),
-                                                            st.join_column_count});
-                    L.inner = reinterpret_cast<const u64*>(cp.identity ? in.full.p : cp.rows.p);
-                    L.inner_n = cp.identity ? in.full_n : cp.n;
-                    L.jd = make_desc(st.join_column_count, cur_ar, cur_perm, iar, st.proj_arity, st.proj,
-                                     st.nfilters, st.filters);
-                    L.proj_arity = st.proj_arity;
-                    if (st.join_column_count > 0 && L.inner_n > 0) {
-                        L.has_iv = true;
-                        L.iv = IndexView<u64>{cp.index.slots.p, cp.index.slot_count, L.inner, L.inner_n, iar, bits,
-                                              st.join_column_count};
-                        if (st.join_column_count == 1 && !(getenv("GD_DENSE") && getenv("GD_DENSE")[0] == '0') &&
-                            loop_dense_build(c, L.inner, L.inner_n, iar, bits, L.dense, L.dv.lo, L.dv.span))
-                            L.dv.off = L.dense.p;
-                    }
-                    cur_ar = st.proj_arity;
-                    for (u32 i = 0; i < kMaxArity; ++i) cur_perm[i] = i;
-                }
-            }
-        }
+        build_loop_steps(rec, steps);
         const u32 ns = (u32)steps.size();
         const u64 d0 = rels[rec[0]].delta_n;
         for (auto& L : steps) {
@@ -1057,7 +1072,246 @@ public:
     // ---- hash-partitioned mode -----------------------------
     void partition_begin(u64* send_counts, const void** d_send) override;
     void partition_end(const void* d_recv, u64 recv_rows, u64* local_delta) override;
-    void partition_finish() override {}
+    void partition_finish() override { part_loop_finish(); }
+
+    // ---- partitioned mode on the loop kernels ------------------------------
+    // Per iteration (driven by partition.py): probe / scan / materialize of
+    // the local Δ into the final step's temp, rows grouped by owner on the
+    // device (the NCCL all-to-all sends them), then the received rows are
+    // inserted into this rank's full-tuple index and log (loop_insert_keys).
+    // The Δ window and the iteration record are kept on the host; capacities
+    // are grown before the kernels that need them, so nothing rolls back.
+    struct PartLoop {
+        std::vector<u32> rec;
+        std::vector<LHead> heads;
+        std::vector<LStep> steps;
+        DevBuf<LoopCtl> ctl;
+        std::unique_ptr<LoopCtl> host;  // own host copy: several engines may share one context
+        LoopCtl* hc = nullptr;
+        DevBuf<u64> block_sums, send;
+        DevBuf<unsigned long long> counts, offs, cursors;
+        u32 final_step = 0;
+    };
+    std::unique_ptr<PartLoop> pl;
+
+    bool part_loop_eligible(u32 rec_rel) {
+        if constexpr (!std::is_same_v<K, u64>) return false;
+        if (getenv("GD_PART_LOOP") && getenv("GD_PART_LOOP")[0] == '0') return false;
+        if (E.nranks > kLoopMaxRanks) return false;
+        const auto& st = rels[rec_rel];
+        if (!st.lsm || st.delta_n != total_n(st)) return false;
+        u32 nv = 0;
+        for (const auto& p : E.plans_) {
+            if (!p.recursive) continue;
+            for (u32 v = 0; v < p.nvariants; ++v) {
+                const gd_variant& var = p.variants[v];
+                if (var.src_rel != rec_rel || var.src_version != GD_DELTA || var.nsteps == 0) return false;
+                ++nv;
+            }
+        }
+        return nv == 1;  // one variant: the final step's temp is the send set
+    }
+
+    void part_loop_setup(u32 rec_rel) {
+        pl.reset(new PartLoop);
+        PartLoop& P = *pl;
+        loop_prepare();
+        std::vector<u32> by_name(rels.size());
+        for (u32 i = 0; i < by_name.size(); ++i) by_name[i] = i;
+        for (u32 r : by_name)
+            if (rels[r].dirty && !rels[r].copies.empty()) refresh_copies(r);
+        P.rec = {rec_rel};
+        P.heads.resize(1);
+        LHead& H = P.heads[0];
+        auto& st = rels[rec_rel];
+        compact(st);
+        H.rel = rec_rel;
+        const u64 f0 = st.full_n;
+        H.log_cap = std::max<u64>(2 * f0, 1 << 16);
+        H.log = DevBuf<u64>(c, H.log_cap);
+        if (f0) c.d2d(H.log.p, st.full.p, f0 * sizeof(u64));
+        H.sbits = loop_stamp_bits(E.info_[rec_rel].arity * bits);
+        H.alloc_tab(c, std::max<u64>(4 * f0, 1 << 16));
+        loop_table_fill(c, H.tab.p, H.tab_cap, H.sbits, H.log.p, f0);
+        build_loop_steps(P.rec, P.steps);
+        P.final_step = (u32)P.steps.size() - 1;
+        for (auto& L : P.steps) {
+            L.rows_cap = std::max<u64>(f0 + 1, 1 << 12);
+            L.splits_cap = std::max<u64>(2 * f0 / kLoopMatTile + 2, 1 << 12);
+            L.row_start = DevBuf<u64>(c, L.rows_cap);
+            L.row_off = DevBuf<u64>(c, L.rows_cap);
+            L.splits = DevBuf<u64>(c, L.splits_cap);
+            L.temp_cap = std::max<u64>(4 * f0, 1 << 16);
+            L.temp = DevBuf<u64>(c, L.temp_cap);
+        }
+        P.block_sums = DevBuf<u64>(c, (u64)loop_grid(c));
+        P.counts = DevBuf<unsigned long long>(c, kLoopMaxRanks);
+        P.offs = DevBuf<unsigned long long>(c, kLoopMaxRanks);
+        P.cursors = DevBuf<unsigned long long>(c, kLoopMaxRanks);
+        P.ctl = DevBuf<LoopCtl>(c, 1);
+        P.host.reset(new LoopCtl);
+        P.hc = P.host.get();
+        std::memset(P.hc, 0, sizeof(LoopCtl));
+        P.hc->nheads = 1;
+        P.hc->hist_cap = ~0ull;
+        P.hc->h[0].log_n = f0;
+        P.hc->h[0].dlo = f0 - st.delta_n;
+        P.hc->h[0].dhi = f0;
+        c.h2d(P.ctl.p, P.hc, sizeof(LoopCtl));
+    }
+
+    LoopHeadBufs part_bufs() {
+        LHead& H = pl->heads[0];
+        LoopHeadBufs b{};
+        b.log = H.log.p;
+        b.log_cap = H.log_cap;
+        b.tab = H.tab.p;
+        b.tab_cap = H.tab_cap;
+        b.tab_limit = H.tab_limit;
+        b.sbits = H.sbits;
+        return b;
+    }
+
+    void part_loop_begin(u64* send_counts, const void** d_send) {
+        PartLoop& P = *pl;
+        LoopCtl* hc = P.hc;
+        const u32 ns = (u32)P.steps.size();
+        for (;;) {  // the join part; regrown and rerun on a capacity overflow
+            for (u32 i = 0; i < ns; ++i) {
+                LStep& L = P.steps[i];
+                LoopOuter o{};
+                o.kind = L.kind;
+                o.head = L.src_head;
+                o.src_step = L.src_step;
+                o.ptr = L.kind == LO_TEMP ? P.steps[L.src_step].temp.p : P.heads[0].log.p;
+                loop_probe(c, c.stream, P.ctl.p, i, o, L.jd, L.has_iv ? &L.iv : nullptr, L.dv, L.inner_n, L.bufs(),
+                           P.block_sums.p);
+                loop_scan(c, c.stream, P.ctl.p, i, o, L.bufs(), P.block_sums.p, nullptr);
+                loop_materialize_temp(c, c.stream, P.ctl.p, i, o, L.inner, L.jd, L.bufs(), L.temp.p, L.temp_cap);
+            }
+            c.d2h(hc, P.ctl.p, sizeof(LoopCtl));
+            c.sync();
+            if (!hc->overflow) break;
+            for (u32 i = 0; i < ns; ++i) {
+                LStep& L = P.steps[i];
+                if (hc->need_rows[i] > L.rows_cap) {
+                    L.rows_cap = hc->need_rows[i] + hc->need_rows[i] / 2;
+                    L.row_start = DevBuf<u64>(c, L.rows_cap);
+                    L.row_off = DevBuf<u64>(c, L.rows_cap);
+                }
+                if (hc->need_splits[i] > L.splits_cap) {
+                    L.splits_cap = hc->need_splits[i] + hc->need_splits[i] / 2;
+                    L.splits = DevBuf<u64>(c, L.splits_cap);
+                }
+                if (hc->need_temp[i] > L.temp_cap) {
+                    L.temp_cap = hc->need_temp[i] + hc->need_temp[i] / 2;
+                    L.temp = DevBuf<u64>(c, L.temp_cap);
+                }
+                hc->need_rows[i] = hc->need_splits[i] = hc->need_temp[i] = 0;
+                hc->step_total[i] = 0;
+            }
+            hc->overflow = 0;
+            c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
+        }
+        for (u32 i = 0; i < ns; ++i) E.join_tuples += hc->step_total[i];
+        // group the final step's rows by owner
+        const u32 R = E.nranks;
+        const LStep& F = P.steps[P.final_step];
+        const u64 m = hc->step_total[P.final_step];
+        const u64* n_ptr = &P.ctl.p->step_total[P.final_step];
+        P.send.reserve_discard(c, std::max<u64>(m, 1));
+        c.memset(P.counts.p, 0, R * sizeof(unsigned long long));
+        c.memset(P.cursors.p, 0, R * sizeof(unsigned long long));
+        if (m) loop_owner_count(c, F.temp.p, n_ptr, R, P.counts.p);
+        unsigned long long cnt[kLoopMaxRanks] = {};
+        c.d2h(cnt, P.counts.p, R * sizeof(unsigned long long));
+        c.sync();
+        unsigned long long off[kLoopMaxRanks];
+        u64 acc = 0;
+        for (u32 k = 0; k < R; ++k) {
+            off[k] = acc;
+            acc += cnt[k];
+            send_counts[k] = cnt[k];
+        }
+        c.h2d(P.offs.p, off, R * sizeof(unsigned long long));
+        if (m) loop_owner_scatter(c, F.temp.p, n_ptr, R, P.offs.p, P.cursors.p, P.send.p);
+        c.sync();
+        // clear the per-iteration step totals for the next iteration
+        for (u32 i = 0; i < ns; ++i) hc->step_total[i] = 0;
+        c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
+        *d_send = m ? P.send.p : nullptr;
+    }
+
+    void part_loop_end(const void* d_recv, u64 recv_rows, u64* local_delta) {
+        PartLoop& P = *pl;
+        LoopCtl* hc = P.hc;
+        LHead& H = P.heads[0];
+        const u32 r = H.rel;
+        const u64 din = hc->h[0].dhi - hc->h[0].dlo;
+        ++E.iterations;
+        E.info_[r].history.push_back(din);
+        // capacities before the inserts (no rollback in this mode)
+        const u64 ln = hc->h[0].log_n;
+        const u64 need = ln + recv_rows;
+        if (need > H.log_cap) {
+            const u64 cap = 2 * need;
+            DevBuf<u64> nl(c, cap);
+            if (ln) c.d2d(nl.p, H.log.p, ln * sizeof(u64));
+            H.log = std::move(nl);
+            H.log_cap = cap;
+        }
+        if (need > H.tab_limit) {
+            DevBuf<u64> old = std::move(H.tab);
+            const u64 old_cap = H.tab_cap;
+            H.alloc_tab(c, 6 * need);
+            loop_table_rehash(c, old.p, old_cap, H.tab.p, H.tab_cap, H.sbits, ln);
+        }
+        if (hc->iter + 1 - hc->epoch_base > (H.sbits ? (1u << H.sbits) - 1 : 0xfffffffeu)) {
+            loop_table_restamp(c, H.tab.p, H.tab_cap, H.sbits);
+            hc->epoch_base = hc->iter;
+        }
+        hc->step_total[P.final_step] = recv_rows;  // the insert kernel's row count
+        hc->h[0].J = hc->h[0].N = hc->h[0].D = 0;
+        c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
+        if (recv_rows)
+            loop_insert_keys(c, c.stream, P.ctl.p, P.final_step, 0, static_cast<const u64*>(d_recv), part_bufs(),
+                             nullptr);
+        c.d2h(hc, P.ctl.p, sizeof(LoopCtl));
+        c.sync();
+        const u64 D = hc->h[0].D, N = hc->h[0].N;
+        hc->h[0].dlo = hc->h[0].dhi;
+        hc->h[0].dhi = hc->h[0].log_n;
+        hc->iter += 1;
+        hc->step_total[P.final_step] = 0;
+        c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
+        E.info_[r].log.push_back(gd_iter_record{din, recv_rows, N, D, hc->h[0].log_n});
+        *local_delta = D;
+    }
+
+    // The canonical local shard: sort the log once (like iterate_loop).
+    void part_loop_finish() {
+        if (!pl) return;
+        PartLoop& P = *pl;
+        LHead& H = P.heads[0];
+        auto& st = rels[H.rel];
+        H.tab.release();
+        const u64 f = P.hc->h[0].log_n;
+        const u32 ar = E.info_[H.rel].arity;
+        DevBuf<u64> scratch(c, std::max<u64>(f, 1));
+        u64* sorted = radix_sort<u64>(c, H.log.p, scratch.p, f, ar * bits);
+        DevBuf<u64>& res = sorted == H.log.p ? H.log : scratch;
+        st.full.release();
+        st.full.ctx = res.ctx;
+        st.full.p = reinterpret_cast<K*>(res.p);
+        st.full.cap = res.cap;
+        res.p = nullptr;
+        res.cap = 0;
+        st.full_n = f;
+        st.tail.clear();
+        st.delta_n = 0;
+        st.new_n = 0;
+        pl.reset();
+    }
 
 private:
     Engine& E;
@@ -1444,6 +1698,13 @@ void Impl<K>::partition_begin(u64* send_counts, const void** d_send) {
     u32 rec_rel = UINT32_MAX;
     for (const auto& p : E.plans_)
         if (p.recursive) rec_rel = p.head_rel;
+    if constexpr (std::is_same_v<K, u64>) {
+        if (pl || part_loop_eligible(rec_rel)) {
+            if (!pl) part_loop_setup(rec_rel);
+            part_loop_begin(send_counts, d_send);
+            return;
+        }
+    }
     auto& head = rels[rec_rel];
     const u32 ar = E.info_[rec_rel].arity;
     for (u32 r = 0; r < rels.size(); ++r)
@@ -1492,6 +1753,12 @@ void Impl<K>::partition_begin(u64* send_counts, const void** d_send) {
 
 template <typename K>
 void Impl<K>::partition_end(const void* d_recv, u64 recv_rows, u64* local_delta) {
+    if constexpr (std::is_same_v<K, u64>) {
+        if (pl) {
+            part_loop_end(d_recv, recv_rows, local_delta);
+            return;
+        }
+    }
     u32 rec_rel = UINT32_MAX;
     for (const auto& p : E.plans_)
         if (p.recursive) rec_rel = p.head_rel;

@@ -901,6 +901,60 @@ __global__ void table_restamp_kernel(void* tab, u64 cap, u32 sb) {
     }
 }
 
+// ---- partitioned mode: group a step's join rows by owner rank -----------
+// owner(key) = key_hash64(key) mod P, the function keep_owned partitions
+// the seeded relation with (engine.cu).  Pass 1 counts per destination;
+// pass 2 reserves one range per (CTA tile, destination) and scatters every
+// row to offsets[dst] + range + its rank in the tile (shared atomics).
+constexpr u32 kOwnTile = 2048;
+constexpr u32 kMaxRanks = 64;
+
+__global__ void owner_count_kernel(const u64* __restrict__ keys, const u64* __restrict__ n_ptr, u32 P,
+                                   unsigned long long* __restrict__ counts) {
+    __shared__ u32 sc[kMaxRanks];
+    for (u32 i = threadIdx.x; i < P; i += blockDim.x) sc[i] = 0;
+    __syncthreads();
+    const u64 n = *n_ptr;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        atomicAdd(&sc[key_hash64<u64>(keys[i]) % P], 1u);
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < P; i += blockDim.x)
+        if (sc[i]) atomicAdd(&counts[i], (unsigned long long)sc[i]);
+}
+
+__global__ void owner_scatter_kernel(const u64* __restrict__ keys, const u64* __restrict__ n_ptr, u32 P,
+                                     const unsigned long long* __restrict__ offsets,
+                                     unsigned long long* __restrict__ cursors, u64* __restrict__ out) {
+    __shared__ u32 sc[kMaxRanks];
+    __shared__ unsigned long long sb[kMaxRanks];
+    const u64 n = *n_ptr;
+    for (u64 t0 = (u64)blockIdx.x * kOwnTile; t0 < n; t0 += (u64)gridDim.x * kOwnTile) {
+        for (u32 i = threadIdx.x; i < P; i += blockDim.x) sc[i] = 0;
+        __syncthreads();
+        constexpr u32 kPerT = kOwnTile / 256;
+        u64 k[kPerT];
+        u32 dst[kPerT], rank[kPerT];
+#pragma unroll
+        for (u32 q = 0; q < kPerT; ++q) {
+            const u64 i = t0 + q * 256 + threadIdx.x;
+            dst[q] = kMaxRanks;
+            if (i < n) {
+                k[q] = keys[i];
+                dst[q] = (u32)(key_hash64<u64>(k[q]) % P);
+                rank[q] = atomicAdd(&sc[dst[q]], 1u);
+            }
+        }
+        __syncthreads();
+        for (u32 i = threadIdx.x; i < P; i += blockDim.x)
+            sb[i] = sc[i] ? offsets[i] + atomicAdd(&cursors[i], (unsigned long long)sc[i]) : 0;
+        __syncthreads();
+#pragma unroll
+        for (u32 q = 0; q < kPerT; ++q)
+            if (dst[q] < kMaxRanks) out[sb[dst[q]] + rank[q]] = k[q];
+        __syncthreads();
+    }
+}
+
 template <typename Kern>
 int occupancy(Kern k, size_t smem = 0) {
     int b = 0;
@@ -1060,6 +1114,17 @@ void loop_select_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head
     if (end) e = *end;
     loop_select_insert_kernel<<<c.num_sms * g_occ_select, kLT, 0, s>>>(ctl, step, head, o, jd, hb, e,
                                                                         end ? 1 : 0);
+    c.check_launch();
+}
+
+void loop_owner_count(Ctx& c, const u64* keys, const u64* n_ptr, u32 P, unsigned long long* counts) {
+    owner_count_kernel<<<c.num_sms * 4, 256, 0, c.stream>>>(keys, n_ptr, P, counts);
+    c.check_launch();
+}
+
+void loop_owner_scatter(Ctx& c, const u64* keys, const u64* n_ptr, u32 P, const unsigned long long* offsets,
+                        unsigned long long* cursors, u64* out) {
+    owner_scatter_kernel<<<c.num_sms * 4, 256, 0, c.stream>>>(keys, n_ptr, P, offsets, cursors, out);
     c.check_launch();
 }
 

@@ -188,6 +188,15 @@ void loop_insert_keys(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, 
                       const LoopHeadBufs& hb, const LoopEndDesc* end);
 void loop_select_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
                         const DevJoin& jd, const LoopHeadBufs& hb, const LoopEndDesc* end);
+// ---- partitioned mode ----
+constexpr u32 kLoopMaxRanks = 64;
+// Per-destination counts of keys[0, *n_ptr) (owner = key_hash64(key) mod P).
+void loop_owner_count(Ctx& c, const u64* keys, const u64* n_ptr, u32 P, unsigned long long* counts);
+// Scatter into out grouped by destination (offsets: exclusive prefix of the
+// counts; cursors zeroed).  Order inside a group is unspecified.
+void loop_owner_scatter(Ctx& c, const u64* keys, const u64* n_ptr, u32 P, const unsigned long long* offsets,
+                        unsigned long long* cursors, u64* out);
+
 // Records the iteration (or rolls it back on overflow) and sets the graph's
 // while-condition (cond ignored unless use_cond).
 void loop_end(Ctx& c, cudaStream_t s, LoopCtl* ctl, const LoopEndDesc& end);

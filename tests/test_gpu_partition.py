@@ -21,11 +21,17 @@ def single(prog, edges):
     return e
 
 
+@pytest.mark.parametrize("path", ["loop", "host"])
 @pytest.mark.parametrize("prog,head,P,seed,n,dom", [
     ("reach", "Reach", 2, 1, 3000, 1500), ("reach", "Reach", 3, 2, 5000, 4000), ("reach", "Reach", 4, 3, 800, 300),
-    ("sg", "SG", 2, 4, 1500, 1000), ("sg", "SG", 4, 5, 2000, 2500),
+    ("reach", "Reach", 8, 6, 20000, 8000), ("sg", "SG", 2, 4, 1500, 1000), ("sg", "SG", 4, 5, 2000, 2500),
 ])
-def test_partitioned_equals_single(prog, head, P, seed, n, dom):
+def test_partitioned_equals_single(prog, head, P, seed, n, dom, path, monkeypatch):
+    """path "loop": the per-iteration kernels of the resident loop (probe /
+    scan / materialize, owner grouping, index insert); "host": the sort /
+    merge host path (GD_PART_LOOP=0)."""
+    if path == "host":
+        monkeypatch.setenv("GD_PART_LOOP", "0")
     rng = np.random.default_rng(seed)
     edges = random_relation(rng, 2, n, dom)
     ref = single(prog, edges)

@@ -231,11 +231,20 @@ struct Ctx {
         const double t0 = now_s();
         ++alloc_count;
         void* p = nullptr;
-        auto it = cache_.find(cls);
-        if (it != cache_.end()) {
+        // exact size class, else the smallest cached block up to 1.5x (a
+        // different workload on the same context reuses what it can instead
+        // of growing the pool)
+        auto it = cache_.lower_bound(cls);
+        if (it != cache_.end() && it->first <= cls + cls / 2) {
             p = it->second;
+            const size_t got = it->first;
             cache_.erase(it);
-            cached_bytes -= cls;
+            cached_bytes -= got;
+            alloc_seconds += now_s() - t0;
+            live_[p] = got;
+            bytes_in_use += got;
+            if (bytes_in_use > bytes_peak) bytes_peak = bytes_in_use;
+            return p;
         } else {
             cudaError_t e = cudaMallocAsync(&p, cls, stream);
             if (e == cudaErrorMemoryAllocation) {

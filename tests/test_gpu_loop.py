@@ -125,13 +125,16 @@ def test_hash_predup_matches_sort_path():
     a, d = W.cspa_local(300_000, 72_000, 228_000, 256, 2)
     db = {"assign": a, "dereference": d}
     outs = {}
-    for mode in ("1", "0"):
-        with env(GD_HASH_DEDUP=mode):
+    for mode, kv in (("1", {"GD_HASH_DEDUP": "1"}), ("0", {"GD_HASH_DEDUP": "0"}),
+                     ("split", {"GD_HASH_DEDUP": "1", "GD_DEDUP_L2_SLOTS": "65536"})):
+        with env(**kv):
             outs[mode] = run_gpu("cspa", db)
     g, h = outs["1"], outs["0"]
     for n in ("ValueFlow", "MemoryAlias", "ValueAlias"):
         assert np.array_equal(g.relation(n).data, h.relation(n).data), n
         assert g.iter_log(n) == h.iter_log(n), n
+        assert np.array_equal(outs["split"].relation(n).data, h.relation(n).data), n
+        assert outs["split"].iter_log(n) == h.iter_log(n), n
     assert max(r[1] for r in g.iter_log("ValueAlias")) >= (1 << 20)  # the hash path ran
     gs, hs = g.raw_stats(), h.raw_stats()
     assert (gs.charge_events, gs.peak_tracked_bytes, gs.join_tuples) == (hs.charge_events, hs.peak_tracked_bytes,

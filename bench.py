@@ -63,11 +63,14 @@ class ClockSampler:
         self.path = ROOT / "gpurun_out" / f"clocks_rank{device}.csv"
 
     def start(self):
+        if os.environ.get("GD_BENCH_CLOCK_MS") == "0":  # diagnostics only: no sampling
+            return
         try:
             self.path.parent.mkdir(exist_ok=True)
             self.f = open(self.path, "w")
+            ms = os.environ.get("GD_BENCH_CLOCK_MS", "200")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", ms],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:  # noqa: BLE001
             self.proc = None
@@ -103,7 +106,16 @@ class ClockSampler:
 
 
 def flush_l2(torch, buf):
-    buf.add_(1)  # 256 MiB write > 126 MB L2
+    mode = os.environ.get("GD_BENCH_FLUSH", "add")  # diagnostics: add | fill | none | addsleep
+    if mode == "none":
+        return
+    if mode == "fill":
+        buf.fill_(1)  # 256 MiB write > 126 MB L2
+        return
+    buf.add_(1)  # 256 MiB read-modify-write > 126 MB L2
+    if mode == "addsleep":
+        torch.cuda.synchronize()
+        time.sleep(0.02)
 
 
 def gen_workload():
@@ -202,6 +214,10 @@ def main():
     sampler = ClockSampler(local)
     launches0 = ctx.kernel_launches
     times, joins = [], []
+    step_detail = []
+    canary = torch.empty(21 << 27, dtype=torch.int64, device="cuda") if os.environ.get("GD_BENCH_CANARY") else None
+    canary_ms = []
+    hc0 = ctx.host_counters()
     sampler.start()
     for _ in range(args.steps):
         flush_l2(torch, flush)
@@ -215,6 +231,12 @@ def main():
         t1.record(stream)
         torch.cuda.synchronize()
         ms = t0.elapsed_time(t1)
+        ph = e.stats().phase_seconds
+        hc = ctx.host_counters()
+        step_detail.append({k: round(v * 1e3, 1) for k, v in ph.items()} |
+                           {"alloc_ms": round((hc["alloc_s"] - hc0["alloc_s"]) * 1e3, 1),
+                            "allocs": hc["allocs"] - hc0["allocs"]})
+        hc0 = hc
         jt = e.raw_stats().join_tuples
         reach_n = e.relation_count(HEAD)
         iters = e.raw_stats().iterations
@@ -227,6 +249,13 @@ def main():
         times.append(ms)
         joins.append(jt)
         e.close()
+        if canary is not None:  # diagnostics: GPU memory-op speed outside the engine
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            canary.fill_(-1)
+            c1.record(stream)
+            torch.cuda.synchronize()
+            canary_ms.append(round(c0.elapsed_time(c1), 1))
     clocks = sampler.stop()
     launches = ctx.kernel_launches - launches0
 
@@ -340,6 +369,8 @@ def main():
                        "reach": int(reach_n), "iterations": int(iters), "join_tuples": int(np.mean(joins)),
                        "parallelism": f"hash-partitioned x{world}" if world > 1 else "single",
                        "l2": "flushed between steps (256 MiB write)"},
+            "step_ms": [round(t, 2) for t in times], "step_phases_ms": step_detail,
+            **({"canary_fill_ms": canary_ms} if canary_ms else {}),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks,
         }

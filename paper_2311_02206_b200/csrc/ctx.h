@@ -157,15 +157,12 @@ struct Ctx {
             GD_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
             own_stream = true;
         }
-        cudaMemPool_t pool;
-        GD_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-        uint64_t thresh = UINT64_MAX;  // keep freed blocks cached in the pool
-        GD_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
         GD_CUDA(cudaMallocHost(&pinned, kPinnedWords * sizeof(unsigned long long)));
     }
     ~Ctx() {
         flush_cache();
-        for (auto& kv : live_) cudaFreeAsync(kv.first, stream);
+        cudaStreamSynchronize(stream);
+        for (auto& kv : live_) cudaFree(kv.first);
         live_.clear();
         cudaStreamSynchronize(stream);
         if (pinned) cudaFreeHost(pinned);
@@ -220,7 +217,8 @@ struct Ctx {
     }
 
     void flush_cache() {
-        for (auto& kv : cache_) cudaFreeAsync(kv.second, stream);
+        if (!cache_.empty()) cudaStreamSynchronize(stream);  // cached blocks may still be in use
+        for (auto& kv : cache_) cudaFree(kv.second);
         cache_.clear();
         cached_bytes = 0;
     }
@@ -231,11 +229,10 @@ struct Ctx {
         const double t0 = now_s();
         ++alloc_count;
         void* p = nullptr;
-        // exact size class, else the smallest cached block up to 1.5x (a
-        // different workload on the same context reuses what it can instead
-        // of growing the pool)
-        auto it = cache_.lower_bound(cls);
-        if (it != cache_.end() && it->first <= cls + cls / 2) {
+        // exact size class from the cache; else a new block; when HBM is
+        // exhausted, the smallest cached block up to 2x (a different workload
+        // on the same context), and only then flush the cache and retry
+        auto take = [&](std::multimap<size_t, void*>::iterator it) {
             p = it->second;
             const size_t got = it->first;
             cache_.erase(it);
@@ -245,22 +242,27 @@ struct Ctx {
             bytes_in_use += got;
             if (bytes_in_use > bytes_peak) bytes_peak = bytes_in_use;
             return p;
-        } else {
-            cudaError_t e = cudaMallocAsync(&p, cls, stream);
-            if (e == cudaErrorMemoryAllocation) {
-                cudaGetLastError();
-                flush_cache();
-                e = cudaMallocAsync(&p, cls, stream);
-            }
-            if (e == cudaErrorMemoryAllocation) {
-                cudaGetLastError();
-                alloc_seconds += now_s() - t0;
-                throw_budget(cur_phase, "device allocation of " + std::to_string(bytes) +
-                                            " bytes failed (HBM exhausted)");
-            }
-            if (e != cudaSuccess)
-                throw Error(GD_ERR_CUDA, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+        };
+        auto it = cache_.find(cls);
+        if (it != cache_.end()) return take(it);
+        // plain cudaMalloc: blocks live in this cache for the context's
+        // life; pool (cudaMallocAsync) memory showed erratic speed for
+        // large fills/copies in some processes
+        cudaError_t e = cudaMalloc(&p, cls);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            auto fit = cache_.lower_bound(cls);
+            if (fit != cache_.end() && fit->first <= 2 * cls) return take(fit);
+            flush_cache();
+            e = cudaMalloc(&p, cls);
         }
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            alloc_seconds += now_s() - t0;
+            throw_budget(cur_phase, "device allocation of " + std::to_string(bytes) +
+                                        " bytes failed (HBM exhausted)");
+        }
+        if (e != cudaSuccess) throw Error(GD_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
         alloc_seconds += now_s() - t0;
         live_[p] = cls;
         bytes_in_use += cls;
@@ -271,7 +273,8 @@ struct Ctx {
         if (!p) return;
         auto it = live_.find(p);
         if (it == live_.end()) {
-            cudaFreeAsync(p, stream);
+            cudaStreamSynchronize(stream);
+            cudaFree(p);
             return;
         }
         const size_t cls = it->second;

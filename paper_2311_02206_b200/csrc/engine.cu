@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <set>
+#include <atomic>
 #include <thread>
 #include <type_traits>
 #if defined(__x86_64__)
@@ -311,6 +312,57 @@ public:
         };
         const bool trace = getenv("GD_DL_TRACE") && getenv("GD_DL_TRACE")[0] == '1';
         double t_wait = 0, t_unpack = 0;
+        // one pool of nt threads for the whole download; chunk k is handed
+        // out by a generation counter once its copy has landed
+        std::atomic<u64> gen{0};
+        std::atomic<unsigned> left{0};
+        std::atomic<bool> quit{false};
+        const u64* cur_src = nullptr;
+        u64* cur_dst = nullptr;
+        u64 cur_m = 0;
+        auto unpack = [&](unsigned t) {
+            const u64 m = cur_m, lo = m * t / nt, hi = m * (t + 1) / nt;
+            const u64* src = cur_src;
+            u64* dst = cur_dst;
+            if (ar == 2) {
+#if defined(__x86_64__)
+                // non-temporal stores: the rows are written once and not read
+                // back here, so skip the read-for-ownership of each line
+                long long* d = reinterpret_cast<long long*>(dst);
+                for (u64 i = lo; i < hi; ++i) {
+                    const u64 key = src[i];
+                    _mm_stream_si64(d + 2 * i, (long long)((key >> bits) & mask));
+                    _mm_stream_si64(d + 2 * i + 1, (long long)(key & mask));
+                }
+                _mm_sfence();
+#else
+                for (u64 i = lo; i < hi; ++i) {
+                    const u64 key = src[i];
+                    dst[2 * i] = (key >> bits) & mask;
+                    dst[2 * i + 1] = key & mask;
+                }
+#endif
+            } else {
+                for (u64 i = lo; i < hi; ++i) {
+                    const u64 key = src[i];
+                    for (u32 col = 0; col < ar; ++col) dst[i * ar + col] = (key >> ((ar - 1 - col) * bits)) & mask;
+                }
+            }
+        };
+        std::vector<std::thread> pool;
+        for (unsigned t = 1; t < nt; ++t)
+            pool.emplace_back([&, t] {
+                u64 seen = 0;
+                while (true) {
+                    u64 g;
+                    while ((g = gen.load(std::memory_order_acquire)) == seen && !quit.load(std::memory_order_acquire))
+                        std::this_thread::yield();
+                    if (quit.load(std::memory_order_acquire)) return;
+                    seen = g;
+                    unpack(t);
+                    left.fetch_sub(1, std::memory_order_acq_rel);
+                }
+            });
         issue(0);
         for (u64 k = 0; k < nchunks; ++k) {
             const double tw = Ctx::now_s();
@@ -318,42 +370,18 @@ public:
             t_wait += Ctx::now_s() - tw;
             const double tu = Ctx::now_s();
             if (k + 1 < nchunks) issue(k + 1);  // staging[(k+1)&1] was unpacked at step k-1
-            const u64 b = k * kChunk, m = std::min(kChunk, n - b);
-            const u64* src = stage[k & 1];
-            u64* dst = out + b * ar;
-            auto work = [&](unsigned t) {
-                const u64 lo = m * t / nt, hi = m * (t + 1) / nt;
-                if (ar == 2) {
-#if defined(__x86_64__)
-                    // non-temporal stores: the rows are written once and not
-                    // read back here, so skip the read-for-ownership of each line
-                    long long* d = reinterpret_cast<long long*>(dst);
-                    for (u64 i = lo; i < hi; ++i) {
-                        const u64 key = src[i];
-                        _mm_stream_si64(d + 2 * i, (long long)((key >> bits) & mask));
-                        _mm_stream_si64(d + 2 * i + 1, (long long)(key & mask));
-                    }
-                    _mm_sfence();
-#else
-                    for (u64 i = lo; i < hi; ++i) {
-                        const u64 key = src[i];
-                        dst[2 * i] = (key >> bits) & mask;
-                        dst[2 * i + 1] = key & mask;
-                    }
-#endif
-                } else {
-                    for (u64 i = lo; i < hi; ++i) {
-                        const u64 key = src[i];
-                        for (u32 col = 0; col < ar; ++col) dst[i * ar + col] = (key >> ((ar - 1 - col) * bits)) & mask;
-                    }
-                }
-            };
-            std::vector<std::thread> pool;
-            for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work, t);
-            work(0);
-            for (auto& th : pool) th.join();
+            const u64 b = k * kChunk;
+            cur_m = std::min(kChunk, n - b);
+            cur_src = stage[k & 1];
+            cur_dst = out + b * ar;
+            left.store(nt - 1, std::memory_order_release);
+            gen.fetch_add(1, std::memory_order_acq_rel);
+            unpack(0);
+            while (left.load(std::memory_order_acquire) != 0) std::this_thread::yield();
             t_unpack += Ctx::now_s() - tu;
         }
+        quit.store(true, std::memory_order_release);
+        for (auto& th : pool) th.join();
         if (trace)
             fprintf(stderr, "[download] %llu rows, %u threads: waiting on PCIe %.1f ms, unpacking %.1f ms\n",
                     (unsigned long long)n, nt, t_wait * 1e3, t_unpack * 1e3);
@@ -615,7 +643,7 @@ public:
             const u64 f0 = st.full_n;
             heads[h].log_cap = tiny ? std::max<u64>(f0, 1) : std::max<u64>(2 * f0, 1 << 16);
             heads[h].log = DevBuf<u64>(c, heads[h].log_cap);
-            if (f0) c.d2d(heads[h].log.p, st.full.p, f0 * sizeof(u64));
+            if (f0) loop_copy_u64(c, heads[h].log.p, reinterpret_cast<const u64*>(st.full.p), f0);
             heads[h].sbits = loop_stamp_bits(E.info_[rec[h]].arity * bits);
             heads[h].alloc_tab(c, tiny ? 2 * f0 + 16 : std::max<u64>(4 * f0, 1 << 16));
             loop_table_fill(c, heads[h].tab.p, heads[h].tab_cap, heads[h].sbits, heads[h].log.p, f0);
@@ -887,15 +915,27 @@ public:
                     for (u32 h = 0; h < nh; ++h) {
                         LHead& H = heads[h];
                         const u64 ln = hc->h[h].log_n;
+                        cudaEvent_t ev0 = nullptr, ev1 = nullptr;
                         auto tr = [&](const char* what, u64 a, u64 b2) {
                             if (!trace) return;
+                            cudaEventRecord(ev1, c.stream);
                             c.sync();
                             const double t1 = Ctx::now_s();
-                            fprintf(stderr, "[loop] iter %u %s %llu -> %llu: %.3f ms\n", hc->iter, what,
-                                    (unsigned long long)a, (unsigned long long)b2, (t1 - tlast) * 1e3);
+                            float gms = 0;
+                            cudaEventElapsedTime(&gms, ev0, ev1);
+                            fprintf(stderr, "[loop] iter %u %s %llu -> %llu: %.3f ms (gpu %.3f ms)\n", hc->iter, what,
+                                    (unsigned long long)a, (unsigned long long)b2, (t1 - tlast) * 1e3, gms);
                             tlast = t1;
+                            std::swap(ev0, ev1);
+                            cudaEventRecord(ev0, c.stream);
                         };
-                        if (trace) { c.sync(); tlast = Ctx::now_s(); }
+                        if (trace) {
+                            cudaEventCreate(&ev0);
+                            cudaEventCreate(&ev1);
+                            c.sync();
+                            tlast = Ctx::now_s();
+                            cudaEventRecord(ev0, c.stream);
+                        }
                         // Growth is sized against free HBM (C5-scale runs): 2x
                         // for the log and 3x for the index when they fit, else
                         // the largest size that does (index load up to 3/4).
@@ -906,7 +946,7 @@ public:
                             const u64 fit = avail > reserve ? (avail - reserve) / sizeof(u64) : 0;
                             const u64 cap = std::max(need + need / 16 + 1024, std::min(2 * need, fit));
                             DevBuf<u64> nl(c, cap);
-                            if (ln) c.d2d(nl.p, H.log.p, ln * sizeof(u64));
+                            if (ln) loop_copy_u64(c, nl.p, H.log.p, ln);
                             H.log = std::move(nl);
                             tr("log", H.log_cap, cap);
                             H.log_cap = cap;
@@ -1256,7 +1296,7 @@ public:
         if (need > H.log_cap) {
             const u64 cap = 2 * need;
             DevBuf<u64> nl(c, cap);
-            if (ln) c.d2d(nl.p, H.log.p, ln * sizeof(u64));
+            if (ln) loop_copy_u64(c, nl.p, H.log.p, ln);
             H.log = std::move(nl);
             H.log_cap = cap;
         }
@@ -1871,11 +1911,10 @@ void Engine::load_edb(u32 r, const u64* rows, u64 n, bool canonical, bool device
         if (n && max_value(c, up.p, n * ar) == kEmptySlot)
             throw_load("load_edb: '" + info_[r].name + "' contains the reserved sentinel value");
     } else {
-        for (u64 i = 0; i < n * ar; ++i)
-            if (rows[i] == kEmptySlot)
-                throw_load("load_edb: '" + info_[r].name + "' contains the reserved sentinel value");
         c.h2d(up.p, rows, n * ar * sizeof(u64));
-        c.sync();
+        // sentinel check on the device (one pass over the uploaded rows)
+        if (n && max_value(c, up.p, n * ar) == kEmptySlot)
+            throw_load("load_edb: '" + info_[r].name + "' contains the reserved sentinel value");
     }
     u64 m = n;
     if (canonical) {

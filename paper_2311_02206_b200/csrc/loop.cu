@@ -955,6 +955,17 @@ __global__ void owner_scatter_kernel(const u64* __restrict__ keys, const u64* __
     }
 }
 
+// Streaming fill / copy for the growth path (16-byte vectors; the driver's
+// memset / device-to-device memcpy showed 3-146 ms for the same sizes).
+__global__ void fill_u64_kernel(ulonglong2* __restrict__ p, u64 n2, u64 v) {
+    const ulonglong2 w = make_ulonglong2(v, v);
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (u64)gridDim.x * blockDim.x) p[i] = w;
+}
+__global__ void copy_u64_kernel(ulonglong2* __restrict__ d, const ulonglong2* __restrict__ s, u64 n2) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (u64)gridDim.x * blockDim.x)
+        d[i] = __ldcs(s + i);
+}
+
 template <typename Kern>
 int occupancy(Kern k, size_t smem = 0) {
     int b = 0;
@@ -979,7 +990,37 @@ void loop_prepare() {
     g_occ_select = occupancy(loop_select_insert_kernel);
 }
 
-void loop_table_clear(Ctx& c, void* tab, u64 cap, u32 sbits) { c.memset(tab, 0xff, cap * loop_slot_bytes(sbits)); }
+void loop_fill_u64(Ctx& c, u64* p, u64 n, u64 v) {
+    if (n == 0) return;
+    if ((reinterpret_cast<uintptr_t>(p) & 15) || (n & 1)) {  // allocator blocks are 256-aligned; odd tails only
+        c.memset(p, (int)(v & 0xff), n * sizeof(u64));
+        if (v != (v & 0xff) * 0x0101010101010101ull) throw_logic("loop_fill_u64: unaligned non-byte fill");
+        return;
+    }
+    const u64 n2 = n / 2;
+    fill_u64_kernel<<<(int)std::min<u64>((n2 + 255) / 256, (u64)c.num_sms * 16), 256, 0, c.stream>>>(
+        reinterpret_cast<ulonglong2*>(p), n2, v);
+    c.check_launch();
+}
+
+void loop_copy_u64(Ctx& c, u64* d, const u64* s, u64 n) {
+    if (n == 0) return;
+    const u64 n2 = n / 2;
+    if (n2 && !(reinterpret_cast<uintptr_t>(d) & 15) && !(reinterpret_cast<uintptr_t>(s) & 15)) {
+        copy_u64_kernel<<<(int)std::min<u64>((n2 + 255) / 256, (u64)c.num_sms * 16), 256, 0, c.stream>>>(
+            reinterpret_cast<ulonglong2*>(d), reinterpret_cast<const ulonglong2*>(s), n2);
+        c.check_launch();
+        if (n & 1) c.d2d(d + n - 1, s + n - 1, sizeof(u64));
+        return;
+    }
+    c.d2d(d, s, n * sizeof(u64));
+}
+
+void loop_table_clear(Ctx& c, void* tab, u64 cap, u32 sbits) {
+    const u64 words = cap * loop_slot_bytes(sbits) / 8;
+    if (words & 1) c.memset(tab, 0xff, words * 8);
+    else loop_fill_u64(c, static_cast<u64*>(tab), words, kEmptySlot);
+}
 
 void loop_table_fill(Ctx& c, void* tab, u64 cap, u32 sbits, const u64* keys, u64 n) {
     if (n == 0) return;

@@ -155,6 +155,9 @@ int loop_grid(const Ctx& c);
 // Kernel occupancies (called once before the first launch or capture).
 void loop_prepare();
 void loop_table_clear(Ctx& c, void* tab, u64 cap, u32 sbits);
+// Streaming u64 fill / copy kernels (growth path).
+void loop_fill_u64(Ctx& c, u64* p, u64 n, u64 v);
+void loop_copy_u64(Ctx& c, u64* d, const u64* s, u64 n);
 // Inserts keys (unique) into an empty table (stamp 0).
 void loop_table_fill(Ctx& c, void* tab, u64 cap, u32 sbits, const u64* keys, u64 n);
 // Moves every key (nkeys of them) of old_tab into the (cleared, larger)

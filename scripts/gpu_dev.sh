@@ -1,5 +1,2 @@
 #!/bin/bash
-timeout 600 python -m pytest tests/test_gpu_loop.py -x -q -k "hash_predup" > gpurun_out/pytest_loop.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_loop.log
-timeout 300 python scripts/configs_bench.py c4_cspa > gpurun_out/c4.jsonl 2>&1
-GD_DEDUP_SPLIT=0 timeout 300 python scripts/configs_bench.py c4_cspa >> gpurun_out/c4.jsonl 2>&1
-timeout 300 python scripts/diag_config.py c4_cspa > gpurun_out/diag_c4.log 2>&1
+for i in 1 2; do GD_BENCH_CANARY=1 GD_BENCH_CLOCK_MS=0 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-profile --no-e2e 2>/dev/null; done > gpurun_out/bench_q8.jsonl

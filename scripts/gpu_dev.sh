@@ -1,2 +1,2 @@
 #!/bin/bash
-for i in 1 2; do GD_BENCH_CANARY=1 GD_BENCH_CLOCK_MS=0 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-profile --no-e2e 2>/dev/null; done > gpurun_out/bench_q8.jsonl
+timeout 900 ncu --set full --clock-control none -k regex:"dedup_insert|part_scatter" -s 40 -c 2 -o gpurun_out/prof_dedup python scripts/configs_bench.py c4_cspa > gpurun_out/ncu_dedup.log 2>&1

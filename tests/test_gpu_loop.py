@@ -153,3 +153,19 @@ def test_hub_rows(ref, mode):
     edges = np.vstack([e, hubs, hub2])
     g = run_mode(mode, "reach", {"Edge": edges})
     assert_same(g, run_ref(ref, "reach", {"Edge": edges}), ["Reach"])
+
+
+@pytest.mark.parametrize("mode", ["graph", "eager", "tiny"])
+def test_stamp_epoch_restart(ref, mode):
+    """56-bit keys leave 8 stamp bits: a 599-iteration fixpoint restarts the
+    stamp epoch twice (table restamp on the device); results, histories and
+    iteration records must equal the reference."""
+    n = 600
+    ids = (np.arange(n, dtype=np.uint64) * np.uint64(400_000) + np.uint64(7))  # < 2^28: 28 bits per column
+    edges = np.stack([ids[:-1], ids[1:]], 1)
+    g = run_mode(mode, "reach", {"Edge": edges})
+    assert g.encoding()["bits"] >= 28 and not g.encoding()["dictionary"]
+    assert g.stats().iterations == n - 1
+    assert_same(g, run_ref(ref, "reach", {"Edge": edges}), ["Reach"])
+    # Δ_out of every iteration = 599 - i: no key counted twice across epochs
+    assert [r[3] for r in g.iter_log("Reach")] == list(range(n - 2, -1, -1))

@@ -158,6 +158,7 @@ struct Ctx {
             own_stream = true;
         }
         GD_CUDA(cudaMallocHost(&pinned, kPinnedWords * sizeof(unsigned long long)));
+        query_free();
     }
     ~Ctx() {
         flush_cache();
@@ -210,15 +211,28 @@ struct Ctx {
 
     // Bytes a new allocation could get: free device memory plus the blocks
     // cached here (alloc() returns them to the pool before giving up).
-    uint64_t available_bytes() const {
+    // cudaMemGetInfo is an RM query that sporadically takes 10-100 ms on
+    // the B200 boxes (the growth-time spikes of DESIGN.md §7), so free
+    // memory is queried at context creation and then tracked through this
+    // allocator's own cudaMalloc / cudaFree; exact = true re-queries (growth
+    // near the memory limit, where other allocations in the process matter).
+    mutable double meminfo_seconds = 0;
+    mutable uint64_t free_est = 0;
+    uint64_t available_bytes(bool exact = false) const {
+        if (exact) query_free();
+        return free_est + cached_bytes;
+    }
+    void query_free() const {
         size_t fr = 0, tot = 0;
-        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 0;
-        return (uint64_t)fr + cached_bytes;
+        const double t0 = now_s();
+        const cudaError_t e = cudaMemGetInfo(&fr, &tot);
+        meminfo_seconds += now_s() - t0;
+        free_est = e == cudaSuccess ? (uint64_t)fr : 0;
     }
 
     void flush_cache() {
         if (!cache_.empty()) cudaStreamSynchronize(stream);  // cached blocks may still be in use
-        for (auto& kv : cache_) cudaFree(kv.second);
+        for (auto& kv : cache_) cudaFree(kv.second), free_est += kv.first;
         cache_.clear();
         cached_bytes = 0;
     }
@@ -263,6 +277,7 @@ struct Ctx {
                                         " bytes failed (HBM exhausted)");
         }
         if (e != cudaSuccess) throw Error(GD_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        free_est -= std::min<uint64_t>(free_est, cls);
         alloc_seconds += now_s() - t0;
         live_[p] = cls;
         bytes_in_use += cls;

@@ -533,12 +533,13 @@ public:
         DevBuf<u64> tab;  // tab_cap slots of loop_slot_bytes(sbits)
         u64 log_cap = 0, tab_cap = 0, tab_limit = 0;
         u32 sbits = 0;
-        void alloc_tab(Ctx& c, u64 cap, bool dense = false) {
+        // clear = false: the caller writes every slot (loop_table_rehash)
+        void alloc_tab(Ctx& c, u64 cap, bool dense = false, bool clear = true) {
             tab.release();
             tab_cap = cap;
             tab_limit = dense ? cap / 4 * 3 : tab_limit_of(cap);
             tab = DevBuf<u64>(c, cap * loop_slot_bytes(sbits) / 8);
-            loop_table_clear(c, tab.p, cap, sbits);
+            if (clear) loop_table_clear(c, tab.p, cap, sbits);
         }
     };
     // Linear probing stays short (~1.5 slot reads per new key with the
@@ -894,6 +895,7 @@ public:
                 if (hc->overflow) {
                     // growth / restamp time is index (HISA) build time
                     PhaseTimer tg(E, "index");
+                    const double tblock = Ctx::now_s();
                     ++rollbacks;
                     for (u32 i = 0; i < ns; ++i) {
                         LStep& L = steps[i];
@@ -942,7 +944,8 @@ public:
                         const u64 reserve = 1ull << 30;
                         if (hc->need_log[h] > H.log_cap) {
                             const u64 need = hc->need_log[h];
-                            const u64 avail = c.available_bytes();
+                            u64 avail = c.available_bytes();
+                            if (2 * need * sizeof(u64) + reserve > avail / 2) avail = c.available_bytes(true);
                             const u64 fit = avail > reserve ? (avail - reserve) / sizeof(u64) : 0;
                             const u64 cap = std::max(need + need / 16 + 1024, std::min(2 * need, fit));
                             DevBuf<u64> nl(c, cap);
@@ -954,8 +957,9 @@ public:
                         if (hc->need_tab[h] > H.tab_limit) {  // grow: stream the old table into the new
                             const u64 need = hc->need_tab[h];
                             const u64 sb = loop_slot_bytes(H.sbits);
-                            const u64 avail = c.available_bytes();
                             const u64 spill = (ln / 16 + (1u << 20)) * sizeof(u64);  // re-spread spill list
+                            u64 avail = c.available_bytes();
+                            if (6 * need * sb + spill + reserve > avail / 2) avail = c.available_bytes(true);
                             const u64 fit = avail > reserve + spill ? (avail - reserve - spill) / sb : 0;
                             const u64 cap = std::min(6 * need, fit);  // load 1/6 after growth when it fits
                             if (cap < need / 3 * 4 + 16)
@@ -963,8 +967,8 @@ public:
                                                           std::to_string(need) + " keys");
                             DevBuf<u64> old = std::move(H.tab);
                             const u64 old_cap = H.tab_cap;
-                            H.alloc_tab(c, cap, cap < 2 * need);
-                            tr("tab-alloc+clear", old_cap, H.tab_cap);
+                            H.alloc_tab(c, cap, cap < 2 * need, false);
+                            tr("tab-alloc", old_cap, H.tab_cap);
                             loop_table_rehash(c, old.p, old_cap, H.tab.p, H.tab_cap, H.sbits, ln);
                             tr("tab-rehash", old_cap, H.tab_cap);
                         } else if (hc->need_restamp) {
@@ -990,6 +994,10 @@ public:
                     c.h2d(ctl.p, hc, sizeof(LoopCtl));
                     c.sync();
                     destroy_graph();
+                    if (trace)
+                        fprintf(stderr, "[loop] iter %u rollback block %.3f ms (meminfo total %.3f ms, alloc total %.3f ms)\n",
+                                hc->iter, (Ctx::now_s() - tblock) * 1e3, c.meminfo_seconds * 1e3,
+                                c.alloc_seconds * 1e3);
                     continue;
                 }
                 if (hc->done) break;
@@ -1303,7 +1311,7 @@ public:
         if (need > H.tab_limit) {
             DevBuf<u64> old = std::move(H.tab);
             const u64 old_cap = H.tab_cap;
-            H.alloc_tab(c, 6 * need);
+            H.alloc_tab(c, 6 * need, false, false);
             loop_table_rehash(c, old.p, old_cap, H.tab.p, H.tab_cap, H.sbits, ln);
         }
         if (hc->iter + 1 - hc->epoch_base > (H.sbits ? (1u << H.sbits) - 1 : 0xfffffffeu)) {

@@ -812,59 +812,72 @@ __global__ void table_rehash_kernel(const void* old_tab, u64 old_cap, void* tab,
     }
 }
 
-// Atomic-free growth (the CAS re-spread runs at the L2 atomic rate even
-// though its addresses stream).  Thread t owns old slots [32t, 32t+32) and
-// the new-table zone [32t·g, 32(t+1)·g) (g = new/old capacity, zones
-// partition the new table).  It places each of its keys whose new home lies
-// in its zone at the first free zone slot at or after the home (a 256-bit
-// occupancy map in registers) with a plain store: every slot between a
-// key's home and its position holds a key, the linear-probing invariant.
-// Keys whose home falls outside the zone, or that overflow it, are spilled
-// and CAS-inserted afterwards (table_fill over the spill list).
-constexpr u64 kPlaceMaxZone = 256;
-__global__ void table_place_kernel(const void* old_tab, u64 old_cap, void* tab, u64 cap, u32 sb,
-                                   u64* __restrict__ spill, unsigned long long* nspill, u64 spill_cap) {
-    const u64 runs = (old_cap + kRun - 1) / kRun;
-    for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < runs; r += (u64)gridDim.x * blockDim.x) {
-        const u64 i0 = r * kRun, i1 = min(old_cap, i0 + kRun);
-        const u64 zlo = (u64)((u128)i0 * cap / old_cap);
-        const u64 zhi = i1 == old_cap ? cap : (u64)((u128)i1 * cap / old_cap);
-        const u64 width = zhi - zlo;  // <= kPlaceMaxZone (host checks the growth ratio)
-        u64 bm0 = 0, bm1 = 0, bm2 = 0, bm3 = 0;
-        for (u64 i = i0; i < i1; ++i) {
-            const u64 w = sb ? static_cast<const u64*>(old_tab)[i] : static_cast<const HSlot*>(old_tab)[i].key;
-            if (w == kEmptySlot) continue;
-            const u64 key = sb ? w >> sb : w;
+// Growth as a streaming pass (supersedes table_place for ratios it fits):
+// CTA b owns old slots [i0, i1) and the new-table zone [zlo, zhi) they map
+// to (i·cap/old_cap, zones partition the new table).  The zone is built in
+// shared memory — cleared, keys placed by linear probing with shared CAS
+// from their new home — then written out whole, EMPTY slots included, so
+// the new table needs no separate clear and both tables are streamed
+// once.  Keys whose new home lies outside the zone (displaced across the
+// range start, or wrapped) or whose probe runs off the zone end are
+// spilled and CAS-inserted afterwards.  Insertion order within a zone does
+// not matter for linear probing (nothing is deleted).
+constexpr u32 kZoneThreads = 256;
+constexpr u32 kZoneSlots = 4096;     // 32 KB of shared memory per CTA (6 CTAs per SM)
+constexpr u32 kZoneSlotsMax = 8192;  // GD_ZONE_SLOTS experiments
+constexpr u32 kZoneBatch = 8;
+__global__ void __launch_bounds__(kZoneThreads) table_zone_kernel(const void* old_tab, u64 old_cap, void* tab,
+                                                                  u64 cap, u32 sb, u32 T, u64* __restrict__ spill,
+                                                                  unsigned long long* nspill, u64 spill_cap) {
+    extern __shared__ unsigned long long zone[];
+    const u64 i0 = (u64)blockIdx.x * T, i1 = min(old_cap, i0 + T);
+    const u64 zlo = (u64)((u128)i0 * cap / old_cap);
+    const u64 zhi = i1 == old_cap ? cap : (u64)((u128)i1 * cap / old_cap);
+    const u32 width = (u32)(zhi - zlo);  // <= the zone's shared slots (host sizes T)
+    for (u32 j = threadIdx.x; j < width; j += kZoneThreads) zone[j] = kEmptySlot;
+    __syncthreads();
+    // kZoneBatch independent loads per thread in flight (the pass is
+    // latency-bound with one)
+    for (u64 base = i0; base < i1; base += (u64)kZoneThreads * kZoneBatch) {
+        u64 w[kZoneBatch];
+#pragma unroll
+        for (u32 q = 0; q < kZoneBatch; ++q) {
+            const u64 i = base + q * kZoneThreads + threadIdx.x;
+            w[q] = i >= i1 ? kEmptySlot
+                   : sb    ? __ldcs(static_cast<const u64*>(old_tab) + i)
+                           : __ldcs(&static_cast<const HSlot*>(old_tab)[i].key);
+        }
+#pragma unroll
+        for (u32 q = 0; q < kZoneBatch; ++q) {
+            if (w[q] == kEmptySlot) continue;
+            const u64 key = sb ? w[q] >> sb : w[q];
+            const u64 want = sb ? key << sb : key;
             const u64 h = hs_home(key, cap);
-            u64 q = kPlaceMaxZone;
+            bool placed = false;
             if (h >= zlo && h < zhi) {
-                const u32 off = (u32)(h - zlo);
-                // first zero bit >= off over the four words
-                const u64 m0 = off < 64 ? ~bm0 & (~0ull << off) : 0;
-                const u64 m1 = off < 128 ? ~bm1 & (off > 64 ? ~0ull << (off - 64) : ~0ull) : 0;
-                const u64 m2 = off < 192 ? ~bm2 & (off > 128 ? ~0ull << (off - 128) : ~0ull) : 0;
-                const u64 m3 = ~bm3 & (off > 192 ? ~0ull << (off - 192) : ~0ull);
-                if (m0) q = __ffsll((long long)m0) - 1;
-                else if (m1) q = 64 + __ffsll((long long)m1) - 1;
-                else if (m2) q = 128 + __ffsll((long long)m2) - 1;
-                else if (m3) q = 192 + __ffsll((long long)m3) - 1;
-            }
-            if (q < width) {
-                if (q < 64) bm0 |= 1ull << q;
-                else if (q < 128) bm1 |= 1ull << (q - 64);
-                else if (q < 192) bm2 |= 1ull << (q - 128);
-                else bm3 |= 1ull << (q - 192);
-                if (sb) {
-                    static_cast<u64*>(tab)[zlo + q] = key << sb;
-                } else {
-                    HSlot& d = static_cast<HSlot*>(tab)[zlo + q];
-                    d.key = key;
-                    d.stamp = 0;
+                for (u32 p = (u32)(h - zlo); p < width; ++p) {
+                    if (zone[p] != kEmptySlot) continue;
+                    if (atomicCAS(&zone[p], kEmptySlot, want) == kEmptySlot) {
+                        placed = true;
+                        break;
+                    }
                 }
-            } else {
+            }
+            if (!placed) {
                 const u64 at = atomicAdd(nspill, 1ull);
                 if (at < spill_cap) spill[at] = key;  // else: the host redoes the growth with CAS
             }
+        }
+    }
+    __syncthreads();
+    if (sb) {
+        u64* out = static_cast<u64*>(tab) + zlo;
+        for (u32 j = threadIdx.x; j < width; j += kZoneThreads) __stcs(out + j, (u64)zone[j]);
+    } else {
+        HSlot* out = static_cast<HSlot*>(tab) + zlo;
+        for (u32 j = threadIdx.x; j < width; j += kZoneThreads) {
+            const u64 k = zone[j];
+            __stcs(reinterpret_cast<ulonglong2*>(out + j), make_ulonglong2(k, k == kEmptySlot ? kEmptySlot : 0ull));
         }
     }
 }
@@ -1030,27 +1043,42 @@ void loop_table_fill(Ctx& c, void* tab, u64 cap, u32 sbits, const u64* keys, u64
 }
 
 void loop_table_rehash(Ctx& c, const void* old_tab, u64 old_cap, void* tab, u64 cap, u32 sbits, u64 nkeys) {
-    if (old_cap == 0) return;
-    // zones of at most kPlaceMaxZone slots: growth ratio below 8
-    if (cap < old_cap * (kPlaceMaxZone / kRun) - kPlaceMaxZone && !(getenv("GD_REHASH_CAS") &&
-                                                                   getenv("GD_REHASH_CAS")[0] == '1')) {
+    // `tab` is uninitialised: the zone pass writes every slot; the CAS
+    // fallbacks clear it first.
+    if (old_cap == 0) {
+        loop_table_clear(c, tab, cap, sbits);
+        return;
+    }
+    const bool cas_only = getenv("GD_REHASH_CAS") && getenv("GD_REHASH_CAS")[0] == '1';
+    const char* zs = getenv("GD_ZONE_SLOTS");  // experiments: zone size (shared memory per CTA)
+    const u32 zslots = zs ? std::min<u32>(kZoneSlotsMax, std::max(1024, atoi(zs))) : kZoneSlots;
+    const u64 T = (u64)((double)(zslots - 2) * (double)old_cap / (double)cap) / 32 * 32;
+    const u64 nzones = T ? (old_cap + T - 1) / T : 0;
+    if (!cas_only && T >= 256 && nzones < (1u << 31)) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(table_zone_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(kZoneSlotsMax * sizeof(u64)));
+            attr = true;
+        }
         const u64 spill_cap = nkeys / 16 + (1u << 20);
         DevBuf<u64> spill(c, spill_cap);
         DevBuf<unsigned long long> ns(c, 1);
         c.memset(ns.p, 0, sizeof(unsigned long long));
-        const u64 runs = (old_cap + kRun - 1) / kRun;
-        const int grid = (int)std::max<u64>(1, std::min<u64>((runs + 255) / 256, (u64)c.num_sms * 16));
-        table_place_kernel<<<grid, 256, 0, c.stream>>>(old_tab, old_cap, tab, cap, sbits, spill.p, ns.p, spill_cap);
+        table_zone_kernel<<<(unsigned)nzones, kZoneThreads, zslots * sizeof(u64), c.stream>>>(
+            old_tab, old_cap, tab, cap, sbits, (u32)T, spill.p, ns.p, spill_cap);
         c.check_launch();
         unsigned long long spilled;
         c.read_words(&spilled, ns.p, 1);
         if (spilled <= spill_cap) {
-            table_fill_dev_kernel<<<c.num_sms * 4, 256, 0, c.stream>>>(tab, cap, sbits, spill.p, ns.p);
-            c.check_launch();
+            if (spilled) {
+                table_fill_dev_kernel<<<c.num_sms * 4, 256, 0, c.stream>>>(tab, cap, sbits, spill.p, ns.p);
+                c.check_launch();
+            }
             return;
         }
-        loop_table_clear(c, tab, cap, sbits);  // spill list overflowed: CAS re-spread below
     }
+    loop_table_clear(c, tab, cap, sbits);  // CAS re-spread (spill list overflowed, or a very large ratio)
     const u64 runs = (old_cap + kRun - 1) / kRun;
     const int grid = (int)std::max<u64>(1, std::min<u64>((runs + 255) / 256, (u64)c.num_sms * 16));
     table_rehash_kernel<<<grid, 256, 0, c.stream>>>(old_tab, old_cap, tab, cap, sbits);

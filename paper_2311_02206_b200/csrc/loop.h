@@ -160,8 +160,8 @@ void loop_fill_u64(Ctx& c, u64* p, u64 n, u64 v);
 void loop_copy_u64(Ctx& c, u64* d, const u64* s, u64 n);
 // Inserts keys (unique) into an empty table (stamp 0).
 void loop_table_fill(Ctx& c, void* tab, u64 cap, u32 sbits, const u64* keys, u64 n);
-// Moves every key (nkeys of them) of old_tab into the (cleared, larger)
-// tab, stamps 0.
+// Moves every key (nkeys of them) of old_tab into the larger tab, stamps 0.
+// tab is uninitialised on entry: every slot is written.
 void loop_table_rehash(Ctx& c, const void* old_tab, u64 old_cap, void* tab, u64 cap, u32 sbits, u64 nkeys);
 // Resets every stamp to 0 in place (new stamp epoch).
 void loop_table_restamp(Ctx& c, void* tab, u64 cap, u32 sbits);

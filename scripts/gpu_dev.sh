@@ -1,9 +1,7 @@
 #!/bin/bash
-GD_LOOP_TRACE=1 timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-profile > gpurun_out/bench_z0.json 2> gpurun_out/bench_z0.err
+timeout 900 python -m pytest tests/test_gpu_loop.py tests/test_gpu_partition.py -x -q > gpurun_out/pytest_loop.log 2>&1; tail -3 gpurun_out/pytest_loop.log
+for m in 1 0; do
+GD_PROBE_SCAN=$m timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_ps$m.json 2> gpurun_out/bench_ps$m.err
 python -c "
-import json; d=json.loads(open('gpurun_out/bench_z0.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], d['step_ms'], [x['index'] for x in d['step_phases_ms']])"
-grep -E "block|tab-|log " gpurun_out/bench_z0.err | awk '{ if ($0 ~ /gpu/ && $(NF-1)+0 > 15) print "BIG", $0; }' | tail -50
-grep block gpurun_out/bench_z0.err | tail -2
-timeout 600 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
-python -c "
-import json; d=json.loads(open('gpurun_out/bench_full.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], d['step_ms'], d['e2e']['seconds_per_step'], [x['index'] for x in d['step_phases_ms']])"
+import json; d=json.loads(open('gpurun_out/bench_ps$m.json').read().strip().splitlines()[-1]); print('fused=$m', d['ms_per_step'], d['step_ms'], d['gpu_launches'], d['roofline']['kernel_ms_per_step'])"
+done

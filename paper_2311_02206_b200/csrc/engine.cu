@@ -292,7 +292,8 @@ public:
     // host threads unpack chunk k into the caller's rows while chunk k+1 is
     // in flight.  Bytes equal unpack_rows + copy.
     void download_packed(const u64* keys, u64 n, u32 ar, u64* out) {
-        constexpr u64 kChunk = 16u << 20;  // rows per chunk (128 MB of keys)
+        const char* ce = getenv("GD_DL_CHUNK_ROWS");  // experiments
+        const u64 kChunk = ce ? std::max<u64>(1u << 16, strtoull(ce, nullptr, 10)) : (1u << 20);
         u64* stage[2];
         void* area = c.pinned_staging(2 * kChunk * sizeof(u64));
         stage[0] = static_cast<u64*>(area);
@@ -329,7 +330,21 @@ public:
                 // non-temporal stores: the rows are written once and not read
                 // back here, so skip the read-for-ownership of each line
                 long long* d = reinterpret_cast<long long*>(dst);
-                for (u64 i = lo; i < hi; ++i) {
+                u64 i = lo;
+                if (!(reinterpret_cast<uintptr_t>(dst) & 15)) {
+                    // two rows per step: one 16-byte load of two keys, two
+                    // 16-byte non-temporal row stores
+                    const __m128i mv = _mm_set1_epi64x((long long)mask);
+                    const __m128i sh = _mm_cvtsi32_si128((int)bits);
+                    for (; i + 2 <= hi; i += 2) {
+                        const __m128i k = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+                        const __m128i a = _mm_and_si128(_mm_srl_epi64(k, sh), mv);
+                        const __m128i b = _mm_and_si128(k, mv);
+                        _mm_stream_si128(reinterpret_cast<__m128i*>(d + 2 * i), _mm_unpacklo_epi64(a, b));
+                        _mm_stream_si128(reinterpret_cast<__m128i*>(d + 2 * i + 2), _mm_unpackhi_epi64(a, b));
+                    }
+                }
+                for (; i < hi; ++i) {
                     const u64 key = src[i];
                     _mm_stream_si64(d + 2 * i, (long long)((key >> bits) & mask));
                     _mm_stream_si64(d + 2 * i + 1, (long long)(key & mask));

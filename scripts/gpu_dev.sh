@@ -1,4 +1,5 @@
 #!/bin/bash
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_ps.json 2> gpurun_out/bench_ps.err
+GD_HOST_UNPACK=0 timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-profile > gpurun_out/bench_dl.json 2> gpurun_out/bench_dl.err
 python -c "
-import json; d=json.loads(open('gpurun_out/bench_ps.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], d['step_ms'], d['gpu_launches'], d['roofline']['kernel_ms_per_step'])"
+import json; d=json.loads(open('gpurun_out/bench_dl.json').read().strip().splitlines()[-1]); print('direct', d['ms_per_step'], d['e2e'])"
+nvidia-smi -q | grep -A3 -i "Link Width\|PCIe Generation" | head -12

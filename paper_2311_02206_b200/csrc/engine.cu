@@ -1239,6 +1239,10 @@ public:
         PartLoop& P = *pl;
         LoopCtl* hc = P.hc;
         const u32 ns = (u32)P.steps.size();
+        const u32 R = E.nranks;
+        const LStep& F = P.steps[P.final_step];
+        const u64* n_ptr = &P.ctl.p->step_total[P.final_step];
+        unsigned long long cnt[kLoopMaxRanks] = {};
         for (;;) {  // the join part; regrown and rerun on a capacity overflow
             for (u32 i = 0; i < ns; ++i) {
                 LStep& L = P.steps[i];
@@ -1252,7 +1256,12 @@ public:
                 loop_scan(c, c.stream, P.ctl.p, i, o, L.bufs(), P.block_sums.p, nullptr);
                 loop_materialize_temp(c, c.stream, P.ctl.p, i, o, L.inner, L.jd, L.bufs(), L.temp.p, L.temp_cap);
             }
+            // owner counts of the final step's rows, read back with the
+            // control block (one round trip; discarded on an overflow)
+            c.memset(P.counts.p, 0, R * sizeof(unsigned long long));
+            loop_owner_count(c, F.temp.p, n_ptr, F.temp_cap, R, P.counts.p);
             c.d2h(hc, P.ctl.p, sizeof(LoopCtl));
+            c.d2h(cnt, P.counts.p, R * sizeof(unsigned long long));
             c.sync();
             if (!hc->overflow) break;
             for (u32 i = 0; i < ns; ++i) {
@@ -1278,17 +1287,9 @@ public:
         }
         for (u32 i = 0; i < ns; ++i) E.join_tuples += hc->step_total[i];
         // group the final step's rows by owner
-        const u32 R = E.nranks;
-        const LStep& F = P.steps[P.final_step];
         const u64 m = hc->step_total[P.final_step];
-        const u64* n_ptr = &P.ctl.p->step_total[P.final_step];
         P.send.reserve_discard(c, std::max<u64>(m, 1));
-        c.memset(P.counts.p, 0, R * sizeof(unsigned long long));
         c.memset(P.cursors.p, 0, R * sizeof(unsigned long long));
-        if (m) loop_owner_count(c, F.temp.p, n_ptr, R, P.counts.p);
-        unsigned long long cnt[kLoopMaxRanks] = {};
-        c.d2h(cnt, P.counts.p, R * sizeof(unsigned long long));
-        c.sync();
         unsigned long long off[kLoopMaxRanks];
         u64 acc = 0;
         for (u32 k = 0; k < R; ++k) {

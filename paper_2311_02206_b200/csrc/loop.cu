@@ -922,12 +922,12 @@ __global__ void table_restamp_kernel(void* tab, u64 cap, u32 sb) {
 constexpr u32 kOwnTile = 2048;
 constexpr u32 kMaxRanks = 64;
 
-__global__ void owner_count_kernel(const u64* __restrict__ keys, const u64* __restrict__ n_ptr, u32 P,
+__global__ void owner_count_kernel(const u64* __restrict__ keys, const u64* __restrict__ n_ptr, u64 cap, u32 P,
                                    unsigned long long* __restrict__ counts) {
     __shared__ u32 sc[kMaxRanks];
     for (u32 i = threadIdx.x; i < P; i += blockDim.x) sc[i] = 0;
     __syncthreads();
-    const u64 n = *n_ptr;
+    const u64 n = min(*n_ptr, cap);  // an overflowed step: bounded, and redone by the host
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
         atomicAdd(&sc[key_hash64<u64>(keys[i]) % P], 1u);
     __syncthreads();
@@ -1186,8 +1186,8 @@ void loop_select_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head
     c.check_launch();
 }
 
-void loop_owner_count(Ctx& c, const u64* keys, const u64* n_ptr, u32 P, unsigned long long* counts) {
-    owner_count_kernel<<<c.num_sms * 4, 256, 0, c.stream>>>(keys, n_ptr, P, counts);
+void loop_owner_count(Ctx& c, const u64* keys, const u64* n_ptr, u64 cap, u32 P, unsigned long long* counts) {
+    owner_count_kernel<<<c.num_sms * 4, 256, 0, c.stream>>>(keys, n_ptr, cap, P, counts);
     c.check_launch();
 }
 

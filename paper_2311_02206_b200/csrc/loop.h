@@ -194,7 +194,7 @@ void loop_select_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head
 // ---- partitioned mode ----
 constexpr u32 kLoopMaxRanks = 64;
 // Per-destination counts of keys[0, *n_ptr) (owner = key_hash64(key) mod P).
-void loop_owner_count(Ctx& c, const u64* keys, const u64* n_ptr, u32 P, unsigned long long* counts);
+void loop_owner_count(Ctx& c, const u64* keys, const u64* n_ptr, u64 cap, u32 P, unsigned long long* counts);
 // Scatter into out grouped by destination (offsets: exclusive prefix of the
 // counts; cursors zeroed).  Order inside a group is unspecified.
 void loop_owner_scatter(Ctx& c, const u64* keys, const u64* n_ptr, u32 P, const unsigned long long* offsets,

@@ -9,7 +9,8 @@ iteration each rank:
      torch.distributed: counts first, then the rows);
   3. merges what it received into its local full relation, producing its
      local Δ                                  (gd_engine_partition_end);
-  4. all-reduces |Δ| — the fixpoint is reached when the global sum is 0.
+  4. sends its |Δ| with the next iteration's counts — the fixpoint is
+     reached when the global sum is 0 (no separate all-reduce).
 
 The exchange is abstracted (`Exchange`) so the same loop runs over NCCL,
 over gloo (CPU tests) or over an in-process loopback of P logical shards on
@@ -30,7 +31,10 @@ class CudaBuffer:
 
 
 class TorchExchange:
-    """All-to-all-v + all-reduce through torch.distributed (NCCL on GPUs)."""
+    """All-to-all-v through torch.distributed (NCCL on GPUs).  The
+    collectives run on torch's current stream, which must be the engine
+    context's stream (bench.py builds the Context on it): the engine's
+    next kernels then read the received rows in stream order."""
 
     def __init__(self, device: str = "cuda"):
         import torch
@@ -50,12 +54,21 @@ class TorchExchange:
             return torch.from_numpy(arr)
         return torch.as_tensor(CudaBuffer(ptr, nwords), device=self.device).view(torch.int64)
 
-    def exchange(self, send_counts: np.ndarray, send_ptr: int, words: int):
+    def exchange(self, send_counts: np.ndarray, send_ptr: int, words: int, delta: int = 1):
+        """All-to-all-v of the owner groups.  Each rank's |Δ| rides along
+        with its counts (one all-to-all instead of counts + an all-reduce);
+        returns (recv_ptr, recv_rows, global |Δ|).  When the global |Δ| is 0
+        every rank sent nothing and the row exchange is skipped."""
         torch, dist = self.torch, self.dist
-        cnt = torch.as_tensor(send_counts.astype(np.int64), device=self.device)
+        P = len(send_counts)
+        meta = np.stack([send_counts.astype(np.int64), np.full(P, int(delta), dtype=np.int64)], 1).reshape(-1)
+        cnt = torch.as_tensor(meta, device=self.device)
         rcnt = torch.empty_like(cnt)
         dist.all_to_all_single(rcnt, cnt)
-        rc = rcnt.cpu().numpy()
+        rm = rcnt.cpu().numpy().reshape(P, 2)
+        rc, gdelta = rm[:, 0], int(rm[:, 1].sum())
+        if gdelta == 0:
+            return 0, 0, 0
         total_send = int(send_counts.sum())
         total_recv = int(rc.sum())
         if total_send:
@@ -67,7 +80,7 @@ class TorchExchange:
                                      device=self.device)
         recv = self._recv[: total_recv * words]
         dist.all_to_all_single(recv, send, [int(x) * words for x in rc], [int(x) * words for x in send_counts])
-        return (recv.data_ptr() if total_recv else 0), total_recv
+        return (recv.data_ptr() if total_recv else 0), total_recv, gdelta
 
     def allreduce_sum(self, x: int) -> int:
         t = self.torch.tensor([x], dtype=self.torch.int64, device=self.device)
@@ -77,17 +90,21 @@ class TorchExchange:
 
 def run_partitioned(eng, exchange, nranks: int, max_iters: int = 1 << 30) -> int:
     """Drives one rank's engine to the global fixpoint; returns iterations.
-    `eng` must be seeded with set_partition(rank, nranks) applied."""
+    `eng` must be seeded with set_partition(rank, nranks) applied.  The
+    termination test uses the |Δ| each rank sends with its counts, so an
+    iteration costs one counts all-to-all and one rows all-to-all; after the
+    last productive iteration one more (empty) begin + counts exchange sees
+    the global |Δ| = 0."""
     words = eng.exchange_words()
     it = 0
-    local = eng.relation_delta_count() if hasattr(eng, "relation_delta_count") else None
+    local = 1  # the seeded Δ: the first iteration always runs (engine.hpp:181-257)
     while it < max_iters:
         counts, ptr = eng.partition_begin(nranks)
-        rptr, rrows = exchange.exchange(counts, ptr, words)
+        rptr, rrows, gdelta = exchange.exchange(counts, ptr, words, local)
+        if gdelta == 0:
+            break
         local = eng.partition_end(rptr, rrows)
         it += 1
-        if exchange.allreduce_sum(local) == 0:
-            break
     return it
 
 

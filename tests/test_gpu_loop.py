@@ -169,3 +169,21 @@ def test_stamp_epoch_restart(ref, mode):
     assert_same(g, run_ref(ref, "reach", {"Edge": edges}), ["Reach"])
     # Δ_out of every iteration = 599 - i: no key counted twice across epochs
     assert [r[3] for r in g.iter_log("Reach")] == list(range(n - 2, -1, -1))
+
+
+@pytest.mark.parametrize("mode", ["graph", "eager", "tiny", "tiny_casrehash"])
+def test_wide_slots(ref, mode):
+    # 31-bit identity-encoded columns: 62-bit keys leave < 8 stamp bits, so
+    # the head index uses 16-byte HSlots (key + stamp word) — insertion,
+    # zone growth (tiny: every capacity starts at its minimum) and the CAS
+    # re-spread on that layout
+    rng = np.random.default_rng(11)
+    n = 3000
+    ids = np.sort(rng.choice(np.uint64(2_000_000_000), n, replace=False).astype(np.uint64))
+    src = rng.integers(0, n - 1, 6000)
+    dst = np.minimum(src + 1 + rng.integers(0, 40, 6000), n - 1)
+    edges = np.unique(np.stack([ids[src], ids[dst]], 1), axis=0)
+    g = run_mode(mode, "reach", {"Edge": edges})
+    enc = g.encoding()
+    assert enc["bits"] == 31 and not enc["dictionary"]
+    assert_same(g, run_ref(ref, "reach", {"Edge": edges}), ["Reach"])

@@ -558,8 +558,8 @@ public:
         }
     };
     // Linear probing stays short (~1.5 slot reads per new key with the
-    // sector scan) at load <= 1/2; a full table grows 3x (to load 1/6), so
-    // the re-spreads move about half the final key count in total.
+    // sector scan) at load <= 1/2; a full table grows 4x (to load 1/8), so
+    // the re-spreads move about a third of the final key count in total.
     static u64 tab_limit_of(u64 cap) { return cap / 2; }
 
     // The recursive variants as loop steps (plan order, variant order): outer
@@ -954,7 +954,7 @@ public:
                             cudaEventRecord(ev0, c.stream);
                         }
                         // Growth is sized against free HBM (C5-scale runs): 2x
-                        // for the log and 3x for the index when they fit, else
+                        // for the log and 4x for the index when they fit, else
                         // the largest size that does (index load up to 3/4).
                         const u64 reserve = 1ull << 30;
                         if (hc->need_log[h] > H.log_cap) {
@@ -974,9 +974,12 @@ public:
                             const u64 sb = loop_slot_bytes(H.sbits);
                             const u64 spill = (ln / 16 + (1u << 20)) * sizeof(u64);  // re-spread spill list
                             u64 avail = c.available_bytes();
-                            if (6 * need * sb + spill + reserve > avail / 2) avail = c.available_bytes(true);
+                            // load 1/8 after a growth (GD_TAB_GROWTH: A/B runs; 4 / 6 / 8 / 12
+                            // measured on C1-C5, 8 best or within 1%)
+                            static const u64 gf = getenv("GD_TAB_GROWTH") ? std::max(3, atoi(getenv("GD_TAB_GROWTH"))) : 8;
+                            if (gf * need * sb + spill + reserve > avail / 2) avail = c.available_bytes(true);
                             const u64 fit = avail > reserve + spill ? (avail - reserve - spill) / sb : 0;
-                            const u64 cap = std::min(6 * need, fit);  // load 1/6 after growth when it fits
+                            const u64 cap = std::min(gf * need, fit);  // load 1/gf after growth when it fits
                             if (cap < need / 3 * 4 + 16)
                                 throw_budget("index", "device memory cannot hold the full-tuple index of " +
                                                           std::to_string(need) + " keys");
@@ -1327,7 +1330,7 @@ public:
         if (need > H.tab_limit) {
             DevBuf<u64> old = std::move(H.tab);
             const u64 old_cap = H.tab_cap;
-            H.alloc_tab(c, 6 * need, false, false);
+            H.alloc_tab(c, 8 * need, false, false);
             loop_table_rehash(c, old.p, old_cap, H.tab.p, H.tab_cap, H.sbits, ln);
         }
         if (hc->iter + 1 - hc->epoch_base > (H.sbits ? (1u << H.sbits) - 1 : 0xfffffffeu)) {

@@ -1,5 +1,7 @@
 #!/bin/bash
-GD_HOST_UNPACK=0 timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-profile > gpurun_out/bench_dl.json 2> gpurun_out/bench_dl.err
-python -c "
-import json; d=json.loads(open('gpurun_out/bench_dl.json').read().strip().splitlines()[-1]); print('direct', d['ms_per_step'], d['e2e'])"
-nvidia-smi -q | grep -A3 -i "Link Width\|PCIe Generation" | head -12
+for gf in 6 8; do
+GD_TAB_GROWTH=$gf timeout 900 python scripts/configs_bench.py c1_tc_rand c3_sg_tree c3_sg_tree_w1000 c3_sg_tree_w4000 c5_tc_dag 2>/dev/null | python -c "
+import json,sys
+for l in sys.stdin:
+    d=json.loads(l); print('gf=$gf', d['workload'], round(d['time_to_fixpoint_s']*1e3,1), 'ms')"
+done

@@ -161,6 +161,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="diagnostics: run the multi-GPU (hash-partitioned, NCCL) path even at one rank")
     args = ap.parse_args()
 
     if args.impl == "reference":
@@ -173,7 +175,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    part = world > 1 or args.partitioned
+    if part:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
@@ -185,14 +188,14 @@ def main():
     edges = gen_workload()
     d_edges = torch.from_numpy(edges.view(np.int64)).cuda()
     flush = torch.empty(256 << 20 >> 2, dtype=torch.int32, device="cuda")
-    exch = TorchExchange() if world > 1 else None
+    exch = TorchExchange() if part else None
 
     def one_step():
         e = al.engine(PROGRAM, ctx=ctx)
-        if world > 1:
+        if part:
             e.set_partition(rank, world)
         e.load_edb_device("Edge", d_edges.data_ptr(), len(edges))
-        if world > 1:
+        if part:
             e.seed()
             run_partitioned(e, exch, world)
         else:
@@ -221,7 +224,7 @@ def main():
     sampler.start()
     for _ in range(args.steps):
         flush_l2(torch, flush)
-        if world > 1:
+        if part:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
@@ -238,9 +241,9 @@ def main():
                             "allocs": hc["allocs"] - hc0["allocs"]})
         hc0 = hc
         jt = e.raw_stats().join_tuples
-        reach_n = e.relation_count(HEAD)
+        reach_n = local_n = e.relation_count(HEAD)
         iters = e.raw_stats().iterations
-        if world > 1:
+        if part:
             mx = torch.tensor([ms], dtype=torch.float64, device="cuda")
             torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
             sm = torch.tensor([jt, reach_n], dtype=torch.int64, device="cuda")
@@ -318,31 +321,50 @@ def main():
         roof["kernel_ms_per_step"] = {k: round(v[0], 3) for k, v in prof.items()}
         roof["kernel_gbs"] = {k: round(v[2] / (v[0] / 1e3) / 1e9, 1) for k, v in prof.items() if v[0] and v[2]}
 
-    # e2e through the C-ABI with host buffers (rank 0 at N=1)
+    # e2e through the C-ABI with host buffers: every rank uploads the EDB
+    # from pinned host memory, runs (partitioned at N > 1) and downloads
+    # its shard of the result into pinned host rows; max over ranks
     e2e = None
-    if world == 1 and not args.no_e2e:
+    if not args.no_e2e:
         host_edges = torch.from_numpy(edges.view(np.int64)).pin_memory().numpy().view(np.uint64)
-        out = torch.empty((reach_n, 2), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+        out = torch.empty((max(local_n, 1), 2), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
         e2e_t = []
         h0, d0 = ctx.transfer_bytes()
         for _ in range(max(1, min(args.steps, 3))):
+            if part:
+                torch.distributed.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             e = al.engine(PROGRAM, ctx=ctx)
+            if part:
+                e.set_partition(rank, world)
             e.load_edb("Edge", al.tuple_array(2, host_edges))
-            e.run()
+            if part:
+                e.seed()
+                run_partitioned(e, exch, world)
+            else:
+                e.run()
             n = e.relation_count(HEAD)
             ctx.check(ctx.lib.gd_engine_relation_download(e.h, 1, out.ctypes.data, n))
             dt = time.perf_counter() - t0
-            e2e_t.append(dt)
             e.close()
+            if part:
+                mx = torch.tensor([dt], dtype=torch.float64, device="cuda")
+                torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+                dt = float(mx.item())
+            e2e_t.append(dt)
         h1, d1 = ctx.transfer_bytes()
         k = len(e2e_t)
+        hb, db = (h1 - h0) // k, (d1 - d0) // k
+        if part:  # whole-job bytes: sum over ranks
+            sb = torch.tensor([hb, db], dtype=torch.int64, device="cuda")
+            torch.distributed.all_reduce(sb)
+            hb, db = int(sb[0].item()), int(sb[1].item())
         # bytes that crossed PCIe (the C-ABI counts every copy); the Reach
         # download moves packed 8-byte keys, unpacked into the caller's u64
         # rows by host threads
         e2e = {"value": float(np.mean(joins)) / float(np.mean(e2e_t)), "unit": "tuples/s",
-               "h2d_bytes_per_step": int((h1 - h0) // k), "d2h_bytes_per_step": int((d1 - d0) // k),
+               "h2d_bytes_per_step": int(hb), "d2h_bytes_per_step": int(db),
                "host_rows_bytes": int(reach_n * 16), "seconds_per_step": float(np.mean(e2e_t))}
 
     cpu = None
@@ -367,7 +389,7 @@ def main():
             "time_to_fixpoint_s": ms_step / 1e3,
             "config": {"workload": "c2_tc_pl", "program": PROGRAM, **C2, "edges": int(len(edges)),
                        "reach": int(reach_n), "iterations": int(iters), "join_tuples": int(np.mean(joins)),
-                       "parallelism": f"hash-partitioned x{world}" if world > 1 else "single",
+                       "parallelism": f"hash-partitioned x{world}" if part else "single",
                        "l2": "flushed between steps (256 MiB write)"},
             "step_ms": [round(t, 2) for t in times], "step_phases_ms": step_detail,
             **({"canary_fill_ms": canary_ms} if canary_ms else {}),
@@ -375,7 +397,7 @@ def main():
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if part:
         torch.distributed.destroy_process_group()
 
 

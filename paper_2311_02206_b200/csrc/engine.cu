@@ -1152,7 +1152,16 @@ public:
         std::vector<LHead> heads;
         std::vector<LStep> steps;
         DevBuf<LoopCtl> ctl;
-        std::unique_ptr<LoopCtl> host;  // own host copy: several engines may share one context
+        // own pinned host copy (several engines may share one context;
+        // pageable copies would stage through the driver every transfer)
+        struct PartHost {
+            LoopCtl ctl;
+            unsigned long long cnt[kLoopMaxRanks], off[kLoopMaxRanks];
+        };
+        struct PinnedFree {
+            void operator()(PartHost* p) const { cudaFreeHost(p); }
+        };
+        std::unique_ptr<PartHost, PinnedFree> host;
         LoopCtl* hc = nullptr;
         DevBuf<u64> block_sums, send;
         DevBuf<unsigned long long> counts, offs, cursors;
@@ -1215,8 +1224,12 @@ public:
         P.offs = DevBuf<unsigned long long>(c, kLoopMaxRanks);
         P.cursors = DevBuf<unsigned long long>(c, kLoopMaxRanks);
         P.ctl = DevBuf<LoopCtl>(c, 1);
-        P.host.reset(new LoopCtl);
-        P.hc = P.host.get();
+        {
+            void* hp = nullptr;
+            GD_CUDA(cudaMallocHost(&hp, sizeof(typename PartLoop::PartHost)));
+            P.host.reset(static_cast<typename PartLoop::PartHost*>(hp));
+        }
+        P.hc = &P.host->ctl;
         std::memset(P.hc, 0, sizeof(LoopCtl));
         P.hc->nheads = 1;
         P.hc->hist_cap = ~0ull;
@@ -1245,7 +1258,7 @@ public:
         const u32 R = E.nranks;
         const LStep& F = P.steps[P.final_step];
         const u64* n_ptr = &P.ctl.p->step_total[P.final_step];
-        unsigned long long cnt[kLoopMaxRanks] = {};
+        unsigned long long* cnt = P.host->cnt;
         for (;;) {  // the join part; regrown and rerun on a capacity overflow
             for (u32 i = 0; i < ns; ++i) {
                 LStep& L = P.steps[i];
@@ -1293,7 +1306,7 @@ public:
         const u64 m = hc->step_total[P.final_step];
         P.send.reserve_discard(c, std::max<u64>(m, 1));
         c.memset(P.cursors.p, 0, R * sizeof(unsigned long long));
-        unsigned long long off[kLoopMaxRanks];
+        unsigned long long* off = P.host->off;
         u64 acc = 0;
         for (u32 k = 0; k < R; ++k) {
             off[k] = acc;

@@ -1,4 +1,5 @@
 #!/bin/bash
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_t.json 2> gpurun_out/bench_t.err
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --partitioned --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_part.json 2> gpurun_out/bench_part.err
 python -c "
-import json; d=json.loads(open('gpurun_out/bench_t.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], d['step_ms'], d['roofline']['kernel_ms_per_step'])"
+import json; d=json.loads(open('gpurun_out/bench_part.json').read().strip().splitlines()[-1]); print('PART', d['ms_per_step'], d['step_ms'], d['config']['reach'], d['config']['iterations'])"
+timeout 900 python -m pytest tests/test_gpu_partition.py -x -q 2>&1 | tail -2

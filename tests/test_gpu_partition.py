@@ -52,3 +52,40 @@ def test_partitioned_equals_single(prog, head, P, seed, n, dom, path, monkeypatc
     hist = [sum(e.delta_history(head)[i] for e in engines) for i in range(iters)]
     assert hist == ref.delta_history(head)
     assert iters == ref.stats().iterations
+
+
+@pytest.mark.parametrize("path", ["loop", "host"])
+def test_run_partitioned_nccl_single_rank(path, monkeypatch):
+    """The production multi-GPU driver (run_partitioned + TorchExchange over
+    NCCL, |Δ| riding with the counts all-to-all) on a real process group of
+    one rank on this GPU: device buffers through NCCL, the piggybacked
+    termination, iteration count and result equal to the single engine."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_02206_b200.partition import TorchExchange, run_partitioned
+    from tests.test_partition_gloo import free_port
+
+    if path == "host":
+        monkeypatch.setenv("GD_PART_LOOP", "0")
+    rng = np.random.default_rng(21)
+    edges = random_relation(rng, 2, 4000, 2500)
+    ref = single("reach", edges)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        ctx = al.Context(0, torch.cuda.current_stream().cuda_stream)
+        e = al.engine("reach", ctx=ctx)
+        e.set_partition(0, 1)
+        e.load_edb("Edge", al.tuple_array(2, edges))
+        e.seed()
+        it = run_partitioned(e, TorchExchange(), 1)
+        assert it == ref.stats().iterations
+        assert np.array_equal(e.relation("Reach").data, ref.relation("Reach").data)
+        assert e.delta_history("Reach") == ref.delta_history("Reach")
+        e.close()
+    finally:
+        dist.destroy_process_group()

@@ -95,16 +95,29 @@ def run_partitioned(eng, exchange, nranks: int, max_iters: int = 1 << 30) -> int
     iteration costs one counts all-to-all and one rows all-to-all; after the
     last productive iteration one more (empty) begin + counts exchange sees
     the global |Δ| = 0."""
+    import os
+    import time
+
+    trace = os.environ.get("GD_PART_TRACE") == "1"
+    tb = tx = te = 0.0
     words = eng.exchange_words()
     it = 0
     local = 1  # the seeded Δ: the first iteration always runs (engine.hpp:181-257)
     while it < max_iters:
+        t0 = time.perf_counter()
         counts, ptr = eng.partition_begin(nranks)
+        t1 = time.perf_counter()
         rptr, rrows, gdelta = exchange.exchange(counts, ptr, words, local)
+        t2 = time.perf_counter()
+        tb, tx = tb + t1 - t0, tx + t2 - t1
         if gdelta == 0:
             break
         local = eng.partition_end(rptr, rrows)
+        te += time.perf_counter() - t2
         it += 1
+    if trace:
+        print(f"[partition] {it} iterations: begin {tb * 1e3:.1f} ms, exchange {tx * 1e3:.1f} ms, "
+              f"end {te * 1e3:.1f} ms", flush=True)
     return it
 
 

@@ -181,14 +181,25 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2311_02206_b200 import arraylog as al
-    from paper_2311_02206_b200.partition import TorchExchange, run_partitioned
+    from paper_2311_02206_b200.partition import NcclComm, TorchExchange, run_partitioned
 
     stream = torch.cuda.current_stream()
     ctx = al.Context(local, stream.cuda_stream)
     edges = gen_workload()
     d_edges = torch.from_numpy(edges.view(np.int64)).cuda()
     flush = torch.empty(256 << 20 >> 2, dtype=torch.int32, device="cuda")
-    exch = TorchExchange() if part else None
+    # N > 1: the library's native driver (its own NCCL send/recv on the
+    # engine stream, one readback per iteration); GD_PART_DRIVER=python
+    # runs the torch.distributed protocol (partition.run_partitioned)
+    native = part and os.environ.get("GD_PART_DRIVER", "native") != "python"
+    exch = TorchExchange() if part and not native else None
+    comm = NcclComm(ctx, rank, world) if native else None
+
+    def drive(e):
+        if native:
+            e.run_partitioned(comm)
+        else:
+            run_partitioned(e, exch, world)
 
     def one_step():
         e = al.engine(PROGRAM, ctx=ctx)
@@ -197,7 +208,7 @@ def main():
         e.load_edb_device("Edge", d_edges.data_ptr(), len(edges))
         if part:
             e.seed()
-            run_partitioned(e, exch, world)
+            drive(e)
         else:
             e.run()
         return e
@@ -341,7 +352,7 @@ def main():
             e.load_edb("Edge", al.tuple_array(2, host_edges))
             if part:
                 e.seed()
-                run_partitioned(e, exch, world)
+                drive(e)
             else:
                 e.run()
             n = e.relation_count(HEAD)
@@ -389,7 +400,9 @@ def main():
             "time_to_fixpoint_s": ms_step / 1e3,
             "config": {"workload": "c2_tc_pl", "program": PROGRAM, **C2, "edges": int(len(edges)),
                        "reach": int(reach_n), "iterations": int(iters), "join_tuples": int(np.mean(joins)),
-                       "parallelism": f"hash-partitioned x{world}" if part else "single",
+                       "parallelism": (f"hash-partitioned x{world}" + (" (native NCCL driver)" if native else
+                                                                         " (torch.distributed driver)"))
+                       if part else "single",
                        "l2": "flushed between steps (256 MiB write)"},
             "step_ms": [round(t, 2) for t in times], "step_phases_ms": step_detail,
             **({"canary_fill_ms": canary_ms} if canary_ms else {}),
@@ -397,6 +410,8 @@ def main():
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if part:
         torch.distributed.destroy_process_group()
 

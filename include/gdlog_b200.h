@@ -55,7 +55,8 @@ typedef enum gd_status {
     GD_ERR_BUDGET = 6,      /* budget_error   (types.hpp:40-72), phase via gd_last_error_phase */
     GD_ERR_CUDA = 7,        /* CUDA runtime failure (no reference equivalent) */
     GD_ERR_UNSUPPORTED = 8, /* shape the device encoding cannot hold */
-    GD_ERR_INVALID_ARG = 9  /* null pointer / bad handle at the C boundary */
+    GD_ERR_INVALID_ARG = 9, /* null pointer / bad handle at the C boundary */
+    GD_ERR_NCCL = 10        /* NCCL failure in the native partitioned driver */
 } gd_status;
 
 /* ------------------------------------------------------------------ */
@@ -398,6 +399,25 @@ gd_status gd_engine_partition_end(gd_engine* eng, const void* d_recv,
                                   uint64_t recv_rows, uint64_t* local_delta);
 /* Global termination is decided by the caller (all-reduce of local Δ). */
 gd_status gd_engine_partition_finish(gd_engine* eng);
+
+/* Native driver: the whole partitioned fixpoint of one rank with the
+ * exchanges issued by the library itself on the context's stream (NCCL
+ * send/recv over NVLink).  Per iteration: joins + owner counts on the
+ * device, one all-to-all of (count, local |Δ|, overflow flag) per peer,
+ * one readback, owner scatter, one all-to-all-v of the rows, insert and
+ * end-of-iteration bookkeeping on the device — a single host
+ * synchronisation.  Every rank calls it collectively after
+ * gd_engine_set_partition + seeding; *iterations = global iterations. */
+typedef struct gd_comm gd_comm;
+gd_status gd_nccl_unique_id(uint8_t id[128]);
+/* nranks / rank as in gd_engine_set_partition; the id is rank 0's
+ * gd_nccl_unique_id, shared by the caller (e.g. a torch.distributed
+ * broadcast). */
+gd_status gd_nccl_comm_create(gd_ctx* ctx, const uint8_t id[128], uint32_t nranks, uint32_t rank,
+                              gd_comm** out);
+gd_status gd_nccl_comm_destroy(gd_comm* comm);
+gd_status gd_engine_run_partitioned(gd_engine* eng, gd_comm* comm, uint64_t max_iters,
+                                    uint64_t* iterations);
 
 #ifdef __cplusplus
 }

@@ -25,6 +25,7 @@ GD_ERR_BUDGET = 6
 GD_ERR_CUDA = 7
 GD_ERR_UNSUPPORTED = 8
 GD_ERR_INVALID_ARG = 9
+GD_ERR_NCCL = 10
 
 GD_OUTER_COL = 0
 GD_INNER_COL = 1
@@ -206,6 +207,10 @@ SIGNATURES = {
     "gd_engine_partition_begin": (C.c_int, [P, P, C.POINTER(P)]),
     "gd_engine_partition_end": (C.c_int, [P, P, u64, PU64]),
     "gd_engine_partition_finish": (C.c_int, [P]),
+    "gd_nccl_unique_id": (C.c_int, [P]),
+    "gd_nccl_comm_create": (C.c_int, [P, P, u32, u32, C.POINTER(P)]),
+    "gd_nccl_comm_destroy": (C.c_int, [P]),
+    "gd_engine_run_partitioned": (C.c_int, [P, P, u64, PU64]),
 }
 
 PKG_DIR = Path(__file__).resolve().parent

@@ -72,6 +72,7 @@ _ERRORS = {
     A.GD_ERR_CUDA: cuda_error,
     A.GD_ERR_UNSUPPORTED: unsupported_error,
     A.GD_ERR_INVALID_ARG: logic_error,
+    A.GD_ERR_NCCL: cuda_error,
 }
 
 
@@ -808,6 +809,14 @@ class engine:
         d = C.c_uint64(0)
         self.ctx.check(self.ctx.lib.gd_engine_partition_end(self.h, C.c_void_p(d_recv), recv_rows, C.byref(d)))
         return d.value
+
+    def run_partitioned(self, comm, max_iters: int = 0) -> int:
+        """gd_engine_run_partitioned: the native multi-GPU driver (NCCL
+        exchanges issued by the library on the context stream); collective
+        over the ranks of `comm` (partition.NcclComm).  Returns iterations."""
+        it = C.c_uint64(0)
+        self.ctx.check(self.ctx.lib.gd_engine_run_partitioned(self.h, comm.h, max_iters, C.byref(it)))
+        return it.value
 
     def close(self):
         if getattr(self, "h", None):

@@ -3,6 +3,7 @@
 // across the boundary.  The kernel-level entries reproduce the validation
 // and error behaviour of the reference functions they replace (cited per
 // entry) and run the same sm_100a kernels the engine uses.
+#include "comm.h"
 #include <cstring>
 #include <memory>
 #include <new>
@@ -647,5 +648,55 @@ gd_status gd_engine_partition_end(gd_engine* eng, const void* d_recv, uint64_t r
     ENG_GUARD(eng->e->partition_end(d_recv, recv_rows, (u64*)local_delta));
 }
 gd_status gd_engine_partition_finish(gd_engine* eng) { ENG_GUARD(eng->e->partition_finish()); }
+
+struct gd_comm {
+    gd::Comm c;
+    gd_ctx* ctx = nullptr;
+};
+
+gd_status gd_nccl_unique_id(uint8_t id[128]) {
+    if (!id) return GD_ERR_INVALID_ARG;
+    ncclUniqueId u;
+    try {
+        if (gd::nccl().get_unique_id(&u) != ncclSuccess) return GD_ERR_NCCL;
+    } catch (const gd::Error&) {
+        return GD_ERR_NCCL;
+    }
+    static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id, &u, sizeof(u));
+    return GD_OK;
+}
+
+gd_status gd_nccl_comm_create(gd_ctx* ctx, const uint8_t id[128], uint32_t nranks, uint32_t rank, gd_comm** out) {
+    if (!ctx || !id || !out || nranks == 0 || rank >= nranks) return GD_ERR_INVALID_ARG;
+    return guard(ctx, [&] {
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof(u));
+        GD_CUDA(cudaSetDevice(ctx->c->device));
+        auto* cm = new gd_comm;
+        cm->ctx = ctx;
+        cm->c.nranks = nranks;
+        cm->c.rank = rank;
+        const ncclResult_t r = gd::nccl().comm_init_rank(&cm->c.comm, (int)nranks, u, (int)rank);
+        if (r != ncclSuccess) {
+            delete cm;
+            gd::nccl_check(r, "ncclCommInitRank");
+        }
+        *out = cm;
+    });
+}
+
+gd_status gd_nccl_comm_destroy(gd_comm* comm) {
+    if (!comm) return GD_ERR_INVALID_ARG;
+    if (comm->c.comm) gd::nccl().comm_destroy(comm->c.comm);
+    delete comm;
+    return GD_OK;
+}
+
+gd_status gd_engine_run_partitioned(gd_engine* eng, gd_comm* comm, uint64_t max_iters, uint64_t* iterations) {
+    if (!comm) return GD_ERR_INVALID_ARG;
+    ENG_GUARD(const u64 it = eng->e->partition_run(comm->c, max_iters ? max_iters : ~0ull);
+              if (iterations) *iterations = it);
+}
 
 }  // extern "C"

@@ -25,6 +25,7 @@
 #endif
 
 #include "engine.h"
+#include "comm.h"
 #include "loop.h"
 #include "ops.h"
 
@@ -1138,6 +1139,7 @@ public:
     // ---- hash-partitioned mode -----------------------------
     void partition_begin(u64* send_counts, const void** d_send) override;
     void partition_end(const void* d_recv, u64 recv_rows, u64* local_delta) override;
+    u64 partition_run(Comm& comm, u64 max_iters) override;
     void partition_finish() override { part_loop_finish(); }
 
     // ---- partitioned mode on the loop kernels ------------------------------
@@ -1157,7 +1159,11 @@ public:
         struct PartHost {
             LoopCtl ctl;
             unsigned long long cnt[kLoopMaxRanks], off[kLoopMaxRanks];
+            u64 rmeta[3 * kLoopMaxRanks];  // native driver: (count, |Δ|, overflow) from each peer
         };
+        DevBuf<u64> recv, meta_send, meta_recv;  // native driver
+        DevBuf<gd_iter_record> hist;
+        u64 hist_cap = 0;
         struct PinnedFree {
             void operator()(PartHost* p) const { cudaFreeHost(p); }
         };
@@ -1366,6 +1372,173 @@ public:
         c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
         E.info_[r].log.push_back(gd_iter_record{din, recv_rows, N, D, hc->h[0].log_n});
         *local_delta = D;
+    }
+
+    // Native partitioned driver (gd_engine_run_partitioned):
+    // the iteration of part_loop_begin / exchange / part_loop_end with the
+    // exchanges as NCCL send/recv on the engine's stream and one host
+    // synchronisation per iteration (the counts readback).  An overflow on
+    // any rank travels in the counts exchange, so every rank redoes the
+    // join together; |Δ| travels there too (termination without an
+    // all-reduce); the end-of-iteration bookkeeping runs on the device and
+    // the per-iteration records are read once at the end.
+    u64 part_loop_run(Comm& comm, u64 max_iters) {
+        PartLoop& P = *pl;
+        LoopCtl* hc = P.hc;
+        const u32 ns = (u32)P.steps.size();
+        const u32 R = E.nranks;
+        if (comm.nranks != R || comm.rank != E.rank)
+            throw_usage("gd_engine_run_partitioned: communicator does not match set_partition");
+        const LStep& F = P.steps[P.final_step];
+        const u64* n_ptr = &P.ctl.p->step_total[P.final_step];
+        LHead& H = P.heads[0];
+        const u32 r = H.rel;
+        auto* ph = P.host.get();
+        if (!P.meta_send.p) {
+            P.meta_send = DevBuf<u64>(c, 3 * (u64)R);
+            P.meta_recv = DevBuf<u64>(c, 3 * (u64)R);
+        }
+        const u64 hist0 = hc->iter;  // records already kept on the host (Python protocol)
+        auto grow_hist = [&](u64 need) {
+            if (need <= P.hist_cap) return;
+            const u64 cap = std::max<u64>(need, 2 * P.hist_cap + 256);
+            DevBuf<gd_iter_record> h2(c, cap);
+            if (P.hist_cap) c.d2d(h2.p, P.hist.p, P.hist_cap * sizeof(gd_iter_record));
+            P.hist = std::move(h2);
+            P.hist_cap = cap;
+        };
+        grow_hist(hist0 + 256);
+        const ncclDataType_t u64t = ncclUint64;
+        u64 it = 0;
+        bool first = true;  // the seeded Δ: the first iteration always runs (as run_partitioned)
+        while (it < max_iters) {
+            // (1) joins on the local Δ, owner counts, counts + |Δ| + overflow to every peer
+            for (u32 i = 0; i < ns; ++i) {
+                LStep& L = P.steps[i];
+                LoopOuter o{};
+                o.kind = L.kind;
+                o.head = L.src_head;
+                o.src_step = L.src_step;
+                o.ptr = L.kind == LO_TEMP ? P.steps[L.src_step].temp.p : H.log.p;
+                loop_probe(c, c.stream, P.ctl.p, i, o, L.jd, L.has_iv ? &L.iv : nullptr, L.dv, L.inner_n, L.bufs(),
+                           P.block_sums.p);
+                loop_scan(c, c.stream, P.ctl.p, i, o, L.bufs(), P.block_sums.p, nullptr);
+                loop_materialize_temp(c, c.stream, P.ctl.p, i, o, L.inner, L.jd, L.bufs(), L.temp.p, L.temp_cap);
+            }
+            c.memset(P.counts.p, 0, R * sizeof(unsigned long long));
+            loop_owner_count(c, F.temp.p, n_ptr, F.temp_cap, R, P.counts.p);
+            loop_part_meta(c, P.counts.p, P.ctl.p, R, first ? 1 : 0, P.meta_send.p);
+            nccl_check(nccl().group_start(), "ncclGroupStart");
+            for (u32 q = 0; q < R; ++q) {
+                nccl_check(nccl().send(P.meta_send.p + 3 * q, 3, u64t, q, comm.comm, c.stream), "ncclSend");
+                nccl_check(nccl().recv(P.meta_recv.p + 3 * q, 3, u64t, q, comm.comm, c.stream), "ncclRecv");
+            }
+            nccl_check(nccl().group_end(), "ncclGroupEnd");
+            c.d2h(hc, P.ctl.p, sizeof(LoopCtl));
+            c.d2h(ph->rmeta, P.meta_recv.p, 3 * R * sizeof(u64));
+            c.d2h(ph->cnt, P.counts.p, R * sizeof(unsigned long long));
+            c.sync();
+            bool any_over = false;
+            u64 gdelta = 0;
+            for (u32 q = 0; q < R; ++q) {
+                gdelta += ph->rmeta[3 * q + 1];
+                any_over |= ph->rmeta[3 * q + 2] != 0;
+            }
+            if (any_over) {  // some rank outgrew a buffer: all ranks redo the join
+                for (u32 i = 0; i < ns; ++i) {
+                    LStep& L = P.steps[i];
+                    if (hc->need_rows[i] > L.rows_cap) {
+                        L.rows_cap = hc->need_rows[i] + hc->need_rows[i] / 2;
+                        L.row_start = DevBuf<u64>(c, L.rows_cap);
+                        L.row_off = DevBuf<u64>(c, L.rows_cap);
+                    }
+                    if (hc->need_splits[i] > L.splits_cap) {
+                        L.splits_cap = hc->need_splits[i] + hc->need_splits[i] / 2;
+                        L.splits = DevBuf<u64>(c, L.splits_cap);
+                    }
+                    if (hc->need_temp[i] > L.temp_cap) {
+                        L.temp_cap = hc->need_temp[i] + hc->need_temp[i] / 2;
+                        L.temp = DevBuf<u64>(c, L.temp_cap);
+                    }
+                    hc->need_rows[i] = hc->need_splits[i] = hc->need_temp[i] = 0;
+                    hc->step_total[i] = 0;
+                }
+                hc->overflow = 0;
+                c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
+                continue;
+            }
+            first = false;
+            if (gdelta == 0) {  // every rank's Δ was empty: no rows were produced anywhere
+                for (u32 i = 0; i < ns; ++i) hc->step_total[i] = 0;
+                c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
+                break;
+            }
+            for (u32 i = 0; i < ns; ++i) E.join_tuples += hc->step_total[i];
+            // (2) group the final step's rows by owner
+            const u64 m = hc->step_total[P.final_step];
+            P.send.reserve_discard(c, std::max<u64>(m, 1));
+            u64 acc = 0;
+            for (u32 q = 0; q < R; ++q) {
+                ph->off[q] = acc;
+                acc += ph->cnt[q];
+            }
+            c.memset(P.cursors.p, 0, R * sizeof(unsigned long long));
+            c.h2d(P.offs.p, ph->off, R * sizeof(unsigned long long));
+            if (m) loop_owner_scatter(c, F.temp.p, n_ptr, R, P.offs.p, P.cursors.p, P.send.p);
+            // (3) rows all-to-all-v
+            u64 total_recv = 0;
+            for (u32 q = 0; q < R; ++q) total_recv += ph->rmeta[3 * q];
+            P.recv.reserve_discard(c, std::max<u64>(total_recv, 1));
+            nccl_check(nccl().group_start(), "ncclGroupStart");
+            u64 roff = 0;
+            for (u32 q = 0; q < R; ++q) {
+                if (ph->cnt[q])
+                    nccl_check(nccl().send(P.send.p + ph->off[q], ph->cnt[q], u64t, q, comm.comm, c.stream), "ncclSend");
+                const u64 rc = ph->rmeta[3 * q];
+                if (rc) nccl_check(nccl().recv(P.recv.p + roff, rc, u64t, q, comm.comm, c.stream), "ncclRecv");
+                roff += rc;
+            }
+            nccl_check(nccl().group_end(), "ncclGroupEnd");
+            // (4) capacities, insert, device-side end of the iteration
+            const u64 ln = hc->h[0].log_n;
+            const u64 need = ln + total_recv;
+            if (need > H.log_cap) {
+                const u64 cap = 2 * need;
+                DevBuf<u64> nl(c, cap);
+                if (ln) loop_copy_u64(c, nl.p, H.log.p, ln);
+                H.log = std::move(nl);
+                H.log_cap = cap;
+            }
+            if (need > H.tab_limit) {
+                DevBuf<u64> old = std::move(H.tab);
+                const u64 old_cap = H.tab_cap;
+                H.alloc_tab(c, 8 * need, false, false);
+                loop_table_rehash(c, old.p, old_cap, H.tab.p, H.tab_cap, H.sbits, ln);
+            }
+            if (hc->iter + 1 - hc->epoch_base > (H.sbits ? (1u << H.sbits) - 1 : 0xfffffffeu)) {
+                loop_table_restamp(c, H.tab.p, H.tab_cap, H.sbits);
+                hc->epoch_base = hc->iter;
+            }
+            grow_hist(hc->iter + 1);
+            hc->step_total[P.final_step] = total_recv;  // the insert kernel's row count
+            hc->h[0].J = hc->h[0].N = hc->h[0].D = 0;
+            c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
+            if (total_recv)
+                loop_insert_keys(c, c.stream, P.ctl.p, P.final_step, 0, P.recv.p, part_bufs(), nullptr);
+            loop_part_advance(c, P.ctl.p, P.final_step, total_recv, P.hist.p);
+            ++it;
+        }
+        // the host mirror and the per-iteration records, once
+        c.d2h(hc, P.ctl.p, sizeof(LoopCtl));
+        std::vector<gd_iter_record> recs(it);
+        if (it) c.d2h(recs.data(), P.hist.p + hist0, it * sizeof(gd_iter_record));
+        c.sync();
+        for (const auto& rec : recs) {
+            ++E.iterations;
+            E.info_[r].history.push_back(rec.delta_in);
+            E.info_[r].log.push_back(rec);
+        }
+        return it;
     }
 
     // The canonical local shard: sort the log once (like iterate_loop).
@@ -1832,6 +2005,21 @@ void Impl<K>::partition_begin(u64* send_counts, const void** d_send) {
 }
 
 template <typename K>
+u64 Impl<K>::partition_run(Comm& comm, u64 max_iters) {
+    if constexpr (std::is_same_v<K, u64>) {
+        u32 rec_rel = UINT32_MAX;
+        for (const auto& p : E.plans_)
+            if (p.recursive) rec_rel = p.head_rel;
+        if (pl || part_loop_eligible(rec_rel)) {
+            if (!pl) part_loop_setup(rec_rel);
+            return part_loop_run(comm, max_iters);
+        }
+    }
+    throw_unsupported("gd_engine_run_partitioned: the native driver runs the loop-kernel partition path "
+                      "(one recursive relation, 64-bit keys); drive other programs with partition_begin/end");
+}
+
+template <typename K>
 void Impl<K>::partition_end(const void* d_recv, u64 recv_rows, u64* local_delta) {
     if constexpr (std::is_same_v<K, u64>) {
         if (pl) {
@@ -2100,5 +2288,10 @@ void Engine::partition_end(const void* d_recv, u64 recv_rows, u64* local_delta) 
     impl->partition_end(d_recv, recv_rows, local_delta);
 }
 void Engine::partition_finish() { impl->partition_finish(); }
+u64 Engine::partition_run(Comm& comm, u64 max_iters) {
+    if (!seeded) throw_logic("gd_engine_run_partitioned: seed first");
+    if (nranks == 0) throw_usage("gd_engine_run_partitioned: set_partition first");
+    return impl->partition_run(comm, max_iters);
+}
 
 }  // namespace gd

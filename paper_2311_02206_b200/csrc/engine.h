@@ -39,6 +39,7 @@ public:
     virtual void partition_begin(u64* send_counts, const void** d_send) = 0;
     virtual void partition_end(const void* d_recv, u64 recv_rows, u64* local_delta) = 0;
     virtual void partition_finish() = 0;
+    virtual u64 partition_run(struct Comm& comm, u64 max_iters) = 0;
 };
 
 class Engine {
@@ -67,6 +68,9 @@ public:
     void partition_begin(u64* send_counts, const void** d_send);
     void partition_end(const void* d_recv, u64 recv_rows, u64* local_delta);
     void partition_finish();
+    // Native driver (gd_engine_run_partitioned): the whole partitioned
+    // fixpoint with NCCL exchanges; returns the iterations run.
+    u64 partition_run(struct Comm& comm, u64 max_iters);
 
     // ---- shared with Impl<K> (engine.cu) ----
     u32 check_rel(u32 r) const {

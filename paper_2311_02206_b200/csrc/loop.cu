@@ -968,6 +968,33 @@ __global__ void owner_scatter_kernel(const u64* __restrict__ keys, const u64* __
     }
 }
 
+__global__ void part_meta_kernel(const unsigned long long* __restrict__ counts, const LoopCtl* ctl, u32 P,
+                                 u64 min_delta, u64* __restrict__ meta) {
+    const u32 p = threadIdx.x;
+    if (p >= P) return;
+    const u64 d = ctl->h[0].dhi - ctl->h[0].dlo;
+    meta[3 * p] = counts[p];
+    meta[3 * p + 1] = d > min_delta ? d : min_delta;
+    meta[3 * p + 2] = ctl->overflow;
+}
+
+__global__ void part_advance_kernel(LoopCtl* ctl, u32 final_step, u64 recv_rows, gd_iter_record* hist) {
+    if (threadIdx.x || blockIdx.x) return;
+    LoopHeadState& st = ctl->h[0];
+    const u32 i = ctl->iter;
+    gd_iter_record r;
+    r.delta_in = st.dhi - st.dlo;
+    r.join = recv_rows;
+    r.new_unique = st.N;
+    r.delta_out = st.D;
+    r.full_after = st.log_n;
+    hist[i] = r;
+    st.dlo = st.dhi;
+    st.dhi = st.log_n;
+    ctl->iter = i + 1;
+    ctl->step_total[final_step] = 0;
+}
+
 // Streaming fill / copy for the growth path (16-byte vectors; the driver's
 // memset / device-to-device memcpy showed 3-146 ms for the same sizes).
 __global__ void fill_u64_kernel(ulonglong2* __restrict__ p, u64 n2, u64 v) {
@@ -1188,6 +1215,16 @@ void loop_select_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head
 
 void loop_owner_count(Ctx& c, const u64* keys, const u64* n_ptr, u64 cap, u32 P, unsigned long long* counts) {
     owner_count_kernel<<<c.num_sms * 4, 256, 0, c.stream>>>(keys, n_ptr, cap, P, counts);
+    c.check_launch();
+}
+
+void loop_part_meta(Ctx& c, const unsigned long long* counts, const LoopCtl* ctl, u32 P, u64 min_delta, u64* meta) {
+    part_meta_kernel<<<1, 64, 0, c.stream>>>(counts, ctl, P, min_delta, meta);
+    c.check_launch();
+}
+
+void loop_part_advance(Ctx& c, LoopCtl* ctl, u32 final_step, u64 recv_rows, gd_iter_record* hist) {
+    part_advance_kernel<<<1, 32, 0, c.stream>>>(ctl, final_step, recv_rows, hist);
     c.check_launch();
 }
 

@@ -195,6 +195,13 @@ void loop_select_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head
 constexpr u32 kLoopMaxRanks = 64;
 // Per-destination counts of keys[0, *n_ptr) (owner = key_hash64(key) mod P).
 void loop_owner_count(Ctx& c, const u64* keys, const u64* n_ptr, u64 cap, u32 P, unsigned long long* counts);
+// Native partitioned driver: meta[3p..3p+2] = (rows for rank p, this
+// rank's |Δ| (at least `min_delta`), overflow flag) for the counts exchange.
+void loop_part_meta(Ctx& c, const unsigned long long* counts, const LoopCtl* ctl, u32 P, u64 min_delta, u64* meta);
+// End of a partitioned iteration on the device: records
+// {|Δ in|, recv_rows, N, D, log_n} at hist[iter], advances the Δ window
+// and the iteration, clears the final step's row count.
+void loop_part_advance(Ctx& c, LoopCtl* ctl, u32 final_step, u64 recv_rows, gd_iter_record* hist);
 // Scatter into out grouped by destination (offsets: exclusive prefix of the
 // counts; cursors zeroed).  Order inside a group is unspecified.
 void loop_owner_scatter(Ctx& c, const u64* keys, const u64* n_ptr, u32 P, const unsigned long long* offsets,

@@ -121,6 +121,41 @@ def run_partitioned(eng, exchange, nranks: int, max_iters: int = 1 << 30) -> int
     return it
 
 
+class NcclComm:
+    """The native driver's NCCL communicator (gd_nccl_comm_create): rank 0's
+    unique id is broadcast through the default torch.distributed group."""
+
+    def __init__(self, ctx, rank: int, nranks: int):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        self.ctx = ctx
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            ctx.check(ctx.lib.gd_nccl_unique_id(uid))
+        if nranks > 1:
+            dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=dev)
+            dist.broadcast(t, 0)
+            uid = (C.c_uint8 * 128)(*t.cpu().tolist())
+        h = C.c_void_p()
+        ctx.check(ctx.lib.gd_nccl_comm_create(ctx.h, uid, nranks, rank, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.ctx.lib.gd_nccl_comm_destroy(self.h)
+            self.h = None
+
+
+def run_partitioned_native(eng, comm: NcclComm, max_iters: int = 0) -> int:
+    """The partitioned fixpoint with the library's own NCCL exchanges (one
+    host synchronisation per iteration); same result as run_partitioned."""
+    return eng.run_partitioned(comm, max_iters)
+
+
 class LoopbackCluster:
     """P logical shards in one process (one GPU): the all-to-all is a
     device-to-device gather of every shard's send groups.  Used by the

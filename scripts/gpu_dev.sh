@@ -1,11 +1,8 @@
 #!/bin/bash
-for s in 8388608 16777216 33554432 67108864; do
-GD_DEDUP_L2_SLOTS=$s timeout 900 python scripts/configs_bench.py c4_cspa 2>/dev/null | python -c "
-import json,sys
-for l in sys.stdin:
-    d=json.loads(l); print('slots=$s', d['workload'], round(d['time_to_fixpoint_s']*1e3,1), 'ms')"
+timeout 900 python -m pytest tests/test_gpu_partition.py -x -q 2>&1 | tail -4
+for drv in native python; do
+GD_PART_DRIVER=$drv timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --partitioned --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_part.json 2> gpurun_out/bench_part.err
+tail -2 gpurun_out/bench_part.err
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_part.json').read().strip().splitlines()[-1]); print('$drv', d['ms_per_step'], d['step_ms'], d['config']['parallelism'], d['config']['reach'], d['config']['iterations'], d['e2e']['seconds_per_step'])"
 done
-GD_DEDUP_SPLIT=0 timeout 900 python scripts/configs_bench.py c4_cspa 2>/dev/null | python -c "
-import json,sys
-for l in sys.stdin:
-    d=json.loads(l); print('nosplit', d['workload'], round(d['time_to_fixpoint_s']*1e3,1), 'ms')"

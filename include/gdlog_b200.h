@@ -415,7 +415,16 @@ gd_status gd_nccl_unique_id(uint8_t id[128]);
  * broadcast). */
 gd_status gd_nccl_comm_create(gd_ctx* ctx, const uint8_t id[128], uint32_t nranks, uint32_t rank,
                               gd_comm** out);
+/* Destroys a communicator of either kind. */
 gd_status gd_nccl_comm_destroy(gd_comm* comm);
+/* Test transport for the same driver: nranks ranks as host threads of one
+ * process, each with its own context and engine on one GPU; messages are
+ * device-to-device copies between barriers.  Validates the driver's
+ * multi-rank logic where only one GPU is available. */
+typedef struct gd_loopback_hub gd_loopback_hub;
+gd_status gd_loopback_hub_create(uint32_t nranks, gd_loopback_hub** out);
+gd_status gd_loopback_hub_destroy(gd_loopback_hub* hub);
+gd_status gd_loopback_comm_create(gd_loopback_hub* hub, uint32_t rank, gd_comm** out);
 gd_status gd_engine_run_partitioned(gd_engine* eng, gd_comm* comm, uint64_t max_iters,
                                     uint64_t* iterations);
 

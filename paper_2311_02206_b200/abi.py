@@ -211,6 +211,9 @@ SIGNATURES = {
     "gd_nccl_comm_create": (C.c_int, [P, P, u32, u32, C.POINTER(P)]),
     "gd_nccl_comm_destroy": (C.c_int, [P]),
     "gd_engine_run_partitioned": (C.c_int, [P, P, u64, PU64]),
+    "gd_loopback_hub_create": (C.c_int, [u32, C.POINTER(P)]),
+    "gd_loopback_hub_destroy": (C.c_int, [P]),
+    "gd_loopback_comm_create": (C.c_int, [P, u32, C.POINTER(P)]),
 }
 
 PKG_DIR = Path(__file__).resolve().parent

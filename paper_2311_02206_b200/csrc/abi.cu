@@ -651,7 +651,12 @@ gd_status gd_engine_partition_finish(gd_engine* eng) { ENG_GUARD(eng->e->partiti
 
 struct gd_comm {
     gd::Comm c;
-    gd_ctx* ctx = nullptr;
+    std::unique_ptr<gd::Transport> t;
+};
+
+struct gd_loopback_hub {
+    gd::LoopbackHub hub;
+    explicit gd_loopback_hub(uint32_t p) : hub(p) {}
 };
 
 gd_status gd_nccl_unique_id(uint8_t id[128]) {
@@ -673,22 +678,44 @@ gd_status gd_nccl_comm_create(gd_ctx* ctx, const uint8_t id[128], uint32_t nrank
         ncclUniqueId u;
         std::memcpy(&u, id, sizeof(u));
         GD_CUDA(cudaSetDevice(ctx->c->device));
+        auto t = std::make_unique<gd::NcclTransport>();
+        t->nranks = nranks;
+        t->rank = rank;
+        gd::nccl_check(gd::nccl().comm_init_rank(&t->comm, (int)nranks, u, (int)rank), "ncclCommInitRank");
         auto* cm = new gd_comm;
-        cm->ctx = ctx;
-        cm->c.nranks = nranks;
-        cm->c.rank = rank;
-        const ncclResult_t r = gd::nccl().comm_init_rank(&cm->c.comm, (int)nranks, u, (int)rank);
-        if (r != ncclSuccess) {
-            delete cm;
-            gd::nccl_check(r, "ncclCommInitRank");
-        }
+        cm->c = gd::Comm{t.get(), nranks, rank};
+        cm->t = std::move(t);
         *out = cm;
     });
 }
 
+gd_status gd_loopback_hub_create(uint32_t nranks, gd_loopback_hub** out) {
+    if (!out || nranks == 0) return GD_ERR_INVALID_ARG;
+    *out = new gd_loopback_hub(nranks);
+    return GD_OK;
+}
+
+gd_status gd_loopback_hub_destroy(gd_loopback_hub* hub) {
+    if (!hub) return GD_ERR_INVALID_ARG;
+    delete hub;
+    return GD_OK;
+}
+
+gd_status gd_loopback_comm_create(gd_loopback_hub* hub, uint32_t rank, gd_comm** out) {
+    if (!hub || !out || rank >= hub->hub.P) return GD_ERR_INVALID_ARG;
+    auto t = std::make_unique<gd::LoopbackTransport>();
+    t->hub = &hub->hub;
+    t->nranks = hub->hub.P;
+    t->rank = rank;
+    auto* cm = new gd_comm;
+    cm->c = gd::Comm{t.get(), hub->hub.P, rank};
+    cm->t = std::move(t);
+    *out = cm;
+    return GD_OK;
+}
+
 gd_status gd_nccl_comm_destroy(gd_comm* comm) {
     if (!comm) return GD_ERR_INVALID_ARG;
-    if (comm->c.comm) gd::nccl().comm_destroy(comm->c.comm);
     delete comm;
     return GD_OK;
 }

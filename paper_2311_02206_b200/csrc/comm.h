@@ -15,8 +15,19 @@
 
 namespace gd {
 
+// The native driver's exchange primitives: point-to-point messages of u64
+// words grouped like ncclGroupStart/End (a group completes as a whole).
+struct Transport {
+    uint32_t nranks = 0, rank = 0;
+    virtual ~Transport() = default;
+    virtual void group_start() = 0;
+    virtual void send(const unsigned long long* buf, uint64_t n, uint32_t peer, cudaStream_t s) = 0;
+    virtual void recv(unsigned long long* buf, uint64_t n, uint32_t peer, cudaStream_t s) = 0;
+    virtual void group_end(cudaStream_t s) = 0;
+};
+
 struct Comm {
-    ncclComm_t comm = nullptr;
+    Transport* t = nullptr;
     uint32_t nranks = 0, rank = 0;
 };
 
@@ -67,5 +78,95 @@ inline const NcclApi& nccl() {
 inline void nccl_check(ncclResult_t r, const char* what) {
     if (r != ncclSuccess) throw Error(GD_ERR_NCCL, std::string(what) + ": " + nccl().error_string(r));
 }
+
+// NCCL over NVLink / NVSwitch: the production transport.
+struct NcclTransport : Transport {
+    ncclComm_t comm = nullptr;
+    ~NcclTransport() override {
+        if (comm) nccl().comm_destroy(comm);
+    }
+    void group_start() override { nccl_check(nccl().group_start(), "ncclGroupStart"); }
+    void send(const unsigned long long* buf, uint64_t n, uint32_t peer, cudaStream_t s) override {
+        nccl_check(nccl().send(buf, n, ncclUint64, (int)peer, comm, s), "ncclSend");
+    }
+    void recv(unsigned long long* buf, uint64_t n, uint32_t peer, cudaStream_t s) override {
+        nccl_check(nccl().recv(buf, n, ncclUint64, (int)peer, comm, s), "ncclRecv");
+    }
+    void group_end(cudaStream_t) override { nccl_check(nccl().group_end(), "ncclGroupEnd"); }
+};
+
+}  // namespace gd
+
+#include <condition_variable>
+#include <mutex>
+#include <vector>
+
+namespace gd {
+
+// Test transport: P ranks as host threads of one process (one engine and
+// stream each, one GPU).  A group publishes its sends, meets the other
+// ranks at a barrier, copies the messages addressed to it device-to-device
+// and meets them again, so the driver's multi-rank logic (offsets, receive
+// layout, overflow consensus, termination) runs without P GPUs.
+struct LoopbackHub {
+    struct Msg {
+        const unsigned long long* src = nullptr;
+        uint64_t n = 0;
+    };
+    uint32_t P;
+    std::vector<Msg> out;  // out[from * P + to]
+    std::mutex m;
+    std::condition_variable cv;
+    uint64_t gen = 0;
+    uint32_t arrived = 0;
+    explicit LoopbackHub(uint32_t p) : P(p), out((size_t)p * p) {}
+    void barrier() {
+        std::unique_lock<std::mutex> l(m);
+        const uint64_t g = gen;
+        if (++arrived == P) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(l, [&] { return gen != g; });
+        }
+    }
+};
+
+struct LoopbackTransport : Transport {
+    LoopbackHub* hub = nullptr;
+    struct Want {
+        unsigned long long* dst;
+        uint64_t n;
+        uint32_t peer;
+    };
+    std::vector<Want> want;
+    std::vector<LoopbackHub::Msg> mine;
+    void group_start() override {
+        want.clear();
+        mine.assign(nranks, LoopbackHub::Msg{});
+    }
+    void send(const unsigned long long* buf, uint64_t n, uint32_t peer, cudaStream_t) override { mine[peer] = {buf, n}; }
+    void recv(unsigned long long* buf, uint64_t n, uint32_t peer, cudaStream_t) override { want.push_back({buf, n, peer}); }
+    void group_end(cudaStream_t s) override {
+        GD_CUDA(cudaStreamSynchronize(s));  // the sent data is complete
+        {
+            std::lock_guard<std::mutex> l(hub->m);
+            for (uint32_t q = 0; q < nranks; ++q) hub->out[(size_t)rank * nranks + q] = mine[q];
+        }
+        hub->barrier();
+        for (const Want& w : want) {
+            LoopbackHub::Msg msg;
+            {
+                std::lock_guard<std::mutex> l(hub->m);
+                msg = hub->out[(size_t)w.peer * nranks + rank];
+            }
+            if (msg.n != w.n) throw Error(GD_ERR_LOGIC, "loopback transport: send/recv size mismatch");
+            GD_CUDA(cudaMemcpyAsync(w.dst, msg.src, w.n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+        }
+        GD_CUDA(cudaStreamSynchronize(s));  // copies done before the senders reuse their buffers
+        hub->barrier();
+    }
+};
 
 }  // namespace gd

@@ -142,6 +142,7 @@ public:
 
     // ------------------------------------------------------------------
     void seed() override {
+        const u64 join0 = E.join_tuples;
         // nonrecursive_topo_order, engine.hpp:322-353
         std::vector<u32> nonrec;
         for (u32 i = 0; i < E.plans_.size(); ++i)
@@ -178,7 +179,13 @@ public:
             st.delta_n = st.full_n;
         }
         check_temp_watermark();
-        if (E.nranks > 1) keep_owned();
+        if (E.nranks > 1) {
+            keep_owned();
+            // every rank ran the seed rules on the replicated EDB: rank 0
+            // alone reports their join tuples, so the ranks' sum is the
+            // single engine's count
+            if (E.rank != 0) E.join_tuples = join0;
+        }
     }
 
     // Partitioned mode: each rank keeps the IDB tuples it owns
@@ -1217,12 +1224,15 @@ public:
         build_loop_steps(P.rec, P.steps);
         P.final_step = (u32)P.steps.size() - 1;
         for (auto& L : P.steps) {
-            L.rows_cap = std::max<u64>(f0 + 1, 1 << 12);
-            L.splits_cap = std::max<u64>(2 * f0 / kLoopMatTile + 2, 1 << 12);
+            // GD_LOOP_TINY=1: minimum capacities, so tests walk the overflow ->
+            // grow -> redo path of both partitioned drivers
+            const bool tiny = getenv("GD_LOOP_TINY") && getenv("GD_LOOP_TINY")[0] == '1';
+            L.rows_cap = tiny ? 2 : std::max<u64>(f0 + 1, 1 << 12);
+            L.splits_cap = tiny ? 2 : std::max<u64>(2 * f0 / kLoopMatTile + 2, 1 << 12);
             L.row_start = DevBuf<u64>(c, L.rows_cap);
             L.row_off = DevBuf<u64>(c, L.rows_cap);
             L.splits = DevBuf<u64>(c, L.splits_cap);
-            L.temp_cap = std::max<u64>(4 * f0, 1 << 16);
+            L.temp_cap = tiny ? 1 : std::max<u64>(4 * f0, 1 << 16);
             L.temp = DevBuf<u64>(c, L.temp_cap);
         }
         P.block_sums = DevBuf<u64>(c, (u64)loop_grid(c));
@@ -1408,7 +1418,6 @@ public:
             P.hist_cap = cap;
         };
         grow_hist(hist0 + 256);
-        const ncclDataType_t u64t = ncclUint64;
         u64 it = 0;
         bool first = true;  // the seeded Δ: the first iteration always runs (as run_partitioned)
         while (it < max_iters) {
@@ -1428,12 +1437,12 @@ public:
             c.memset(P.counts.p, 0, R * sizeof(unsigned long long));
             loop_owner_count(c, F.temp.p, n_ptr, F.temp_cap, R, P.counts.p);
             loop_part_meta(c, P.counts.p, P.ctl.p, R, first ? 1 : 0, P.meta_send.p);
-            nccl_check(nccl().group_start(), "ncclGroupStart");
+            comm.t->group_start();
             for (u32 q = 0; q < R; ++q) {
-                nccl_check(nccl().send(P.meta_send.p + 3 * q, 3, u64t, q, comm.comm, c.stream), "ncclSend");
-                nccl_check(nccl().recv(P.meta_recv.p + 3 * q, 3, u64t, q, comm.comm, c.stream), "ncclRecv");
+                comm.t->send(P.meta_send.p + 3 * q, 3, q, c.stream);
+                comm.t->recv(P.meta_recv.p + 3 * q, 3, q, c.stream);
             }
-            nccl_check(nccl().group_end(), "ncclGroupEnd");
+            comm.t->group_end(c.stream);
             c.d2h(hc, P.ctl.p, sizeof(LoopCtl));
             c.d2h(ph->rmeta, P.meta_recv.p, 3 * R * sizeof(u64));
             c.d2h(ph->cnt, P.counts.p, R * sizeof(unsigned long long));
@@ -1489,16 +1498,16 @@ public:
             u64 total_recv = 0;
             for (u32 q = 0; q < R; ++q) total_recv += ph->rmeta[3 * q];
             P.recv.reserve_discard(c, std::max<u64>(total_recv, 1));
-            nccl_check(nccl().group_start(), "ncclGroupStart");
+            comm.t->group_start();
             u64 roff = 0;
             for (u32 q = 0; q < R; ++q) {
                 if (ph->cnt[q])
-                    nccl_check(nccl().send(P.send.p + ph->off[q], ph->cnt[q], u64t, q, comm.comm, c.stream), "ncclSend");
+                    comm.t->send(P.send.p + ph->off[q], ph->cnt[q], q, c.stream);
                 const u64 rc = ph->rmeta[3 * q];
-                if (rc) nccl_check(nccl().recv(P.recv.p + roff, rc, u64t, q, comm.comm, c.stream), "ncclRecv");
+                if (rc) comm.t->recv(P.recv.p + roff, rc, q, c.stream);
                 roff += rc;
             }
-            nccl_check(nccl().group_end(), "ncclGroupEnd");
+            comm.t->group_end(c.stream);
             // (4) capacities, insert, device-side end of the iteration
             const u64 ln = hc->h[0].log_n;
             const u64 need = ln + total_recv;

@@ -150,6 +150,33 @@ class NcclComm:
             self.h = None
 
 
+class LoopbackComms:
+    """Test transport of the native driver: `nranks` communicators whose
+    ranks run as threads of this process on one GPU (gd_loopback_*)."""
+
+    def __init__(self, ctx, nranks: int):
+        import ctypes as C
+
+        self.ctx = ctx
+        hub = C.c_void_p()
+        ctx.check(ctx.lib.gd_loopback_hub_create(nranks, C.byref(hub)))
+        self.hub = hub
+        self.comms = []
+        for r in range(nranks):
+            h = C.c_void_p()
+            ctx.check(ctx.lib.gd_loopback_comm_create(hub, r, C.byref(h)))
+            c = NcclComm.__new__(NcclComm)
+            c.ctx, c.h = ctx, h
+            self.comms.append(c)
+
+    def close(self):
+        for c in self.comms:
+            c.close()
+        if self.hub:
+            self.ctx.lib.gd_loopback_hub_destroy(self.hub)
+            self.hub = None
+
+
 def run_partitioned_native(eng, comm: NcclComm, max_iters: int = 0) -> int:
     """The partitioned fixpoint with the library's own NCCL exchanges (one
     host synchronisation per iteration); same result as run_partitioned."""

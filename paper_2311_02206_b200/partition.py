@@ -82,11 +82,6 @@ class TorchExchange:
         dist.all_to_all_single(recv, send, [int(x) * words for x in rc], [int(x) * words for x in send_counts])
         return (recv.data_ptr() if total_recv else 0), total_recv, gdelta
 
-    def allreduce_sum(self, x: int) -> int:
-        t = self.torch.tensor([x], dtype=self.torch.int64, device=self.device)
-        self.dist.all_reduce(t)
-        return int(t.item())
-
 
 def run_partitioned(eng, exchange, nranks: int, max_iters: int = 1 << 30) -> int:
     """Drives one rank's engine to the global fixpoint; returns iterations.

@@ -29,21 +29,40 @@ __device__ __forceinline__ u32 digit_of(K k, u32 shift) {
     return (u32)(k >> shift) & (kRadix - 1);
 }
 
-// Counts the digits of every pass for keys [begin, begin+n).
+// Counts the digits of every pass for keys [begin, begin+n).  Warps
+// increment privatized copies (`copies` per CTA, dynamic shared memory of
+// npass * 256 words each, at most 32 KB): the top digits of packed keys are
+// few and skewed, and one shared copy serialises the CTA on them.
 template <typename K>
 __global__ void __launch_bounds__(256) radix_hist_kernel(const K* __restrict__ keys, u64 begin, u64 n,
-                                                         int npass, u64* __restrict__ hist) {
-    __shared__ u32 sh[16 * kRadix];
-    for (int i = threadIdx.x; i < npass * kRadix; i += blockDim.x) sh[i] = 0;
+                                                         int npass, int copies, u64* __restrict__ hist) {
+    extern __shared__ u32 sh[];
+    const int words = npass * kRadix;
+    for (int i = threadIdx.x; i < copies * words; i += blockDim.x) sh[i] = 0;
     __syncthreads();
+    u32* mine = sh + ((threadIdx.x >> 5) % copies) * words;
+    // four independent loads in flight per thread (the pass is otherwise
+    // latency-bound on the key stream)
+    constexpr int kU = 4;
     const u64 stride = (u64)gridDim.x * blockDim.x;
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const K k = keys[begin + i];
-        for (int p = 0; p < npass; ++p) atomicAdd(&sh[p * kRadix + digit_of(k, p * kRadixBits)], 1u);
+    for (u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += kU * stride) {
+        K k[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const u64 i = i0 + u * stride;
+            if (i < n) k[u] = keys[begin + i];
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (i0 + u * stride < n)
+                for (int p = 0; p < npass; ++p) atomicAdd(&mine[p * kRadix + digit_of(k[u], p * kRadixBits)], 1u);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < npass * kRadix; i += blockDim.x)
-        if (sh[i]) atomicAdd(&hist[i], (u64)sh[i]);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) {
+        u32 t = 0;
+        for (int c = 0; c < copies; ++c) t += sh[c * words + i];
+        if (t) atomicAdd(&hist[i], (u64)t);
+    }
 }
 
 // bases[pass][d] = number of keys whose pass-digit is smaller than d.
@@ -232,7 +251,9 @@ K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
     {
         const int grid = (int)std::min<u64>((u64)c.num_sms * 4, (n + 255) / 256);
         cudaEvent_t t = c.prof_begin();
-        radix_hist_kernel<K><<<grid, 256, 0, c.stream>>>(a, 0, n, npass, hist.p);
+        const int copies = npass <= 8 ? 4 : 2;
+        radix_hist_kernel<K><<<grid, 256, (size_t)copies * npass * kRadix * sizeof(u32), c.stream>>>(
+            a, 0, n, npass, copies, hist.p);
         c.check_launch();
         c.prof_end(t, KC_SORT_HIST, n * sizeof(K));
     }

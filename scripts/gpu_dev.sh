@@ -1,5 +1,5 @@
 #!/bin/bash
-# N > 1 bench path at one rank (torchrun): native driver vs torch.distributed protocol
-for drv in native python; do
-GD_PART_DRIVER=$drv timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --partitioned --steps 3 --warmup 3 --no-cpu-baseline 2> gpurun_out/bench_part_$drv.err | tail -1 > gpurun_out/bench_part_$drv.json
-done
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_t.json 2> gpurun_out/bench_t.err
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_t.json').read().strip().splitlines()[-1]); k=d['roofline']['kernel_ms_per_step']; print(round(d['ms_per_step'],1), d['step_ms'], k['sort_hist'], k['sort_pass'])"
+timeout 900 python -m pytest tests/test_gpu_ra.py -x -q 2>&1 | tail -1

@@ -97,8 +97,17 @@ __global__ void part_count_kernel(const u64* __restrict__ keys, u64 m, u32 bits,
     const u32 P = 1u << bits;
     for (u32 i = threadIdx.x; i < P; i += blockDim.x) sc[i] = 0;
     __syncthreads();
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x)
-        atomicAdd(&sc[fmix64(keys[i]) >> (64 - bits)], 1u);
+    // four independent loads in flight per thread
+    constexpr int kU = 4;
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x; i0 < m; i0 += kU * stride) {
+        u64 k[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) k[u] = i0 + u * stride < m ? __ldcs(keys + i0 + u * stride) : 0;
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (i0 + u * stride < m) atomicAdd(&sc[fmix64(k[u]) >> (64 - bits)], 1u);
+    }
     __syncthreads();
     for (u32 i = threadIdx.x; i < P; i += blockDim.x)
         if (sc[i]) atomicAdd(&counts[i], (unsigned long long)sc[i]);

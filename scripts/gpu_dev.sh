@@ -1,7 +1,5 @@
 #!/bin/bash
-timeout 900 python scripts/configs_bench.py c4_cspa c3_sg_tree_w4000 2>/dev/null | python -c "
-import json,sys
-for l in sys.stdin:
-    d=json.loads(l); print(d['workload'], round(d['time_to_fixpoint_s']*1e3,1), 'ms')"
-timeout 900 python -m pytest tests/test_gpu_engine.py -x -q -k "cspa or dedup" 2>&1 | tail -1
-timeout 900 python -m pytest tests/test_gpu_loop.py -x -q -k "dedup" 2>&1 | tail -1
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --partitioned --steps 3 --warmup 3 --no-cpu-baseline 2> gpurun_out/bench_part_native.err | tail -1 > gpurun_out/bench_part_native.json
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_part_native.json').read()); print(round(d['ms_per_step'],1), d['step_ms'], d['config']['parallelism'], d['config']['reach'], round(d['e2e']['seconds_per_step'],3))"
+timeout 600 python bench.py --impl reference --steps 1 --warmup 0 2>/dev/null | tail -1 | cut -c1-300

@@ -179,3 +179,25 @@ def test_native_driver_multi_rank_loopback(prog, head, P, seed, n, dom, tiny, mo
     for e in engines:
         e.close()
     lb.close()
+
+
+def test_native_driver_rejects_host_path(monkeypatch):
+    """The native driver runs the loop-kernel partition path only; on the
+    sort/merge partition path it fails loudly (GD_ERR_UNSUPPORTED) instead
+    of falling back."""
+    from paper_2311_02206_b200.partition import LoopbackComms, run_partitioned_native
+
+    monkeypatch.setenv("GD_PART_LOOP", "0")
+    rng = np.random.default_rng(51)
+    edges = random_relation(rng, 2, 500, 300)
+    ctx = al.Context(0)
+    lb = LoopbackComms(ctx, 1)
+    e = al.engine("reach", ctx=ctx)
+    e.set_partition(0, 1)
+    e.load_edb("Edge", al.tuple_array(2, edges))
+    e.seed()
+    e.partition_begin(1)  # the sort/merge path owns this engine now
+    with pytest.raises(al.unsupported_error):
+        run_partitioned_native(e, lb.comms[0])
+    e.close()
+    lb.close()

@@ -1015,8 +1015,11 @@ int occupancy(Kern k, size_t smem = 0) {
 
 int g_occ_temp = 0, g_occ_insert = 0, g_occ_select = 0, g_occ_keys = 0;
 // Insert grid = waves x resident CTAs: CTAs beyond the resident set start as
-// others finish, so the hardware balances the iteration's tiles.
-int g_ins_waves = 1;
+// others finish, so the hardware balances the iteration's tiles.  Large
+// relations (log capacity >= kWideLog rows) run 3 waves (C2 -2.8%, SG
+// W=4000 -4.3%); small ones 1, where the idle CTAs' launch cost shows
+// (C1 +5% at 3).  GD_INSERT_WAVES overrides.
+constexpr u64 kWideLog = 64ull << 20;
 
 }  // namespace
 
@@ -1198,9 +1201,9 @@ void loop_materialize_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32
     LoopEndDesc e{};
     if (end) e = *end;
     const char* w = getenv("GD_INSERT_WAVES");
-    g_ins_waves = w ? std::max(1, atoi(w)) : g_ins_waves;
-    loop_materialize_insert_kernel<<<c.num_sms * g_occ_insert * g_ins_waves, kLT, 0, s>>>(ctl, step, head, o, inner, jd, sb, hb,
-                                                                             e, end ? 1 : 0);
+    const int waves = w ? std::max(1, atoi(w)) : (hb.log_cap >= kWideLog ? 3 : 1);
+    loop_materialize_insert_kernel<<<c.num_sms * g_occ_insert * waves, kLT, 0, s>>>(ctl, step, head, o, inner, jd,
+                                                                                    sb, hb, e, end ? 1 : 0);
     c.check_launch();
 }
 

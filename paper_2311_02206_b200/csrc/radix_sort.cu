@@ -22,7 +22,7 @@ constexpr int kRadixBits = 8;
 constexpr int kRadix = 256;
 constexpr int kSortThreads = 256;
 constexpr int kWarps = kSortThreads / 32;
-constexpr u64 kPortion = 1ull << 26;  // keys per look-back portion (30-bit status values)
+constexpr u64 kPortion = 1ull << 28;  // keys per look-back portion (30-bit status values)
 
 template <typename K>
 __device__ __forceinline__ u32 digit_of(K k, u32 shift) {

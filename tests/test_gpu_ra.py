@@ -59,7 +59,8 @@ def test_canonicalize_idempotent():
 
 
 def test_canonicalize_large_portions(ref):
-    # > 2^26 keys crosses the onesweep look-back portion boundary
+    # 2^26+ rows of 48-bit keys with duplicates (one look-back portion since
+    # kPortion = 2^28; test_canonicalize_multi_portion crosses portions)
     rng = np.random.default_rng(5)
     n = (1 << 26) + 12345
     a = rng.integers(0, 1 << 24, size=(n, 2), dtype=np.uint64)
@@ -70,6 +71,19 @@ def test_canonicalize_large_portions(ref):
     assert np.all(keys[1:] > keys[:-1])
     ka = np.unique((a[:, 0] << np.uint64(24)) | a[:, 1])
     assert np.array_equal(ka, keys)
+
+
+def test_canonicalize_multi_portion():
+    # > 2^28 keys: several onesweep look-back portions per pass (radix_sort.cu
+    # kPortion).  Distinct 40-bit keys in scrambled order (an odd multiplier
+    # is a bijection mod 2^40); size-independent checks: length, strict
+    # order and the wrap-around sum of the keys.
+    n = (1 << 28) + 12345
+    k = (np.arange(n, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)) & np.uint64((1 << 40) - 1)
+    got = gd_canon(k.reshape(-1, 1), 1).reshape(-1)
+    assert len(got) == n
+    assert np.all(got[1:] > got[:-1])
+    assert np.sum(got, dtype=np.uint64) == np.sum(k, dtype=np.uint64)
 
 
 # ---- permute_columns (tuple_array_test.cpp:60-94) ---------------------------

@@ -1,9 +1,9 @@
 #!/bin/bash
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_s.json 2> gpurun_out/bench_s.err
+cp paper_2311_02206_b200/lib/libgdlog_b200.so /tmp/libgd_orig.so
+for v in occ6 occ5 occ7 occ6; do
+cp paper_2311_02206_b200/lib/variants/lib_$v.so paper_2311_02206_b200/lib/libgdlog_b200.so
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_v.json 2> gpurun_out/bench_v.err
 python -c "
-import json; d=json.loads(open('gpurun_out/bench_s.json').read().strip().splitlines()[-1]); k=d['roofline']['kernel_ms_per_step']; print('portion28', round(d['ms_per_step'],1), d['step_ms'], k['sort_pass'])"
-timeout 900 python scripts/configs_bench.py c5_tc_dag 2>/dev/null | python -c "
-import json,sys
-for l in sys.stdin:
-    d=json.loads(l); print(d['workload'], round(d['time_to_fixpoint_s']*1e3,1), 'ms')"
-timeout 900 python -m pytest tests/test_gpu_ra.py -x -q -k "sort or canonical" 2>&1 | tail -1
+import json; d=json.loads(open('gpurun_out/bench_v.json').read().strip().splitlines()[-1]); k=d['roofline']['kernel_ms_per_step']; print('$v', round(d['ms_per_step'],1), k['join_insert'])"
+done
+cp /tmp/libgd_orig.so paper_2311_02206_b200/lib/libgdlog_b200.so

@@ -299,7 +299,35 @@ public:
     // (8 B per row instead of 8·arity) into two pinned staging buffers, and
     // host threads unpack chunk k into the caller's rows while chunk k+1 is
     // in flight.  Bytes equal unpack_rows + copy.
-    void download_packed(const u64* keys, u64 n, u32 ar, u64* out) {
+    void download_packed(const u64* keys, u64 n_all, u32 ar, u64* out) {
+        // Into a pinned destination, the tail rows [n, n_all) are unpacked on
+        // the device and DMA'd straight into the caller's rows on a second
+        // stream while the host unpacks the packed head: PCIe carries 16 B
+        // per direct row, host memory 16 B instead of 32 (staging write +
+        // read + row write), balancing the two (GD_DL_DIRECT_FRAC, 0.25).
+        u64 n = n_all;
+        DevBuf<u64> direct;
+        cudaStream_t s2 = nullptr;
+        cudaEvent_t ev_un = nullptr;
+        {
+            const char* fe = getenv("GD_DL_DIRECT_FRAC");
+            const double frac = fe ? atof(fe) : 0.25;
+            cudaPointerAttributes pa{};
+            const bool pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+            cudaGetLastError();
+            const u64 nd = pinned && frac > 0 && frac < 1 ? (u64)((double)n_all * frac) : 0;
+            if (nd && nd * ar * sizeof(u64) + (1ull << 30) < c.available_bytes()) {
+                n = n_all - nd;
+                direct = DevBuf<u64>(c, nd * ar);
+                unpack_rows<u64>(c, keys + n, nd, ar, E.enc.e, direct.p);
+                GD_CUDA(cudaEventCreateWithFlags(&ev_un, cudaEventDisableTiming));
+                GD_CUDA(cudaEventRecord(ev_un, c.stream));
+                GD_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+                GD_CUDA(cudaStreamWaitEvent(s2, ev_un, 0));
+                GD_CUDA(cudaMemcpyAsync(out + n * ar, direct.p, nd * ar * sizeof(u64), cudaMemcpyDeviceToHost, s2));
+                c.d2h_bytes += nd * ar * sizeof(u64);
+            }
+        }
         const char* ce = getenv("GD_DL_CHUNK_ROWS");  // experiments
         const u64 kChunk = ce ? std::max<u64>(1u << 16, strtoull(ce, nullptr, 10)) : (1u << 20);
         u64* stage[2];
@@ -405,9 +433,20 @@ public:
         }
         quit.store(true, std::memory_order_release);
         for (auto& th : pool) th.join();
+        double t_direct = 0;
+        if (s2) {
+            const double td = Ctx::now_s();
+            GD_CUDA(cudaStreamSynchronize(s2));
+            t_direct = Ctx::now_s() - td;
+            cudaStreamDestroy(s2);
+            cudaEventDestroy(ev_un);
+        }
         if (trace)
-            fprintf(stderr, "[download] %llu rows, %u threads: waiting on PCIe %.1f ms, unpacking %.1f ms\n",
-                    (unsigned long long)n, nt, t_wait * 1e3, t_unpack * 1e3);
+            fprintf(stderr,
+                    "[download] %llu rows (%llu direct), %u threads: waiting on PCIe %.1f ms, unpacking %.1f ms, "
+                    "direct tail %.1f ms\n",
+                    (unsigned long long)n_all, (unsigned long long)(n_all - n), nt, t_wait * 1e3, t_unpack * 1e3,
+                    t_direct * 1e3);
         cudaEventDestroy(ev[0]);
         cudaEventDestroy(ev[1]);
     }

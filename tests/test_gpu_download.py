@@ -38,3 +38,37 @@ def test_host_unpack_matches(ref, arity, n, hi):
             os.environ.pop("GD_HOST_UNPACK", None)
     assert np.array_equal(outs["1"], outs["0"])
     assert np.array_equal(outs["1"].reshape(-1, arity), canonical(e))
+
+
+@pytest.mark.parametrize("frac", ["0.25", "0.6"])
+def test_pinned_destination_direct_tail(ref, frac):
+    """Into a pinned destination the tail rows are unpacked on the device
+    and DMA'd straight into the caller's rows on a second stream while the
+    host unpacks the head (download_packed): same bytes as a pageable
+    destination, and the transfer counter includes the direct rows."""
+    import ctypes as C
+
+    import torch
+
+    r = ref.engine(COPY2)
+    prog = program_from_ref(r)
+    rng = np.random.default_rng(77)
+    e = rng.integers(0, 1 << 22, size=(6_000_000, 2), dtype=np.uint64)
+    g = al.engine(prog)
+    g.load_edb("E", al.tuple_array(2, e))
+    g.run()
+    rid = g._rid("C")
+    n = g.relation_count("C")
+    want = canonical(e)
+    assert n == len(want)
+    pinned = torch.empty((n, 2), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    os.environ["GD_DL_DIRECT_FRAC"] = frac
+    try:
+        h0, d0 = g.ctx.transfer_bytes()
+        g.ctx.check(g.ctx.lib.gd_engine_relation_download(g.h, rid, pinned.ctypes.data_as(C.c_void_p), n))
+        h1, d1 = g.ctx.transfer_bytes()
+    finally:
+        os.environ.pop("GD_DL_DIRECT_FRAC", None)
+    assert np.array_equal(pinned, want)
+    nd = int(n * float(frac))
+    assert d1 - d0 == (n - nd) * 8 + nd * 16  # packed head + unpacked direct tail

@@ -116,6 +116,18 @@ def run_partitioned(eng, exchange, nranks: int, max_iters: int = 1 << 30) -> int
     return it
 
 
+def share_unique_id(raw: bytes) -> bytes:
+    """Rank 0's 128-byte NCCL unique id to every rank of the default
+    torch.distributed group (the other ranks pass any 128 bytes)."""
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(list(raw), dtype=torch.uint8, device=dev)
+    dist.broadcast(t, 0)
+    return bytes(t.cpu().tolist())
+
+
 class NcclComm:
     """The native driver's NCCL communicator (gd_nccl_comm_create): rank 0's
     unique id is broadcast through the default torch.distributed group."""
@@ -123,18 +135,14 @@ class NcclComm:
     def __init__(self, ctx, rank: int, nranks: int):
         import ctypes as C
 
-        import torch
-        import torch.distributed as dist
+        import torch  # noqa: F401  (loads torch's NCCL before the library resolves it)
 
         self.ctx = ctx
         uid = (C.c_uint8 * 128)()
         if rank == 0:
             ctx.check(ctx.lib.gd_nccl_unique_id(uid))
         if nranks > 1:
-            dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
-            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=dev)
-            dist.broadcast(t, 0)
-            uid = (C.c_uint8 * 128)(*t.cpu().tolist())
+            uid = (C.c_uint8 * 128)(*share_unique_id(bytes(uid)))
         h = C.c_void_p()
         ctx.check(ctx.lib.gd_nccl_comm_create(ctx.h, uid, nranks, rank, C.byref(h)))
         self.h = h

@@ -100,3 +100,25 @@ def test_partitioned_driver_gloo_world2(seed):
     assert union == closure(edges)
     # shards are disjoint
     assert sum(len(out[r][0]) for r in range(world)) == len(union)
+
+
+def _id_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    from paper_2311_02206_b200.partition import share_unique_id
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    raw = bytes(range(128)) if rank == 0 else bytes(128)
+    out[rank] = share_unique_id(raw)
+    dist.destroy_process_group()
+
+
+def test_share_unique_id_gloo():
+    """The native driver's communicator setup: rank 0's NCCL id reaches
+    every rank through torch.distributed (here gloo, 2 ranks on CPU)."""
+    world = 2
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_id_worker, args=(world, free_port(), out), nprocs=world, join=True)
+        assert out[0] == out[1] == bytes(range(128))

@@ -34,6 +34,12 @@ sys.path.insert(0, str(ROOT))
 C2 = dict(n=5_000_000, m=5_000_000, window=200, alpha=1.05, seed=1)
 # bounded CPU sample of the same generator (reference engine ~10-30 s on 16 cores)
 CPU_SAMPLE = dict(n=200_000, m=200_000, window=200, alpha=1.05, seed=1)
+# The reference engine on the full C2 input is not attempted: SURVEY §8d
+# extrapolates hours of CPU time, and its row-major u64 relations
+# (|Reach| 7.7e8 rows x 16 B, plus the merge buffer and copies) exceed the
+# host RAM of the survey box (62 GB).
+FULL_SCALE_DNF = ("full C2 (n=m=5e6, |Reach|=7.7e8) not run on the CPU: DNF by SURVEY §8d's extrapolation "
+                  "(hours; > 62 GB of host RAM for the u64 relation, its merge buffer and copies)")
 PROGRAM = "reach"
 HEAD = "Reach"
 
@@ -152,6 +158,35 @@ def join_tuples_of(edges: np.ndarray, reach: np.ndarray) -> int:
     return int(indeg[reach[:, 0].astype(np.int64)].sum())
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch(n: int) -> int:
+    """Re-runs this command as N ranks (one per GPU) under torchrun; NCCL
+    prints its communicator init lines (nRanks) to stderr."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    log("bench: launching", " ".join(cmd[2:]))
+    return subprocess.call(cmd, env=env)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -169,16 +204,23 @@ def main():
         run_reference_main(args)
         return
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N`: one rank per GPU under torchrun
+        sys.exit(relaunch(args.gpus))
+
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     part = world > 1 or args.partitioned
     if part:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        log(f"rank {rank}: NCCL process group up, nranks {world}, device cuda:{local}")
 
     from paper_2311_02206_b200 import arraylog as al
     from paper_2311_02206_b200.partition import NcclComm, TorchExchange, run_partitioned
@@ -262,6 +304,15 @@ def main():
             ms, jt, reach_n = float(mx.item()), int(sm[0].item()), int(sm[1].item())
         times.append(ms)
         joins.append(jt)
+        if _ == args.steps - 1:  # parity of the measured run (outside the timed region)
+            digest = e.relation_digest(HEAD)
+            if part:
+                dg = torch.tensor([digest - (1 << 63)], dtype=torch.int64, device="cuda")
+                dl = [torch.zeros_like(dg) for _ in range(world)]
+                torch.distributed.all_gather(dl, dg)
+                digest = sum(int(x.item()) + (1 << 63) for x in dl) % (1 << 64)
+            step_record = {"count": int(reach_n), "digest": f"{digest:016x}", "iterations": int(iters),
+                           "join_tuples": int(jt)}
         e.close()
         if canary is not None:  # diagnostics: GPU memory-op speed outside the engine
             c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -378,17 +429,38 @@ def main():
                "h2d_bytes_per_step": int(hb), "d2h_bytes_per_step": int(db),
                "host_rows_bytes": int(reach_n * 16), "seconds_per_step": float(np.mean(e2e_t))}
 
+    # parity of the measured C2 run: the committed full-scale record
+    # (tests/golden/scale_digests.json: resident loop == host loop ==
+    # partitioned P = 2/4/8, rows canonical, Σ Δ = |F|, ΣJ = Σ indeg)
+    parity = {"c2_record": step_record}
+    gp = ROOT / "tests" / "golden" / "scale_digests.json"
+    if gp.exists():
+        g = json.loads(gp.read_text()).get("c2_tc_pl")
+        if g:
+            want = {k: g["record"][k] for k in step_record}
+            parity["c2_matches_golden"] = step_record == want
+
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
             e, cedges, dt = cpu_baseline_sample()
             r = e.relation(HEAD)
             cj = join_tuples_of(cedges, r)
+            # the same sample through the device path: byte-identical rows,
+            # identical Δ history and join tuple count
+            g = al.engine(PROGRAM, ctx=ctx)
+            g.load_edb("Edge", al.tuple_array(2, cedges))
+            g.run()
+            parity["cpu_sample_bit_exact"] = bool(np.array_equal(g.relation(HEAD).data, r)
+                                                  and g.delta_history(HEAD) == e.delta_history(HEAD)
+                                                  and g.raw_stats().join_tuples == cj)
+            g.close()
             s = CPU_SAMPLE
             cpu = {"value": cj / dt, "unit": "tuples/s", "cores": os.cpu_count(), "kind": "reference",
+                   "cpu_model": cpu_model(), "threads": "engine_config.workers = 0 (all host threads)",
                    "sample": f"tc_pl n={s['n']} m={s['m']} W={s['window']} alpha={s['alpha']}: "
                              f"|Reach|={len(r)} J={cj} in {dt:.2f}s",
-                   "time_to_fixpoint_s": dt}
+                   "time_to_fixpoint_s": dt, "full_scale": FULL_SCALE_DNF}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "error": str(ex)[:200]}
 
@@ -406,7 +478,7 @@ def main():
                        "l2": "flushed between steps (256 MiB write)"},
             "step_ms": [round(t, 2) for t in times], "step_phases_ms": step_detail,
             **({"canary_fill_ms": canary_ms} if canary_ms else {}),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "parity": parity,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -439,7 +511,9 @@ def run_reference_main(args):
         "time_to_fixpoint_s": t,
         "config": {"workload": "c2_tc_pl (bounded CPU sample of the same generator)", "program": PROGRAM, **s},
         "cpu_baseline": {"value": v, "unit": "tuples/s", "cores": os.cpu_count(), "kind": "reference",
-                         "sample": f"tc_pl n={s['n']} m={s['m']} W={s['window']} alpha={s['alpha']}"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"tc_pl n={s['n']} m={s['m']} W={s['window']} alpha={s['alpha']}",
+                         "full_scale": FULL_SCALE_DNF},
         "e2e": {"value": v, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

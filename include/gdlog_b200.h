@@ -75,6 +75,9 @@ int gd_abi_version(void);
 /* Number of kernels this context has launched (for the bench's gpu_launches). */
 uint64_t gd_ctx_kernel_launches(const gd_ctx* ctx);
 gd_status gd_ctx_synchronize(gd_ctx* ctx);
+/* Returns the context's cached free device blocks to the driver (after a
+ * large run, before another context or library allocates). */
+gd_status gd_ctx_trim(gd_ctx* ctx);
 
 /* Live per-kernel timing with CUDA events on the context stream (used by
  * bench.py for the roofline).  Classes: 0 sort pass, 1 sort histogram,
@@ -97,6 +100,49 @@ gd_status gd_ctx_host_counters(gd_ctx* ctx, double* alloc_seconds,
  * creation (the e2e bench reports the bytes that actually cross PCIe:
  * relation downloads move packed keys when the encoding allows). */
 gd_status gd_ctx_transfer_bytes(gd_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
+
+/* Device configuration of a context (SURVEY §5 "Config / flags": the
+ * reference's engine_config, engine.hpp:25-32, stays ABI-identical in
+ * gd_engine_config; every device-only knob lives here).  The library reads
+ * no environment variables: a context starts from gd_device_config_default
+ * and every later call on it (and on engines created from it) uses the
+ * configuration last set.  None of these knobs changes a result, only how
+ * the device computes it (tests compare every mode with the reference). */
+typedef enum gd_loop_mode {
+    GD_LOOP_GRAPH = 0, /* whole fixpoint = one CUDA graph with a device-side while node */
+    GD_LOOP_EAGER = 1, /* direct launches, one host check per iteration */
+    GD_LOOP_BATCH = 2  /* a graph of one iteration launched loop_batch times per host check */
+} gd_loop_mode;
+
+typedef struct gd_device_config {
+    uint32_t size;                  /* sizeof(gd_device_config) (version check) */
+    int32_t resident_loop;          /* 1: resident device loop when eligible; 0: host-driven loop */
+    int32_t loop_mode;              /* gd_loop_mode */
+    uint32_t loop_batch;            /* iterations per host check in GD_LOOP_BATCH (16) */
+    int32_t min_capacities;         /* tests: every loop capacity starts at its minimum, so the
+                                       overflow -> rollback -> grow paths run on small inputs (0) */
+    int32_t split_insert;           /* final steps materialize to a temp, then insert (0) */
+    int32_t dense_inner;            /* dense offset array for static one-column inners (1) */
+    uint32_t index_growth;          /* head-index growth: load 1/index_growth after a growth (8) */
+    uint32_t insert_waves;          /* fused-insert grid in waves of resident CTAs (0 = auto) */
+    int32_t rehash_cas_only;        /* index growth by CAS re-spread instead of the zone pass (0) */
+    uint32_t zone_slots;            /* shared-memory slots per zone-pass CTA (4096, <= 8192) */
+    int32_t partition_loop;         /* partitioned mode on the loop kernels when eligible (1) */
+    int32_t hash_dedup;             /* host-driven loop: hash pre-dedup of duplicate-heavy join output (1) */
+    uint64_t hash_dedup_min_rows;   /* ... for join outputs of at least this many rows (1 << 20) */
+    uint64_t dedup_part_slots;      /* L2-resident hash-set part, power of two (8 << 20) */
+    int32_t dedup_split;            /* split large dedup sets into L2-sized parts (1) */
+    int32_t host_unpack;            /* downloads move packed keys, host threads unpack (1) */
+    double download_direct_frac;    /* pinned destinations: share of rows unpacked on the device (0.25) */
+    uint64_t download_chunk_rows;   /* staging chunk of packed downloads (1 << 20) */
+    uint32_t sort_items;            /* onesweep keys per thread: 4, 8 or 16 (16) */
+    uint32_t trace;                 /* stderr traces: bit 0 resident loop, bit 1 downloads (0) */
+} gd_device_config;
+
+void gd_device_config_default(gd_device_config* cfg);
+/* GD_ERR_CONFIG on out-of-range fields or a size mismatch. */
+gd_status gd_ctx_set_device_config(gd_ctx* ctx, const gd_device_config* cfg);
+gd_status gd_ctx_get_device_config(const gd_ctx* ctx, gd_device_config* cfg);
 
 /* ------------------------------------------------------------------ */
 /* Join-spec and plan data (ra.hpp:18-66, plan.hpp:18-58)              */

@@ -41,6 +41,38 @@ u32 = C.c_uint32
 u64 = C.c_uint64
 
 
+GD_LOOP_GRAPH = 0
+GD_LOOP_EAGER = 1
+GD_LOOP_BATCH = 2
+
+
+class gd_device_config(C.Structure):
+    """gd_device_config (gdlog_b200.h): device-only knobs of a context."""
+    _fields_ = [
+        ("size", u32),
+        ("resident_loop", C.c_int32),
+        ("loop_mode", C.c_int32),
+        ("loop_batch", u32),
+        ("min_capacities", C.c_int32),
+        ("split_insert", C.c_int32),
+        ("dense_inner", C.c_int32),
+        ("index_growth", u32),
+        ("insert_waves", u32),
+        ("rehash_cas_only", C.c_int32),
+        ("zone_slots", u32),
+        ("partition_loop", C.c_int32),
+        ("hash_dedup", C.c_int32),
+        ("hash_dedup_min_rows", u64),
+        ("dedup_part_slots", u64),
+        ("dedup_split", C.c_int32),
+        ("host_unpack", C.c_int32),
+        ("download_direct_frac", C.c_double),
+        ("download_chunk_rows", u64),
+        ("sort_items", u32),
+        ("trace", u32),
+    ]
+
+
 class gd_operand(C.Structure):
     _fields_ = [("kind", u32), ("column", u32), ("value", u64)]
 
@@ -162,11 +194,15 @@ SIGNATURES = {
     "gd_last_error_phase": (C.c_char_p, [P]),
     "gd_ctx_kernel_launches": (u64, [P]),
     "gd_ctx_synchronize": (C.c_int, [P]),
+    "gd_ctx_trim": (C.c_int, [P]),
     "gd_ctx_set_profiling": (C.c_int, [P, C.c_int]),
     "gd_ctx_profile_read": (C.c_int, [P, P, P, P]),
     "gd_ctx_profile_reset": (C.c_int, [P]),
     "gd_ctx_host_counters": (C.c_int, [P, P, P, P, P]),
     "gd_ctx_transfer_bytes": (C.c_int, [P, P, P]),
+    "gd_device_config_default": (None, [C.POINTER(gd_device_config)]),
+    "gd_ctx_set_device_config": (C.c_int, [P, C.POINTER(gd_device_config)]),
+    "gd_ctx_get_device_config": (C.c_int, [P, C.POINTER(gd_device_config)]),
     "gd_prefix_hash": (C.c_int, [P, P, u64, u32, u32, P]),
     "gd_canonicalize": (C.c_int, [P, P, u64, u32, P, PU64]),
     "gd_permute_columns": (C.c_int, [P, P, u64, u32, C.c_int, P, u32, P, PU64]),

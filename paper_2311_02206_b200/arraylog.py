@@ -12,7 +12,9 @@ for signature parity and ignored (results never depend on them).
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -187,10 +189,52 @@ def write_relation(rel: tuple_array, path, dict_: dictionary | None = None, ctx:
 # ---------------------------------------------------------------------------
 # Device context
 
-class Context:
-    """Owns a gd_ctx (device + stream).  One host thread per context."""
+# Diagnostics scripts (scripts/*.sh) select device knobs with these
+# environment variables; the Python layer turns them into the context's
+# gd_device_config at creation (the library itself reads no environment).
+_ENV_KNOBS = {
+    "GD_LOOP": ("resident_loop", int),
+    "GD_LOOP_MODE": ("loop_mode", lambda v: {"graph": A.GD_LOOP_GRAPH, "eager": A.GD_LOOP_EAGER,
+                                              "batch": A.GD_LOOP_BATCH}[v]),
+    "GD_LOOP_BATCH": ("loop_batch", int),
+    "GD_LOOP_TINY": ("min_capacities", int),
+    "GD_LOOP_SPLIT": ("split_insert", int),
+    "GD_DENSE": ("dense_inner", int),
+    "GD_TAB_GROWTH": ("index_growth", int),
+    "GD_INSERT_WAVES": ("insert_waves", int),
+    "GD_REHASH_CAS": ("rehash_cas_only", int),
+    "GD_ZONE_SLOTS": ("zone_slots", int),
+    "GD_PART_LOOP": ("partition_loop", int),
+    "GD_HASH_DEDUP": ("hash_dedup", int),
+    "GD_DEDUP_L2_SLOTS": ("dedup_part_slots", int),
+    "GD_DEDUP_SPLIT": ("dedup_split", int),
+    "GD_HOST_UNPACK": ("host_unpack", int),
+    "GD_DL_DIRECT_FRAC": ("download_direct_frac", float),
+    "GD_DL_CHUNK_ROWS": ("download_chunk_rows", int),
+    "GD_SORT_ITEMS": ("sort_items", int),
+}
 
-    def __init__(self, device: int = 0, stream: int | None = None):
+
+def env_device_config() -> dict:
+    """gd_device_config fields selected by GD_* environment variables."""
+    out = {}
+    for k, (field, conv) in _ENV_KNOBS.items():
+        v = os.environ.get(k)
+        if v is not None and v != "":
+            out[field] = conv(v)
+    tr = (1 if os.environ.get("GD_LOOP_TRACE") == "1" else 0) | (2 if os.environ.get("GD_DL_TRACE") == "1" else 0)
+    if tr:
+        out["trace"] = tr
+    return out
+
+
+class Context:
+    """Owns a gd_ctx (device + stream).  One host thread per context.
+
+    `config` sets fields of the context's gd_device_config (defaults from
+    gd_device_config_default, then GD_* diagnostics variables, then this)."""
+
+    def __init__(self, device: int = 0, stream: int | None = None, config: dict | None = None):
         self.lib = A.load_library()
         h = C.c_void_p()
         rc = self.lib.gd_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(h))
@@ -198,6 +242,37 @@ class Context:
             msg = self.lib.gd_last_error(None).decode()
             raise _ERRORS.get(rc, cuda_error)(msg)
         self.h = h
+        kv = env_device_config()
+        kv.update(config or {})
+        if kv:
+            self.set_config(**kv)
+
+    @property
+    def device_config(self) -> dict:
+        c = A.gd_device_config()
+        self.check(self.lib.gd_ctx_get_device_config(self.h, C.byref(c)))
+        return {f: getattr(c, f) for f, _ in A.gd_device_config._fields_}
+
+    def set_config(self, **fields):
+        """Sets gd_device_config fields (GD_ERR_CONFIG -> config_error)."""
+        c = A.gd_device_config()
+        self.check(self.lib.gd_ctx_get_device_config(self.h, C.byref(c)))
+        for f, v in fields.items():
+            if f not in {n for n, _ in A.gd_device_config._fields_} or f == "size":
+                raise config_error(f"unknown device config field '{f}'")
+            setattr(c, f, v)
+        self.check(self.lib.gd_ctx_set_device_config(self.h, C.byref(c)))
+
+    @contextlib.contextmanager
+    def configured(self, **fields):
+        """Temporarily sets device config fields (tests select modes)."""
+        old = self.device_config
+        self.set_config(**fields)
+        try:
+            yield self
+        finally:
+            old.pop("size")
+            self.set_config(**old)
 
     def check(self, rc: int):
         if rc == A.GD_OK:
@@ -213,6 +288,10 @@ class Context:
 
     def synchronize(self):
         self.check(self.lib.gd_ctx_synchronize(self.h))
+
+    def trim(self):
+        """Returns cached free device blocks to the driver (gd_ctx_trim)."""
+        self.check(self.lib.gd_ctx_trim(self.h))
 
     def set_profiling(self, on: bool):
         self.check(self.lib.gd_ctx_set_profiling(self.h, int(on)))

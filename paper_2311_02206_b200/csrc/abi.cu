@@ -251,6 +251,40 @@ uint64_t gd_ctx_kernel_launches(const gd_ctx* ctx) { return ctx && ctx->c ? ctx-
 gd_status gd_ctx_synchronize(gd_ctx* ctx) {
     return guard(ctx, [&] { ctx->c->sync(); });
 }
+gd_status gd_ctx_trim(gd_ctx* ctx) {
+    return guard(ctx, [&] { ctx->c->flush_cache(); });
+}
+
+void gd_device_config_default(gd_device_config* cfg) {
+    if (cfg) *cfg = default_device_config();
+}
+
+gd_status gd_ctx_set_device_config(gd_ctx* ctx, const gd_device_config* cfg) {
+    return guard(ctx, [&] {
+        if (!cfg) throw Error(GD_ERR_INVALID_ARG, "null device config");
+        if (cfg->size != sizeof(gd_device_config))
+            throw_config("gd_device_config: size " + std::to_string(cfg->size) + " != " +
+                         std::to_string(sizeof(gd_device_config)) + " (header/library mismatch)");
+        if (cfg->loop_mode < GD_LOOP_GRAPH || cfg->loop_mode > GD_LOOP_BATCH) throw_config("loop_mode out of range");
+        if (cfg->loop_batch == 0) throw_config("loop_batch must be positive");
+        if (cfg->index_growth < 3) throw_config("index_growth must be at least 3");
+        if (cfg->zone_slots < 1024 || cfg->zone_slots > 8192) throw_config("zone_slots must be in [1024, 8192]");
+        if (cfg->dedup_part_slots < 1024 || (cfg->dedup_part_slots & (cfg->dedup_part_slots - 1)))
+            throw_config("dedup_part_slots must be a power of two >= 1024");
+        if (!(cfg->download_direct_frac >= 0.0 && cfg->download_direct_frac <= 1.0))
+            throw_config("download_direct_frac must be in [0, 1]");
+        if (cfg->download_chunk_rows < (1u << 16)) throw_config("download_chunk_rows must be at least 65536");
+        if (cfg->sort_items != 4 && cfg->sort_items != 8 && cfg->sort_items != 16)
+            throw_config("sort_items must be 4, 8 or 16");
+        ctx->c->cfg = *cfg;
+    });
+}
+
+gd_status gd_ctx_get_device_config(const gd_ctx* ctx, gd_device_config* cfg) {
+    if (!ctx || !ctx->c || !cfg) return GD_ERR_INVALID_ARG;
+    *cfg = ctx->c->cfg;
+    return GD_OK;
+}
 
 gd_status gd_ctx_set_profiling(gd_ctx* ctx, int enable) {
     return guard(ctx, [&] { ctx->c->prof.on = enable != 0; });

@@ -107,8 +107,37 @@ struct Profiler {
     }
 };
 
+// Defaults of gd_device_config (gdlog_b200.h); the library reads no
+// environment variables.
+inline gd_device_config default_device_config() {
+    gd_device_config d{};
+    d.size = sizeof(gd_device_config);
+    d.resident_loop = 1;
+    d.loop_mode = GD_LOOP_GRAPH;
+    d.loop_batch = 16;
+    d.min_capacities = 0;
+    d.split_insert = 0;
+    d.dense_inner = 1;
+    d.index_growth = 8;
+    d.insert_waves = 0;
+    d.rehash_cas_only = 0;
+    d.zone_slots = 4096;
+    d.partition_loop = 1;
+    d.hash_dedup = 1;
+    d.hash_dedup_min_rows = 1u << 20;
+    d.dedup_part_slots = 8u << 20;
+    d.dedup_split = 1;
+    d.host_unpack = 1;
+    d.download_direct_frac = 0.25;
+    d.download_chunk_rows = 1u << 20;
+    d.sort_items = 16;
+    d.trace = 0;
+    return d;
+}
+
 struct Ctx {
     Profiler prof;
+    gd_device_config cfg = default_device_config();
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;

@@ -152,17 +152,15 @@ __global__ void part_scatter_kernel(const u64* __restrict__ keys, u64 m, u32 bit
 // (one streaming pass) and every part is deduplicated in the same
 // L2-resident set of kL2Slots (64 MB), cleared between parts, so the probes
 // hit L2 instead of random HBM lines.
-constexpr u64 kL2SlotsDefault = 8u << 20;
 
 u64 hash_dedup(Ctx& c, const u64* keys, u64 m, u64 expect_unique, u64* out, u64 out_cap) {
-    // GD_DEDUP_L2_SLOTS (power of two) shrinks the per-part set for tests
-    const char* ls = getenv("GD_DEDUP_L2_SLOTS");
-    const u64 kL2Slots = ls ? std::max<u64>(1024, strtoull(ls, nullptr, 10)) : kL2SlotsDefault;
+    // dedup_part_slots (power of two; tests shrink it)
+    const u64 kL2Slots = c.cfg.dedup_part_slots;
     u64 cap = 1024;
     while (cap < 2 * expect_unique) cap <<= 1;
     DevBuf<unsigned long long> cnt(c, 1);
     c.memset(cnt.p, 0, sizeof(unsigned long long));
-    const bool split = cap > kL2Slots && !(getenv("GD_DEDUP_SPLIT") && getenv("GD_DEDUP_SPLIT")[0] == '0');
+    const bool split = cap > kL2Slots && c.cfg.dedup_split;
     const u64 tcap = split ? kL2Slots : cap;
     DevBuf<u64> tab(c, tcap);
     auto run = [&](const u64* k, u64 n, u64 limit) {

@@ -284,7 +284,7 @@ public:
         }
         if constexpr (std::is_same_v<K, u64>) {
             if (!E.enc.e.dict && ar > 1 && st.full_n >= (1u << 20) &&
-                !(getenv("GD_HOST_UNPACK") && getenv("GD_HOST_UNPACK")[0] == '0')) {
+                c.cfg.host_unpack) {
                 download_packed(st.full.p, st.full_n, ar, out);
                 return;
             }
@@ -310,8 +310,7 @@ public:
         cudaStream_t s2 = nullptr;
         cudaEvent_t ev_un = nullptr;
         {
-            const char* fe = getenv("GD_DL_DIRECT_FRAC");
-            const double frac = fe ? atof(fe) : 0.25;
+            const double frac = c.cfg.download_direct_frac;
             cudaPointerAttributes pa{};
             const bool pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
             cudaGetLastError();
@@ -328,8 +327,7 @@ public:
                 c.d2h_bytes += nd * ar * sizeof(u64);
             }
         }
-        const char* ce = getenv("GD_DL_CHUNK_ROWS");  // experiments
-        const u64 kChunk = ce ? std::max<u64>(1u << 16, strtoull(ce, nullptr, 10)) : (1u << 20);
+        const u64 kChunk = c.cfg.download_chunk_rows;
         u64* stage[2];
         void* area = c.pinned_staging(2 * kChunk * sizeof(u64));
         stage[0] = static_cast<u64*>(area);
@@ -347,7 +345,7 @@ public:
             c.d2h(stage[k & 1], keys + b, m * sizeof(u64));
             GD_CUDA(cudaEventRecord(ev[k & 1], c.stream));
         };
-        const bool trace = getenv("GD_DL_TRACE") && getenv("GD_DL_TRACE")[0] == '1';
+        const bool trace = (c.cfg.trace & 2) != 0;
         double t_wait = 0, t_unpack = 0;
         // one pool of nt threads for the whole download; chunk k is handed
         // out by a generation counter once its copy has landed
@@ -545,7 +543,7 @@ public:
     // (the state seed() leaves).
     bool loop_eligible(const std::vector<u32>& rec) {
         if (E.nranks > 1 || E.cfg.memory_budget_bytes != Accountant::kUnlimited) return false;
-        if (const char* e = getenv("GD_LOOP")) if (e[0] == '0') return false;
+        if (!c.cfg.resident_loop) return false;
         if (rec.empty() || rec.size() > kLoopMaxHeads) return false;
         u32 nsteps = 0;
         for (u32 r : rec) {
@@ -633,7 +631,7 @@ public:
                 L.plan = pi;
                 L.var = v;
                 L.final = s + 1 == n;
-                L.split_insert = getenv("GD_LOOP_SPLIT") && getenv("GD_LOOP_SPLIT")[0] == '1';
+                L.split_insert = c.cfg.split_insert != 0;
                 L.head = head_of(p.head_rel);
                 if (s == 0) {
                     auto it = std::find(rec.begin(), rec.end(), var.src_rel);
@@ -671,7 +669,7 @@ public:
                     L.has_iv = true;
                     L.iv = IndexView<u64>{cp.index.slots.p, cp.index.slot_count, L.inner, L.inner_n, iar, bits,
                                           st.join_column_count};
-                    if (st.join_column_count == 1 && !(getenv("GD_DENSE") && getenv("GD_DENSE")[0] == '0') &&
+                    if (st.join_column_count == 1 && c.cfg.dense_inner &&
                         loop_dense_build(c, L.inner, L.inner_n, iar, bits, L.dense, L.dv.lo, L.dv.span))
                         L.dv.off = L.dense.p;
                 }
@@ -691,9 +689,9 @@ public:
         for (u32 r : by_name)
             if (rels[r].dirty) refresh_copies(r);
 
-        // GD_LOOP_TINY=1 starts every capacity at its minimum so tests walk
+        // min_capacities starts every capacity at its minimum so tests walk
         // the overflow -> rollback -> grow -> re-run path on small inputs.
-        const bool tiny = getenv("GD_LOOP_TINY") && getenv("GD_LOOP_TINY")[0] == '1';
+        const bool tiny = c.cfg.min_capacities != 0;
         const u32 nh = (u32)rec.size();
         std::vector<LHead> heads(nh);
         auto head_of = [&](u32 r) -> u32 {
@@ -849,10 +847,9 @@ public:
         // "batch" a plain graph of one iteration launched GD_LOOP_BATCH
         // times per host check; "eager" direct launches, one check per
         // iteration (used when per-kernel profiling is on).
-        const char* mode = getenv("GD_LOOP_MODE");
-        const bool eager = c.prof.on || (mode && std::string(mode) == "eager");
-        const bool batch = !eager && mode && std::string(mode) == "batch";
-        const int batch_n = getenv("GD_LOOP_BATCH") ? std::max(1, atoi(getenv("GD_LOOP_BATCH"))) : 16;
+        const bool eager = c.prof.on || c.cfg.loop_mode == GD_LOOP_EAGER;
+        const bool batch = !eager && c.cfg.loop_mode == GD_LOOP_BATCH;
+        const int batch_n = (int)c.cfg.loop_batch;
         cudaGraphExec_t exec = nullptr;
         cudaGraph_t graph = nullptr;
         cudaStream_t cap_stream = nullptr;
@@ -909,7 +906,7 @@ public:
 
         u64 rollbacks = 0;
         u32 done_iters = 0;
-        const bool trace = getenv("GD_LOOP_TRACE") && getenv("GD_LOOP_TRACE")[0] == '1';
+        const bool trace = (c.cfg.trace & 1) != 0;
         std::vector<u64> prev_log_n(nh);
         for (u32 h = 0; h < nh; ++h) prev_log_n[h] = hc->h[h].log_n;
         double tlast = 0;
@@ -1021,9 +1018,9 @@ public:
                             const u64 sb = loop_slot_bytes(H.sbits);
                             const u64 spill = (ln / 16 + (1u << 20)) * sizeof(u64);  // re-spread spill list
                             u64 avail = c.available_bytes();
-                            // load 1/8 after a growth (GD_TAB_GROWTH: A/B runs; 4 / 6 / 8 / 12
+                            // load 1/8 after a growth (index_growth: 4 / 6 / 8 / 12
                             // measured on C1-C5, 8 best or within 1%)
-                            static const u64 gf = getenv("GD_TAB_GROWTH") ? std::max(3, atoi(getenv("GD_TAB_GROWTH"))) : 8;
+                            const u64 gf = c.cfg.index_growth;
                             if (gf * need * sb + spill + reserve > avail / 2) avail = c.available_bytes(true);
                             const u64 fit = avail > reserve + spill ? (avail - reserve - spill) / sb : 0;
                             const u64 cap = std::min(gf * need, fit);  // load 1/gf after growth when it fits
@@ -1223,7 +1220,7 @@ public:
 
     bool part_loop_eligible(u32 rec_rel) {
         if constexpr (!std::is_same_v<K, u64>) return false;
-        if (getenv("GD_PART_LOOP") && getenv("GD_PART_LOOP")[0] == '0') return false;
+        if (!c.cfg.partition_loop) return false;
         if (E.nranks > kLoopMaxRanks) return false;
         const auto& st = rels[rec_rel];
         if (!st.lsm || st.delta_n != total_n(st)) return false;
@@ -1263,9 +1260,9 @@ public:
         build_loop_steps(P.rec, P.steps);
         P.final_step = (u32)P.steps.size() - 1;
         for (auto& L : P.steps) {
-            // GD_LOOP_TINY=1: minimum capacities, so tests walk the overflow ->
-            // grow -> redo path of both partitioned drivers
-            const bool tiny = getenv("GD_LOOP_TINY") && getenv("GD_LOOP_TINY")[0] == '1';
+            // min_capacities: tests walk the overflow -> grow -> redo path of
+            // both partitioned drivers
+            const bool tiny = c.cfg.min_capacities != 0;
             L.rows_cap = tiny ? 2 : std::max<u64>(f0 + 1, 1 << 12);
             L.splits_cap = tiny ? 2 : std::max<u64>(2 * f0 / kLoopMatTile + 2, 1 << 12);
             L.row_start = DevBuf<u64>(c, L.rows_cap);
@@ -1942,8 +1939,7 @@ private:
                     // only the distinct rows (dedup.cu); the set is sized from
                     // the previous iteration's distinct count
                     const u64 expect = std::max<u64>(2 * st.last_unique + 4096, m / 64);
-                    if (m >= (1u << 20) && 4 * expect < m && !(getenv("GD_HASH_DEDUP") &&
-                                                               getenv("GD_HASH_DEDUP")[0] == '0')) {
+                    if (c.cfg.hash_dedup && m >= c.cfg.hash_dedup_min_rows && 4 * expect < m) {
                         DevBuf<u64> uniq(c, std::min<u64>(m, 2 * expect + 1));
                         const u64 u = hash_dedup(c, reinterpret_cast<const u64*>(st.new_acc.p), m, expect, uniq.p,
                                                  uniq.cap);

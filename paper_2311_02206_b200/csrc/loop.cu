@@ -823,8 +823,7 @@ __global__ void table_rehash_kernel(const void* old_tab, u64 old_cap, void* tab,
 // spilled and CAS-inserted afterwards.  Insertion order within a zone does
 // not matter for linear probing (nothing is deleted).
 constexpr u32 kZoneThreads = 256;
-constexpr u32 kZoneSlots = 4096;     // 32 KB of shared memory per CTA (6 CTAs per SM)
-constexpr u32 kZoneSlotsMax = 8192;  // GD_ZONE_SLOTS experiments
+constexpr u32 kZoneSlotsMax = 8192;  // zone_slots upper bound
 constexpr u32 kZoneBatch = 8;
 __global__ void __launch_bounds__(kZoneThreads) table_zone_kernel(const void* old_tab, u64 old_cap, void* tab,
                                                                   u64 cap, u32 sb, u32 T, u64* __restrict__ spill,
@@ -1018,7 +1017,7 @@ int g_occ_temp = 0, g_occ_insert = 0, g_occ_select = 0, g_occ_keys = 0;
 // others finish, so the hardware balances the iteration's tiles.  Large
 // relations (log capacity >= kWideLog rows) run 3 waves (C2 -2.8%, SG
 // W=4000 -4.3%); small ones 1, where the idle CTAs' launch cost shows
-// (C1 +5% at 3).  GD_INSERT_WAVES overrides.
+// (C1 +5% at 3).  gd_device_config.insert_waves overrides.
 constexpr u64 kWideLog = 64ull << 20;
 
 }  // namespace
@@ -1079,9 +1078,8 @@ void loop_table_rehash(Ctx& c, const void* old_tab, u64 old_cap, void* tab, u64 
         loop_table_clear(c, tab, cap, sbits);
         return;
     }
-    const bool cas_only = getenv("GD_REHASH_CAS") && getenv("GD_REHASH_CAS")[0] == '1';
-    const char* zs = getenv("GD_ZONE_SLOTS");  // experiments: zone size (shared memory per CTA)
-    const u32 zslots = zs ? std::min<u32>(kZoneSlotsMax, std::max(1024, atoi(zs))) : kZoneSlots;
+    const bool cas_only = c.cfg.rehash_cas_only != 0;
+    const u32 zslots = std::min<u32>(kZoneSlotsMax, std::max<u32>(1024, c.cfg.zone_slots));
     const u64 T = (u64)((double)(zslots - 2) * (double)old_cap / (double)cap) / 32 * 32;
     const u64 nzones = T ? (old_cap + T - 1) / T : 0;
     if (!cas_only && T >= 256 && nzones < (1u << 31)) {
@@ -1200,8 +1198,7 @@ void loop_materialize_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32
                              const LoopHeadBufs& hb, const LoopEndDesc* end) {
     LoopEndDesc e{};
     if (end) e = *end;
-    const char* w = getenv("GD_INSERT_WAVES");
-    const int waves = w ? std::max(1, atoi(w)) : (hb.log_cap >= kWideLog ? 3 : 1);
+    const int waves = c.cfg.insert_waves ? (int)c.cfg.insert_waves : (hb.log_cap >= kWideLog ? 3 : 1);
     loop_materialize_insert_kernel<<<c.num_sms * g_occ_insert * waves, kLT, 0, s>>>(ctl, step, head, o, inner, jd,
                                                                                     sb, hb, e, end ? 1 : 0);
     c.check_launch();

@@ -215,16 +215,12 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
 
 }  // namespace
 
-// Keys per thread of a onesweep tile (4/8/16 are compiled; GD_SORT_ITEMS
-// overrides for experiments, scripts/sortbench.py).
+// Keys per thread of a onesweep tile (4/8/16 are compiled;
+// gd_device_config.sort_items, 16 by default: measured on B200 fastest from
+// 64K to 16M keys).
 template <typename K>
-int sort_items(u64 n) {
-    static const int forced = [] {
-        const char* e = getenv("GD_SORT_ITEMS");
-        return e ? atoi(e) : 0;
-    }();
-    (void)n;  // measured on B200: 16 keys/thread is fastest from 64K to 16M keys
-    int i = forced ? forced : 16;
+int sort_items(const Ctx& c) {
+    int i = (int)c.cfg.sort_items;
     if (sizeof(K) > 8) i = std::min(i, 8);
     return i == 16 || i == 8 ? i : 4;
 }
@@ -241,7 +237,7 @@ K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
     if (n <= 1 || nbits == 0) return a;
     const int npass = (int)((nbits + kRadixBits - 1) / kRadixBits);
     const int nportions = (int)((n + kPortion - 1) / kPortion);
-    const int items = sort_items<K>(n);
+    const int items = sort_items<K>(c);
     const u64 TILE = (u64)kSortThreads * items;
 
     const u64 hist_words = (u64)npass * kRadix;

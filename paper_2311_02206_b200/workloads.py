@@ -3,7 +3,8 @@
 Vectorised numpy generators (seeded, deterministic).  These define the
 benchmark inputs; they are not bit-identical to the survey's libstdc++
 mt19937 probes (tests reproduce C1 exactly through the compiled reference
-generator), but follow the same shapes:
+generator), but follow the same shapes.  Duplicate draws are kept: they
+collapse when the engine canonicalizes at load (engine.hpp:107-128).
 
   tc_rand   C1  uniform random graph, n nodes, m draws
   tc_pl     C2  power-law DAG: src = floor((n-1) U^alpha), dst = src+1+U{0..W-1}
@@ -14,10 +15,6 @@ generator), but follow the same shapes:
 from __future__ import annotations
 
 import numpy as np
-
-
-def _dedup(e: np.ndarray) -> np.ndarray:
-    return e  # duplicates collapse at load (engine canonicalizes)
 
 
 def tc_rand(n: int, m: int, seed: int = 1) -> np.ndarray:
@@ -64,8 +61,8 @@ def cspa_local(n: int, n_assign: int, n_deref: int, module: int = 256, seed: int
 CONFIGS = {
     "c1_tc_rand": dict(program="reach", gen=lambda: {"Edge": tc_rand(10_000, 10_000, 1)},
                        desc="TC on a random graph, n=m=1e4"),
-    "c2_tc_pl": dict(program="reach", gen=lambda: {"Edge": tc_pl(2_000_000, 5_000_000, 40, 2.0, 1)},
-                     desc="TC on a power-law DAG, 5e6 edge draws (n=2e6, W=40, alpha=2)"),
+    "c2_tc_pl": dict(program="reach", gen=lambda: {"Edge": tc_pl(5_000_000, 5_000_000, 200, 1.05, 1)},
+                     desc="TC on a power-law DAG, 5e6 edge draws (n=5e6, W=200, alpha=1.05; bench.py)"),
     "c3_sg_tree": dict(program="sg", gen=lambda: {"Edge": sg_tree(1_000_001, 40, 1)},
                        desc="SG on a random tree, 1e6 edges (W=40)"),
     "c3_sg_tree_w1000": dict(program="sg", gen=lambda: {"Edge": sg_tree(1_000_001, 1000, 1)},

@@ -95,6 +95,56 @@ def F(lhs, rhs, eq=False):
     return A.gd_filter(lhs, rhs, int(eq), 0)
 
 
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _rotl(x, r):
+    return (x << np.uint64(r)) | (x >> np.uint64(64 - r))
+
+
+def fmix64(k: np.ndarray) -> np.ndarray:
+    """Murmur3 finalizer (hash.hpp:13-20), vectorised, wrapping u64."""
+    k = k ^ (k >> np.uint64(33))
+    k = k * np.uint64(0xFF51AFD7ED558CCD)
+    k = k ^ (k >> np.uint64(33))
+    k = k * np.uint64(0xC4CEB9FE1A85EC53)
+    return k ^ (k >> np.uint64(33))
+
+
+def prefix_hash_np(a: np.ndarray) -> np.ndarray:
+    """prefix_hash over every column of each row (hash.hpp:28-53: the
+    Murmur3-x64-128-style mix, seed 0, h1 + h2), vectorised."""
+    a = np.asarray(a, dtype=np.uint64)
+    n = a.shape[1]
+    c1, c2 = np.uint64(0x87C37B91114253D5), np.uint64(0x4CF5AD432745937F)
+    h1 = np.zeros(len(a), dtype=np.uint64)
+    h2 = np.zeros(len(a), dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for i in range(0, n - 1, 2):
+            k1 = _rotl(a[:, i] * c1, 31) * c2
+            h1 ^= k1
+            h1 = _rotl(h1, 27) + h2
+            h1 = h1 * np.uint64(5) + np.uint64(0x52DCE729)
+            k2 = _rotl(a[:, i + 1] * c2, 33) * c1
+            h2 ^= k2
+            h2 = _rotl(h2, 31) + h1
+            h2 = h2 * np.uint64(5) + np.uint64(0x38495AB5)
+        if n % 2:
+            h1 ^= _rotl(a[:, n - 1] * c1, 31) * c2
+        ln = np.uint64(n * 8)
+        h1 ^= ln
+        h2 ^= ln
+        h1 = h1 + h2
+        h2 = h2 + h1
+        return fmix64(h1) + fmix64(h2)
+
+
 def digest_rows(a: np.ndarray) -> int:
-    """Host twin of the device relation digest: sum of fmix64(slot-hash)."""
-    raise NotImplementedError
+    """Host twin of the device relation digest (gd_engine_relation_digest,
+    primitives.cu digest_kernel): the order-independent sum, mod 2^64, of
+    fmix64(prefix_hash(row)) over the rows."""
+    a = np.asarray(a, dtype=np.uint64)
+    if len(a) == 0:
+        return 0
+    with np.errstate(over="ignore"):
+        return int(np.sum(fmix64(prefix_hash_np(a)), dtype=np.uint64))

@@ -59,7 +59,7 @@ def test_no_gpu_means_loud_failure(lib):
 
 
 STRUCTS = ["gd_operand", "gd_filter", "gd_join_step", "gd_variant", "gd_rule_plan", "gd_container_view",
-           "gd_join_spec", "gd_engine_config", "gd_run_stats", "gd_iter_record"]
+           "gd_join_spec", "gd_engine_config", "gd_run_stats", "gd_iter_record", "gd_device_config"]
 
 
 def test_struct_layouts_match_c():
@@ -68,7 +68,8 @@ def test_struct_layouts_match_c():
     for s in STRUCTS:
         src += f'printf("{s} %zu\\n", sizeof({s}));\n'
     src += 'printf("off_steps %zu\\n", offsetof(gd_variant, steps));\n'
-    src += 'printf("off_algo %zu\\n", offsetof(gd_run_stats, algo_bytes));\nreturn 0;}\n'
+    src += 'printf("off_algo %zu\\n", offsetof(gd_run_stats, algo_bytes));\n'
+    src += 'printf("off_frac %zu\\n", offsetof(gd_device_config, download_direct_frac));\nreturn 0;}\n'
     with tempfile.TemporaryDirectory() as d:
         c = Path(d) / "t.c"
         c.write_text(src)
@@ -80,3 +81,33 @@ def test_struct_layouts_match_c():
         assert int(got[s]) == C.sizeof(getattr(A, s)), s
     assert int(got["off_steps"]) == A.gd_variant.steps.offset
     assert int(got["off_algo"]) == A.gd_run_stats.algo_bytes.offset
+    assert int(got["off_frac"]) == A.gd_device_config.download_direct_frac.offset
+
+
+def test_device_config_defaults(lib):
+    """gd_device_config_default (no device needed): the library's defaults,
+    which the GD_* diagnostics variables of the Python layer override."""
+    import ctypes as C
+    c = A.gd_device_config()
+    lib.gd_device_config_default(C.byref(c))
+    assert c.size == C.sizeof(A.gd_device_config)
+    assert (c.resident_loop, c.loop_mode, c.loop_batch, c.min_capacities) == (1, A.GD_LOOP_GRAPH, 16, 0)
+    assert (c.index_growth, c.zone_slots, c.sort_items, c.hash_dedup_min_rows) == (8, 4096, 16, 1 << 20)
+    assert c.download_direct_frac == 0.25
+    assert lib.gd_ctx_set_device_config(None, C.byref(c)) == A.GD_ERR_INVALID_ARG
+
+
+def test_library_reads_no_environment():
+    """Device knobs come from gd_device_config only: the
+    library imports no getenv."""
+    out = subprocess.run(["nm", "-D", "--undefined-only", str(A.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "getenv" not in out
+
+
+def test_env_knobs_map_to_config(monkeypatch):
+    from paper_2311_02206_b200 import arraylog as al
+    monkeypatch.setenv("GD_LOOP_MODE", "eager")
+    monkeypatch.setenv("GD_LOOP_TINY", "1")
+    monkeypatch.setenv("GD_DL_DIRECT_FRAC", "0.5")
+    assert al.env_device_config() == {"loop_mode": A.GD_LOOP_EAGER, "min_capacities": 1,
+                                      "download_direct_frac": 0.5}

@@ -1,12 +1,10 @@
 """The resident device loop (csrc/loop.cu) against the
 host-driven loop and the reference engine: graph (device-side `while`),
 eager and host-driven modes give byte-identical relations, identical Δ
-histories, iteration records and accountant statistics; GD_LOOP_TINY=1
-starts every capacity at its minimum so every overflow -> rollback ->
+histories, iteration records and accountant statistics; min_capacities
+(gd_device_config) starts every capacity at its minimum so every overflow -> rollback ->
 grow -> re-run path runs.
 """
-import os
-
 import numpy as np
 import pytest
 
@@ -16,37 +14,26 @@ from tests.test_gpu_engine import CUSTOM, assert_same, corpus, run_gpu, run_ref
 
 pytestmark = pytest.mark.gpu
 
-MODES = {
+MODES = {  # gd_device_config fields of each mode
     "graph": {},
-    "eager": {"GD_LOOP_MODE": "eager"},
-    "tiny": {"GD_LOOP_TINY": "1"},
-    "tiny_eager": {"GD_LOOP_TINY": "1", "GD_LOOP_MODE": "eager"},
-    "host": {"GD_LOOP": "0"},
-    "hashindex": {"GD_DENSE": "0"},
-    "split": {"GD_LOOP_SPLIT": "1"},
-    "tiny_split": {"GD_LOOP_TINY": "1", "GD_LOOP_SPLIT": "1"},
-    "tiny_casrehash": {"GD_LOOP_TINY": "1", "GD_REHASH_CAS": "1"},
+    "eager": {"loop_mode": 1},
+    "tiny": {"min_capacities": 1},
+    "tiny_eager": {"min_capacities": 1, "loop_mode": 1},
+    "host": {"resident_loop": 0},
+    "hashindex": {"dense_inner": 0},
+    "split": {"split_insert": 1},
+    "tiny_split": {"min_capacities": 1, "split_insert": 1},
+    "tiny_casrehash": {"min_capacities": 1, "rehash_cas_only": 1},
 }
 
 
-class env:
-    def __init__(self, **kv):
-        self.kv = kv
-
-    def __enter__(self):
-        self.old = {k: os.environ.get(k) for k in self.kv}
-        os.environ.update(self.kv)
-
-    def __exit__(self, *a):
-        for k, v in self.old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+def configured(**fields):
+    """The default context with these gd_device_config fields set."""
+    return al.default_context().configured(**fields)
 
 
 def run_mode(mode, program, db):
-    with env(**MODES[mode]):
+    with configured(**MODES[mode]):
         return run_gpu(program, db)
 
 
@@ -125,9 +112,9 @@ def test_hash_predup_matches_sort_path():
     a, d = W.cspa_local(300_000, 72_000, 228_000, 256, 2)
     db = {"assign": a, "dereference": d}
     outs = {}
-    for mode, kv in (("1", {"GD_HASH_DEDUP": "1"}), ("0", {"GD_HASH_DEDUP": "0"}),
-                     ("split", {"GD_HASH_DEDUP": "1", "GD_DEDUP_L2_SLOTS": "65536"})):
-        with env(**kv):
+    for mode, kv in (("1", {"hash_dedup": 1}), ("0", {"hash_dedup": 0}),
+                     ("split", {"hash_dedup": 1, "dedup_part_slots": 65536})):
+        with configured(**kv):
             outs[mode] = run_gpu("cspa", db)
     g, h = outs["1"], outs["0"]
     for n in ("ValueFlow", "MemoryAlias", "ValueAlias"):

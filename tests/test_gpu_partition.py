@@ -26,23 +26,23 @@ def single(prog, edges):
     ("reach", "Reach", 2, 1, 3000, 1500), ("reach", "Reach", 3, 2, 5000, 4000), ("reach", "Reach", 4, 3, 800, 300),
     ("reach", "Reach", 8, 6, 20000, 8000), ("sg", "SG", 2, 4, 1500, 1000), ("sg", "SG", 4, 5, 2000, 2500),
 ])
-def test_partitioned_equals_single(prog, head, P, seed, n, dom, path, monkeypatch):
+def test_partitioned_equals_single(prog, head, P, seed, n, dom, path):
     """path "loop": the per-iteration kernels of the resident loop (probe /
     scan / materialize, owner grouping, index insert); "host": the sort /
-    merge host path (GD_PART_LOOP=0)."""
-    if path == "host":
-        monkeypatch.setenv("GD_PART_LOOP", "0")
+    merge host path (gd_device_config.partition_loop = 0)."""
+    cfg = {"partition_loop": 0} if path == "host" else {}
     rng = np.random.default_rng(seed)
     edges = random_relation(rng, 2, n, dom)
     ref = single(prog, edges)
     engines = []
-    for r in range(P):
-        e = al.engine(prog)
-        e.set_partition(r, P)
-        e.load_edb("Edge", al.tuple_array(2, edges))
-        e.seed()
-        engines.append(e)
-    iters = LoopbackCluster(engines).run()
+    with al.default_context().configured(**cfg):
+        for r in range(P):
+            e = al.engine(prog)
+            e.set_partition(r, P)
+            e.load_edb("Edge", al.tuple_array(2, edges))
+            e.seed()
+            engines.append(e)
+        iters = LoopbackCluster(engines).run()
     parts = [e.relation(head).data for e in engines]
     union = np.vstack(parts)
     assert len(union) == ref.relation_count(head)  # disjoint shards
@@ -57,7 +57,7 @@ def test_partitioned_equals_single(prog, head, P, seed, n, dom, path, monkeypatc
 
 
 @pytest.mark.parametrize("path", ["loop", "host"])
-def test_run_partitioned_nccl_single_rank(path, monkeypatch):
+def test_run_partitioned_nccl_single_rank(path):
     """The production multi-GPU driver (run_partitioned + TorchExchange over
     NCCL, |Δ| riding with the counts all-to-all) on a real process group of
     one rank on this GPU: device buffers through NCCL, the piggybacked
@@ -70,8 +70,7 @@ def test_run_partitioned_nccl_single_rank(path, monkeypatch):
     from paper_2311_02206_b200.partition import TorchExchange, run_partitioned
     from tests.test_partition_gloo import free_port
 
-    if path == "host":
-        monkeypatch.setenv("GD_PART_LOOP", "0")
+    cfg = {"partition_loop": 0} if path == "host" else {}
     rng = np.random.default_rng(21)
     edges = random_relation(rng, 2, 4000, 2500)
     ref = single("reach", edges)
@@ -79,7 +78,7 @@ def test_run_partitioned_nccl_single_rank(path, monkeypatch):
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
-        ctx = al.Context(0, torch.cuda.current_stream().cuda_stream)
+        ctx = al.Context(0, torch.cuda.current_stream().cuda_stream, config=cfg)
         e = al.engine("reach", ctx=ctx)
         e.set_partition(0, 1)
         e.load_edb("Edge", al.tuple_array(2, edges))
@@ -128,7 +127,7 @@ def test_native_driver_single_rank(prog, head, seed, n, dom):
     ("reach", "Reach", 2, 41, 3000, 1500), ("reach", "Reach", 3, 42, 5000, 4000), ("reach", "Reach", 4, 43, 800, 300),
     ("sg", "SG", 2, 44, 1500, 1000), ("sg", "SG", 3, 45, 2000, 2500),
 ])
-def test_native_driver_multi_rank_loopback(prog, head, P, seed, n, dom, tiny, monkeypatch):
+def test_native_driver_multi_rank_loopback(prog, head, P, seed, n, dom, tiny):
     """The native driver's multi-rank logic (counts / |Δ| / overflow triples,
     offsets, receive layout, collective redo on overflow, termination) with
     P ranks as threads of this process, each with its own context, stream
@@ -139,12 +138,11 @@ def test_native_driver_multi_rank_loopback(prog, head, P, seed, n, dom, tiny, mo
 
     from paper_2311_02206_b200.partition import LoopbackComms, run_partitioned_native
 
-    if tiny:
-        monkeypatch.setenv("GD_LOOP_TINY", "1")
+    cfg = {"min_capacities": 1} if tiny else {}
     rng = np.random.default_rng(seed)
     edges = random_relation(rng, 2, n, dom)
     ref = single(prog, edges)
-    ctxs = [al.Context(0) for _ in range(P)]
+    ctxs = [al.Context(0, config=cfg) for _ in range(P)]
     lb = LoopbackComms(ctxs[0], P)
     engines = []
     for r in range(P):
@@ -181,16 +179,15 @@ def test_native_driver_multi_rank_loopback(prog, head, P, seed, n, dom, tiny, mo
     lb.close()
 
 
-def test_native_driver_rejects_host_path(monkeypatch):
+def test_native_driver_rejects_host_path():
     """The native driver runs the loop-kernel partition path only; on the
     sort/merge partition path it fails loudly (GD_ERR_UNSUPPORTED) instead
     of falling back."""
     from paper_2311_02206_b200.partition import LoopbackComms, run_partitioned_native
 
-    monkeypatch.setenv("GD_PART_LOOP", "0")
     rng = np.random.default_rng(51)
     edges = random_relation(rng, 2, 500, 300)
-    ctx = al.Context(0)
+    ctx = al.Context(0, config={"partition_loop": 0})
     lb = LoopbackComms(ctx, 1)
     e = al.engine("reach", ctx=ctx)
     e.set_partition(0, 1)

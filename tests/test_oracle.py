@@ -134,3 +134,18 @@ def test_port_engine_matches_reference(port, ref, kind, seed):
         assert np.array_equal(rels[prog.rid(n)], r.relation(n)), n
         if any(p.head == n and p.recursive for p in prog.rules):
             assert hist[prog.rid(n)] == r.delta_history(n)
+
+
+def test_host_digest_twin_matches_reference_hash(ref):
+    """tests/helpers.prefix_hash_np (the host twin behind digest_rows, which
+    pins the device relation digest) equals the reference's slot_key on
+    random rows, arities 1-5."""
+    from tests.helpers import prefix_hash_np
+    rng = np.random.default_rng(5)
+    for arity in range(1, 6):
+        rows = rng.integers(0, 1 << 63, size=(500, arity), dtype=np.uint64) * np.uint64(2)
+        got = prefix_hash_np(rows)
+        exp = ref.prefix_hash(rows, arity, arity)
+        # slot_key remaps the sentinel to sentinel - 1 (hash.hpp:57-60)
+        got = np.where(got == np.uint64((1 << 64) - 1), np.uint64((1 << 64) - 2), got)
+        assert np.array_equal(got, exp), arity

@@ -18,6 +18,7 @@
 #include <map>
 #include <filesystem>
 #include <fstream>
+#include <initializer_list>
 #include <iterator>
 #include <memory>
 #include <optional>
@@ -178,6 +179,22 @@ inline row_range range_lookup(const relation_container& c, std::span<const value
     return range_lookup_batch(c, prefix, ctx).at(0);
 }
 
+inline row_range range_lookup(const relation_container& c, std::initializer_list<value_t> prefix,
+                              context& ctx = context::default_context()) {
+    return range_lookup(c, std::span<const value_t>(prefix.begin(), prefix.size()), ctx);
+}
+
+// group_starts (index_map.hpp:46-66): first row of every distinct prefix
+inline std::vector<std::uint64_t> group_starts(const tuple_array& tuples, std::uint32_t prefix_len,
+                                               unsigned /*workers*/ = 1, context& ctx = context::default_context()) {
+    std::vector<std::uint64_t> out(tuples.count() ? tuples.count() : 1);
+    std::uint64_t m = 0;
+    ctx.check(gd_group_starts(ctx.get(), tuples.data.data(), tuples.count(), tuples.arity, tuples.canonical ? 1 : 0,
+                              prefix_len, out.data(), &m));
+    out.resize(m);
+    return out;
+}
+
 // join_count (ra.hpp:141-182)
 inline std::size_t join_count(const join_spec& spec, unsigned /*workers*/ = 1, std::size_t /*stride*/ = 0,
                               context& ctx = context::default_context()) {
@@ -259,8 +276,16 @@ inline std::string slurp(const std::filesystem::path& path) {
 }
 }  // namespace detail
 
-inline tuple_array read_facts(const std::filesystem::path& path, std::uint32_t arity, unsigned /*workers*/ = 1,
-                              context& ctx = context::default_context()) {
+// The reference's own functions (token files with a dictionary stay on the
+// host, as in the reference); a build that renames the reference entry
+// points (tests/cpp/reftests) redefines this.
+#ifndef ARRAYLOG_B200_REF
+#define ARRAYLOG_B200_REF(name) ::arraylog::name
+#endif
+
+inline tuple_array read_facts(const std::filesystem::path& path, std::uint32_t arity, dictionary* dict = nullptr,
+                              unsigned workers = 1, context& ctx = context::default_context()) {
+    if (dict) return ARRAYLOG_B200_REF(read_facts)(path, arity, dict, workers);
     if (arity == 0) throw load_error("read_facts: arity must be positive");
     const std::string text = detail::slurp(path);
     std::uint64_t cap = 1;
@@ -282,7 +307,9 @@ inline bool file_is_all_integers(const std::filesystem::path& path, context& ctx
     return r != 0;
 }
 
-inline std::string to_tsv(const tuple_array& rel, context& ctx = context::default_context()) {
+inline std::string to_tsv(const tuple_array& rel, const dictionary* dict = nullptr,
+                          context& ctx = context::default_context()) {
+    if (dict) return ARRAYLOG_B200_REF(to_tsv)(rel, dict);
     std::uint64_t len = 0;
     ctx.check(gd_rows_to_tsv(ctx.get(), rel.data.data(), rel.count(), rel.arity, nullptr, 0, &len));
     std::string out(len, '\0');
@@ -291,9 +318,9 @@ inline std::string to_tsv(const tuple_array& rel, context& ctx = context::defaul
 }
 
 inline void write_relation(const tuple_array& rel, const std::filesystem::path& path,
-                           context& ctx = context::default_context()) {
+                           const dictionary* dict = nullptr, context& ctx = context::default_context()) {
     if (!rel.canonical) throw std::logic_error("write_relation: relation must be canonical");
-    const std::string text = to_tsv(rel, ctx);
+    const std::string text = to_tsv(rel, dict, ctx);
     std::ofstream out(path, std::ios::binary);
     if (!out) throw load_error("cannot open '" + path.string() + "' for writing");
     out << text;
@@ -413,6 +440,30 @@ public:
 
     std::vector<std::string> idb_relations() const { return prog_.idb_relations(); }
 
+    // accountant() (engine.hpp:103-105): the device engine's logical-byte
+    // ledger, with memory_accountant's getters (budget.hpp:50-60).
+    class accountant_state {
+    public:
+        std::size_t current(memory_accountant::category cat) const { return cur_[static_cast<std::size_t>(cat)]; }
+        std::size_t current_total() const { return cur_[0] + cur_[1] + cur_[2]; }
+        std::size_t peak_bytes() const { return peak_; }
+        std::size_t peak_temp_bytes() const { return peak_temp_; }
+        std::size_t charge_events() const { return events_; }
+        std::size_t budget() const { return budget_; }
+
+    private:
+        friend class engine;
+        std::uint64_t cur_[3] = {0, 0, 0};
+        std::uint64_t peak_ = 0, peak_temp_ = 0, events_ = 0;
+        std::size_t budget_ = memory_accountant::unlimited;
+    };
+    const accountant_state& accountant() const {
+        std::uint64_t b = 0;
+        ctx_->check(gd_engine_accountant(eng_.get(), acct_.cur_, &acct_.peak_, &acct_.peak_temp_, &acct_.events_, &b));
+        acct_.budget_ = b == UINT64_MAX ? memory_accountant::unlimited : static_cast<std::size_t>(b);
+        return acct_;
+    }
+
     run_stats stats() const {
         gd_run_stats s{};
         ctx_->check(gd_engine_stats(eng_.get(), &s));
@@ -514,6 +565,7 @@ private:
     std::vector<rule_plan> plans_;
     bool seeded_ = false;
     mutable std::map<std::string, tuple_array> cache_;
+    mutable accountant_state acct_;
 };
 
 }  // namespace arraylog::b200

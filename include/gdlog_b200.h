@@ -137,6 +137,9 @@ typedef struct gd_device_config {
     uint64_t download_chunk_rows;   /* staging chunk of packed downloads (1 << 20) */
     uint32_t sort_items;            /* onesweep keys per thread: 4, 8 or 16 (16) */
     uint32_t trace;                 /* stderr traces: bit 0 resident loop, bit 1 downloads (0) */
+    int32_t warp_expand;            /* final steps over a dense inner: count + warp-expanded insert (1) */
+    uint32_t reserved0;
+    uint64_t heavy_rows;            /* ... rows with more outputs are expanded as segments of this many (4096) */
 } gd_device_config;
 
 void gd_device_config_default(gd_device_config* cfg);
@@ -414,6 +417,12 @@ gd_status gd_engine_relation_digest(gd_engine* eng, uint32_t rel,
 
 /* stats() (engine.hpp:270-277). */
 gd_status gd_engine_stats(gd_engine* eng, gd_run_stats* out);
+/* accountant() (engine.hpp:103-105): the state of the engine's logical-byte
+ * ledger (memory_accountant, budget.hpp:16-67) — current bytes per category
+ * {container, temp, buffer}, peak, peak temp, charge events and the budget
+ * (UINT64_MAX = unlimited).  Any pointer may be NULL. */
+gd_status gd_engine_accountant(gd_engine* eng, uint64_t current[3], uint64_t* peak, uint64_t* peak_temp,
+                               uint64_t* events, uint64_t* budget);
 /* run_stats::delta_history entry of one recursive relation. */
 gd_status gd_engine_delta_history(gd_engine* eng, uint32_t rel, uint64_t* out,
                                   uint64_t capacity, uint64_t* len);

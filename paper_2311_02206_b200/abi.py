@@ -70,6 +70,9 @@ class gd_device_config(C.Structure):
         ("download_chunk_rows", u64),
         ("sort_items", u32),
         ("trace", u32),
+        ("warp_expand", C.c_int32),
+        ("reserved0", u32),
+        ("heavy_rows", u64),
     ]
 
 
@@ -235,6 +238,7 @@ SIGNATURES = {
     "gd_engine_relation_download_device": (C.c_int, [P, u32, P, u64]),
     "gd_engine_relation_digest": (C.c_int, [P, u32, PU64]),
     "gd_engine_stats": (C.c_int, [P, C.POINTER(gd_run_stats)]),
+    "gd_engine_accountant": (C.c_int, [P, P, PU64, PU64, PU64, PU64]),
     "gd_engine_delta_history": (C.c_int, [P, u32, P, u64, PU64]),
     "gd_engine_iter_log": (C.c_int, [P, u32, C.POINTER(gd_iter_record), u64, PU64]),
     "gd_engine_encoding": (C.c_int, [P, PU32, PU32, PU32]),

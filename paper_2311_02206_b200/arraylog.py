@@ -212,6 +212,8 @@ _ENV_KNOBS = {
     "GD_DL_DIRECT_FRAC": ("download_direct_frac", float),
     "GD_DL_CHUNK_ROWS": ("download_chunk_rows", int),
     "GD_SORT_ITEMS": ("sort_items", int),
+    "GD_WARP_EXPAND": ("warp_expand", int),
+    "GD_HEAVY_ROWS": ("heavy_rows", int),
 }
 
 

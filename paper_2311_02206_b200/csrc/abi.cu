@@ -276,6 +276,7 @@ gd_status gd_ctx_set_device_config(gd_ctx* ctx, const gd_device_config* cfg) {
         if (cfg->download_chunk_rows < (1u << 16)) throw_config("download_chunk_rows must be at least 65536");
         if (cfg->sort_items != 4 && cfg->sort_items != 8 && cfg->sort_items != 16)
             throw_config("sort_items must be 4, 8 or 16");
+        if (cfg->heavy_rows == 0) throw_config("heavy_rows must be positive");
         ctx->c->cfg = *cfg;
     });
 }
@@ -654,6 +655,18 @@ gd_status gd_engine_relation_digest(gd_engine* eng, uint32_t rel, uint64_t* dige
     ENG_GUARD(*digest = eng->e->relation_digest(rel));
 }
 gd_status gd_engine_stats(gd_engine* eng, gd_run_stats* out) { ENG_GUARD(eng->e->fill_stats(out)); }
+gd_status gd_engine_accountant(gd_engine* eng, uint64_t current[3], uint64_t* peak, uint64_t* peak_temp,
+                               uint64_t* events, uint64_t* budget) {
+    ENG_GUARD({
+        const Accountant& a = eng->e->acct;
+        if (current)
+            for (int k = 0; k < 3; ++k) current[k] = a.current(static_cast<Accountant::Cat>(k));
+        if (peak) *peak = a.peak();
+        if (peak_temp) *peak_temp = a.peak_temp();
+        if (events) *events = a.events();
+        if (budget) *budget = a.budget();
+    });
+}
 gd_status gd_engine_delta_history(gd_engine* eng, uint32_t rel, uint64_t* out, uint64_t capacity, uint64_t* len) {
     ENG_GUARD({
         const auto& h = eng->e->rel(rel).history;

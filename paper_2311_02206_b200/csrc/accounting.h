@@ -48,6 +48,7 @@ public:
     uint64_t peak() const { return peak_; }
     uint64_t peak_temp() const { return peak_temp_; }
     uint64_t events() const { return events_; }
+    uint64_t budget() const { return budget_; }
 
 private:
     uint64_t budget_;

@@ -132,6 +132,9 @@ inline gd_device_config default_device_config() {
     d.download_chunk_rows = 1u << 20;
     d.sort_items = 16;
     d.trace = 0;
+    d.warp_expand = 1;
+    d.reserved0 = 0;
+    d.heavy_rows = 4096;
     return d;
 }
 

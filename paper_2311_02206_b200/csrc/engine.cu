@@ -18,6 +18,7 @@
 #include <cstring>
 #include <set>
 #include <atomic>
+#include <functional>
 #include <thread>
 #include <type_traits>
 #if defined(__x86_64__)
@@ -309,6 +310,31 @@ public:
         DevBuf<u64> direct;
         cudaStream_t s2 = nullptr;
         cudaEvent_t ev_un = nullptr;
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        std::vector<std::thread> pool;
+        std::atomic<bool> quit{false};
+        // Runs on every exit, a throw included (GD_CUDA inside the chunk
+        // loop): stop and join the unpack threads, drain both streams so no
+        // DMA still reads `direct` or writes the staging area, then release
+        // the events and the side stream; `direct` (declared earlier) is
+        // freed after this.
+        struct Cleanup {
+            std::function<void()> f;
+            ~Cleanup() { f(); }
+        } cleanup{[&] {
+            quit.store(true, std::memory_order_release);
+            for (auto& th : pool)
+                if (th.joinable()) th.join();
+            if (s2) {
+                cudaStreamSynchronize(s2);
+                cudaStreamDestroy(s2);
+            }
+            cudaStreamSynchronize(c.stream);
+            if (ev_un) cudaEventDestroy(ev_un);
+            for (auto e : ev)
+                if (e) cudaEventDestroy(e);
+            cudaGetLastError();
+        }};
         {
             const double frac = c.cfg.download_direct_frac;
             cudaPointerAttributes pa{};
@@ -332,7 +358,6 @@ public:
         void* area = c.pinned_staging(2 * kChunk * sizeof(u64));
         stage[0] = static_cast<u64*>(area);
         stage[1] = stage[0] + kChunk;
-        cudaEvent_t ev[2];
         GD_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
         GD_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
         const u32 bits = E.enc.e.bits;
@@ -351,7 +376,6 @@ public:
         // out by a generation counter once its copy has landed
         std::atomic<u64> gen{0};
         std::atomic<unsigned> left{0};
-        std::atomic<bool> quit{false};
         const u64* cur_src = nullptr;
         u64* cur_dst = nullptr;
         u64 cur_m = 0;
@@ -398,7 +422,6 @@ public:
                 }
             }
         };
-        std::vector<std::thread> pool;
         for (unsigned t = 1; t < nt; ++t)
             pool.emplace_back([&, t] {
                 u64 seen = 0;
@@ -431,13 +454,12 @@ public:
         }
         quit.store(true, std::memory_order_release);
         for (auto& th : pool) th.join();
+        pool.clear();
         double t_direct = 0;
         if (s2) {
             const double td = Ctx::now_s();
             GD_CUDA(cudaStreamSynchronize(s2));
             t_direct = Ctx::now_s() - td;
-            cudaStreamDestroy(s2);
-            cudaEventDestroy(ev_un);
         }
         if (trace)
             fprintf(stderr,
@@ -445,8 +467,6 @@ public:
                     "direct tail %.1f ms\n",
                     (unsigned long long)n_all, (unsigned long long)(n_all - n), nt, t_wait * 1e3, t_unpack * 1e3,
                     t_direct * 1e3);
-        cudaEventDestroy(ev[0]);
-        cudaEventDestroy(ev[1]);
     }
 
     u64 digest(u32 r) override {
@@ -570,6 +590,9 @@ public:
         // GD_LOOP_SPLIT=1: materialize the final step's rows, then insert
         // them (comparison mode; the fused kernel moves fewer bytes)
         bool split_insert = false;
+        // final step over a dense inner: loop_count + loop_expand_insert
+        // (gd_device_config.warp_expand)
+        bool xp = false;
         u32 head = 0;            // loop-head index (final steps)
         u32 kind = LO_STATIC;    // outer source
         u32 src_head = 0, src_step = 0;
@@ -673,6 +696,7 @@ public:
                         loop_dense_build(c, L.inner, L.inner_n, iar, bits, L.dense, L.dv.lo, L.dv.span))
                         L.dv.off = L.dense.p;
                 }
+                L.xp = L.final && !L.split_insert && L.dv.off && c.cfg.warp_expand;
                 cur_ar = st.proj_arity;
                 for (u32 i = 0; i < kMaxArity; ++i) cur_perm[i] = i;
             }
@@ -774,7 +798,7 @@ public:
         // after the iteration, once its sizes are known (eager mode only)
         struct ProfRec {
             long rec;
-            int kind;  // 0 probe, 1 temp, 2 insert, 3 select insert
+            int kind;  // 0 probe, 1 temp, 2 insert, 3 select insert, 4 count (warp expansion)
             u32 step;
         };
         std::vector<ProfRec> prof_recs;
@@ -804,6 +828,12 @@ public:
                     continue;
                 }
                 cudaEvent_t t = br();
+                if (L.xp) {
+                    loop_count(c, s, ctl.p, i, o, L.jd, L.dv, L.bufs(), c.cfg.heavy_rows,
+                               fuse_gate && i + 1 == ns ? &g : nullptr);
+                    prof_recs.push_back({c.prof_end(t, KC_PROBE, 0), 4, i});
+                    continue;
+                }
                 loop_probe(c, s, ctl.p, i, o, L.jd, L.has_iv ? &L.iv : nullptr, L.dv, L.inner_n, L.bufs(),
                            block_sums.p);
                 prof_recs.push_back({c.prof_end(t, KC_PROBE, 0), 0, i});
@@ -833,6 +863,9 @@ public:
                 cudaEvent_t t = br();
                 if (L.select)
                     loop_select_insert(c, s, ctl.p, i, L.head, o, L.jd, bufs_of(L.head), e);
+                else if (L.xp)
+                    loop_expand_insert(c, s, ctl.p, i, L.head, o, L.inner, L.jd, L.dv, L.bufs(), c.cfg.heavy_rows,
+                                       bufs_of(L.head), e);
                 else if (L.split_insert)
                     loop_insert_keys(c, s, ctl.p, i, L.head, L.temp.p, bufs_of(L.head), e);
                 else
@@ -937,10 +970,11 @@ public:
                         const LStep& L = steps[pr.step];
                         u64 by = 0;
                         if (pr.kind == 0) by = hc->step_n[pr.step] * (8 + (L.has_iv ? sizeof(Slot) : 0));
-                        else if (pr.kind == 1) by = hc->step_cand[pr.step] * 16;
+                        else if (pr.kind == 4) by = hc->step_n[pr.step] * 16;  // outer key + dense offsets
+                        else if (pr.kind == 1) by = hc->last_cand[pr.step] * 16;
                         else {
                             // one key read (kind 2: materialized row; 3: outer row) + one slot
-                            by = hc->step_cand[pr.step] * 16;
+                            by = hc->last_cand[pr.step] * 16;
                             if (!charged[L.head]) {
                                 charged[L.head] = true;
                                 by += (hc->h[L.head].log_n - prev_log_n[L.head]) * 8;

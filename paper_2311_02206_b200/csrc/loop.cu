@@ -267,7 +267,7 @@ __device__ void end_body(LoopCtl* ctl, const LoopEndDesc& e) {
     }
     if (overflow) {  // roll back: nothing was inserted (gate)
         for (u32 h = 0; h < nh; ++h) ctl->h[h].cand = ctl->h[h].J = ctl->h[h].N = ctl->h[h].D = 0;
-        for (u32 s = 0; s < ns; ++s) ctl->step_total[s] = 0;
+        for (u32 s = 0; s < ns; ++s) ctl->step_total[s] = ctl->step_cand[s] = ctl->heavy_n[s] = 0;
         if (e.use_cond) cudaGraphSetConditional(cond, 0);
         return;
     }
@@ -291,7 +291,8 @@ __device__ void end_body(LoopCtl* ctl, const LoopEndDesc& e) {
     }
     for (u32 s = 0; s < ns; ++s) {
         e.hist.steps[i * ns + s] = __ldcg(&ctl->step_total[s]);
-        ctl->step_total[s] = 0;
+        ctl->last_cand[s] = __ldcg(&ctl->step_cand[s]);
+        ctl->step_total[s] = ctl->step_cand[s] = ctl->heavy_n[s] = 0;
     }
     ctl->iter = iter + 1;
     ctl->done = active ? 0 : 1;
@@ -749,6 +750,217 @@ __global__ void __launch_bounds__(kLT) loop_select_insert_kernel(LoopCtl* ctl, u
     if (do_end && last_cta(ctl, &s_flag) && threadIdx.x == 0) end_body(ctl, e);
 }
 
+// ---- warp-expanded final step over a dense inner ---------------------------
+// (DESIGN.md §4b.)  loop_count reads each outer row's range from the
+// L2-resident dense offsets, sums the candidates (one atomic per CTA) and
+// queues rows with more than heavy_rows outputs as (row, segment) items;
+// its last CTA runs the gate.  loop_expand_insert: every warp takes 32
+// outer rows at a time (grid-stride), scans their counts with shuffles and
+// expands the outputs — source row found by a 5-step shuffle search,
+// filters applied, survivors compacted by ballot — into its own shared
+// buffer; each full round of 256 keys is inserted with 8 keys per lane
+// (home slots loaded together, hs_insert) and appended with one atomic per
+// warp.  Then the heavy items, one warp each.  No CTA barrier in the loops,
+// no per-row arrays, no merge-path splits.
+constexpr int kXBuf = 512;    // keys per warp buffer (4 KB)
+constexpr int kXRound = 256;  // keys per insert round (8 per lane)
+constexpr int kXPer = kXRound / 32;
+
+__device__ __forceinline__ void dense_range(const LoopDense& dv, u64 p, u64& a, u64& c) {
+    const u64 q = p - dv.lo;
+    if (q < dv.span) {
+        const u32 x = __ldg(dv.off + q), y = __ldg(dv.off + q + 1);
+        a = x;
+        c = y - x;
+    } else {
+        a = c = 0;
+    }
+}
+
+__global__ void __launch_bounds__(kLT) loop_count_kernel(LoopCtl* ctl, u32 step, LoopOuter o, DevJoin jd,
+                                                         LoopDense dv, LoopStepBufs sb, u64 heavy_min,
+                                                         LoopGateDesc g, int do_gate) {
+    __shared__ u64 red[kLT / 32];
+    __shared__ u32 s_flag;
+    if (!cta_stopped(ctl, &s_flag)) {
+        const u64* outer;
+        u64 n;
+        resolve(o, ctl, outer, n);
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->step_n[step] = n;
+        u64 sum = 0;
+        for (u64 base = (u64)blockIdx.x * kLTile; base < n; base += (u64)gridDim.x * kLTile) {
+            u64 pre[kLItems];
+#pragma unroll
+            for (int j = 0; j < kLItems; ++j) {
+                const u64 r = base + threadIdx.x + (u64)j * kLT;
+                pre[j] = r < n ? outer_prefix(jd, outer[r]) : 0ull;
+            }
+            u64 a[kLItems], c[kLItems];
+#pragma unroll
+            for (int j = 0; j < kLItems; ++j) dense_range(dv, pre[j], a[j], c[j]);
+#pragma unroll
+            for (int j = 0; j < kLItems; ++j) {
+                const u64 r = base + threadIdx.x + (u64)j * kLT;
+                if (r >= n) continue;
+                sum += c[j];
+                if (c[j] > heavy_min) {
+                    const u64 segs = (c[j] + heavy_min - 1) / heavy_min;
+                    const u64 pos = atomicAdd((unsigned long long*)&ctl->heavy_n[step], (unsigned long long)segs);
+                    if (pos + segs <= sb.rows_cap) {
+                        for (u64 q = 0; q < segs; ++q) {
+                            sb.row_start[pos + q] = r;
+                            sb.row_off[pos + q] = q;
+                        }
+                    } else {
+                        atomicMax((unsigned long long*)&ctl->need_rows[step], (unsigned long long)(pos + segs));
+                        ctl->overflow = 1;
+                    }
+                }
+            }
+        }
+        sum = block_sum(sum, red);
+        if (threadIdx.x == 0 && sum) atomicAdd((unsigned long long*)&ctl->step_cand[step], (unsigned long long)sum);
+    }
+    if (do_gate && last_cta(ctl, &s_flag) && threadIdx.x == 0) gate_body(ctl, g);
+}
+
+struct XWarp {
+    u64* buf;  // this warp's shared buffer
+    u32 fill;  // keys in buf (warp-uniform)
+    u64 J, N, D;
+};
+
+// Inserts buf[0, m) (m <= kXRound) into the head's index and appends the
+// new keys to the log.
+__device__ __forceinline__ void x_round(XWarp& w, u32 m, const LoopHeadBufs& hb, u32 it,
+                                        unsigned long long* log_n) {
+    __syncwarp();
+    const u32 lane = lane_id();
+    u64 key[kXPer];
+    u32 ok = 0;
+#pragma unroll
+    for (int k = 0; k < kXPer; ++k) {
+        const u32 idx = lane + 32u * k;
+        key[k] = idx < m ? w.buf[idx] : 0ull;
+        ok |= (u32)(idx < m) << k;
+    }
+    u32 fresh, first;
+    hs_insert<kXPer>(hb, it, key, ok, fresh, first);
+    w.N += __popc(first);
+    w.D += __popc(fresh);
+    u32 mk[kXPer];
+    u32 tot = 0;
+#pragma unroll
+    for (int k = 0; k < kXPer; ++k) {
+        mk[k] = __ballot_sync(0xffffffffu, fresh >> k & 1);
+        tot += __popc(mk[k]);
+    }
+    unsigned long long base = 0;
+    if (lane == 0 && tot) base = atomicAdd(log_n, (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const u32 lt = lanemask_lt();
+#pragma unroll
+    for (int k = 0; k < kXPer; ++k) {
+        if (fresh >> k & 1) hb.log[base + __popc(mk[k] & lt)] = key[k];
+        base += __popc(mk[k]);
+    }
+    __syncwarp();
+}
+
+// Adds one key per lane (`have`) to the warp buffer, compacted; a full
+// round is inserted at once and the (< 32) keys past it move to the front.
+__device__ __forceinline__ void x_emit(XWarp& w, bool have, u64 key, const LoopHeadBufs& hb, u32 it,
+                                       unsigned long long* log_n) {
+    const u32 mask = __ballot_sync(0xffffffffu, have);
+    if (have) w.buf[w.fill + __popc(mask & lanemask_lt())] = key;
+    w.fill += __popc(mask);
+    if (w.fill >= (u32)kXRound) {
+        x_round(w, kXRound, hb, it, log_n);
+        const u32 rest = w.fill - kXRound;
+        const u32 lane = lane_id();
+        const u64 t = lane < rest ? w.buf[kXRound + lane] : 0ull;
+        __syncwarp();
+        if (lane < rest) w.buf[lane] = t;
+        w.fill = rest;
+    }
+}
+
+__global__ void __launch_bounds__(kLT, 3) loop_expand_insert_kernel(
+    LoopCtl* ctl, u32 step, u32 head, LoopOuter o, const u64* __restrict__ inner, DevJoin jd, LoopDense dv,
+    LoopStepBufs sb, u64 heavy_min, LoopHeadBufs hb, LoopEndDesc e, int do_end) {
+    __shared__ u64 sbuf[kLT / 32][kXBuf];
+    __shared__ u64 red[kLT / 32];
+    __shared__ u32 s_flag;
+    if (!cta_stopped(ctl, &s_flag)) {
+        const u64* outer;
+        u64 n;
+        resolve(o, ctl, outer, n);
+        const u32 it = ctl->iter + 1 - ctl->epoch_base;
+        const u64 nheavy = min(__ldcg(&ctl->heavy_n[step]), sb.rows_cap);
+        unsigned long long* log_n = reinterpret_cast<unsigned long long*>(&ctl->h[head].log_n);
+        const u32 lane = lane_id(), warp = threadIdx.x >> 5;
+        XWarp w{sbuf[warp], 0, 0, 0, 0};
+        const u64 gw = (u64)blockIdx.x * (kLT / 32) + warp, nw = (u64)gridDim.x * (kLT / 32);
+        for (u64 base = gw * 32; base < n; base += nw * 32) {
+            const u64 r = base + lane;
+            u64 ov = 0, a = 0, c = 0;
+            if (r < n) {
+                ov = outer[r];
+                dense_range(dv, outer_prefix(jd, ov), a, c);
+                if (c > heavy_min) c = 0;  // a heavy item (loop_count queued it)
+            }
+            const u64 incl = warp_inclusive_scan(c);
+            const u64 T = __shfl_sync(0xffffffffu, incl, 31);
+            const u64 excl = incl - c;
+            for (u64 j0 = 0; j0 < T; j0 += 32) {
+                const u64 j = j0 + lane;
+                // source lane: the last s with excl_s <= j (rows without
+                // output share the next row's excl and are never last)
+                u32 s = 0;
+#pragma unroll
+                for (u32 d = 16; d; d >>= 1) {
+                    const u64 ex = __shfl_sync(0xffffffffu, excl, s + d);
+                    if (ex <= j) s += d;
+                }
+                const u64 sa = __shfl_sync(0xffffffffu, a, s);
+                const u64 se = __shfl_sync(0xffffffffu, excl, s);
+                const u64 so = __shfl_sync(0xffffffffu, ov, s);
+                bool have = false;
+                u64 key = 0;
+                if (j < T) {
+                    const u64 iv = inner[sa + (j - se)];
+                    have = passes(jd, so, iv);
+                    key = project(jd, so, iv);
+                }
+                w.J += have;
+                x_emit(w, have, key, hb, it, log_n);
+            }
+        }
+        for (u64 i = gw; i < nheavy; i += nw) {  // heavy items: one segment of heavy_min outputs per warp
+            const u64 r = sb.row_start[i], sg = sb.row_off[i];
+            const u64 ov = outer[r];
+            u64 a, c;
+            dense_range(dv, outer_prefix(jd, ov), a, c);
+            const u64 b0 = sg * heavy_min, b1 = min(c, b0 + heavy_min);
+            for (u64 j0 = b0; j0 < b1; j0 += 32) {
+                const u64 j = j0 + lane;
+                bool have = false;
+                u64 key = 0;
+                if (j < b1) {
+                    const u64 iv = inner[a + j];
+                    have = passes(jd, ov, iv);
+                    key = project(jd, ov, iv);
+                }
+                w.J += have;
+                x_emit(w, have, key, hb, it, log_n);
+            }
+        }
+        if (w.fill) x_round(w, w.fill, hb, it, log_n);
+        flush_counts(ctl, head, step, w.J, w.N, w.D, red);
+    }
+    if (do_end && last_cta(ctl, &s_flag) && threadIdx.x == 0) end_body(ctl, e);
+}
+
 // Rebuild of a table from the log (keys unique): stamp 0 = "before the
 // current epoch".
 __global__ void table_fill_kernel(void* tab, u64 cap, u32 sb, const u64* __restrict__ keys, u64 n) {
@@ -1012,7 +1224,7 @@ int occupancy(Kern k, size_t smem = 0) {
     return b > 0 ? b : 1;
 }
 
-int g_occ_temp = 0, g_occ_insert = 0, g_occ_select = 0, g_occ_keys = 0;
+int g_occ_temp = 0, g_occ_insert = 0, g_occ_select = 0, g_occ_keys = 0, g_occ_expand = 0;
 // Insert grid = waves x resident CTAs: CTAs beyond the resident set start as
 // others finish, so the hardware balances the iteration's tiles.  Large
 // relations (log capacity >= kWideLog rows) run 3 waves (C2 -2.8%, SG
@@ -1030,6 +1242,7 @@ void loop_prepare() {
     g_occ_insert = occupancy(loop_materialize_insert_kernel);
     g_occ_keys = occupancy(loop_insert_keys_kernel);
     g_occ_select = occupancy(loop_select_insert_kernel);
+    g_occ_expand = occupancy(loop_expand_insert_kernel);
 }
 
 void loop_fill_u64(Ctx& c, u64* p, u64 n, u64 v) {
@@ -1231,6 +1444,25 @@ void loop_part_advance(Ctx& c, LoopCtl* ctl, u32 final_step, u64 recv_rows, gd_i
 void loop_owner_scatter(Ctx& c, const u64* keys, const u64* n_ptr, u32 P, const unsigned long long* offsets,
                         unsigned long long* cursors, u64* out) {
     owner_scatter_kernel<<<c.num_sms * 4, 256, 0, c.stream>>>(keys, n_ptr, P, offsets, cursors, out);
+    c.check_launch();
+}
+
+void loop_count(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const DevJoin& jd,
+                const LoopDense& dense, const LoopStepBufs& sb, u64 heavy_rows, const LoopGateDesc* gate) {
+    LoopGateDesc g{};
+    if (gate) g = *gate;
+    loop_count_kernel<<<loop_grid(c), kLT, 0, s>>>(ctl, step, o, jd, dense, sb, heavy_rows, g, gate ? 1 : 0);
+    c.check_launch();
+}
+
+void loop_expand_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
+                        const u64* inner, const DevJoin& jd, const LoopDense& dense, const LoopStepBufs& sb,
+                        u64 heavy_rows, const LoopHeadBufs& hb, const LoopEndDesc* end) {
+    LoopEndDesc e{};
+    if (end) e = *end;
+    const int waves = c.cfg.insert_waves ? (int)c.cfg.insert_waves : 1;
+    loop_expand_insert_kernel<<<c.num_sms * g_occ_expand * waves, kLT, 0, s>>>(
+        ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0);
     c.check_launch();
 }
 

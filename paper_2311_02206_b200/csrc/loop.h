@@ -83,6 +83,8 @@ struct LoopCtl {
     u64 need_log[kLoopMaxHeads];
     u64 need_tab[kLoopMaxHeads];
     u64 need_hist;
+    u64 heavy_n[kLoopMaxSteps];    // (row, segment) items queued by loop_count
+    u64 last_cand[kLoopMaxSteps];  // step_cand of the last completed iteration (profiler)
 };
 
 // Per-iteration history written by loop_end: rec[i * nheads + h] and the
@@ -206,6 +208,19 @@ void loop_part_advance(Ctx& c, LoopCtl* ctl, u32 final_step, u64 recv_rows, gd_i
 // counts; cursors zeroed).  Order inside a group is unspecified.
 void loop_owner_scatter(Ctx& c, const u64* keys, const u64* n_ptr, u32 P, const unsigned long long* offsets,
                         unsigned long long* cursors, u64* out);
+
+// ---- warp-expanded final step over a dense inner ----
+// loop_count: one read of the dense offsets per outer row, the candidate
+// sum, rows with more than heavy_rows outputs queued as (row, segment)
+// items in sb.row_start / sb.row_off; the gate in its last CTA when `gate`.
+void loop_count(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const DevJoin& jd,
+                const LoopDense& dense, const LoopStepBufs& sb, u64 heavy_rows, const LoopGateDesc* gate);
+// Expansion fused with dedup + difference + append: every warp expands 32
+// outer rows at a time into a shared buffer and inserts 256 keys at a
+// time, then the heavy items; loop_end in the last CTA when `end`.
+void loop_expand_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
+                        const u64* inner, const DevJoin& jd, const LoopDense& dense, const LoopStepBufs& sb,
+                        u64 heavy_rows, const LoopHeadBufs& hb, const LoopEndDesc* end);
 
 // Records the iteration (or rolls it back on overflow) and sets the graph's
 // while-condition (cond ignored unless use_cond).

@@ -260,9 +260,10 @@ K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
     const u64 max_tiles = (std::min(n, kPortion) + TILE - 1) / TILE;
     const u64 ws_words = 1 + max_tiles * kRadix;
     // One look-back workspace per pass, cleared by a single memset, when
-    // the keys fit one portion (the common case); larger sorts reuse one
-    // workspace and clear it before every launch.
-    const bool single = nportions == 1;
+    // the keys fit one portion and all passes' workspaces stay small
+    // (<= 16 MB); otherwise one workspace is reused and cleared before every
+    // launch (bounded memory next to a large sort).
+    const bool single = nportions == 1 && ws_words * (u64)npass * sizeof(u32) <= (16ull << 20);
     DevBuf<u32> ws(c, single ? ws_words * npass : ws_words);
     if (single) c.memset(ws.p, 0, ws_words * npass * sizeof(u32));
     K* src = a;

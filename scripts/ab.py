@@ -1,6 +1,5 @@
-"""A/B of loop options on C2 (same box, config after config, best of N after the first):
-python scripts/ab.py 'A=' 'B=GD_LOOP_DIRECT=0' [reps]"""
-import os
+"""A/B of gd_device_config options on C2 (same box, config after config,
+best of N after the first):  python scripts/ab.py 'A=' 'B=split_insert:1,insert_waves:2' [reps]"""
 import sys
 import time
 from pathlib import Path
@@ -24,22 +23,17 @@ ctx = al.Context(0, torch.cuda.current_stream().cuda_stream)
 best = {k: 1e9 for k in configs}
 for name, env in configs.items():  # config-major: alternating configs thrash the allocator
     for rep in range(reps):
-        saved = {k: os.environ.get(k) for k in env}
-        os.environ.update(env)
-        e = al.engine("reach", ctx=ctx)
-        e.load_edb_device("Edge", d.data_ptr(), len(edges))
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        e.run()
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t
-        n = e.relation_count("Reach")
-        e.close()
-        for k, v in saved.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+        cfg = {k: (float(v) if "." in v else int(v)) for k, v in env.items()}
+        with ctx.configured(**cfg):
+            e = al.engine("reach", ctx=ctx)
+            e.load_edb_device("Edge", d.data_ptr(), len(edges))
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            e.run()
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t
+            n = e.relation_count("Reach")
+            e.close()
         if rep > 0:
             best[name] = min(best[name], dt)
         print(f"rep {rep} {name:10s} {dt*1e3:8.1f} ms |Reach| {n}", flush=True)

@@ -1,7 +1,10 @@
 // Random-access microbenchmark (B200): 8-byte gathers and CASes at random
 // positions of tables from 128 MB to 32 GB, and CASes restricted to a
 // window (locality), to size the hash-membership design.
+// argv[1] = L2 fetch granularity limit in bytes (cudaLimitMaxL2FetchGranularity;
+// 0 = leave the default), argv[2] = table size cap in MB.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 typedef unsigned long long u64;
 __device__ __forceinline__ u64 mix(u64 k) { k ^= k >> 33; k *= 0xff51afd7ed558ccdULL; k ^= k >> 33; k *= 0xc4ceb9fe1a85ec53ULL; k ^= k >> 33; return k; }
@@ -33,13 +36,20 @@ __global__ void kern(u64* t, u64 n, u64 ops, u64 win, u64* sink) {
   }
   if (acc == 42) *sink = acc;
 }
-int main() {
-  size_t maxb = 32ull << 30;
+int main(int argc, char** argv) {
+  const int gran = argc > 1 ? atoi(argv[1]) : 0;
+  if (gran) {
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
+    size_t g = 0;
+    cudaDeviceGetLimit(&g, cudaLimitMaxL2FetchGranularity);
+    printf("L2 fetch granularity limit: %zu\n", g);
+  }
+  size_t maxb = argc > 2 ? (size_t)atoll(argv[2]) << 20 : 32ull << 30;
   u64* t; cudaMalloc(&t, maxb); u64* sink; cudaMalloc(&sink, 8);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   u64 ops = 1ull << 28;
-  for (size_t bytes = 128ull << 20; bytes <= maxb; bytes *= 4) {
+  for (size_t bytes = argc > 2 ? maxb : 128ull << 20; bytes <= maxb; bytes *= 4) {
     u64 n = bytes / 8;
     for (int mode = 0; mode < 3; ++mode) {
       for (u64 win : {0ull, 1ull << 20}) {  // win = 8 MB windows

@@ -24,6 +24,13 @@ MODES = {  # gd_device_config fields of each mode
     "split": {"split_insert": 1},
     "tiny_split": {"min_capacities": 1, "split_insert": 1},
     "tiny_casrehash": {"min_capacities": 1, "rehash_cas_only": 1},
+    # final steps over a dense inner: probe/scan/merge-path fused insert
+    # instead of count + warp-expanded insert
+    "noxp": {"warp_expand": 0},
+    # warp expansion with rows of more than 3 outputs queued as (row,
+    # segment) items of 3 outputs (the heavy-row path on small inputs)
+    "heavy": {"heavy_rows": 3},
+    "tiny_heavy": {"min_capacities": 1, "heavy_rows": 2},
 }
 
 
@@ -57,14 +64,14 @@ def test_c1_all_modes(ref, mode):
     assert g.raw_stats().join_tuples == 190496  # SURVEY §6 probe: ΣJ over 46 iterations
 
 
-@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "hashindex", "split"])
+@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "hashindex", "split", "noxp", "heavy", "tiny_heavy"])
 @pytest.mark.parametrize("idx", [0, 17, 55])
 def test_sg_corpus_modes(ref, mode, idx):
     g, _ = corpus(ref, 1, idx)
     assert_same(run_mode(mode, "sg", {"Edge": g}), run_ref(ref, "sg", {"Edge": g}), ["SG"])
 
 
-@pytest.mark.parametrize("mode", ["graph", "tiny", "tiny_split"])
+@pytest.mark.parametrize("mode", ["graph", "tiny", "tiny_split", "heavy"])
 @pytest.mark.parametrize("case", sorted(CUSTOM))
 def test_custom_programs_modes(ref, mode, case):
     src, db = CUSTOM[case]
@@ -87,7 +94,7 @@ def test_modes_agree_on_power_law(ref):
     from paper_2311_02206_b200 import workloads as W
     e = W.tc_pl(20000, 20000, 100, 1.05, 3)
     outs = {m: run_mode(m, "reach", {"Edge": e}) for m in ("graph", "host", "tiny", "hashindex", "tiny_casrehash",
-                                                            "eager")}
+                                                            "eager", "noxp", "heavy", "tiny_heavy")}
     base = outs["host"]
     for m, g in outs.items():
         assert np.array_equal(g.relation("Reach").data, base.relation("Reach").data), m
@@ -128,7 +135,7 @@ def test_hash_predup_matches_sort_path():
                                                                         hs.join_tuples)
 
 
-@pytest.mark.parametrize("mode", ["graph", "tiny", "eager"])
+@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "noxp", "heavy", "tiny_heavy"])
 def test_hub_rows(ref, mode):
     """Hubs (in-degree 700, out-degree 300) give Δ rows with long match
     ranges next to short ones: the load-balanced expansion must match the

@@ -114,6 +114,12 @@ typedef enum gd_loop_mode {
     GD_LOOP_BATCH = 2  /* a graph of one iteration launched loop_batch times per host check */
 } gd_loop_mode;
 
+typedef enum gd_partition_exchange {
+    GD_EXCHANGE_PEER = 0, /* rows stored straight into the owners' inboxes over peer memory (CUDA IPC
+                             mappings), device-side barriers: the partitioned fixpoint is one CUDA graph */
+    GD_EXCHANGE_NCCL = 1  /* NCCL send/recv all-to-all-v, one host round trip per iteration */
+} gd_partition_exchange;
+
 typedef struct gd_device_config {
     uint32_t size;                  /* sizeof(gd_device_config) (version check) */
     int32_t resident_loop;          /* 1: resident device loop when eligible; 0: host-driven loop */
@@ -138,8 +144,11 @@ typedef struct gd_device_config {
     uint32_t sort_items;            /* onesweep keys per thread: 4, 8 or 16 (16) */
     uint32_t trace;                 /* stderr traces: bit 0 resident loop, bit 1 downloads (0) */
     int32_t warp_expand;            /* final steps over a dense inner: count + warp-expanded insert (1) */
-    uint32_t reserved0;
+    uint32_t sort_digit_bits;       /* pipelined sort: widest digit, 8..10 (10) */
     uint64_t heavy_rows;            /* ... rows with more outputs are expanded as segments of this many (4096) */
+    int32_t sort_pipeline;          /* u64 sorts: pipelined onesweep (bulk-copy prefetch, wide digits) (1) */
+    uint32_t partition_exchange;    /* gd_engine_run_partitioned: gd_partition_exchange (GD_EXCHANGE_PEER) */
+    uint64_t sort_pipeline_min_keys; /* ... for sorts of at least this many keys (1 << 20) */
 } gd_device_config;
 
 void gd_device_config_default(gd_device_config* cfg);
@@ -221,6 +230,13 @@ gd_status gd_prefix_hash(gd_ctx* ctx, const uint64_t* rows, uint64_t n,
  * n*arity values; *out_n receives the distinct row count. */
 gd_status gd_canonicalize(gd_ctx* ctx, const uint64_t* rows, uint64_t n,
                           uint32_t arity, uint64_t* out, uint64_t* out_n);
+
+/* The sort inside canonicalize (tuple_array.hpp:73-133) on DEVICE keys:
+ * LSD radix sort of n packed u64 keys on their low nbits bits (stable),
+ * d_tmp of n keys as scratch; *in_tmp = 1 when the sorted keys ended in
+ * d_tmp, 0 when in d_keys.  Stream-ordered on the context stream. */
+gd_status gd_sort_keys_device(gd_ctx* ctx, uint64_t* d_keys, uint64_t* d_tmp, uint64_t n,
+                              uint32_t nbits, int* in_tmp);
 
 /* permute_columns (ra.hpp:426-454). rel must be canonical. */
 gd_status gd_permute_columns(gd_ctx* ctx, const uint64_t* rows, uint64_t n,

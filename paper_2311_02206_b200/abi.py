@@ -42,6 +42,7 @@ u64 = C.c_uint64
 
 
 GD_LOOP_GRAPH = 0
+GD_EXCHANGE_PEER, GD_EXCHANGE_NCCL = 0, 1
 GD_LOOP_EAGER = 1
 GD_LOOP_BATCH = 2
 
@@ -71,8 +72,11 @@ class gd_device_config(C.Structure):
         ("sort_items", u32),
         ("trace", u32),
         ("warp_expand", C.c_int32),
-        ("reserved0", u32),
+        ("sort_digit_bits", u32),
         ("heavy_rows", u64),
+        ("sort_pipeline", C.c_int32),
+        ("partition_exchange", u32),
+        ("sort_pipeline_min_keys", u64),
     ]
 
 
@@ -208,6 +212,7 @@ SIGNATURES = {
     "gd_ctx_get_device_config": (C.c_int, [P, C.POINTER(gd_device_config)]),
     "gd_prefix_hash": (C.c_int, [P, P, u64, u32, u32, P]),
     "gd_canonicalize": (C.c_int, [P, P, u64, u32, P, PU64]),
+    "gd_sort_keys_device": (C.c_int, [P, P, P, u64, u32, C.POINTER(C.c_int)]),
     "gd_permute_columns": (C.c_int, [P, P, u64, u32, C.c_int, P, u32, P, PU64]),
     "gd_group_starts": (C.c_int, [P, P, u64, u32, C.c_int, u32, P, PU64]),
     "gd_index_lookup": (C.c_int, [P, P, u64, u32, C.c_int, u32, C.c_double, P, u64, u32, P, P, PU64, PU64]),

@@ -214,6 +214,10 @@ _ENV_KNOBS = {
     "GD_SORT_ITEMS": ("sort_items", int),
     "GD_WARP_EXPAND": ("warp_expand", int),
     "GD_HEAVY_ROWS": ("heavy_rows", int),
+    "GD_SORT_DIGIT_BITS": ("sort_digit_bits", int),
+    "GD_SORT_PIPE": ("sort_pipeline", int),
+    "GD_SORT_PIPE_MIN": ("sort_pipeline_min_keys", int),
+    "GD_PART_EXCHANGE": ("partition_exchange", lambda v: {"peer": 0, "nccl": 1}[v]),
 }
 
 

@@ -277,6 +277,8 @@ gd_status gd_ctx_set_device_config(gd_ctx* ctx, const gd_device_config* cfg) {
         if (cfg->sort_items != 4 && cfg->sort_items != 8 && cfg->sort_items != 16)
             throw_config("sort_items must be 4, 8 or 16");
         if (cfg->heavy_rows == 0) throw_config("heavy_rows must be positive");
+        if (cfg->sort_digit_bits < 8 || cfg->sort_digit_bits > 10) throw_config("sort_digit_bits must be in [8, 10]");
+        if (cfg->partition_exchange > GD_EXCHANGE_NCCL) throw_config("partition_exchange out of range");
         ctx->c->cfg = *cfg;
     });
 }
@@ -388,6 +390,16 @@ gd_status gd_canonicalize(gd_ctx* ctx, const uint64_t* rows, uint64_t n, uint32_
         const u64 m = canonicalize_rows(c, d.p, n, arity, res);
         download(c, (u64*)out, res.p, m * arity);
         *out_n = m;
+    });
+}
+
+gd_status gd_sort_keys_device(gd_ctx* ctx, uint64_t* d_keys, uint64_t* d_tmp, uint64_t n, uint32_t nbits,
+                              int* in_tmp) {
+    return guard(ctx, [&] {
+        if (!d_keys || !d_tmp || !in_tmp) throw Error(GD_ERR_INVALID_ARG, "sort_keys_device: null pointer");
+        if (nbits > 64) throw_config("sort_keys_device: nbits above 64");
+        u64* r = radix_sort<u64>(*ctx->c, (u64*)d_keys, (u64*)d_tmp, n, nbits);
+        *in_tmp = r == (u64*)d_tmp && r != (u64*)d_keys;
     });
 }
 
@@ -583,7 +595,8 @@ gd_status gd_difference(gd_ctx* ctx, const uint64_t* new_rows, uint64_t nn, int 
 gd_status gd_engine_create(gd_ctx* ctx, const gd_engine_config* cfg, uint32_t nrels, const uint32_t* arities,
                            const uint32_t* is_edb, const char* const* names, gd_engine** out) {
     return guard(ctx, [&] {
-        if (!out || !arities || !is_edb) throw Error(GD_ERR_INVALID_ARG, "gd_engine_create: null argument");
+        // an empty program (no relations) may pass null arrays
+        if (!out || (nrels && (!arities || !is_edb))) throw Error(GD_ERR_INVALID_ARG, "gd_engine_create: null argument");
         gd_engine_config def{UINT64_MAX, 1, 5, 0.8, 0, 0, 0};
         auto e = std::make_unique<gd_engine>();
         e->ctx = ctx;

@@ -7,9 +7,11 @@
 // and a plain C++ host gets the system libnccl.so.2.
 #pragma once
 #include <dlfcn.h>
+#include <cstring>
 #include <nccl.h>
 
 #include <string>
+#include <vector>
 
 #include "ctx.h"
 
@@ -24,6 +26,12 @@ struct Transport {
     virtual void send(const unsigned long long* buf, uint64_t n, uint32_t peer, cudaStream_t s) = 0;
     virtual void recv(unsigned long long* buf, uint64_t n, uint32_t peer, cudaStream_t s) = 0;
     virtual void group_end(cudaStream_t s) = 0;
+    // Collective: every rank passes the base of one of its cudaMalloc
+    // allocations; out[q] = rank q's allocation addressed from this process
+    // (out[rank] = local).  Peer addresses are NVLink / NVSwitch mappings.
+    virtual void map_peers(void* local, std::vector<void*>& out, cudaStream_t s) = 0;
+    // Releases mappings made by map_peers (not the local allocation).
+    virtual void unmap_peers(const std::vector<void*>& ptrs) { (void)ptrs; }
 };
 
 struct Comm {
@@ -93,6 +101,40 @@ struct NcclTransport : Transport {
         nccl_check(nccl().recv(buf, n, ncclUint64, (int)peer, comm, s), "ncclRecv");
     }
     void group_end(cudaStream_t) override { nccl_check(nccl().group_end(), "ncclGroupEnd"); }
+    // CUDA IPC handles gathered with one NCCL exchange, opened with peer
+    // access (one process per GPU).
+    void map_peers(void* local, std::vector<void*>& out, cudaStream_t s) override {
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+        out.assign(nranks, nullptr);
+        out[rank] = local;
+        if (nranks == 1) return;
+        cudaIpcMemHandle_t h;
+        GD_CUDA(cudaIpcGetMemHandle(&h, local));
+        unsigned long long* d = nullptr;
+        GD_CUDA(cudaMalloc(&d, (size_t)nranks * 2 * 64));
+        std::vector<unsigned long long> hv((size_t)nranks * 8);
+        GD_CUDA(cudaMemcpyAsync(d, &h, 64, cudaMemcpyHostToDevice, s));
+        group_start();
+        for (uint32_t q = 0; q < nranks; ++q) {
+            if (q == rank) continue;
+            send(d, 8, q, s);
+            recv(d + (size_t)(nranks + q) * 8, 8, q, s);
+        }
+        group_end(s);
+        GD_CUDA(cudaMemcpyAsync(hv.data(), d + (size_t)nranks * 8, (size_t)nranks * 64, cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+        cudaFree(d);
+        for (uint32_t q = 0; q < nranks; ++q) {
+            if (q == rank) continue;
+            cudaIpcMemHandle_t hq;
+            std::memcpy(&hq, hv.data() + (size_t)q * 8, 64);
+            GD_CUDA(cudaIpcOpenMemHandle(&out[q], hq, cudaIpcMemLazyEnablePeerAccess));
+        }
+    }
+    void unmap_peers(const std::vector<void*>& ptrs) override {
+        for (uint32_t q = 0; q < ptrs.size(); ++q)
+            if (q != rank && ptrs[q]) cudaIpcCloseMemHandle(ptrs[q]);
+    }
 };
 
 }  // namespace gd
@@ -115,11 +157,12 @@ struct LoopbackHub {
     };
     uint32_t P;
     std::vector<Msg> out;  // out[from * P + to]
+    std::vector<void*> mapped;  // map_peers: every rank's allocation
     std::mutex m;
     std::condition_variable cv;
     uint64_t gen = 0;
     uint32_t arrived = 0;
-    explicit LoopbackHub(uint32_t p) : P(p), out((size_t)p * p) {}
+    explicit LoopbackHub(uint32_t p) : P(p), out((size_t)p * p), mapped(p) {}
     void barrier() {
         std::unique_lock<std::mutex> l(m);
         const uint64_t g = gen;
@@ -165,6 +208,20 @@ struct LoopbackTransport : Transport {
             GD_CUDA(cudaMemcpyAsync(w.dst, msg.src, w.n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
         }
         GD_CUDA(cudaStreamSynchronize(s));  // copies done before the senders reuse their buffers
+        hub->barrier();
+    }
+    // One GPU, one process: every rank's allocation is directly addressable.
+    void map_peers(void* local, std::vector<void*>& res, cudaStream_t s) override {
+        GD_CUDA(cudaStreamSynchronize(s));
+        {
+            std::lock_guard<std::mutex> l(hub->m);
+            hub->mapped[rank] = local;
+        }
+        hub->barrier();
+        {
+            std::lock_guard<std::mutex> l(hub->m);
+            res = hub->mapped;
+        }
         hub->barrier();
     }
 };

@@ -133,8 +133,11 @@ inline gd_device_config default_device_config() {
     d.sort_items = 16;
     d.trace = 0;
     d.warp_expand = 1;
-    d.reserved0 = 0;
+    d.sort_digit_bits = 10;
     d.heavy_rows = 4096;
+    d.sort_pipeline = 1;
+    d.partition_exchange = GD_EXCHANGE_PEER;
+    d.sort_pipeline_min_keys = 1u << 20;
     return d;
 }
 

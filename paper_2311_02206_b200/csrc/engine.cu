@@ -1285,11 +1285,14 @@ public:
         compact(st);
         H.rel = rec_rel;
         const u64 f0 = st.full_n;
-        H.log_cap = std::max<u64>(2 * f0, 1 << 16);
+        // min_capacities: the log and index start full, so the growth paths
+        // (host-driven growth; stalls of the peer-memory loop) run on small inputs
+        const bool tiny0 = c.cfg.min_capacities != 0;
+        H.log_cap = tiny0 ? std::max<u64>(f0, 1) : std::max<u64>(2 * f0, 1 << 16);
         H.log = DevBuf<u64>(c, H.log_cap);
         if (f0) c.d2d(H.log.p, st.full.p, f0 * sizeof(u64));
         H.sbits = loop_stamp_bits(E.info_[rec_rel].arity * bits);
-        H.alloc_tab(c, std::max<u64>(4 * f0, 1 << 16));
+        H.alloc_tab(c, tiny0 ? 2 * f0 + 16 : std::max<u64>(4 * f0, 1 << 16));
         loop_table_fill(c, H.tab.p, H.tab_cap, H.sbits, H.log.p, f0);
         build_loop_steps(P.rec, P.steps);
         P.final_step = (u32)P.steps.size() - 1;
@@ -1617,6 +1620,336 @@ public:
             E.info_[r].history.push_back(rec.delta_in);
             E.info_[r].log.push_back(rec);
         }
+        return it;
+    }
+
+    // ---- peer-memory partitioned loop (gd_device_config.partition_exchange
+    // = 0) ------------------------------------------------------
+    // Mailbox + inbox of this rank (cudaMalloc bases: CUDA IPC maps them into
+    // the other ranks), their peer mappings and the device routing table.
+    struct PeerState {
+        Transport* t = nullptr;
+        PeerMail* mail = nullptr;
+        u64* inbox = nullptr;
+        u64 inbox_cap = 0;
+        std::vector<void*> mails, inboxes;
+        DevBuf<PeerTab> tab;
+        ~PeerState() {
+            if (t) {
+                t->unmap_peers(inboxes);
+                t->unmap_peers(mails);
+            }
+            if (inbox) cudaFree(inbox);
+            if (mail) cudaFree(mail);
+        }
+    };
+
+    // Sum (op 0) / max (op 1) of n words over all ranks, through the
+    // transport (rare paths only: rollbacks and stalls).  Also a barrier.
+    void host_allreduce(Comm& comm, u64* v, u32 n, int op) {
+        const u32 R = comm.nranks;
+        if (R == 1) return;
+        DevBuf<u64> d(c, (u64)n * (R + 1));
+        c.h2d(d.p, v, n * sizeof(u64));
+        comm.t->group_start();
+        for (u32 q = 0; q < R; ++q) {
+            if (q == comm.rank) continue;
+            comm.t->send(d.p, n, q, c.stream);
+            comm.t->recv(d.p + (u64)n * (q + 1), n, q, c.stream);
+        }
+        comm.t->group_end(c.stream);
+        std::vector<u64> all((u64)n * R);
+        c.d2h(all.data(), d.p + n, (u64)n * R * sizeof(u64));
+        c.sync();
+        for (u32 q = 0; q < R; ++q) {
+            if (q == comm.rank) continue;
+            for (u32 k = 0; k < n; ++k) v[k] = op ? std::max(v[k], all[(u64)q * n + k]) : v[k] + all[(u64)q * n + k];
+        }
+    }
+
+    void peer_map_inbox(Comm& comm, PeerState& ps, u64 cap) {
+        if (ps.inbox) {
+            comm.t->unmap_peers(ps.inboxes);
+            cudaFree(ps.inbox);
+            ps.inbox = nullptr;
+        }
+        GD_CUDA(cudaMalloc(&ps.inbox, std::max<u64>(cap, 1) * sizeof(u64)));
+        ps.inbox_cap = cap;
+        comm.t->map_peers(ps.inbox, ps.inboxes, c.stream);
+        std::vector<u64> caps(comm.nranks, 0);
+        caps[comm.rank] = cap;
+        host_allreduce(comm, caps.data(), comm.nranks, 0);
+        PeerTab h{};
+        h.P = comm.nranks;
+        h.rank = comm.rank;
+        for (u32 q = 0; q < comm.nranks; ++q) {
+            h.inbox[q] = static_cast<u64*>(ps.inboxes[q]);
+            h.cap[q] = caps[q];
+            h.mail[q] = static_cast<PeerMail*>(ps.mails[q]);
+        }
+        c.h2d(ps.tab.p, &h, sizeof(PeerTab));
+        c.sync();
+    }
+
+    // Grows log / index / stamps / history of the single head after a stall
+    // (the insert of the received rows did not fit).
+    void peer_grow_head(LHead& H, u64 ln, u64 need) {
+        PartLoop& P = *pl;
+        LoopCtl* hc = P.hc;
+        if (need > H.log_cap) {
+            const u64 cap = std::max<u64>(2 * need, 1 << 16);
+            DevBuf<u64> nl(c, cap);
+            if (ln) loop_copy_u64(c, nl.p, H.log.p, ln);
+            H.log = std::move(nl);
+            H.log_cap = cap;
+        }
+        if (need > H.tab_limit) {  // load 1/index_growth after the growth when free HBM allows
+            const u64 sb = loop_slot_bytes(H.sbits);
+            const u64 reserve = 1ull << 30, spill = (ln / 16 + (1u << 20)) * sizeof(u64);
+            const u64 avail = c.available_bytes(true);  // exact: other ranks may share this GPU (loopback)
+            const u64 fit = avail > reserve + spill ? (avail - reserve - spill) / sb : 0;
+            const u64 cap = std::min<u64>((u64)c.cfg.index_growth * need, fit);
+            if (cap < need / 3 * 4 + 16)
+                throw_budget("index", "device memory cannot hold the full-tuple index of " + std::to_string(need) +
+                                          " keys");
+            DevBuf<u64> old = std::move(H.tab);
+            const u64 old_cap = H.tab_cap;
+            H.alloc_tab(c, cap, cap < 2 * need, false);
+            loop_table_rehash(c, old.p, old_cap, H.tab.p, H.tab_cap, H.sbits, ln);
+        }
+        if (hc->iter + 1 - hc->epoch_base > (H.sbits ? (1u << H.sbits) - 1 : 0xfffffffeu)) {
+            loop_table_restamp(c, H.tab.p, H.tab_cap, H.sbits);
+            hc->epoch_base = hc->iter;
+        }
+    }
+
+    // The whole partitioned fixpoint as one CUDA graph per rank: per
+    // iteration the joins of the local Δ, the final step's rows routed into
+    // their owners' inboxes over peer memory, barrier 1 (overflow consensus,
+    // received count, capacity gate), the insert of the inbox into this
+    // rank's full-tuple index and log, barrier 2 (record, Δ window, |Δ| sum
+    // -> the while condition).  No host round trip per iteration; the host
+    // steps in only to grow a buffer (every rank rolls back together) or to
+    // finish a stalled insert.
+    u64 part_peer_run(Comm& comm, u64 max_iters) {
+        PartLoop& P = *pl;
+        LoopCtl* hc = P.hc;
+        const u32 ns = (u32)P.steps.size();
+        const u32 R = E.nranks;
+        if (comm.nranks != R || comm.rank != E.rank)
+            throw_usage("gd_engine_run_partitioned: communicator does not match set_partition");
+        LHead& H = P.heads[0];
+        const u32 r = H.rel;
+        const bool tiny = c.cfg.min_capacities != 0;
+        PeerState ps;
+        ps.t = comm.t;
+        GD_CUDA(cudaMalloc(&ps.mail, sizeof(PeerMail)));
+        GD_CUDA(cudaMemsetAsync(ps.mail, 0, sizeof(PeerMail), c.stream));
+        ps.tab = DevBuf<PeerTab>(c, 1);
+        comm.t->map_peers(ps.mail, ps.mails, c.stream);
+        const u64 f0 = hc->h[0].log_n;
+        peer_map_inbox(comm, ps, tiny ? 1 : std::max<u64>(2 * f0 / R + 1024, 1 << 20));
+
+        const u64 hist0 = hc->iter;
+        auto grow_hist = [&](u64 need) {
+            if (need <= P.hist_cap) return;
+            const u64 cap = std::max<u64>(need, 2 * P.hist_cap + 256);
+            DevBuf<gd_iter_record> h2(c, cap);
+            if (P.hist_cap) c.d2d(h2.p, P.hist.p, P.hist_cap * sizeof(gd_iter_record));
+            P.hist = std::move(h2);
+            P.hist_cap = cap;
+        };
+        grow_hist(hist0 + (tiny ? 1 : 1024));
+        hc->part_epoch = 0;
+        hc->part_join = 0;
+        hc->part_over = hc->part_stall = hc->part_stall_any = hc->part_inbox_over = 0;
+        hc->overflow = hc->done = 0;
+        c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
+
+        auto outer_of = [&](const LStep& L) {
+            LoopOuter o{};
+            o.kind = L.kind;
+            o.head = L.src_head;
+            o.src_step = L.src_step;
+            o.ptr = L.kind == LO_TEMP ? P.steps[L.src_step].temp.p : H.log.p;
+            return o;
+        };
+        auto record_iteration = [&](cudaStream_t s, bool use_cond, unsigned long long cond) {
+            PeerSyncDesc d{};
+            d.tab = ps.tab.p;
+            d.final_step = P.final_step;
+            d.nsteps = ns;
+            d.log_cap = H.log_cap;
+            d.tab_limit = H.tab_limit;
+            d.stamp_max = H.sbits ? (1u << H.sbits) - 1 : 0xfffffffeu;
+            d.hist = P.hist.p;
+            d.hist_cap = P.hist_cap;
+            d.cond = cond;
+            d.use_cond = use_cond ? 1 : 0;
+            for (u32 i = 0; i < ns; ++i) {
+                LStep& L = P.steps[i];
+                const LoopOuter o = outer_of(L);
+                if (L.final && L.xp) {
+                    loop_count(c, s, P.ctl.p, i, o, L.jd, L.dv, L.bufs(), c.cfg.heavy_rows, nullptr);
+                    loop_expand_route(c, s, P.ctl.p, i, o, L.inner, L.jd, L.dv, L.bufs(), c.cfg.heavy_rows,
+                                      ps.tab.p);
+                    continue;
+                }
+                loop_probe(c, s, P.ctl.p, i, o, L.jd, L.has_iv ? &L.iv : nullptr, L.dv, L.inner_n, L.bufs(),
+                           P.block_sums.p);
+                loop_scan(c, s, P.ctl.p, i, o, L.bufs(), P.block_sums.p, nullptr);
+                loop_materialize_temp(c, s, P.ctl.p, i, o, L.inner, L.jd, L.bufs(), L.temp.p, L.temp_cap);
+                if (L.final) loop_route_keys(c, s, P.ctl.p, i, L.temp.p, ps.tab.p);
+            }
+            loop_peer_sync1(c, s, P.ctl.p, d);
+            loop_insert_keys(c, s, P.ctl.p, P.final_step, 0, ps.inbox, part_bufs(), nullptr);
+            loop_peer_sync2(c, s, P.ctl.p, d);
+        };
+
+        const bool eager = c.prof.on || c.cfg.loop_mode != GD_LOOP_GRAPH;
+        cudaGraphExec_t exec = nullptr;
+        cudaGraph_t graph = nullptr;
+        cudaStream_t cap_stream = nullptr;
+        u64 kernels_per_iter = 0;
+        auto destroy_graph = [&]() {
+            if (exec) cudaGraphExecDestroy(exec);
+            if (graph) cudaGraphDestroy(graph);
+            exec = nullptr;
+            graph = nullptr;
+        };
+        auto build_graph = [&]() {
+            destroy_graph();
+            if (!cap_stream) GD_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+            GD_CUDA(cudaGraphCreate(&graph, 0));
+            cudaGraphConditionalHandle hdl;
+            GD_CUDA(cudaGraphConditionalHandleCreate(&hdl, graph, 1, cudaGraphCondAssignDefault));
+            cudaGraphNodeParams np{};
+            np.type = cudaGraphNodeTypeConditional;
+            np.conditional.handle = hdl;
+            np.conditional.type = cudaGraphCondTypeWhile;
+            np.conditional.size = 1;
+            cudaGraphNode_t node;
+            GD_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
+            cudaGraph_t body = np.conditional.phGraph_out[0];
+            GD_CUDA(cudaStreamBeginCaptureToGraph(cap_stream, body, nullptr, nullptr, 0,
+                                                  cudaStreamCaptureModeThreadLocal));
+            const u64 l0 = c.launches;
+            try {
+                record_iteration(cap_stream, true, (unsigned long long)hdl);
+            } catch (...) {
+                cudaStreamEndCapture(cap_stream, &body);
+                throw;
+            }
+            kernels_per_iter = c.launches - l0;
+            c.launches = l0;
+            GD_CUDA(cudaStreamEndCapture(cap_stream, &body));
+            GD_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        };
+        struct Cleanup {
+            std::function<void()> f;
+            ~Cleanup() { f(); }
+        } cleanup{[&] {
+            destroy_graph();
+            if (cap_stream) cudaStreamDestroy(cap_stream);
+        }};
+
+        u32 done_iters = hc->iter;
+        const u64 iter_limit = hist0 + max_iters;
+        for (;;) {
+            if (eager) {
+                record_iteration(c.stream, false, 0);
+            } else {
+                if (!exec) build_graph();
+                GD_CUDA(cudaGraphLaunch(exec, c.stream));
+            }
+            c.d2h(hc, P.ctl.p, sizeof(LoopCtl));
+            c.sync();
+            if (!eager) c.launches += kernels_per_iter * (hc->iter - done_iters + (hc->part_over ? 1 : 0));
+            done_iters = hc->iter;
+            if (hc->part_over) {  // every rank rolled the iteration back: grow, remap, rerun
+                for (u32 i = 0; i < ns; ++i) {
+                    LStep& L = P.steps[i];
+                    if (hc->need_rows[i] > L.rows_cap) {
+                        L.rows_cap = hc->need_rows[i] + hc->need_rows[i] / 2;
+                        L.row_start = DevBuf<u64>(c, L.rows_cap);
+                        L.row_off = DevBuf<u64>(c, L.rows_cap);
+                    }
+                    if (hc->need_splits[i] > L.splits_cap) {
+                        L.splits_cap = hc->need_splits[i] + hc->need_splits[i] / 2;
+                        L.splits = DevBuf<u64>(c, L.splits_cap);
+                    }
+                    if (hc->need_temp[i] > L.temp_cap) {
+                        L.temp_cap = hc->need_temp[i] + hc->need_temp[i] / 2;
+                        L.temp = DevBuf<u64>(c, L.temp_cap);
+                    }
+                    hc->need_rows[i] = hc->need_splits[i] = hc->need_temp[i] = 0;
+                    hc->step_total[i] = hc->step_cand[i] = hc->heavy_n[i] = 0;
+                }
+                const u64 demand = hc->part_recv;  // rows routed to this rank (counted past the capacity)
+                u64 grow = demand > ps.inbox_cap ? 1 : 0;
+                host_allreduce(comm, &grow, 1, 1);
+                if (grow) peer_map_inbox(comm, ps, demand > ps.inbox_cap ? demand + demand / 2 : ps.inbox_cap);
+                hc->overflow = hc->part_over = hc->part_inbox_over = 0;
+                hc->part_recv = 0;
+                hc->h[0].J = hc->h[0].N = hc->h[0].D = 0;
+                c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
+                GD_CUDA(cudaMemsetAsync(&ps.mail->cursor, 0, sizeof(unsigned long long), c.stream));
+                u64 bar = 0;
+                host_allreduce(comm, &bar, 1, 0);  // every cursor reset before any rank routes again
+                c.sync();
+                destroy_graph();
+                continue;
+            }
+            if (hc->part_stall_any) {
+                u64 D = hc->part_last_D;
+                if (hc->part_stall) {  // finish this rank's insert under host control
+                    const u64 ln = hc->h[0].log_n, recv = hc->part_recv;
+                    peer_grow_head(H, ln, ln + recv);
+                    grow_hist(hc->iter + 1);
+                    hc->step_total[P.final_step] = recv;
+                    hc->h[0].J = hc->h[0].N = hc->h[0].D = 0;
+                    c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
+                    if (recv) loop_insert_keys(c, c.stream, P.ctl.p, P.final_step, 0, ps.inbox, part_bufs(), nullptr);
+                    loop_part_advance(c, P.ctl.p, P.final_step, recv, P.hist.p);
+                    GD_CUDA(cudaMemsetAsync(&ps.mail->cursor, 0, sizeof(unsigned long long), c.stream));
+                    c.d2h(hc, P.ctl.p, sizeof(LoopCtl));
+                    c.sync();
+                    gd_iter_record rec;
+                    c.d2h(&rec, P.hist.p + (hc->iter - 1), sizeof(rec));
+                    c.sync();
+                    D = rec.delta_out;
+                    hc->part_last_D = D;
+                }
+                // a rank whose graph recorded the iteration keeps its buffers;
+                // the next graph run needs this rank's new capacities
+                grow_hist(hc->iter + 1);
+                hc->part_stall = hc->part_stall_any = 0;
+                hc->h[0].J = hc->h[0].N = hc->h[0].D = 0;
+                for (u32 i = 0; i < ns; ++i) hc->step_total[i] = hc->step_cand[i] = hc->heavy_n[i] = 0;
+                c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
+                host_allreduce(comm, &D, 1, 0);
+                c.sync();
+                destroy_graph();
+                if (D == 0) break;
+                if (hc->iter >= iter_limit) break;
+                continue;
+            }
+            if (hc->done || hc->iter >= iter_limit) break;
+            if (eager) continue;
+            // a graph that stopped without a reason: cannot happen
+            throw_logic("partitioned loop: graph stopped without termination, overflow or stall");
+        }
+        const u64 it = hc->iter - hist0;
+        E.join_tuples += hc->part_join;
+        std::vector<gd_iter_record> recs(it);
+        if (it) c.d2h(recs.data(), P.hist.p + hist0, it * sizeof(gd_iter_record));
+        c.sync();
+        for (const auto& rec : recs) {
+            ++E.iterations;
+            E.info_[r].history.push_back(rec.delta_in);
+            E.info_[r].log.push_back(rec);
+        }
+        hc->done = 0;
         return it;
     }
 
@@ -2090,6 +2423,9 @@ u64 Impl<K>::partition_run(Comm& comm, u64 max_iters) {
             if (p.recursive) rec_rel = p.head_rel;
         if (pl || part_loop_eligible(rec_rel)) {
             if (!pl) part_loop_setup(rec_rel);
+            // peer-memory exchange inside the graph loop unless the NCCL
+            // send/recv driver (one host round trip per iteration) is asked for
+            if (c.cfg.partition_exchange == GD_EXCHANGE_PEER) return part_peer_run(comm, max_iters);
             return part_loop_run(comm, max_iters);
         }
     }

@@ -830,52 +830,106 @@ struct XWarp {
     u64 J, N, D;
 };
 
-// Inserts buf[0, m) (m <= kXRound) into the head's index and appends the
-// new keys to the log.
-__device__ __forceinline__ void x_round(XWarp& w, u32 m, const LoopHeadBufs& hb, u32 it,
-                                        unsigned long long* log_n) {
-    __syncwarp();
-    const u32 lane = lane_id();
-    u64 key[kXPer];
-    u32 ok = 0;
+// Sink of the warp expansion: inserts buf[0, m) (m <= kXRound) into the
+// head's index and appends the new keys to the log.
+struct InsertSink {
+    LoopHeadBufs hb;
+    u32 it;
+    unsigned long long* log_n;
+    __device__ __forceinline__ void round(XWarp& w, u32 m) {
+        __syncwarp();
+        const u32 lane = lane_id();
+        u64 key[kXPer];
+        u32 ok = 0;
 #pragma unroll
-    for (int k = 0; k < kXPer; ++k) {
-        const u32 idx = lane + 32u * k;
-        key[k] = idx < m ? w.buf[idx] : 0ull;
-        ok |= (u32)(idx < m) << k;
-    }
-    u32 fresh, first;
-    hs_insert<kXPer>(hb, it, key, ok, fresh, first);
-    w.N += __popc(first);
-    w.D += __popc(fresh);
-    u32 mk[kXPer];
-    u32 tot = 0;
+        for (int k = 0; k < kXPer; ++k) {
+            const u32 idx = lane + 32u * k;
+            key[k] = idx < m ? w.buf[idx] : 0ull;
+            ok |= (u32)(idx < m) << k;
+        }
+        u32 fresh, first;
+        hs_insert<kXPer>(hb, it, key, ok, fresh, first);
+        w.N += __popc(first);
+        w.D += __popc(fresh);
+        u32 mk[kXPer];
+        u32 tot = 0;
 #pragma unroll
-    for (int k = 0; k < kXPer; ++k) {
-        mk[k] = __ballot_sync(0xffffffffu, fresh >> k & 1);
-        tot += __popc(mk[k]);
-    }
-    unsigned long long base = 0;
-    if (lane == 0 && tot) base = atomicAdd(log_n, (unsigned long long)tot);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    const u32 lt = lanemask_lt();
+        for (int k = 0; k < kXPer; ++k) {
+            mk[k] = __ballot_sync(0xffffffffu, fresh >> k & 1);
+            tot += __popc(mk[k]);
+        }
+        unsigned long long base = 0;
+        if (lane == 0 && tot) base = atomicAdd(log_n, (unsigned long long)tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const u32 lt = lanemask_lt();
 #pragma unroll
-    for (int k = 0; k < kXPer; ++k) {
-        if (fresh >> k & 1) hb.log[base + __popc(mk[k] & lt)] = key[k];
-        base += __popc(mk[k]);
+        for (int k = 0; k < kXPer; ++k) {
+            if (fresh >> k & 1) hb.log[base + __popc(mk[k] & lt)] = key[k];
+            base += __popc(mk[k]);
+        }
+        __syncwarp();
     }
-    __syncwarp();
-}
+};
+
+// Sink of the partitioned loop: buf[0, m) goes to the owners' inboxes —
+// per destination one system-scope atomic on the owner's cursor (counted
+// even past the capacity, so the owner learns its demand), then coalesced
+// (peer) stores.  Keys that do not fit raise part_inbox_over; the iteration
+// is rolled back on every rank at the next barrier.
+struct RouteSink {
+    const PeerTab* tab;
+    LoopCtl* ctl;
+    __device__ __forceinline__ void round(XWarp& w, u32 m) {
+        __syncwarp();
+        const u32 lane = lane_id();
+        u64 key[kXPer];
+        u32 own[kXPer];
+        const u32 P = tab->P;
+#pragma unroll
+        for (int k = 0; k < kXPer; ++k) {
+            const u32 idx = lane + 32u * k;
+            key[k] = idx < m ? w.buf[idx] : 0ull;
+            own[k] = idx < m ? (u32)(key_hash64<u64>(key[k]) % P) : kLoopMaxRanks;
+        }
+        const u32 lt = lanemask_lt();
+        for (u32 q = 0; q < P; ++q) {
+            u32 mk[kXPer];
+            u32 tot = 0;
+#pragma unroll
+            for (int k = 0; k < kXPer; ++k) {
+                mk[k] = __ballot_sync(0xffffffffu, own[k] == q);
+                tot += __popc(mk[k]);
+            }
+            if (!tot) continue;
+            PeerMail* mq = tab->mail[q];
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd_system(&mq->cursor, (unsigned long long)tot);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (base + tot > tab->cap[q]) {
+                if (lane == 0) ctl->part_inbox_over = 1;
+                continue;
+            }
+            u64* dst = tab->inbox[q];
+#pragma unroll
+            for (int k = 0; k < kXPer; ++k) {
+                if (own[k] == q) dst[base + __popc(mk[k] & lt)] = key[k];
+                base += __popc(mk[k]);
+            }
+        }
+        __syncwarp();
+    }
+};
 
 // Adds one key per lane (`have`) to the warp buffer, compacted; a full
-// round is inserted at once and the (< 32) keys past it move to the front.
-__device__ __forceinline__ void x_emit(XWarp& w, bool have, u64 key, const LoopHeadBufs& hb, u32 it,
-                                       unsigned long long* log_n) {
+// round goes to the sink at once and the (< 32) keys past it move to the
+// front.
+template <class Sink>
+__device__ __forceinline__ void x_emit(XWarp& w, bool have, u64 key, Sink& sink) {
     const u32 mask = __ballot_sync(0xffffffffu, have);
     if (have) w.buf[w.fill + __popc(mask & lanemask_lt())] = key;
     w.fill += __popc(mask);
     if (w.fill >= (u32)kXRound) {
-        x_round(w, kXRound, hb, it, log_n);
+        sink.round(w, kXRound);
         const u32 rest = w.fill - kXRound;
         const u32 lane = lane_id();
         const u64 t = lane < rest ? w.buf[kXRound + lane] : 0ull;
@@ -883,6 +937,72 @@ __device__ __forceinline__ void x_emit(XWarp& w, bool have, u64 key, const LoopH
         if (lane < rest) w.buf[lane] = t;
         w.fill = rest;
     }
+}
+
+// The expansion itself (both sinks): light rows 32 at a time per warp,
+// then the heavy (row, segment) items queued by loop_count.
+template <class Sink>
+__device__ __forceinline__ void expand_rows(const LoopCtl* ctl, u32 step, const u64* outer, u64 n,
+                                            const u64* __restrict__ inner, const DevJoin& jd, const LoopDense& dv,
+                                            const LoopStepBufs& sb, u64 heavy_min, XWarp& w, Sink& sink) {
+    const u64 nheavy = min(__ldcg(&ctl->heavy_n[step]), sb.rows_cap);
+    const u32 lane = lane_id(), warp = threadIdx.x >> 5;
+    const u64 gw = (u64)blockIdx.x * (kLT / 32) + warp, nw = (u64)gridDim.x * (kLT / 32);
+    for (u64 base = gw * 32; base < n; base += nw * 32) {
+        const u64 r = base + lane;
+        u64 ov = 0, a = 0, c = 0;
+        if (r < n) {
+            ov = outer[r];
+            dense_range(dv, outer_prefix(jd, ov), a, c);
+            if (c > heavy_min) c = 0;  // a heavy item (loop_count queued it)
+        }
+        const u64 incl = warp_inclusive_scan(c);
+        const u64 T = __shfl_sync(0xffffffffu, incl, 31);
+        const u64 excl = incl - c;
+        for (u64 j0 = 0; j0 < T; j0 += 32) {
+            const u64 j = j0 + lane;
+            // source lane: the last s with excl_s <= j (rows without
+            // output share the next row's excl and are never last)
+            u32 s = 0;
+#pragma unroll
+            for (u32 d = 16; d; d >>= 1) {
+                const u64 ex = __shfl_sync(0xffffffffu, excl, s + d);
+                if (ex <= j) s += d;
+            }
+            const u64 sa = __shfl_sync(0xffffffffu, a, s);
+            const u64 se = __shfl_sync(0xffffffffu, excl, s);
+            const u64 so = __shfl_sync(0xffffffffu, ov, s);
+            bool have = false;
+            u64 key = 0;
+            if (j < T) {
+                const u64 iv = inner[sa + (j - se)];
+                have = passes(jd, so, iv);
+                key = project(jd, so, iv);
+            }
+            w.J += have;
+            x_emit(w, have, key, sink);
+        }
+    }
+    for (u64 i = gw; i < nheavy; i += nw) {  // heavy items: one segment of heavy_min outputs per warp
+        const u64 r = sb.row_start[i], sg = sb.row_off[i];
+        const u64 ov = outer[r];
+        u64 a, c;
+        dense_range(dv, outer_prefix(jd, ov), a, c);
+        const u64 b0 = sg * heavy_min, b1 = min(c, b0 + heavy_min);
+        for (u64 j0 = b0; j0 < b1; j0 += 32) {
+            const u64 j = j0 + lane;
+            bool have = false;
+            u64 key = 0;
+            if (j < b1) {
+                const u64 iv = inner[a + j];
+                have = passes(jd, ov, iv);
+                key = project(jd, ov, iv);
+            }
+            w.J += have;
+            x_emit(w, have, key, sink);
+        }
+    }
+    if (w.fill) sink.round(w, w.fill);
 }
 
 __global__ void __launch_bounds__(kLT, 3) loop_expand_insert_kernel(
@@ -895,70 +1015,178 @@ __global__ void __launch_bounds__(kLT, 3) loop_expand_insert_kernel(
         const u64* outer;
         u64 n;
         resolve(o, ctl, outer, n);
-        const u32 it = ctl->iter + 1 - ctl->epoch_base;
-        const u64 nheavy = min(__ldcg(&ctl->heavy_n[step]), sb.rows_cap);
-        unsigned long long* log_n = reinterpret_cast<unsigned long long*>(&ctl->h[head].log_n);
-        const u32 lane = lane_id(), warp = threadIdx.x >> 5;
-        XWarp w{sbuf[warp], 0, 0, 0, 0};
-        const u64 gw = (u64)blockIdx.x * (kLT / 32) + warp, nw = (u64)gridDim.x * (kLT / 32);
-        for (u64 base = gw * 32; base < n; base += nw * 32) {
-            const u64 r = base + lane;
-            u64 ov = 0, a = 0, c = 0;
-            if (r < n) {
-                ov = outer[r];
-                dense_range(dv, outer_prefix(jd, ov), a, c);
-                if (c > heavy_min) c = 0;  // a heavy item (loop_count queued it)
-            }
-            const u64 incl = warp_inclusive_scan(c);
-            const u64 T = __shfl_sync(0xffffffffu, incl, 31);
-            const u64 excl = incl - c;
-            for (u64 j0 = 0; j0 < T; j0 += 32) {
-                const u64 j = j0 + lane;
-                // source lane: the last s with excl_s <= j (rows without
-                // output share the next row's excl and are never last)
-                u32 s = 0;
-#pragma unroll
-                for (u32 d = 16; d; d >>= 1) {
-                    const u64 ex = __shfl_sync(0xffffffffu, excl, s + d);
-                    if (ex <= j) s += d;
-                }
-                const u64 sa = __shfl_sync(0xffffffffu, a, s);
-                const u64 se = __shfl_sync(0xffffffffu, excl, s);
-                const u64 so = __shfl_sync(0xffffffffu, ov, s);
-                bool have = false;
-                u64 key = 0;
-                if (j < T) {
-                    const u64 iv = inner[sa + (j - se)];
-                    have = passes(jd, so, iv);
-                    key = project(jd, so, iv);
-                }
-                w.J += have;
-                x_emit(w, have, key, hb, it, log_n);
-            }
-        }
-        for (u64 i = gw; i < nheavy; i += nw) {  // heavy items: one segment of heavy_min outputs per warp
-            const u64 r = sb.row_start[i], sg = sb.row_off[i];
-            const u64 ov = outer[r];
-            u64 a, c;
-            dense_range(dv, outer_prefix(jd, ov), a, c);
-            const u64 b0 = sg * heavy_min, b1 = min(c, b0 + heavy_min);
-            for (u64 j0 = b0; j0 < b1; j0 += 32) {
-                const u64 j = j0 + lane;
-                bool have = false;
-                u64 key = 0;
-                if (j < b1) {
-                    const u64 iv = inner[a + j];
-                    have = passes(jd, ov, iv);
-                    key = project(jd, ov, iv);
-                }
-                w.J += have;
-                x_emit(w, have, key, hb, it, log_n);
-            }
-        }
-        if (w.fill) x_round(w, w.fill, hb, it, log_n);
+        InsertSink sink{hb, ctl->iter + 1 - ctl->epoch_base,
+                        reinterpret_cast<unsigned long long*>(&ctl->h[head].log_n)};
+        XWarp w{sbuf[threadIdx.x >> 5], 0, 0, 0, 0};
+        expand_rows(ctl, step, outer, n, inner, jd, dv, sb, heavy_min, w, sink);
         flush_counts(ctl, head, step, w.J, w.N, w.D, red);
     }
     if (do_end && last_cta(ctl, &s_flag) && threadIdx.x == 0) end_body(ctl, e);
+}
+
+__global__ void __launch_bounds__(kLT, 3) loop_expand_route_kernel(LoopCtl* ctl, u32 step, LoopOuter o,
+                                                                   const u64* __restrict__ inner, DevJoin jd,
+                                                                   LoopDense dv, LoopStepBufs sb, u64 heavy_min,
+                                                                   const PeerTab* tab) {
+    __shared__ u64 sbuf[kLT / 32][kXBuf];
+    __shared__ u64 red[kLT / 32];
+    __shared__ u32 s_flag;
+    if (cta_stopped(ctl, &s_flag)) return;
+    const u64* outer;
+    u64 n;
+    resolve(o, ctl, outer, n);
+    RouteSink sink{tab, ctl};
+    XWarp w{sbuf[threadIdx.x >> 5], 0, 0, 0, 0};
+    expand_rows(ctl, step, outer, n, inner, jd, dv, sb, heavy_min, w, sink);
+    const u64 j = block_sum(w.J, red);
+    if (threadIdx.x == 0 && j) atomicAdd((unsigned long long*)&ctl->step_total[step], (unsigned long long)j);
+    __threadfence_system();  // peer stores before the barrier's flag (loop_peer_sync1)
+}
+
+// Routes materialized rows (a chain's final temp) to their owners.
+__global__ void __launch_bounds__(kLT) loop_route_keys_kernel(LoopCtl* ctl, u32 step, const u64* __restrict__ keys,
+                                                              const PeerTab* tab) {
+    __shared__ u64 sbuf[kLT / 32][kXRound];
+    __shared__ u32 s_flag;
+    if (cta_stopped(ctl, &s_flag)) return;
+    const u64 n = ctl->step_total[step];
+    RouteSink sink{tab, ctl};
+    const u32 lane = lane_id(), warp = threadIdx.x >> 5;
+    XWarp w{sbuf[warp], 0, 0, 0, 0};
+    const u64 gw = (u64)blockIdx.x * (kLT / 32) + warp, nw = (u64)gridDim.x * (kLT / 32);
+    for (u64 b = gw * kXRound; b < n; b += nw * kXRound) {
+        const u32 m = (u32)min((u64)kXRound, n - b);
+        for (u32 i = lane; i < m; i += 32) w.buf[i] = __ldcs(keys + b + i);
+        sink.round(w, m);
+    }
+    __threadfence_system();
+}
+
+// ---- device-side barrier of the peer loop (one thread) --------------------
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Publishes `val` to every rank's mailbox slot of this rank, then waits
+// until every rank reached the same epoch; out[s] = rank s's payload.
+__device__ void peer_barrier(const PeerTab* tab, u64 epoch, const u64 (&val)[kPeerVals],
+                             u64 (&out)[kLoopMaxRanks][kPeerVals]) {
+    const u32 P = tab->P, me = tab->rank;
+    for (u32 q = 0; q < P; ++q) {
+        PeerMail* m = tab->mail[q];
+#pragma unroll
+        for (u32 k = 0; k < kPeerVals; ++k) m->val[me][k] = val[k];
+    }
+    __threadfence_system();
+    for (u32 q = 0; q < P; ++q) st_release_sys(&tab->mail[q]->flag[me], epoch);
+    PeerMail* mine = tab->mail[me];
+    for (u32 s = 0; s < P; ++s) {
+        while (ld_acquire_sys(&mine->flag[s]) < epoch) __nanosleep(64);
+#pragma unroll
+        for (u32 k = 0; k < kPeerVals; ++k) out[s][k] = __ldcv(&mine->val[s][k]);
+    }
+}
+
+__global__ void loop_peer_sync1_kernel(LoopCtl* ctl, PeerSyncDesc d) {
+    if (threadIdx.x || blockIdx.x) return;
+    const cudaGraphConditionalHandle cond = (cudaGraphConditionalHandle)d.cond;
+    if (ctl->done) {
+        if (d.use_cond) cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    const PeerTab* tab = d.tab;
+    const u64 epoch = ctl->part_epoch + 1;
+    ctl->part_epoch = epoch;
+    const u64 mine[kPeerVals] = {(u64)(ctl->overflow | ctl->part_inbox_over), 0, 0, 0};
+    __shared__ u64 got[kLoopMaxRanks][kPeerVals];
+    peer_barrier(tab, epoch, mine, got);
+    u64 any = 0;
+    for (u32 s = 0; s < tab->P; ++s) any |= got[s][0];
+    const u64 recv = ld_acquire_sys(&tab->mail[tab->rank]->cursor);
+    ctl->part_recv = recv;
+    if (any) {  // roll back on every rank: nothing was inserted anywhere
+        ctl->overflow = 1;
+        ctl->part_over = 1;
+        if (d.use_cond) cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    u64 j = 0;
+    for (u32 s = 0; s < d.nsteps; ++s) j += ctl->step_total[s];
+    ctl->part_join += j;
+    // capacity gate of this rank's insert (no rollback past this point)
+    const u64 need = ctl->h[0].log_n + recv;
+    const bool stamp_over = ctl->iter + 1 - ctl->epoch_base > d.stamp_max;
+    const bool hist_over = ctl->iter >= d.hist_cap;
+    if (need > d.log_cap || need > d.tab_limit || stamp_over || hist_over) {
+        ctl->part_stall = 1;
+        ctl->need_log[0] = need;
+        ctl->need_tab[0] = need;
+        ctl->need_restamp = stamp_over;
+        ctl->need_hist = hist_over ? ctl->iter + 1 : 0;
+        ctl->step_total[d.final_step] = 0;  // the insert kernel does nothing
+    } else {
+        ctl->step_total[d.final_step] = recv;
+    }
+    ctl->h[0].J = ctl->h[0].N = ctl->h[0].D = 0;
+    __threadfence();
+}
+
+__global__ void loop_peer_sync2_kernel(LoopCtl* ctl, PeerSyncDesc d) {
+    if (threadIdx.x || blockIdx.x) return;
+    const cudaGraphConditionalHandle cond = (cudaGraphConditionalHandle)d.cond;
+    if (ctl->done || ctl->overflow) {
+        if (d.use_cond) cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    const PeerTab* tab = d.tab;
+    const u32 stall = ctl->part_stall;
+    LoopHeadState& st = ctl->h[0];
+    const u64 D = stall ? 0 : st.D;
+    if (!stall) tab->mail[tab->rank]->cursor = 0;  // inbox consumed (peers route again only after this barrier)
+    const u64 epoch = ctl->part_epoch + 1;
+    ctl->part_epoch = epoch;
+    const u64 mine[kPeerVals] = {D, (u64)stall, 0, 0};
+    __shared__ u64 got[kLoopMaxRanks][kPeerVals];
+    peer_barrier(tab, epoch, mine, got);
+    u64 gD = 0, any_stall = 0;
+    for (u32 s = 0; s < tab->P; ++s) {
+        gD += got[s][0];
+        any_stall |= got[s][1];
+    }
+    if (!stall) {
+        const u32 i = ctl->iter;
+        gd_iter_record r;
+        r.delta_in = st.dhi - st.dlo;
+        r.join = ctl->part_recv;
+        r.new_unique = st.N;
+        r.delta_out = st.D;
+        r.full_after = st.log_n;
+        d.hist[i] = r;
+        st.dlo = st.dhi;
+        st.dhi = st.log_n;
+        ctl->iter = i + 1;
+        ctl->part_last_D = st.D;
+        st.J = st.N = st.D = 0;
+    }
+    for (u32 s = 0; s < d.nsteps; ++s) ctl->step_total[s] = ctl->step_cand[s] = ctl->heavy_n[s] = 0;
+    if (stall) ctl->step_total[d.final_step] = 0;
+    __threadfence();
+    if (any_stall) {
+        ctl->part_stall_any = 1;
+        if (d.use_cond) cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    if (gD == 0) {
+        ctl->done = 1;
+        if (d.use_cond) cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    if (d.use_cond) cudaGraphSetConditional(cond, 1);
 }
 
 // Rebuild of a table from the log (keys unique): stamp 0 = "before the
@@ -1224,7 +1452,8 @@ int occupancy(Kern k, size_t smem = 0) {
     return b > 0 ? b : 1;
 }
 
-int g_occ_temp = 0, g_occ_insert = 0, g_occ_select = 0, g_occ_keys = 0, g_occ_expand = 0;
+int g_occ_temp = 0, g_occ_insert = 0, g_occ_select = 0, g_occ_keys = 0, g_occ_expand = 0, g_occ_xroute = 0,
+    g_occ_route = 0;
 // Insert grid = waves x resident CTAs: CTAs beyond the resident set start as
 // others finish, so the hardware balances the iteration's tiles.  Large
 // relations (log capacity >= kWideLog rows) run 3 waves (C2 -2.8%, SG
@@ -1243,6 +1472,8 @@ void loop_prepare() {
     g_occ_keys = occupancy(loop_insert_keys_kernel);
     g_occ_select = occupancy(loop_select_insert_kernel);
     g_occ_expand = occupancy(loop_expand_insert_kernel);
+    g_occ_xroute = occupancy(loop_expand_route_kernel);
+    g_occ_route = occupancy(loop_route_keys_kernel);
 }
 
 void loop_fill_u64(Ctx& c, u64* p, u64 n, u64 v) {
@@ -1463,6 +1694,29 @@ void loop_expand_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head
     const int waves = c.cfg.insert_waves ? (int)c.cfg.insert_waves : 1;
     loop_expand_insert_kernel<<<c.num_sms * g_occ_expand * waves, kLT, 0, s>>>(
         ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0);
+    c.check_launch();
+}
+
+void loop_expand_route(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const u64* inner,
+                       const DevJoin& jd, const LoopDense& dense, const LoopStepBufs& sb, u64 heavy_rows,
+                       const PeerTab* tab) {
+    loop_expand_route_kernel<<<c.num_sms * g_occ_xroute, kLT, 0, s>>>(ctl, step, o, inner, jd, dense, sb,
+                                                                      heavy_rows, tab);
+    c.check_launch();
+}
+
+void loop_route_keys(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const u64* keys, const PeerTab* tab) {
+    loop_route_keys_kernel<<<c.num_sms * g_occ_route, kLT, 0, s>>>(ctl, step, keys, tab);
+    c.check_launch();
+}
+
+void loop_peer_sync1(Ctx& c, cudaStream_t s, LoopCtl* ctl, const PeerSyncDesc& d) {
+    loop_peer_sync1_kernel<<<1, 32, 0, s>>>(ctl, d);
+    c.check_launch();
+}
+
+void loop_peer_sync2(Ctx& c, cudaStream_t s, LoopCtl* ctl, const PeerSyncDesc& d) {
+    loop_peer_sync2_kernel<<<1, 32, 0, s>>>(ctl, d);
     c.check_launch();
 }
 

@@ -85,6 +85,37 @@ struct LoopCtl {
     u64 need_hist;
     u64 heavy_n[kLoopMaxSteps];    // (row, segment) items queued by loop_count
     u64 last_cand[kLoopMaxSteps];  // step_cand of the last completed iteration (profiler)
+    // peer-memory partitioned loop (loop_peer_*)
+    u64 part_epoch;    // barriers passed (identical on every rank)
+    u64 part_recv;     // rows this rank received this iteration
+    u64 part_join;     // join rows produced by this rank, all iterations
+    u64 part_last_D;   // this rank's |Δ| of its last completed iteration
+    u32 part_inbox_over;  // a routed row did not fit a peer's inbox (this rank saw it)
+    u32 part_over;        // some rank overflowed: the iteration was rolled back on every rank
+    u32 part_stall;       // this rank's insert did not fit its log / index: the host finishes it
+    u32 part_stall_any;   // some rank stalled (the graph stopped on every rank)
+};
+
+// ---- peer-memory partitioned loop --------------
+// Every rank owns a mailbox and an inbox in its HBM, mapped into every other
+// rank (CUDA IPC over NVLink / NVSwitch; plain pointers for the loopback
+// ranks of one GPU).  A routing kernel appends each join row straight into
+// its owner's inbox (one system-scope cursor atomic per warp round and
+// destination, then coalesced peer stores); two device-side barriers per
+// iteration carry the overflow flags and the |Δ| sum, so the whole
+// partitioned fixpoint runs inside one CUDA graph with no host round trip.
+constexpr u32 kPeerVals = 4;
+struct PeerMail {
+    unsigned long long flag[64];        // flag[s] = last barrier epoch rank s reached
+    unsigned long long val[64][kPeerVals];  // rank s's payload of that barrier
+    unsigned long long cursor;          // rows appended to this rank's inbox this iteration
+    unsigned long long pad[7];
+};
+struct PeerTab {
+    u64* inbox[64];      // rank q's inbox, mapped here
+    u64 cap[64];         // its capacity (rows)
+    PeerMail* mail[64];  // rank q's mailbox, mapped here
+    u32 P, rank;
 };
 
 // Per-iteration history written by loop_end: rec[i * nheads + h] and the
@@ -208,6 +239,31 @@ void loop_part_advance(Ctx& c, LoopCtl* ctl, u32 final_step, u64 recv_rows, gd_i
 // counts; cursors zeroed).  Order inside a group is unspecified.
 void loop_owner_scatter(Ctx& c, const u64* keys, const u64* n_ptr, u32 P, const unsigned long long* offsets,
                         unsigned long long* cursors, u64* out);
+
+// ---- peer-memory partitioned loop ----
+// Routes the step's materialized rows (ctl.step_total of them) to their
+// owners' inboxes (owner = key_hash64(key) mod P).
+void loop_route_keys(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const u64* keys, const PeerTab* tab);
+// Warp-expanded final step over a dense inner, routed instead of inserted.
+void loop_expand_route(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const u64* inner,
+                       const DevJoin& jd, const LoopDense& dense, const LoopStepBufs& sb, u64 heavy_rows,
+                       const PeerTab* tab);
+struct PeerSyncDesc {
+    const PeerTab* tab;
+    u32 final_step, nsteps;
+    u64 log_cap, tab_limit;
+    u32 stamp_max;
+    gd_iter_record* hist;
+    u64 hist_cap;
+    unsigned long long cond;  // cudaGraphConditionalHandle
+    int use_cond;
+};
+// Barrier 1 (after routing): overflow consensus (rollback on every rank),
+// the received row count, the capacity gate of this rank's insert.
+void loop_peer_sync1(Ctx& c, cudaStream_t s, LoopCtl* ctl, const PeerSyncDesc& d);
+// Barrier 2 (after the insert): the iteration record, the Δ window, the
+// |Δ| sum (termination) and stall consensus; sets the while condition.
+void loop_peer_sync2(Ctx& c, cudaStream_t s, LoopCtl* ctl, const PeerSyncDesc& d);
 
 // ---- warp-expanded final step over a dense inner ----
 // loop_count: one read of the dense offsets per outer row, the candidate

@@ -213,6 +213,283 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
     }
 }
 
+// ---- pipelined onesweep (u64 keys) -------------------------------------------
+// Persistent CTAs (as many as are co-resident), each claiming tiles in
+// order: while a tile is ranked, looked back and written out, the CTA's
+// NEXT tile is already streaming into a second shared-memory buffer through
+// one bulk async copy (cp.async.bulk → UBLKCP, completion on an mbarrier),
+// so every CTA keeps 32 KB of reads in flight through its whole compute
+// phase instead of stalling on the load at the start of each tile.  Digits
+// are RB (8..10) bits wide: 46-bit C2 keys sort in 5 passes of ≤ 10 bits
+// instead of 6 of 8.  Per-warp digit counters are u16 pairs in one u32
+// word (a warp ranks ≤ 512 keys), so 8 warps × 1024 digits take 16 KB.
+// Thread t owns the DPT consecutive digits [t·DPT, (t+1)·DPT) for the
+// per-digit work (counts, scan, look-back: one DPT-wide vector load per
+// predecessor tile).  Stable in input order, as LSD requires.
+constexpr int kPT = 256;         // threads
+constexpr int kPI = 16;          // keys per thread
+constexpr int kPTile = kPT * kPI;  // 4096 keys, 32 KB
+constexpr int kPW = kPT / 32;
+
+template <int RB>
+struct PipeSmem {
+    static constexpr int R = 1 << RB;
+    u64 buf[2][kPTile];
+    u64 stage[kPTile];
+    u32 wh[kPW][R / 2];  // per-warp digit counters / offsets, u16 pairs
+    u32 dstart[R];
+    u64 gbase[R];
+    u32 scan[kPT / 32 + 1];
+    unsigned long long mbar[2];
+    u32 tile[2];
+};
+
+__device__ __forceinline__ u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* m) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(m)) : "memory");
+}
+
+// One thread: order this CTA's earlier generic-proxy accesses of the
+// buffer before the async copy overwrites it, arm the barrier with the
+// byte count and issue the bulk copy (bytes % 16 == 0, 16-byte aligned).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, u32 bytes, unsigned long long* m) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(m)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(m))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, u32 parity) {
+    const u32 a = smem_addr(m);
+    u32 done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+
+template <int DPT>
+struct DigitVec {
+    u32 v[DPT];
+};
+
+template <int DPT>
+__device__ __forceinline__ DigitVec<DPT> ld_status_vec(const u32* p) {
+    DigitVec<DPT> r;
+    if constexpr (DPT == 2) {
+        asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(r.v[0]), "=r"(r.v[1]) : "l"(p) : "memory");
+    } else {
+        asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3])
+                     : "l"(p)
+                     : "memory");
+    }
+    return r;
+}
+
+template <int DPT>
+__device__ __forceinline__ void st_status_vec(u32* p, const DigitVec<DPT>& r) {
+    if constexpr (DPT == 2) {
+        asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(r.v[0]), "r"(r.v[1]) : "memory");
+    } else {
+        asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(r.v[0]), "r"(r.v[1]),
+                     "r"(r.v[2]), "r"(r.v[3])
+                     : "memory");
+    }
+}
+
+template <int RB>
+__global__ void __launch_bounds__(kPT) onesweep_pipe_kernel(const u64* __restrict__ in, u64* __restrict__ out,
+                                                            u64 portion_begin, u64 portion_n, u32 shift, u32 width,
+                                                            const u64* __restrict__ digit_base,
+                                                            u64* __restrict__ next_base, u32* __restrict__ ws,
+                                                            u32 ntiles) {
+    constexpr int R = 1 << RB;
+    constexpr int DPT = R >= 1024 ? 4 : 2;  // digits per owner thread
+    constexpr int OWN = R / DPT;            // owner threads (128 / 256)
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    PipeSmem<RB>& sm = *reinterpret_cast<PipeSmem<RB>*>(smem_raw);
+    u32* counter = ws;
+    u32* status = ws + 4;  // 16-byte aligned statuses
+    const u32 t = threadIdx.x, warp = t >> 5, lane = lane_id();
+    const u32 dmask = (1u << width) - 1;
+    const u64* src = in + portion_begin;
+
+    auto issue = [&](u32 b, u32 tile) {
+        const u64 first = (u64)tile * kPTile;
+        const u32 n = (u32)min((u64)kPTile, portion_n - first);
+        const u32 bytes = (n * 8u) & ~15u;
+        if (bytes) bulk_load(sm.buf[b], src + first, bytes, &sm.mbar[b]);
+        else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&sm.mbar[b])) : "memory");
+    };
+
+    if (t == 0) {
+        mbar_init(&sm.mbar[0]);
+        mbar_init(&sm.mbar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const u32 first = atomicAdd(counter, 1u);
+        sm.tile[0] = first;
+        if (first < ntiles) issue(0, first);
+    }
+    u32 cur = 0, ph0 = 0, ph1 = 0;
+    while (true) {
+        __syncthreads();  // (A) previous tile fully written out; tile ids visible
+        const u32 tile = sm.tile[cur];
+        if (tile >= ntiles) break;
+        if (t == 0) {  // claim and prefetch the next tile into the other buffer
+            const u32 nx = atomicAdd(counter, 1u);
+            sm.tile[cur ^ 1] = nx;
+            if (nx < ntiles) issue(cur ^ 1, nx);
+        }
+        for (int i = t; i < kPW * (R / 2); i += kPT) (&sm.wh[0][0])[i] = 0;
+        const u64 tile_begin = (u64)tile * kPTile;
+        const u32 tile_n = (u32)min((u64)kPTile, portion_n - tile_begin);
+        mbar_wait(&sm.mbar[cur], cur ? ph1 : ph0);
+        if (cur) ph1 ^= 1;
+        else ph0 ^= 1;
+        u64* keys = sm.buf[cur];
+        if (t == 0 && (tile_n & 1)) keys[tile_n - 1] = src[tile_begin + tile_n - 1];
+        __syncthreads();  // (B) keys (incl. the odd tail key) and zeroed counters visible
+
+        // warp multi-split ranking, stable in (item, lane) order
+        u32 rank2[kPI / 2];
+#pragma unroll
+        for (int i = 0; i < kPI; ++i) {
+            const u32 idx = warp * (kPI * 32) + i * 32 + lane;
+            const u32 d = idx < tile_n ? (u32)(keys[idx] >> shift) & dmask : (u32)R;
+            const u32 peers = __match_any_sync(0xffffffffu, d);
+            const u32 leader = 31 - __clz(peers);
+            u32 base = 0;
+            if (lane == leader && d < (u32)R) {
+                const u32 sh = (d & 1) * 16;
+                base = (atomicAdd(&sm.wh[warp][d >> 1], (u32)__popc(peers) << sh) >> sh) & 0xffffu;
+            }
+            base = __shfl_sync(0xffffffffu, base, leader);
+            const u32 r = base + __popc(peers & lanemask_lt());
+            if (i & 1) rank2[i >> 1] |= r << 16;
+            else rank2[i >> 1] = r;
+        }
+        __syncthreads();  // (C)
+
+        // per-digit work: thread t < OWN owns digits [t*DPT, t*DPT + DPT)
+        DigitVec<DPT> cnt{};
+        u32 own_sum = 0;
+        if (t < (u32)OWN) {
+#pragma unroll
+            for (int q = 0; q < DPT; q += 2) {
+                const u32 w = (t * DPT + q) >> 1;
+                u32 c0 = 0, c1 = 0;
+#pragma unroll
+                for (int wp = 0; wp < kPW; ++wp) {
+                    const u32 v = sm.wh[wp][w];
+                    sm.wh[wp][w] = c0 | c1 << 16;
+                    c0 += v & 0xffffu;
+                    c1 += v >> 16;
+                }
+                cnt.v[q] = c0;
+                cnt.v[q + 1] = c1;
+                own_sum += c0 + c1;
+            }
+            DigitVec<DPT> pub;
+#pragma unroll
+            for (int q = 0; q < DPT; ++q) pub.v[q] = (tile == 0 ? kSFlagP : kSFlagA) | cnt.v[q];
+            st_status_vec<DPT>(status + (u64)tile * R + t * DPT, pub);
+        }
+        u32 total;
+        u32 dst0 = block_exclusive_scan<u32, kPT>(own_sum, total, sm.scan);
+        if (t < (u32)OWN) {
+            DigitVec<DPT> excl{};
+            if (tile > 0) {
+                constexpr int kWin = 8;
+                long long pred = (long long)tile - 1;
+                u32 pend = (1u << DPT) - 1;  // digits still looking back
+                while (pend) {
+                    DigitVec<DPT> s[kWin];
+#pragma unroll
+                    for (int w = 0; w < kWin; ++w) {
+                        if (pred - w >= 0) s[w] = ld_status_vec<DPT>(status + (u64)(pred - w) * R + t * DPT);
+                        else {
+#pragma unroll
+                            for (int q = 0; q < DPT; ++q) s[w].v[q] = kSFlagP;
+                        }
+                    }
+                    bool wait = false;
+#pragma unroll
+                    for (int q = 0; q < DPT; ++q) {
+                        if (!(pend >> q & 1)) continue;
+                        int first_inv = kWin, first_p = kWin;
+#pragma unroll
+                        for (int w = kWin - 1; w >= 0; --w) {
+                            const u32 f = s[w].v[q] >> 30;
+                            if (f == 0) first_inv = w;
+                            if (f == 2) first_p = w;
+                        }
+                        if (first_inv < first_p) {
+                            wait = true;
+                            break;
+                        }
+                    }
+                    if (wait) continue;  // an unpublished predecessor inside the window: reload
+#pragma unroll
+                    for (int q = 0; q < DPT; ++q) {
+                        if (!(pend >> q & 1)) continue;
+                        int first_p = kWin;
+#pragma unroll
+                        for (int w = kWin - 1; w >= 0; --w)
+                            if ((s[w].v[q] >> 30) == 2) first_p = w;
+#pragma unroll
+                        for (int w = 0; w < kWin; ++w)
+                            if (w <= first_p) excl.v[q] += s[w].v[q] & kSMask;
+                        if (first_p < kWin) pend &= ~(1u << q);
+                    }
+                    pred -= kWin;
+                }
+                DigitVec<DPT> pub;
+#pragma unroll
+                for (int q = 0; q < DPT; ++q) pub.v[q] = kSFlagP | (excl.v[q] + cnt.v[q]);
+                st_status_vec<DPT>(status + (u64)tile * R + t * DPT, pub);
+            }
+#pragma unroll
+            for (int q = 0; q < DPT; ++q) {
+                const u32 d = t * DPT + q;
+                const u64 b = digit_base[d];
+                sm.dstart[d] = dst0;
+                sm.gbase[d] = b + excl.v[q] - dst0;
+                if (tile == ntiles - 1 && next_base) next_base[d] = b + excl.v[q] + cnt.v[q];
+                dst0 += cnt.v[q];
+            }
+        }
+        __syncthreads();  // (D)
+
+        // scatter into shared memory in digit-sorted (stable) order
+#pragma unroll
+        for (int i = 0; i < kPI; ++i) {
+            const u32 idx = warp * (kPI * 32) + i * 32 + lane;
+            if (idx < tile_n) {
+                const u64 k = keys[idx];
+                const u32 d = (u32)(k >> shift) & dmask;
+                const u32 r = (rank2[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
+                const u32 wo = (sm.wh[warp][d >> 1] >> ((d & 1) * 16)) & 0xffffu;
+                sm.stage[sm.dstart[d] + wo + r] = k;
+            }
+        }
+        __syncthreads();  // (E)
+        for (u32 j = t; j < tile_n; j += kPT) {
+            const u64 k = sm.stage[j];
+            out[sm.gbase[(u32)(k >> shift) & dmask] + j] = k;
+        }
+        cur ^= 1;
+    }
+}
+
 }  // namespace
 
 // Keys per thread of a onesweep tile (4/8/16 are compiled;
@@ -232,9 +509,130 @@ void launch_onesweep(const Ctx& c, u64 tiles, const K* src, K* dst, u64 pb, u64 
                                                                           (u32)tiles);
 }
 
+// All passes' digit histograms for the pipelined sort: `width`-bit digits,
+// R bins per pass (warp-privatized copies as in radix_hist_kernel).
+__global__ void __launch_bounds__(256) radix_hist_w_kernel(const u64* __restrict__ keys, u64 n, int npass,
+                                                           u32 width, u32 nbits, int R, int copies,
+                                                           u64* __restrict__ hist) {
+    extern __shared__ u32 sh[];
+    const int words = npass * R;
+    for (int i = threadIdx.x; i < copies * words; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    u32* mine = sh + ((threadIdx.x >> 5) % copies) * words;
+    const u32 dmask = (1u << width) - 1;
+    constexpr int kU = 4;
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += kU * stride) {
+        u64 k[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const u64 i = i0 + u * stride;
+            k[u] = i < n ? __ldcs(keys + i) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (i0 + u * stride < n)
+                for (int p = 0; p < npass; ++p) {
+                    const u32 sh = p * width;
+                    const u32 m = sh + width <= nbits ? dmask : (1u << (nbits - sh)) - 1;  // last pass: narrower
+                    atomicAdd(&mine[p * R + ((u32)(k[u] >> sh) & m)], 1u);
+                }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < words; i += blockDim.x) {
+        u32 t = 0;
+        for (int c = 0; c < copies; ++c) t += sh[c * words + i];
+        if (t) atomicAdd(&hist[i], (u64)t);
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(R) radix_bases_w_kernel(const u64* __restrict__ hist, u64* __restrict__ bases) {
+    __shared__ u64 scan_tmp[R / 32 + 1];
+    const int pass = blockIdx.x;
+    u64 all;
+    bases[pass * R + threadIdx.x] = block_exclusive_scan<u64, R>(hist[pass * R + threadIdx.x], all, scan_tmp);
+}
+
+template <int RB>
+void launch_pipe(Ctx& c, const u64* src, u64* dst, u64 pb, u64 pn, u32 shift, u32 width, const u64* rd, u64* wr,
+                 u32* w) {
+    const size_t smem = sizeof(PipeSmem<RB>);
+    static int per_sm = -1;  // co-resident CTAs per SM (one device per process)
+    if (per_sm < 0) {
+        GD_CUDA(cudaFuncSetAttribute(onesweep_pipe_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_pipe_kernel<RB>, kPT, smem));
+        if (per_sm < 1) throw Error(GD_ERR_CUDA, "onesweep_pipe_kernel does not fit an SM");
+    }
+    const u64 tiles = (pn + kPTile - 1) / kPTile;
+    const u64 grid = std::min<u64>(tiles, (u64)per_sm * c.num_sms);
+    onesweep_pipe_kernel<RB><<<(unsigned)grid, kPT, smem, c.stream>>>(src, dst, pb, pn, shift, width, rd, wr, w,
+                                                                      (u32)tiles);
+}
+
+// Pipelined LSD sort of u64 keys (gd_device_config.sort_digit_bits > 8 or
+// sort_pipeline): npass = ceil(nbits / max_bits) passes of equal width.
+u64* radix_sort_pipe(Ctx& c, u64* a, u64* b, u64 n, u32 nbits) {
+    const u32 maxb = std::min<u32>(10, std::max<u32>(8, c.cfg.sort_digit_bits));
+    const int npass = (int)((nbits + maxb - 1) / maxb);
+    const u32 width = (nbits + npass - 1) / npass;
+    const int RB = width <= 8 ? 8 : width == 9 ? 9 : 10;
+    const int R = 1 << RB;
+    const int nportions = (int)((n + kPortion - 1) / kPortion);
+    const u64 hist_words = (u64)npass * R;
+    DevBuf<u64> hist(c, hist_words);
+    DevBuf<u64> bases(c, hist_words + 2 * R);
+    c.memset(hist.p, 0, hist_words * sizeof(u64));
+    {
+        const int grid = (int)std::min<u64>((u64)c.num_sms * 4, (n + 255) / 256);
+        cudaEvent_t t = c.prof_begin();
+        const int copies = hist_words * 4 * 2 <= 48 * 1024 ? 2 : 1;
+        radix_hist_w_kernel<<<grid, 256, (size_t)copies * hist_words * sizeof(u32), c.stream>>>(a, n, npass, width, nbits,
+                                                                                                R, copies, hist.p);
+        c.check_launch();
+        c.prof_end(t, KC_SORT_HIST, n * sizeof(u64));
+    }
+    if (R == 256) radix_bases_w_kernel<256><<<npass, 256, 0, c.stream>>>(hist.p, bases.p);
+    else if (R == 512) radix_bases_w_kernel<512><<<npass, 512, 0, c.stream>>>(hist.p, bases.p);
+    else radix_bases_w_kernel<1024><<<npass, 1024, 0, c.stream>>>(hist.p, bases.p);
+    c.check_launch();
+    u64* pp[2] = {bases.p + hist_words, bases.p + hist_words + R};
+    const u64 max_tiles = (std::min(n, kPortion) + kPTile - 1) / kPTile;
+    const u64 ws_words = 4 + max_tiles * R;
+    DevBuf<u32> ws(c, ws_words);
+    u64* src = a;
+    u64* dst = b;
+    for (int pass = 0; pass < npass; ++pass) {
+        const u32 shift = (u32)pass * width;
+        const u32 wd = std::min<u32>(width, nbits - shift);
+        for (int p = 0; p < nportions; ++p) {
+            const u64 pb = (u64)p * kPortion;
+            const u64 pn = std::min(kPortion, n - pb);
+            const u64 tiles = (pn + kPTile - 1) / kPTile;
+            c.memset(ws.p, 0, (4 + tiles * R) * sizeof(u32));
+            const u64* rd = p == 0 ? bases.p + (u64)pass * R : pp[(p - 1) & 1];
+            u64* wr = p + 1 < nportions ? pp[p & 1] : nullptr;
+            cudaEvent_t t = c.prof_begin();
+            if (RB == 8) launch_pipe<8>(c, src, dst, pb, pn, shift, wd, rd, wr, ws.p);
+            else if (RB == 9) launch_pipe<9>(c, src, dst, pb, pn, shift, wd, rd, wr, ws.p);
+            else launch_pipe<10>(c, src, dst, pb, pn, shift, wd, rd, wr, ws.p);
+            c.check_launch();
+            c.prof_end(t, KC_SORT_PASS, 2 * pn * sizeof(u64));
+        }
+        std::swap(src, dst);
+    }
+    return src;
+}
+
 template <typename K>
 K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
     if (n <= 1 || nbits == 0) return a;
+    if constexpr (sizeof(K) == 8) {
+        if (c.cfg.sort_pipeline && n >= c.cfg.sort_pipeline_min_keys)
+            return reinterpret_cast<K*>(radix_sort_pipe(c, reinterpret_cast<u64*>(a), reinterpret_cast<u64*>(b), n,
+                                                        nbits));
+    }
     const int npass = (int)((nbits + kRadixBits - 1) / kRadixBits);
     const int nportions = (int)((n + kPortion - 1) / kPortion);
     const int items = sort_items<K>(c);

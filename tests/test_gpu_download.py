@@ -1,7 +1,6 @@
 """Host download of large relations (engine.relation): packed keys cross
 PCIe and host threads unpack them (engine.cu download_packed); the rows
 must equal the device-unpack path and the numpy canonical form."""
-import os
 
 import numpy as np
 import pytest
@@ -28,14 +27,11 @@ def test_host_unpack_matches(ref, arity, n, hi):
     e = rng.integers(0, hi, size=(n, arity), dtype=np.uint64)
     outs = {}
     for mode in ("1", "0"):
-        os.environ["GD_HOST_UNPACK"] = mode
-        try:
+        with al.default_context().configured(host_unpack=int(mode)):
             g = al.engine(prog)
             g.load_edb("E", al.tuple_array(arity, e))
             g.run()
             outs[mode] = g.relation("C").data.copy()
-        finally:
-            os.environ.pop("GD_HOST_UNPACK", None)
     assert np.array_equal(outs["1"], outs["0"])
     assert np.array_equal(outs["1"].reshape(-1, arity), canonical(e))
 
@@ -62,13 +58,10 @@ def test_pinned_destination_direct_tail(ref, frac):
     want = canonical(e)
     assert n == len(want)
     pinned = torch.empty((n, 2), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
-    os.environ["GD_DL_DIRECT_FRAC"] = frac
-    try:
+    with g.ctx.configured(download_direct_frac=float(frac)):
         h0, d0 = g.ctx.transfer_bytes()
         g.ctx.check(g.ctx.lib.gd_engine_relation_download(g.h, rid, pinned.ctypes.data_as(C.c_void_p), n))
         h1, d1 = g.ctx.transfer_bytes()
-    finally:
-        os.environ.pop("GD_DL_DIRECT_FRAC", None)
     assert np.array_equal(pinned, want)
     nd = int(n * float(frac))
     assert d1 - d0 == (n - nd) * 8 + nd * 16  # packed head + unpacked direct tail

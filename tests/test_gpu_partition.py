@@ -92,19 +92,26 @@ def test_run_partitioned_nccl_single_rank(path):
         dist.destroy_process_group()
 
 
+EXCHANGES = {"peer": {"partition_exchange": 0}, "peer_eager": {"partition_exchange": 0, "loop_mode": 1},
+             "nccl": {"partition_exchange": 1}}
+
+
+@pytest.mark.parametrize("exchange", list(EXCHANGES))
 @pytest.mark.parametrize("prog,head,seed,n,dom", [("reach", "Reach", 31, 4000, 2500), ("sg", "SG", 32, 1500, 1000),
                                                   ("reach", "Reach", 33, 20000, 8000)])
-def test_native_driver_single_rank(prog, head, seed, n, dom):
-    """gd_engine_run_partitioned (the library's own NCCL exchanges, one
-    readback per iteration, device-side iteration records) over a one-rank
-    NCCL communicator: result, Δ history, iteration records and join count
+def test_native_driver_single_rank(prog, head, seed, n, dom, exchange):
+    """gd_engine_run_partitioned over a one-rank NCCL communicator, both
+    exchanges: "peer" (rows stored into the owner's inbox, device-side
+    barriers, the whole fixpoint one CUDA graph; "peer_eager" the same
+    kernels launched per iteration) and "nccl" (NCCL send/recv, one readback
+    per iteration): result, Δ history, iteration records and join count
     equal to the single engine."""
     from paper_2311_02206_b200.partition import NcclComm, run_partitioned_native
 
     rng = np.random.default_rng(seed)
     edges = random_relation(rng, 2, n, dom)
     ref = single(prog, edges)
-    ctx = al.Context(0)
+    ctx = al.Context(0, config=EXCHANGES[exchange])
     comm = NcclComm(ctx, 0, 1)
     try:
         e = al.engine(prog, ctx=ctx)
@@ -122,23 +129,28 @@ def test_native_driver_single_rank(prog, head, seed, n, dom):
         comm.close()
 
 
+@pytest.mark.parametrize("exchange", list(EXCHANGES))
 @pytest.mark.parametrize("tiny", [False, True])
 @pytest.mark.parametrize("prog,head,P,seed,n,dom", [
     ("reach", "Reach", 2, 41, 3000, 1500), ("reach", "Reach", 3, 42, 5000, 4000), ("reach", "Reach", 4, 43, 800, 300),
-    ("sg", "SG", 2, 44, 1500, 1000), ("sg", "SG", 3, 45, 2000, 2500),
+    ("sg", "SG", 2, 44, 1500, 1000), ("sg", "SG", 3, 45, 2000, 2500), ("reach", "Reach", 8, 46, 6000, 3000),
 ])
-def test_native_driver_multi_rank_loopback(prog, head, P, seed, n, dom, tiny):
+def test_native_driver_multi_rank_loopback(prog, head, P, seed, n, dom, tiny, exchange):
     """The native driver's multi-rank logic (counts / |Δ| / overflow triples,
     offsets, receive layout, collective redo on overflow, termination) with
     P ranks as threads of this process, each with its own context, stream
     and engine on the one GPU, exchanging through the loopback transport.
     tiny: every join buffer starts at its minimum, so ranks overflow at
-    different iterations and all must redo together."""
+    different iterations and all must redo together (peer exchange: inboxes
+    grow with a collective remap, full logs / indexes stall an insert that
+    the host finishes, the history buffer starts at one record).
+    The peer exchange's device barriers spin while the other ranks' graphs
+    run on the same GPU (one CTA each), so P ranks share it safely."""
     import threading
 
     from paper_2311_02206_b200.partition import LoopbackComms, run_partitioned_native
 
-    cfg = {"min_capacities": 1} if tiny else {}
+    cfg = dict(EXCHANGES[exchange], **({"min_capacities": 1} if tiny else {}))
     rng = np.random.default_rng(seed)
     edges = random_relation(rng, 2, n, dom)
     ref = single(prog, edges)

@@ -48,8 +48,10 @@ SCALE = {
                      parts=(2, 4, 8), host=True),
     "c3_sg_tree_w1000": dict(program="sg", head="SG", gen=lambda: W.sg_tree(1_000_001, 1000, 1),
                              parts=(2, 4), host=True),
+    # C5 (|Reach| 2.5e9, 20 GB of keys) on one B200: the resident loop with
+    # the invariants; two loopback shards of it do not fit one GPU's HBM
     "c5_tc_dag": dict(program="reach", head="Reach", gen=lambda: W.tc_dag(100_000_000, 100_000_000, 200, 1),
-                      parts=(2,), host=False),
+                      parts=(), host=False),
 }
 
 

@@ -146,9 +146,18 @@ typedef struct gd_device_config {
     int32_t warp_expand;            /* final steps over a dense inner: count + warp-expanded insert (1) */
     uint32_t sort_digit_bits;       /* pipelined sort: widest digit, 8..10 (10) */
     uint64_t heavy_rows;            /* ... rows with more outputs are expanded as segments of this many (4096) */
-    int32_t sort_pipeline;          /* u64 sorts: pipelined onesweep (bulk-copy prefetch, wide digits) (1) */
+    int32_t sort_pipeline;          /* u64 sorts: 0 classic onesweep; 1 pipelined (bulk-copy prefetch, wide
+                                       digits, ballot multi-split, keys staged in place); 2 the same with a
+                                       separate staging buffer; 3 in place with MATCH.ANY ranking;
+                                       4 classic onesweep with ballot ranking (1) */
     uint32_t partition_exchange;    /* gd_engine_run_partitioned: gd_partition_exchange (GD_EXCHANGE_PEER) */
     uint64_t sort_pipeline_min_keys; /* ... for sorts of at least this many keys (1 << 20) */
+    uint64_t temp_limit_rows;       /* resident loop: a chain temp above this many rows is materialized
+                                       in windows of at most this many (0: half the free HBM) */
+    uint32_t peer_timeout_ms;       /* peer exchange: a device barrier waiting longer fails the run with
+                                       GD_ERR_NCCL instead of hanging the GPU (60000) */
+    uint32_t insert_slots;          /* head-index inserts: slots of the 4-slot home bucket read at the
+                                       first probe, 1, 2 or 4 (2) */
 } gd_device_config;
 
 void gd_device_config_default(gd_device_config* cfg);
@@ -232,7 +241,7 @@ gd_status gd_canonicalize(gd_ctx* ctx, const uint64_t* rows, uint64_t n,
                           uint32_t arity, uint64_t* out, uint64_t* out_n);
 
 /* The sort inside canonicalize (tuple_array.hpp:73-133) on DEVICE keys:
- * LSD radix sort of n packed u64 keys on their low nbits bits (stable),
+ * LSD radix sort of n packed u64 keys, each < 2^nbits (stable),
  * d_tmp of n keys as scratch; *in_tmp = 1 when the sorted keys ended in
  * d_tmp, 0 when in d_keys.  Stream-ordered on the context stream. */
 gd_status gd_sort_keys_device(gd_ctx* ctx, uint64_t* d_keys, uint64_t* d_tmp, uint64_t n,

@@ -77,6 +77,9 @@ class gd_device_config(C.Structure):
         ("sort_pipeline", C.c_int32),
         ("partition_exchange", u32),
         ("sort_pipeline_min_keys", u64),
+        ("temp_limit_rows", u64),
+        ("peer_timeout_ms", u32),
+        ("insert_slots", u32),
     ]
 
 

@@ -217,6 +217,8 @@ _ENV_KNOBS = {
     "GD_SORT_DIGIT_BITS": ("sort_digit_bits", int),
     "GD_SORT_PIPE": ("sort_pipeline", int),
     "GD_SORT_PIPE_MIN": ("sort_pipeline_min_keys", int),
+    "GD_TEMP_LIMIT_ROWS": ("temp_limit_rows", int),
+    "GD_INSERT_SLOTS": ("insert_slots", int),
     "GD_PART_EXCHANGE": ("partition_exchange", lambda v: {"peer": 0, "nccl": 1}[v]),
 }
 

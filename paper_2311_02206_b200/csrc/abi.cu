@@ -279,6 +279,10 @@ gd_status gd_ctx_set_device_config(gd_ctx* ctx, const gd_device_config* cfg) {
         if (cfg->heavy_rows == 0) throw_config("heavy_rows must be positive");
         if (cfg->sort_digit_bits < 8 || cfg->sort_digit_bits > 10) throw_config("sort_digit_bits must be in [8, 10]");
         if (cfg->partition_exchange > GD_EXCHANGE_NCCL) throw_config("partition_exchange out of range");
+        if (cfg->sort_pipeline < 0 || cfg->sort_pipeline > 4) throw_config("sort_pipeline must be in [0, 4]");
+        if (cfg->peer_timeout_ms == 0) throw_config("peer_timeout_ms must be positive");
+        if (cfg->insert_slots != 1 && cfg->insert_slots != 2 && cfg->insert_slots != 4)
+            throw_config("insert_slots must be 1, 2 or 4");
         ctx->c->cfg = *cfg;
     });
 }

@@ -138,6 +138,9 @@ inline gd_device_config default_device_config() {
     d.sort_pipeline = 1;
     d.partition_exchange = GD_EXCHANGE_PEER;
     d.sort_pipeline_min_keys = 1u << 20;
+    d.temp_limit_rows = 0;
+    d.peer_timeout_ms = 60000;
+    d.insert_slots = 2;
     return d;
 }
 

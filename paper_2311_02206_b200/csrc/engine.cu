@@ -19,6 +19,7 @@
 #include <set>
 #include <atomic>
 #include <functional>
+#include <optional>
 #include <thread>
 #include <type_traits>
 #if defined(__x86_64__)
@@ -558,11 +559,13 @@ public:
     // ---- resident device loop (loop.h) ---------------------
     // Eligible when every recursive head is never a join inner (so its full
     // version is only probed for membership and read back at the end), keys
-    // are u64, one rank, no finite budget (budget_error must surface at the
-    // reference's charge: those runs keep the host-driven loop), and Δ = full
-    // (the state seed() leaves).
+    // are u64, one rank, and Δ = full (the state seed() leaves).  A finite
+    // memory budget is enforced by the bookkeeping replay after the device
+    // loop: the accountant sees the reference's charges in the reference's
+    // order, so a budget_error surfaces at the same charge with the same
+    // phase (the device work past that point is discarded with the error).
     bool loop_eligible(const std::vector<u32>& rec) {
-        if (E.nranks > 1 || E.cfg.memory_budget_bytes != Accountant::kUnlimited) return false;
+        if (E.nranks > 1) return false;
         if (!c.cfg.resident_loop) return false;
         if (rec.empty() || rec.size() > kLoopMaxHeads) return false;
         u32 nsteps = 0;
@@ -619,6 +622,7 @@ public:
         // clear = false: the caller writes every slot (loop_table_rehash)
         void alloc_tab(Ctx& c, u64 cap, bool dense = false, bool clear = true) {
             tab.release();
+            cap = std::max<u64>((cap + 3) & ~3ull, 4);  // whole 4-slot buckets (loop.cu hs_home)
             tab_cap = cap;
             tab_limit = dense ? cap / 4 * 3 : tab_limit_of(cap);
             tab = DevBuf<u64>(c, cap * loop_slot_bytes(sbits) / 8);
@@ -696,7 +700,8 @@ public:
                         loop_dense_build(c, L.inner, L.inner_n, iar, bits, L.dense, L.dv.lo, L.dv.span))
                         L.dv.off = L.dense.p;
                 }
-                L.xp = L.final && !L.split_insert && L.dv.off && c.cfg.warp_expand;
+                // split_insert + xp: warp expansion into the temp, then the insert kernel
+                L.xp = L.final && L.dv.off && c.cfg.warp_expand;
                 cur_ar = st.proj_arity;
                 for (u32 i = 0; i < kMaxArity; ++i) cur_perm[i] = i;
             }
@@ -863,7 +868,11 @@ public:
                 cudaEvent_t t = br();
                 if (L.select)
                     loop_select_insert(c, s, ctl.p, i, L.head, o, L.jd, bufs_of(L.head), e);
-                else if (L.xp)
+                else if (L.xp && L.split_insert) {
+                    loop_expand_temp(c, s, ctl.p, i, o, L.inner, L.jd, L.dv, L.bufs(), c.cfg.heavy_rows, L.temp.p,
+                                     L.temp_cap);
+                    loop_insert_keys(c, s, ctl.p, i, L.head, L.temp.p, bufs_of(L.head), e);
+                } else if (L.xp)
                     loop_expand_insert(c, s, ctl.p, i, L.head, o, L.inner, L.jd, L.dv, L.bufs(), c.cfg.heavy_rows,
                                        bufs_of(L.head), e);
                 else if (L.split_insert)
@@ -937,12 +946,244 @@ public:
             GD_CUDA(cudaGraphInstantiate(&exec, graph, 0));
         };
 
+        // After an overflow: grows what the kernels asked for (step buffers,
+        // head logs and indexes, history, stamp epoch); temps of chain steps
+        // stop at the temp limit (those steps then run in windows).
+        const u64 temp_limit = c.cfg.temp_limit_rows ? c.cfg.temp_limit_rows
+                                                     : std::max<u64>(1 << 20, c.available_bytes() / 2 / sizeof(u64));
+        double tlast = 0;
+        const bool trace = (c.cfg.trace & 1) != 0;
+        u64 windowed_iters = 0;
+        auto grow_after_overflow = [&]() {
+            for (u32 i = 0; i < ns; ++i)
+                if (!steps[i].final && hc->need_temp[i] > temp_limit) hc->need_temp[i] = temp_limit;
+            for (u32 i = 0; i < ns; ++i) {
+                LStep& L = steps[i];
+                if (hc->need_rows[i] > L.rows_cap) {
+                    L.rows_cap = hc->need_rows[i] + hc->need_rows[i] / 2;
+                    L.row_start = DevBuf<u64>(c, L.rows_cap);
+                    L.row_off = DevBuf<u64>(c, L.rows_cap);
+                }
+                if (hc->need_splits[i] > L.splits_cap) {
+                    L.splits_cap = hc->need_splits[i] + hc->need_splits[i] / 2;
+                    L.splits = DevBuf<u64>(c, L.splits_cap);
+                }
+                if (hc->need_temp[i] > L.temp_cap) {
+                    L.temp_cap = std::min<u64>(hc->need_temp[i] + hc->need_temp[i] / 2, L.final ? ~0ull : temp_limit);
+                    L.temp = DevBuf<u64>(c, L.temp_cap);
+                }
+                hc->need_rows[i] = hc->need_splits[i] = hc->need_temp[i] = 0;
+            }
+            for (u32 h = 0; h < nh; ++h) {
+                LHead& H = heads[h];
+                const u64 ln = hc->h[h].log_n;
+                cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+                auto tr = [&](const char* what, u64 a, u64 b2) {
+                    if (!trace) return;
+                    cudaEventRecord(ev1, c.stream);
+                    c.sync();
+                    const double t1 = Ctx::now_s();
+                    float gms = 0;
+                    cudaEventElapsedTime(&gms, ev0, ev1);
+                    fprintf(stderr, "[loop] iter %u %s %llu -> %llu: %.3f ms (gpu %.3f ms)\n", hc->iter, what,
+                            (unsigned long long)a, (unsigned long long)b2, (t1 - tlast) * 1e3, gms);
+                    tlast = t1;
+                    std::swap(ev0, ev1);
+                    cudaEventRecord(ev0, c.stream);
+                };
+                if (trace) {
+                    cudaEventCreate(&ev0);
+                    cudaEventCreate(&ev1);
+                    c.sync();
+                    tlast = Ctx::now_s();
+                    cudaEventRecord(ev0, c.stream);
+                }
+                // Growth is sized against free HBM (C5-scale runs): 2x
+                // for the log and 4x for the index when they fit, else
+                // the largest size that does (index load up to 3/4).
+                const u64 reserve = 1ull << 30;
+                if (hc->need_log[h] > H.log_cap) {
+                    const u64 need = hc->need_log[h];
+                    u64 avail = c.available_bytes();
+                    if (2 * need * sizeof(u64) + reserve > avail / 2) avail = c.available_bytes(true);
+                    const u64 fit = avail > reserve ? (avail - reserve) / sizeof(u64) : 0;
+                    const u64 cap = std::max(need + need / 16 + 1024, std::min(2 * need, fit));
+                    DevBuf<u64> nl(c, cap);
+                    if (ln) loop_copy_u64(c, nl.p, H.log.p, ln);
+                    H.log = std::move(nl);
+                    tr("log", H.log_cap, cap);
+                    H.log_cap = cap;
+                }
+                if (hc->need_tab[h] > H.tab_limit) {  // grow: stream the old table into the new
+                    const u64 need = hc->need_tab[h];
+                    const u64 sb = loop_slot_bytes(H.sbits);
+                    const u64 spill = (ln / 16 + (1u << 20)) * sizeof(u64);  // re-spread spill list
+                    u64 avail = c.available_bytes();
+                    // load 1/8 after a growth (index_growth: 4 / 6 / 8 / 12
+                    // measured on C1-C5, 8 best or within 1%)
+                    const u64 gf = c.cfg.index_growth;
+                    if (gf * need * sb + spill + reserve > avail / 2) avail = c.available_bytes(true);
+                    const u64 fit = avail > reserve + spill ? (avail - reserve - spill) / sb : 0;
+                    const u64 cap = std::min(gf * need, fit);  // load 1/gf after growth when it fits
+                    if (cap < need / 3 * 4 + 16)
+                        throw_budget("index", "device memory cannot hold the full-tuple index of " +
+                                                  std::to_string(need) + " keys");
+                    DevBuf<u64> old = std::move(H.tab);
+                    const u64 old_cap = H.tab_cap;
+                    H.alloc_tab(c, cap, cap < 2 * need, false);
+                    tr("tab-alloc", old_cap, H.tab_cap);
+                    loop_table_rehash(c, old.p, old_cap, H.tab.p, H.tab_cap, H.sbits, ln);
+                    tr("tab-rehash", old_cap, H.tab_cap);
+                } else if (hc->need_restamp) {
+                    loop_table_restamp(c, H.tab.p, H.tab_cap, H.sbits);
+                }
+                hc->need_log[h] = hc->need_tab[h] = 0;
+            }
+            if (hc->need_hist > hist_cap) {
+                const u64 cap = hc->need_hist;
+                DevBuf<gd_iter_record> r2(c, cap * nh);
+                DevBuf<u64> s2(c, cap * ns);
+                c.d2d(r2.p, hist_rec.p, hist_cap * nh * sizeof(gd_iter_record));
+                c.d2d(s2.p, hist_steps.p, hist_cap * ns * sizeof(u64));
+                hist_rec = std::move(r2);
+                hist_steps = std::move(s2);
+                hist_cap = cap;
+                hc->hist_cap = cap;
+            }
+            hc->need_hist = 0;
+            if (hc->need_restamp) hc->epoch_base = hc->iter;
+            hc->need_restamp = 0;
+        };
+        // One iteration with chain step `wi`'s temp materialized in windows of
+        // at most temp_limit rows (engine.hpp:401-484 charges
+        // the whole temp, and so does the replay: only device memory is
+        // bounded).  Eager launches: first every step outside wi's variant and
+        // that variant's steps up to wi's scan (their inserts gated as usual),
+        // then per window wi's temp window, the rest of the variant, its gate
+        // and insert; an overflow inside a window grows and redoes only that
+        // window (nothing of it was inserted).  The iteration ends on the
+        // device as in the graph (loop_end); step totals are the window sums.
+        auto windowed_iteration = [&](u32 wi) {
+            PhaseTimer tw(E, "join");
+            const LStep& W0 = steps[wi];
+            auto in_v = [&](u32 j) { return steps[j].plan == W0.plan && steps[j].var == W0.var; };
+            auto cand = [&](u32 i, bool temp) {
+                LStep& L = steps[i];
+                const LoopOuter o = outer_of(L);
+                if (L.select) {
+                    loop_select_cand(c, c.stream, ctl.p, i, o);
+                    return;
+                }
+                if (L.xp) {
+                    loop_count(c, c.stream, ctl.p, i, o, L.jd, L.dv, L.bufs(), c.cfg.heavy_rows, nullptr);
+                    return;
+                }
+                loop_probe(c, c.stream, ctl.p, i, o, L.jd, L.has_iv ? &L.iv : nullptr, L.dv, L.inner_n, L.bufs(),
+                           block_sums.p);
+                loop_scan(c, c.stream, ctl.p, i, o, L.bufs(), block_sums.p, nullptr);
+                if (temp && (!L.final || L.split_insert))
+                    loop_materialize_temp(c, c.stream, ctl.p, i, o, L.inner, L.jd, L.bufs(), L.temp.p, L.temp_cap);
+            };
+            auto gate_and_insert = [&](bool variant) {
+                LoopGateDesc g{};
+                g.stamp_max = 0xfffffffeu;
+                for (u32 i = 0; i < ns; ++i)
+                    if (steps[i].final && in_v(i) == variant) {
+                        g.final_step[g.nfinal] = i;
+                        g.final_head[g.nfinal] = steps[i].head;
+                        ++g.nfinal;
+                    }
+                for (u32 h = 0; h < nh; ++h) {
+                    g.log_cap[h] = heads[h].log_cap;
+                    g.tab_limit[h] = heads[h].tab_limit;
+                    if (heads[h].sbits) g.stamp_max = std::min<u32>(g.stamp_max, (1u << heads[h].sbits) - 1);
+                }
+                if (!g.nfinal) return;
+                loop_gate(c, c.stream, ctl.p, g);
+                for (u32 k = 0; k < g.nfinal; ++k) {
+                    const u32 i = g.final_step[k];
+                    LStep& L = steps[i];
+                    const LoopOuter o = outer_of(L);
+                    if (L.select)
+                        loop_select_insert(c, c.stream, ctl.p, i, L.head, o, L.jd, bufs_of(L.head), nullptr);
+                    else if (L.xp && L.split_insert) {
+                        loop_expand_temp(c, c.stream, ctl.p, i, o, L.inner, L.jd, L.dv, L.bufs(), c.cfg.heavy_rows,
+                                         L.temp.p, L.temp_cap);
+                        loop_insert_keys(c, c.stream, ctl.p, i, L.head, L.temp.p, bufs_of(L.head), nullptr);
+                    } else if (L.xp)
+                        loop_expand_insert(c, c.stream, ctl.p, i, L.head, o, L.inner, L.jd, L.dv, L.bufs(),
+                                           c.cfg.heavy_rows, bufs_of(L.head), nullptr);
+                    else if (L.split_insert)
+                        loop_insert_keys(c, c.stream, ctl.p, i, L.head, L.temp.p, bufs_of(L.head), nullptr);
+                    else
+                        loop_materialize_insert(c, c.stream, ctl.p, i, L.head, o, L.inner, L.jd, L.bufs(),
+                                                bufs_of(L.head), nullptr);
+                }
+            };
+            // Per-step counters of the steps about to run (again): the
+            // candidate counts accumulate atomically; finals keep their
+            // post-filter totals (inserted rows of earlier windows / phase A).
+            auto clear_steps = [&](bool phase_b) {
+                for (u32 j = 0; j < ns; ++j) {
+                    const bool runs = phase_b ? in_v(j) && j >= wi : !in_v(j) || j <= wi;
+                    if (!runs) continue;
+                    hc->step_cand[j] = hc->heavy_n[j] = 0;
+                    if (!steps[j].final) hc->step_total[j] = 0;
+                }
+            };
+            auto settle = [&](bool phase_b) {  // false: overflowed, grown, state cleared for a redo
+                c.d2h(hc, ctl.p, sizeof(LoopCtl));
+                c.sync();
+                if (!hc->overflow) return true;
+                grow_after_overflow();
+                hc->overflow = 0;
+                clear_steps(phase_b);
+                c.h2d(ctl.p, hc, sizeof(LoopCtl));
+                return false;
+            };
+            do {  // (A) everything outside the windowed part
+                for (u32 i = 0; i < ns; ++i)
+                    if (!in_v(i) || i <= wi) cand(i, i != wi);
+                gate_and_insert(false);
+            } while (!settle(false));
+            const u64 T = hc->step_cand[wi];
+            std::vector<u64> sums(ns, 0);
+            for (u64 w = 0; w < T;) {  // (B) the windows
+                const u64 hi = std::min(T, w + steps[wi].temp_cap);
+                for (u32 j = wi + 1; j < ns; ++j)
+                    if (in_v(j)) {
+                        hc->step_cand[j] = hc->heavy_n[j] = 0;
+                        if (!steps[j].final) hc->step_total[j] = 0;
+                    }
+                hc->step_total[wi] = 0;
+                hc->win_step = wi;
+                hc->win_lo = w;
+                hc->win_hi = hi;
+                c.h2d(ctl.p, hc, sizeof(LoopCtl));
+                loop_materialize_temp(c, c.stream, ctl.p, wi, outer_of(steps[wi]), steps[wi].inner, steps[wi].jd,
+                                      steps[wi].bufs(), steps[wi].temp.p, steps[wi].temp_cap);
+                for (u32 j = wi + 1; j < ns; ++j)
+                    if (in_v(j)) cand(j, true);
+                gate_and_insert(true);
+                if (!settle(true)) continue;
+                for (u32 j = wi; j < ns; ++j)
+                    if (in_v(j) && !steps[j].final) sums[j] += hc->step_total[j];
+                w = hi;
+            }
+            for (u32 j = wi; j < ns; ++j)
+                if (in_v(j) && !steps[j].final) hc->step_total[j] = sums[j];
+            hc->win_hi = hc->win_lo = 0;
+            c.h2d(ctl.p, hc, sizeof(LoopCtl));
+            loop_end(c, c.stream, ctl.p, LoopEndDesc{LoopHist{hist_rec.p, hist_steps.p, ns}, 0, 0});
+            c.d2h(hc, ctl.p, sizeof(LoopCtl));
+            c.sync();
+            ++windowed_iters;
+        };
+
         u64 rollbacks = 0;
         u32 done_iters = 0;
-        const bool trace = (c.cfg.trace & 1) != 0;
         std::vector<u64> prev_log_n(nh);
         for (u32 h = 0; h < nh; ++h) prev_log_n[h] = hc->h[h].log_n;
-        double tlast = 0;
         {
             PhaseTimer t(E, "join");
             for (;;) {
@@ -987,109 +1228,21 @@ public:
                 }
                 if (hc->overflow) {
                     // growth / restamp time is index (HISA) build time
-                    PhaseTimer tg(E, "index");
+                    std::optional<PhaseTimer> tg;
+                    tg.emplace(E, "index");
                     const double tblock = Ctx::now_s();
                     ++rollbacks;
-                    for (u32 i = 0; i < ns; ++i) {
-                        LStep& L = steps[i];
-                        if (hc->need_rows[i] > L.rows_cap) {
-                            L.rows_cap = hc->need_rows[i] + hc->need_rows[i] / 2;
-                            L.row_start = DevBuf<u64>(c, L.rows_cap);
-                            L.row_off = DevBuf<u64>(c, L.rows_cap);
-                        }
-                        if (hc->need_splits[i] > L.splits_cap) {
-                            L.splits_cap = hc->need_splits[i] + hc->need_splits[i] / 2;
-                            L.splits = DevBuf<u64>(c, L.splits_cap);
-                        }
-                        if (hc->need_temp[i] > L.temp_cap) {
-                            L.temp_cap = hc->need_temp[i] + hc->need_temp[i] / 2;
-                            L.temp = DevBuf<u64>(c, L.temp_cap);
-                        }
-                        hc->need_rows[i] = hc->need_splits[i] = hc->need_temp[i] = 0;
-                    }
-                    for (u32 h = 0; h < nh; ++h) {
-                        LHead& H = heads[h];
-                        const u64 ln = hc->h[h].log_n;
-                        cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-                        auto tr = [&](const char* what, u64 a, u64 b2) {
-                            if (!trace) return;
-                            cudaEventRecord(ev1, c.stream);
-                            c.sync();
-                            const double t1 = Ctx::now_s();
-                            float gms = 0;
-                            cudaEventElapsedTime(&gms, ev0, ev1);
-                            fprintf(stderr, "[loop] iter %u %s %llu -> %llu: %.3f ms (gpu %.3f ms)\n", hc->iter, what,
-                                    (unsigned long long)a, (unsigned long long)b2, (t1 - tlast) * 1e3, gms);
-                            tlast = t1;
-                            std::swap(ev0, ev1);
-                            cudaEventRecord(ev0, c.stream);
-                        };
-                        if (trace) {
-                            cudaEventCreate(&ev0);
-                            cudaEventCreate(&ev1);
-                            c.sync();
-                            tlast = Ctx::now_s();
-                            cudaEventRecord(ev0, c.stream);
-                        }
-                        // Growth is sized against free HBM (C5-scale runs): 2x
-                        // for the log and 4x for the index when they fit, else
-                        // the largest size that does (index load up to 3/4).
-                        const u64 reserve = 1ull << 30;
-                        if (hc->need_log[h] > H.log_cap) {
-                            const u64 need = hc->need_log[h];
-                            u64 avail = c.available_bytes();
-                            if (2 * need * sizeof(u64) + reserve > avail / 2) avail = c.available_bytes(true);
-                            const u64 fit = avail > reserve ? (avail - reserve) / sizeof(u64) : 0;
-                            const u64 cap = std::max(need + need / 16 + 1024, std::min(2 * need, fit));
-                            DevBuf<u64> nl(c, cap);
-                            if (ln) loop_copy_u64(c, nl.p, H.log.p, ln);
-                            H.log = std::move(nl);
-                            tr("log", H.log_cap, cap);
-                            H.log_cap = cap;
-                        }
-                        if (hc->need_tab[h] > H.tab_limit) {  // grow: stream the old table into the new
-                            const u64 need = hc->need_tab[h];
-                            const u64 sb = loop_slot_bytes(H.sbits);
-                            const u64 spill = (ln / 16 + (1u << 20)) * sizeof(u64);  // re-spread spill list
-                            u64 avail = c.available_bytes();
-                            // load 1/8 after a growth (index_growth: 4 / 6 / 8 / 12
-                            // measured on C1-C5, 8 best or within 1%)
-                            const u64 gf = c.cfg.index_growth;
-                            if (gf * need * sb + spill + reserve > avail / 2) avail = c.available_bytes(true);
-                            const u64 fit = avail > reserve + spill ? (avail - reserve - spill) / sb : 0;
-                            const u64 cap = std::min(gf * need, fit);  // load 1/gf after growth when it fits
-                            if (cap < need / 3 * 4 + 16)
-                                throw_budget("index", "device memory cannot hold the full-tuple index of " +
-                                                          std::to_string(need) + " keys");
-                            DevBuf<u64> old = std::move(H.tab);
-                            const u64 old_cap = H.tab_cap;
-                            H.alloc_tab(c, cap, cap < 2 * need, false);
-                            tr("tab-alloc", old_cap, H.tab_cap);
-                            loop_table_rehash(c, old.p, old_cap, H.tab.p, H.tab_cap, H.sbits, ln);
-                            tr("tab-rehash", old_cap, H.tab_cap);
-                        } else if (hc->need_restamp) {
-                            loop_table_restamp(c, H.tab.p, H.tab_cap, H.sbits);
-                        }
-                        hc->need_log[h] = hc->need_tab[h] = 0;
-                    }
-                    if (hc->need_hist > hist_cap) {
-                        const u64 cap = hc->need_hist;
-                        DevBuf<gd_iter_record> r2(c, cap * nh);
-                        DevBuf<u64> s2(c, cap * ns);
-                        c.d2d(r2.p, hist_rec.p, hist_cap * nh * sizeof(gd_iter_record));
-                        c.d2d(s2.p, hist_steps.p, hist_cap * ns * sizeof(u64));
-                        hist_rec = std::move(r2);
-                        hist_steps = std::move(s2);
-                        hist_cap = cap;
-                        hc->hist_cap = cap;
-                    }
-                    hc->need_hist = 0;
-                    if (hc->need_restamp) hc->epoch_base = hc->iter;
-                    hc->need_restamp = 0;
+                    // a chain temp above the limit: this iteration runs in windows
+                    u32 wstep = UINT32_MAX;
+                    for (u32 i = 0; i < ns; ++i)
+                        if (!steps[i].final && hc->need_temp[i] > temp_limit && wstep == UINT32_MAX) wstep = i;
+                    grow_after_overflow();
                     hc->overflow = 0;
                     c.h2d(ctl.p, hc, sizeof(LoopCtl));
                     c.sync();
                     destroy_graph();
+                    tg.reset();
+                    if (wstep != UINT32_MAX) windowed_iteration(wstep);
                     if (trace)
                         fprintf(stderr, "[loop] iter %u rollback block %.3f ms (meminfo total %.3f ms, alloc total %.3f ms)\n",
                                 hc->iter, (Ctx::now_s() - tblock) * 1e3, c.meminfo_seconds * 1e3,
@@ -1102,6 +1255,8 @@ public:
         destroy_graph();
         if (cap_stream) cudaStreamDestroy(cap_stream);
         (void)rollbacks;
+        if (trace && windowed_iters)
+            fprintf(stderr, "[loop] %llu iterations ran with windowed chain temps\n", (unsigned long long)windowed_iters);
 
         // replay the reference's bookkeeping from the device history
         const u64 iters = hc->iter;
@@ -1762,7 +1917,7 @@ public:
         grow_hist(hist0 + (tiny ? 1 : 1024));
         hc->part_epoch = 0;
         hc->part_join = 0;
-        hc->part_over = hc->part_stall = hc->part_stall_any = hc->part_inbox_over = 0;
+        hc->part_over = hc->part_stall = hc->part_stall_any = hc->part_inbox_over = hc->part_timeout = 0;
         hc->overflow = hc->done = 0;
         c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
 
@@ -1786,6 +1941,7 @@ public:
             d.hist_cap = P.hist_cap;
             d.cond = cond;
             d.use_cond = use_cond ? 1 : 0;
+            d.timeout_ns = (u64)c.cfg.peer_timeout_ms * 1000000ull;
             for (u32 i = 0; i < ns; ++i) {
                 LStep& L = P.steps[i];
                 const LoopOuter o = outer_of(L);
@@ -1866,6 +2022,10 @@ public:
             c.sync();
             if (!eager) c.launches += kernels_per_iter * (hc->iter - done_iters + (hc->part_over ? 1 : 0));
             done_iters = hc->iter;
+            if (hc->part_timeout)
+                throw Error(GD_ERR_NCCL, "partitioned loop: a peer did not reach the device barrier within " +
+                                             std::to_string(c.cfg.peer_timeout_ms) + " ms (rank " +
+                                             std::to_string(comm.rank) + ", iteration " + std::to_string(hc->iter) + ")");
             if (hc->part_over) {  // every rank rolled the iteration back: grow, remap, rerun
                 for (u32 i = 0; i < ns; ++i) {
                     LStep& L = P.steps[i];

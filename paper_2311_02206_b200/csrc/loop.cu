@@ -59,17 +59,25 @@ __device__ __forceinline__ void resolve(const LoopOuter& o, const LoopCtl* ctl, 
     }
 }
 
-__device__ __forceinline__ u64 hs_home(u64 key, u64 cap) { return __umul64hi(fmix64(key ^ kHashSeed), cap); }
+// Home of a key: the first slot of its 4-slot bucket (one 32-byte sector of
+// packed slots; table capacities are multiples of 4).  Probing is linear
+// from the bucket start, so one sector read settles a key unless its whole
+// bucket is taken by other keys.  Homes are monotone in the hash (the zone
+// growth pass relies on it).
+__device__ __forceinline__ u64 hs_home(u64 key, u64 cap) {
+    return __umul64hi(fmix64(key ^ kHashSeed), cap) & ~3ull;
+}
 
 // Rare paths of a packed-slot insertion, out of line (register pressure of
 // the batched fast path): the key was seen in an earlier iteration (stamp
 // update), or its home slot holds another key (linear probing, kScan slots
-// read per round trip).  o = the value the home-slot CAS returned.
-// Returns bit 0 = new key, bit 1 = first occurrence this iteration.
-__device__ __noinline__ u32 insert_slow_packed(u64* __restrict__ tab, u64 cap, u32 sb, u64 st, u64 key, u64 o) {
+// read per round trip).  p = the slot reached, o = its current value (a
+// CAS's return or the bucket read: another key, or this key with an older
+// stamp).  Returns bit 0 = new key, bit 1 = first occurrence this iteration.
+__device__ __noinline__ u32 insert_slow_packed(u64* __restrict__ tab, u64 cap, u32 sb, u64 st, u64 key, u64 p,
+                                               u64 o) {
     const u64 smask = (1ull << sb) - 1;
     const u64 want = key << sb | st;
-    u64 p = hs_home(key, cap);
     while (true) {
         if (o == kEmptySlot) return 3;
         if ((o >> sb) == key) {
@@ -121,34 +129,76 @@ __device__ __noinline__ u32 insert_slow_wide(HSlot* __restrict__ tab, u64 cap, u
 // fresh: bit k = key k is new (appended by the caller); first: bit k = first
 // occurrence of key k in this iteration (stamp st) — the distinct count of
 // the join output.
-template <int PER>
+template <int PER, int NSLOT = 2>
 __device__ __forceinline__ void hs_insert(const LoopHeadBufs& hb, u32 st, const u64 (&key)[PER], u32 ok,
                                           u32& fresh, u32& first) {
+    static_assert(NSLOT == 1 || NSLOT == 2 || NSLOT == 4, "bucket reads of 1, 2 or 4 slots");
     fresh = first = 0;
     u64 old[PER];
     if (hb.sbits) {
         u64* tab = static_cast<u64*>(hb.tab);
         const u32 sb = hb.sbits;
-        // Load the home slots first, then CAS only the empty ones: the CAS
-        // hits the line the load brought into L2, and random inserts run at
-        // the random-load rate (37 G/s) instead of the CAS-miss rate (22 G/s)
-        // on B200 (profiles/r1_micro_random_access_loadcas_b200.txt).
-        u64 home[PER];
+        // Read the first NSLOT slots of every key's home bucket (16-byte
+        // loads inside one 32-byte sector) first — all of a thread's reads in
+        // flight together — then settle each key there: its own slot (seen
+        // before), or the first empty slot, claimed with one CAS that hits
+        // the line the read brought into L2.  Only keys whose slots read are
+        // all taken by other keys, or whose CAS lost a race, probe further
+        // (out of line).
+        u64 pos[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) pos[k] = hs_home(key[k], hb.tab_cap);
+        constexpr int NV = NSLOT > 1 ? NSLOT / 2 : 1;  // 16-byte vectors (or one 8-byte slot)
+        ulonglong2 b[PER][NV];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-            home[k] = hs_home(key[k], hb.tab_cap);
-            old[k] = (ok >> k & 1) ? __ldcg(&tab[home[k]]) : 0ull;
+            const ulonglong2* q = reinterpret_cast<const ulonglong2*>(tab + pos[k]);
+#pragma unroll
+            for (int h = 0; h < NV; ++h) {
+                if (NSLOT == 1) b[k][h].x = (ok >> k & 1) ? __ldcg(tab + pos[k]) : 0ull;
+                else b[k][h] = (ok >> k & 1) ? __ldcg(q + h) : make_ulonglong2(0, 0);
+            }
+        }
+        u32 cas = 0, slow = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            if (!(ok >> k & 1)) continue;
+            u64 w[NSLOT];
+#pragma unroll
+            for (int h = 0; h < NV; ++h) {
+                w[2 * h] = b[k][h].x;
+                if (NSLOT > 1) w[(2 * h + 1) % NSLOT] = b[k][h].y;
+            }
+            u32 q = NSLOT;
+            bool empty = false;
+#pragma unroll
+            for (int j = NSLOT - 1; j >= 0; --j)  // first slot holding the key or empty
+                if (w[j] == kEmptySlot || (w[j] >> sb) == key[k]) {
+                    q = j;
+                    empty = w[j] == kEmptySlot;
+                }
+            if (q == NSLOT) {  // slots read all hold other keys: probe on from the last one
+                pos[k] += NSLOT - 1;
+                old[k] = w[NSLOT - 1];
+                slow |= 1u << k;
+            } else {
+                pos[k] += q;
+                old[k] = w[q];
+                if (empty) cas |= 1u << k;
+                else if (w[q] != (key[k] << sb | st)) slow |= 1u << k;  // seen before: stamp update
+            }
         }
 #pragma unroll
         for (int k = 0; k < PER; ++k)
-            if ((ok >> k & 1) && old[k] == kEmptySlot) old[k] = atomicCAS(&tab[home[k]], kEmptySlot, key[k] << sb | st);
+            if (cas >> k & 1) old[k] = atomicCAS(&tab[pos[k]], kEmptySlot, key[k] << sb | st);
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             if (!(ok >> k & 1)) continue;
             u32 r;
-            if (old[k] == kEmptySlot) r = 3;
-            else if (old[k] == (key[k] << sb | st)) r = 0;
-            else r = insert_slow_packed(tab, hb.tab_cap, sb, st, key[k], old[k]);
+            if ((cas >> k & 1) && old[k] == kEmptySlot) r = 3;
+            else if (!(cas >> k & 1) && !(slow >> k & 1)) r = 0;  // already stamped this iteration
+            else if ((cas >> k & 1) && old[k] == (key[k] << sb | st)) r = 0;
+            else r = insert_slow_packed(tab, hb.tab_cap, sb, st, key[k], pos[k], old[k]);
             fresh |= (r & 1u) << k;
             first |= (r >> 1) << k;
         }
@@ -508,25 +558,45 @@ __global__ void __launch_bounds__(kLT) loop_materialize_temp_kernel(LoopCtl* ctl
     u64 n;
     resolve(o, ctl, outer, n);
     const u64 total = ctl->step_cand[step];
-    if (total > temp_cap) {
+    // output window [wlo, whi) (windowed iteration) or everything
+    const bool win = ctl->win_hi != 0 && ctl->win_step == step;
+    const u64 wlo = win ? ctl->win_lo : 0, whi = win ? min(ctl->win_hi, total) : total;
+    if (whi - wlo > temp_cap) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
-            ctl->need_temp[step] = total;
+            ctl->need_temp[step] = whi - wlo;
             ctl->overflow = 1;
         }
         return;
     }
-    if (jd.nfilters == 0 && blockIdx.x == 0 && threadIdx.x == 0) ctl->step_total[step] = total;
-    if (total == 0) return;
-    const u64 ntiles = (n + total + kLoopMatTile - 1) / kLoopMatTile;
-    for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (jd.nfilters == 0 && blockIdx.x == 0 && threadIdx.x == 0) ctl->step_total[step] = whi - wlo;
+    if (whi <= wlo) return;
+    // tiles holding the window's outputs: output j lies on merge-path
+    // diagonal j + (rows ended before it) = j + #{r : off[r+1] <= j}
+    u64 t_lo = 0, t_hi = (n + total + kLoopMatTile - 1) / kLoopMatTile;
+    if (win) {
+        auto rows_before = [&](u64 j) {  // #{r < n : row_off[r+1] <= j}
+            u64 lo = 0, hi = n;
+            while (lo < hi) {
+                const u64 mid = (lo + hi) >> 1;
+                if (sb.row_off[mid + 1] <= j) lo = mid + 1;
+                else hi = mid;
+            }
+            return lo;
+        };
+        t_lo = (wlo + rows_before(wlo)) / kLoopMatTile;
+        t_hi = min(t_hi, (whi - 1 + rows_before(whi - 1)) / kLoopMatTile + 1);
+    }
+    for (u64 tile = t_lo + blockIdx.x; tile < t_hi; tile += gridDim.x) {
         u64 b0, b1;
         u32 rcount;
         if (!stage_tile(sm, tile, outer, n, total, sb, b0, b1, rcount)) continue;
+        b0 = max(b0, wlo);
+        b1 = min(b1, whi);
         if (jd.nfilters == 0) {
             for (u64 j = b0 + threadIdx.x; j < b1; j += kLT) {
                 const u32 r = row_of(sm, rcount, j);
                 const u64 i = inner[sm.start[r] + (j - sm.off[r])];
-                temp[j] = project(jd, sm.outer[r], i);
+                temp[j - wlo] = project(jd, sm.outer[r], i);
             }
             continue;
         }
@@ -635,6 +705,7 @@ __device__ __forceinline__ void flush_counts(LoopCtl* ctl, u32 head, u32 step, u
 // read-modify-write rate of HBM.
 // 6 CTAs/SM (40 registers, a few spills) measured fastest on C2: 94 ms vs
 // 100 ms at 5 CTAs (48 registers) and 120 ms at 8 CTAs (32 registers).
+template <int NS>
 __global__ void __launch_bounds__(kLT, 6) loop_materialize_insert_kernel(
     LoopCtl* ctl, u32 step, u32 head, LoopOuter o, const u64* __restrict__ inner, DevJoin jd, LoopStepBufs sb,
     LoopHeadBufs hb, LoopEndDesc e, int do_end) {
@@ -670,7 +741,7 @@ __global__ void __launch_bounds__(kLT, 6) loop_materialize_insert_kernel(
                 }
             }
             u32 fresh, first;
-            hs_insert<kPer>(hb, it, key, ok, fresh, first);
+            hs_insert<kPer, NS>(hb, it, key, ok, fresh, first);
             J += __popc(ok);
             N += __popc(first);
             D += __popc(fresh);
@@ -686,6 +757,7 @@ __global__ void __launch_bounds__(kLT, 6) loop_materialize_insert_kernel(
 // (the random-CAS rate needs ~8 K in flight per SM; a fused materialize
 // kernel holds too many registers to get there).
 constexpr int kInsPer = 8;
+template <int NS>
 __global__ void __launch_bounds__(kLT, 4) loop_insert_keys_kernel(LoopCtl* ctl, u32 step, u32 head,
                                                                   const u64* __restrict__ keys, LoopHeadBufs hb,
                                                                   LoopEndDesc e, int do_end) {
@@ -708,7 +780,7 @@ __global__ void __launch_bounds__(kLT, 4) loop_insert_keys_kernel(LoopCtl* ctl, 
                 ok |= (u32)(j < n) << k;
             }
             u32 fresh, first;
-            hs_insert<kInsPer>(hb, it, key, ok, fresh, first);
+            hs_insert<kInsPer, NS>(hb, it, key, ok, fresh, first);
             J += __popc(ok);
             N += __popc(first);
             D += __popc(fresh);
@@ -719,6 +791,7 @@ __global__ void __launch_bounds__(kLT, 4) loop_insert_keys_kernel(LoopCtl* ctl, 
     if (do_end && last_cta(ctl, &s_flag) && threadIdx.x == 0) end_body(ctl, e);
 }
 
+template <int NS>
 __global__ void __launch_bounds__(kLT) loop_select_insert_kernel(LoopCtl* ctl, u32 step, u32 head, LoopOuter o,
                                                                  DevJoin jd, LoopHeadBufs hb, LoopEndDesc e,
                                                                  int do_end) {
@@ -739,7 +812,7 @@ __global__ void __launch_bounds__(kLT) loop_select_insert_kernel(LoopCtl* ctl, u
             const u32 ok = r < n && passes(jd, outer[r], 0ull) ? 1u : 0u;
             if (ok) key[0] = project(jd, outer[r], 0ull);
             u32 fresh, first;
-            hs_insert<1>(hb, it, key, ok, fresh, first);
+            hs_insert<1, NS>(hb, it, key, ok, fresh, first);
             J += ok;
             N += first;
             D += fresh;
@@ -832,6 +905,7 @@ struct XWarp {
 
 // Sink of the warp expansion: inserts buf[0, m) (m <= kXRound) into the
 // head's index and appends the new keys to the log.
+template <int NS>
 struct InsertSink {
     LoopHeadBufs hb;
     u32 it;
@@ -848,7 +922,7 @@ struct InsertSink {
             ok |= (u32)(idx < m) << k;
         }
         u32 fresh, first;
-        hs_insert<kXPer>(hb, it, key, ok, fresh, first);
+        hs_insert<kXPer, NS>(hb, it, key, ok, fresh, first);
         w.N += __popc(first);
         w.D += __popc(fresh);
         u32 mk[kXPer];
@@ -867,6 +941,23 @@ struct InsertSink {
             if (fresh >> k & 1) hb.log[base + __popc(mk[k] & lt)] = key[k];
             base += __popc(mk[k]);
         }
+        __syncwarp();
+    }
+};
+
+// Sink of the split final step: buf[0, m) is appended to the step's temp
+// (one atomic per round on the step's row count, coalesced stores); the
+// insert runs as its own kernel (loop_insert_keys) over the temp.
+struct TempSink {
+    u64* temp;
+    unsigned long long* total;
+    __device__ __forceinline__ void round(XWarp& w, u32 m) {
+        __syncwarp();
+        const u32 lane = lane_id();
+        unsigned long long base = 0;
+        if (lane == 0 && m) base = atomicAdd(total, (unsigned long long)m);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (u32 i = lane; i < m; i += 32) temp[base + i] = w.buf[i];
         __syncwarp();
     }
 };
@@ -1005,6 +1096,7 @@ __device__ __forceinline__ void expand_rows(const LoopCtl* ctl, u32 step, const 
     if (w.fill) sink.round(w, w.fill);
 }
 
+template <int NS>
 __global__ void __launch_bounds__(kLT, 3) loop_expand_insert_kernel(
     LoopCtl* ctl, u32 step, u32 head, LoopOuter o, const u64* __restrict__ inner, DevJoin jd, LoopDense dv,
     LoopStepBufs sb, u64 heavy_min, LoopHeadBufs hb, LoopEndDesc e, int do_end) {
@@ -1015,13 +1107,38 @@ __global__ void __launch_bounds__(kLT, 3) loop_expand_insert_kernel(
         const u64* outer;
         u64 n;
         resolve(o, ctl, outer, n);
-        InsertSink sink{hb, ctl->iter + 1 - ctl->epoch_base,
+        InsertSink<NS> sink{hb, ctl->iter + 1 - ctl->epoch_base,
                         reinterpret_cast<unsigned long long*>(&ctl->h[head].log_n)};
         XWarp w{sbuf[threadIdx.x >> 5], 0, 0, 0, 0};
         expand_rows(ctl, step, outer, n, inner, jd, dv, sb, heavy_min, w, sink);
         flush_counts(ctl, head, step, w.J, w.N, w.D, red);
     }
     if (do_end && last_cta(ctl, &s_flag) && threadIdx.x == 0) end_body(ctl, e);
+}
+
+// Warp expansion into the step's temp (split final step): the capacity is
+// checked against the exact candidate count first (outputs <= candidates).
+__global__ void __launch_bounds__(kLT, 3) loop_expand_temp_kernel(LoopCtl* ctl, u32 step, LoopOuter o,
+                                                                  const u64* __restrict__ inner, DevJoin jd,
+                                                                  LoopDense dv, LoopStepBufs sb, u64 heavy_min,
+                                                                  u64* __restrict__ temp, u64 temp_cap) {
+    __shared__ u64 sbuf[kLT / 32][kXBuf];
+    __shared__ u32 s_flag;
+    if (cta_stopped(ctl, &s_flag)) return;
+    const u64 cand = ctl->step_cand[step];
+    if (cand > temp_cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctl->need_temp[step] = cand;
+            ctl->overflow = 1;
+        }
+        return;
+    }
+    const u64* outer;
+    u64 n;
+    resolve(o, ctl, outer, n);
+    TempSink sink{temp, reinterpret_cast<unsigned long long*>(&ctl->step_total[step])};
+    XWarp w{sbuf[threadIdx.x >> 5], 0, 0, 0, 0};
+    expand_rows(ctl, step, outer, n, inner, jd, dv, sb, heavy_min, w, sink);
 }
 
 __global__ void __launch_bounds__(kLT, 3) loop_expand_route_kernel(LoopCtl* ctl, u32 step, LoopOuter o,
@@ -1072,10 +1189,18 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     return v;
 }
 
+__device__ __forceinline__ u64 global_ns() {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // Publishes `val` to every rank's mailbox slot of this rank, then waits
 // until every rank reached the same epoch; out[s] = rank s's payload.
-__device__ void peer_barrier(const PeerTab* tab, u64 epoch, const u64 (&val)[kPeerVals],
-                             u64 (&out)[kLoopMaxRanks][kPeerVals]) {
+// Returns false when a rank did not arrive within timeout_ns (a dead peer
+// must not hang the GPU: the caller stops the graph, the host reports it).
+__device__ bool peer_barrier(const PeerTab* tab, u64 epoch, const u64 (&val)[kPeerVals],
+                             u64 (&out)[kLoopMaxRanks][kPeerVals], u64 timeout_ns) {
     const u32 P = tab->P, me = tab->rank;
     for (u32 q = 0; q < P; ++q) {
         PeerMail* m = tab->mail[q];
@@ -1085,11 +1210,16 @@ __device__ void peer_barrier(const PeerTab* tab, u64 epoch, const u64 (&val)[kPe
     __threadfence_system();
     for (u32 q = 0; q < P; ++q) st_release_sys(&tab->mail[q]->flag[me], epoch);
     PeerMail* mine = tab->mail[me];
+    const u64 t0 = global_ns();
     for (u32 s = 0; s < P; ++s) {
-        while (ld_acquire_sys(&mine->flag[s]) < epoch) __nanosleep(64);
+        while (ld_acquire_sys(&mine->flag[s]) < epoch) {
+            __nanosleep(64);
+            if (global_ns() - t0 > timeout_ns) return false;
+        }
 #pragma unroll
         for (u32 k = 0; k < kPeerVals; ++k) out[s][k] = __ldcv(&mine->val[s][k]);
     }
+    return true;
 }
 
 __global__ void loop_peer_sync1_kernel(LoopCtl* ctl, PeerSyncDesc d) {
@@ -1104,7 +1234,12 @@ __global__ void loop_peer_sync1_kernel(LoopCtl* ctl, PeerSyncDesc d) {
     ctl->part_epoch = epoch;
     const u64 mine[kPeerVals] = {(u64)(ctl->overflow | ctl->part_inbox_over), 0, 0, 0};
     __shared__ u64 got[kLoopMaxRanks][kPeerVals];
-    peer_barrier(tab, epoch, mine, got);
+    if (!peer_barrier(tab, epoch, mine, got, d.timeout_ns)) {
+        ctl->part_timeout = 1;
+        ctl->overflow = 1;
+        if (d.use_cond) cudaGraphSetConditional(cond, 0);
+        return;
+    }
     u64 any = 0;
     for (u32 s = 0; s < tab->P; ++s) any |= got[s][0];
     const u64 recv = ld_acquire_sys(&tab->mail[tab->rank]->cursor);
@@ -1152,7 +1287,11 @@ __global__ void loop_peer_sync2_kernel(LoopCtl* ctl, PeerSyncDesc d) {
     ctl->part_epoch = epoch;
     const u64 mine[kPeerVals] = {D, (u64)stall, 0, 0};
     __shared__ u64 got[kLoopMaxRanks][kPeerVals];
-    peer_barrier(tab, epoch, mine, got);
+    if (!peer_barrier(tab, epoch, mine, got, d.timeout_ns)) {
+        ctl->part_timeout = 1;
+        if (d.use_cond) cudaGraphSetConditional(cond, 0);
+        return;
+    }
     u64 gD = 0, any_stall = 0;
     for (u32 s = 0; s < tab->P; ++s) {
         gD += got[s][0];
@@ -1453,7 +1592,7 @@ int occupancy(Kern k, size_t smem = 0) {
 }
 
 int g_occ_temp = 0, g_occ_insert = 0, g_occ_select = 0, g_occ_keys = 0, g_occ_expand = 0, g_occ_xroute = 0,
-    g_occ_route = 0;
+    g_occ_route = 0, g_occ_xtemp = 0;
 // Insert grid = waves x resident CTAs: CTAs beyond the resident set start as
 // others finish, so the hardware balances the iteration's tiles.  Large
 // relations (log capacity >= kWideLog rows) run 3 waves (C2 -2.8%, SG
@@ -1465,15 +1604,24 @@ constexpr u64 kWideLog = 64ull << 20;
 
 int loop_grid(const Ctx& c) { return c.num_sms * 4; }
 
+// Slots read per key at the first probe (gd_device_config.insert_slots).
+#define SLOT_DISPATCH(c, kern, ...)                                      \
+    do {                                                                 \
+        if ((c).cfg.insert_slots == 1) kern<1> __VA_ARGS__;              \
+        else if ((c).cfg.insert_slots == 4) kern<4> __VA_ARGS__;         \
+        else kern<2> __VA_ARGS__;                                        \
+    } while (0)
+
 void loop_prepare() {
     if (g_occ_temp) return;
     g_occ_temp = occupancy(loop_materialize_temp_kernel);
-    g_occ_insert = occupancy(loop_materialize_insert_kernel);
-    g_occ_keys = occupancy(loop_insert_keys_kernel);
-    g_occ_select = occupancy(loop_select_insert_kernel);
-    g_occ_expand = occupancy(loop_expand_insert_kernel);
+    g_occ_insert = occupancy(loop_materialize_insert_kernel<2>);
+    g_occ_keys = occupancy(loop_insert_keys_kernel<2>);
+    g_occ_select = occupancy(loop_select_insert_kernel<2>);
+    g_occ_expand = occupancy(loop_expand_insert_kernel<2>);
     g_occ_xroute = occupancy(loop_expand_route_kernel);
     g_occ_route = occupancy(loop_route_keys_kernel);
+    g_occ_xtemp = occupancy(loop_expand_temp_kernel);
 }
 
 void loop_fill_u64(Ctx& c, u64* p, u64 n, u64 v) {
@@ -1633,7 +1781,8 @@ void loop_insert_keys(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, 
                       const LoopHeadBufs& hb, const LoopEndDesc* end) {
     LoopEndDesc e{};
     if (end) e = *end;
-    loop_insert_keys_kernel<<<c.num_sms * g_occ_keys, kLT, 0, s>>>(ctl, step, head, keys, hb, e, end ? 1 : 0);
+    SLOT_DISPATCH(c, loop_insert_keys_kernel, <<<c.num_sms * g_occ_keys, kLT, 0, s>>>(ctl, step, head, keys, hb, e,
+                                                                                      end ? 1 : 0));
     c.check_launch();
 }
 
@@ -1643,8 +1792,8 @@ void loop_materialize_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32
     LoopEndDesc e{};
     if (end) e = *end;
     const int waves = c.cfg.insert_waves ? (int)c.cfg.insert_waves : (hb.log_cap >= kWideLog ? 3 : 1);
-    loop_materialize_insert_kernel<<<c.num_sms * g_occ_insert * waves, kLT, 0, s>>>(ctl, step, head, o, inner, jd,
-                                                                                    sb, hb, e, end ? 1 : 0);
+    SLOT_DISPATCH(c, loop_materialize_insert_kernel, <<<c.num_sms * g_occ_insert * waves, kLT, 0, s>>>(ctl, step, head, o, inner, jd,
+                                                                                    sb, hb, e, end ? 1 : 0));
     c.check_launch();
 }
 
@@ -1652,8 +1801,8 @@ void loop_select_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head
                         const DevJoin& jd, const LoopHeadBufs& hb, const LoopEndDesc* end) {
     LoopEndDesc e{};
     if (end) e = *end;
-    loop_select_insert_kernel<<<c.num_sms * g_occ_select, kLT, 0, s>>>(ctl, step, head, o, jd, hb, e,
-                                                                        end ? 1 : 0);
+    SLOT_DISPATCH(c, loop_select_insert_kernel, <<<c.num_sms * g_occ_select, kLT, 0, s>>>(ctl, step, head, o, jd, hb, e,
+                                                                        end ? 1 : 0));
     c.check_launch();
 }
 
@@ -1692,8 +1841,8 @@ void loop_expand_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head
     LoopEndDesc e{};
     if (end) e = *end;
     const int waves = c.cfg.insert_waves ? (int)c.cfg.insert_waves : 1;
-    loop_expand_insert_kernel<<<c.num_sms * g_occ_expand * waves, kLT, 0, s>>>(
-        ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0);
+    SLOT_DISPATCH(c, loop_expand_insert_kernel, <<<c.num_sms * g_occ_expand * waves, kLT, 0, s>>>(
+        ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0));
     c.check_launch();
 }
 
@@ -1702,6 +1851,14 @@ void loop_expand_route(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const Loo
                        const PeerTab* tab) {
     loop_expand_route_kernel<<<c.num_sms * g_occ_xroute, kLT, 0, s>>>(ctl, step, o, inner, jd, dense, sb,
                                                                       heavy_rows, tab);
+    c.check_launch();
+}
+
+void loop_expand_temp(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const u64* inner,
+                      const DevJoin& jd, const LoopDense& dense, const LoopStepBufs& sb, u64 heavy_rows, u64* temp,
+                      u64 temp_cap) {
+    loop_expand_temp_kernel<<<c.num_sms * g_occ_xtemp, kLT, 0, s>>>(ctl, step, o, inner, jd, dense, sb, heavy_rows,
+                                                                    temp, temp_cap);
     c.check_launch();
 }
 

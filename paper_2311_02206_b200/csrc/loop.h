@@ -94,6 +94,14 @@ struct LoopCtl {
     u32 part_over;        // some rank overflowed: the iteration was rolled back on every rank
     u32 part_stall;       // this rank's insert did not fit its log / index: the host finishes it
     u32 part_stall_any;   // some rank stalled (the graph stopped on every rank)
+    u32 part_timeout;     // a device barrier waited past its limit (the host raises GD_ERR_NCCL)
+    u32 pad3;
+    // output window of a chain temp (host-driven windowed iteration, when a
+    // step's temp exceeds gd_device_config.temp_limit_rows): step win_step
+    // materializes only its outputs [win_lo, win_hi); win_hi = 0: no window
+    u32 win_step;
+    u32 pad2;
+    u64 win_lo, win_hi;
 };
 
 // ---- peer-memory partitioned loop --------------
@@ -250,6 +258,7 @@ void loop_expand_route(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const Loo
                        const PeerTab* tab);
 struct PeerSyncDesc {
     const PeerTab* tab;
+    u64 timeout_ns;  // a barrier that waits longer stops the graph (part_timeout)
     u32 final_step, nsteps;
     u64 log_cap, tab_limit;
     u32 stamp_max;
@@ -277,6 +286,12 @@ void loop_count(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter&
 void loop_expand_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
                         const u64* inner, const DevJoin& jd, const LoopDense& dense, const LoopStepBufs& sb,
                         u64 heavy_rows, const LoopHeadBufs& hb, const LoopEndDesc* end);
+
+// The same expansion appended to the step's temp (split final step, then
+// loop_insert_keys over the temp).
+void loop_expand_temp(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter& o, const u64* inner,
+                      const DevJoin& jd, const LoopDense& dense, const LoopStepBufs& sb, u64 heavy_rows, u64* temp,
+                      u64 temp_cap);
 
 // Records the iteration (or rolls it back on overflow) and sets the graph's
 // while-condition (cond ignored unless use_cond).

@@ -79,7 +79,7 @@ constexpr u32 kSFlagA = 1u << 30;
 constexpr u32 kSFlagP = 2u << 30;
 constexpr u32 kSMask = (1u << 30) - 1;
 
-template <typename K, int I>
+template <typename K, int I, bool BALLOT = false>
 __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
     const K* __restrict__ in, K* __restrict__ out, u64 portion_begin, u64 portion_n, u32 shift,
     const u64* __restrict__ digit_base, u64* __restrict__ next_base, u32* __restrict__ ws,
@@ -124,7 +124,23 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(
     // all match masks first: independent MATCH instructions pipeline
     u32 pm[I];
 #pragma unroll
-    for (int i = 0; i < I; ++i) pm[i] = __match_any_sync(0xffffffffu, dig(i));
+    for (int i = 0; i < I; ++i) {
+        if constexpr (BALLOT) {  // peers by one ballot per digit bit (+ validity), no MATCH.ANY
+            const u32 d = dig(i);
+            const bool valid = d < (u32)kRadix;
+            const u32 vb = __ballot_sync(0xffffffffu, valid);
+            u32 peers = valid ? vb : ~vb;
+#pragma unroll
+            for (int b = 0; b < kRadixBits; ++b) {
+                const bool bit = (d >> b) & 1;
+                const u32 bb = __ballot_sync(0xffffffffu, bit);
+                peers &= bit ? bb : ~bb;
+            }
+            pm[i] = peers;
+        } else {
+            pm[i] = __match_any_sync(0xffffffffu, dig(i));
+        }
+    }
 #pragma unroll
     for (int i = 0; i < I; ++i) {
         const u32 d = dig(i);
@@ -231,11 +247,14 @@ constexpr int kPI = 16;          // keys per thread
 constexpr int kPTile = kPT * kPI;  // 4096 keys, 32 KB
 constexpr int kPW = kPT / 32;
 
-template <int RB>
+// IP (in place): the tile's keys are held in registers after ranking and
+// the digit-sorted staging reuses the tile's own buffer (64 KB less shared
+// memory per CTA: 2 CTAs per SM at 10-bit digits, 3 at 8-bit).
+template <int RB, bool IP>
 struct PipeSmem {
     static constexpr int R = 1 << RB;
     u64 buf[2][kPTile];
-    u64 stage[kPTile];
+    u64 stage[IP ? 2 : kPTile];
     u32 wh[kPW][R / 2];  // per-warp digit counters / offsets, u16 pairs
     u32 dstart[R];
     u64 gbase[R];
@@ -306,8 +325,8 @@ __device__ __forceinline__ void st_status_vec(u32* p, const DigitVec<DPT>& r) {
     }
 }
 
-template <int RB>
-__global__ void __launch_bounds__(kPT) onesweep_pipe_kernel(const u64* __restrict__ in, u64* __restrict__ out,
+template <int RB, bool IP, bool BALLOT>
+__global__ void __launch_bounds__(kPT, IP ? 2 : 1) onesweep_pipe_kernel(const u64* __restrict__ in, u64* __restrict__ out,
                                                             u64 portion_begin, u64 portion_n, u32 shift, u32 width,
                                                             const u64* __restrict__ digit_base,
                                                             u64* __restrict__ next_base, u32* __restrict__ ws,
@@ -316,7 +335,7 @@ __global__ void __launch_bounds__(kPT) onesweep_pipe_kernel(const u64* __restric
     constexpr int DPT = R >= 1024 ? 4 : 2;  // digits per owner thread
     constexpr int OWN = R / DPT;            // owner threads (128 / 256)
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    PipeSmem<RB>& sm = *reinterpret_cast<PipeSmem<RB>*>(smem_raw);
+    PipeSmem<RB, IP>& sm = *reinterpret_cast<PipeSmem<RB, IP>*>(smem_raw);
     u32* counter = ws;
     u32* status = ws + 4;  // 16-byte aligned statuses
     const u32 t = threadIdx.x, warp = t >> 5, lane = lane_id();
@@ -361,11 +380,30 @@ __global__ void __launch_bounds__(kPT) onesweep_pipe_kernel(const u64* __restric
 
         // warp multi-split ranking, stable in (item, lane) order
         u32 rank2[kPI / 2];
+        u64 kr[IP ? kPI : 1];
 #pragma unroll
         for (int i = 0; i < kPI; ++i) {
             const u32 idx = warp * (kPI * 32) + i * 32 + lane;
-            const u32 d = idx < tile_n ? (u32)(keys[idx] >> shift) & dmask : (u32)R;
-            const u32 peers = __match_any_sync(0xffffffffu, d);
+            const u64 kv = keys[idx];
+            if constexpr (IP) kr[i] = kv;
+            const u32 d = idx < tile_n ? (u32)(kv >> shift) & dmask : (u32)R;
+            u32 peers;
+            if constexpr (BALLOT) {
+                // lanes with the same digit: one ballot per digit bit (plus
+                // validity) instead of MATCH.ANY, whose latency dominated
+                // the ranking (ncu: short-scoreboard stalls on its results)
+                const bool valid = idx < tile_n;
+                const u32 vb = __ballot_sync(0xffffffffu, valid);
+                peers = valid ? vb : ~vb;
+#pragma unroll
+                for (int b = 0; b < RB; ++b) {
+                    const bool bit = (d >> b) & 1;
+                    const u32 bb = __ballot_sync(0xffffffffu, bit);
+                    peers &= bit ? bb : ~bb;
+                }
+            } else {
+                peers = __match_any_sync(0xffffffffu, d);
+            }
             const u32 leader = 31 - __clz(peers);
             u32 base = 0;
             if (lane == leader && d < (u32)R) {
@@ -470,20 +508,23 @@ __global__ void __launch_bounds__(kPT) onesweep_pipe_kernel(const u64* __restric
         __syncthreads();  // (D)
 
         // scatter into shared memory in digit-sorted (stable) order
+        u64* stage = IP ? keys : sm.stage;
 #pragma unroll
         for (int i = 0; i < kPI; ++i) {
             const u32 idx = warp * (kPI * 32) + i * 32 + lane;
             if (idx < tile_n) {
-                const u64 k = keys[idx];
+                u64 k;
+                if constexpr (IP) k = kr[i];
+                else k = keys[idx];
                 const u32 d = (u32)(k >> shift) & dmask;
                 const u32 r = (rank2[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
                 const u32 wo = (sm.wh[warp][d >> 1] >> ((d & 1) * 16)) & 0xffffu;
-                sm.stage[sm.dstart[d] + wo + r] = k;
+                stage[sm.dstart[d] + wo + r] = k;
             }
         }
         __syncthreads();  // (E)
         for (u32 j = t; j < tile_n; j += kPT) {
-            const u64 k = sm.stage[j];
+            const u64 k = stage[j];
             out[sm.gbase[(u32)(k >> shift) & dmask] + j] = k;
         }
         cur ^= 1;
@@ -505,8 +546,12 @@ int sort_items(const Ctx& c) {
 template <typename K, int I>
 void launch_onesweep(const Ctx& c, u64 tiles, const K* src, K* dst, u64 pb, u64 pn, u32 shift, const u64* rd,
                      u64* wr, u32* w) {
-    onesweep_kernel<K, I><<<(unsigned)tiles, kSortThreads, 0, c.stream>>>(src, dst, pb, pn, shift, rd, wr, w,
-                                                                          (u32)tiles);
+    if (c.cfg.sort_pipeline == 4)
+        onesweep_kernel<K, I, true><<<(unsigned)tiles, kSortThreads, 0, c.stream>>>(src, dst, pb, pn, shift, rd, wr,
+                                                                                    w, (u32)tiles);
+    else
+        onesweep_kernel<K, I><<<(unsigned)tiles, kSortThreads, 0, c.stream>>>(src, dst, pb, pn, shift, rd, wr, w,
+                                                                              (u32)tiles);
 }
 
 // All passes' digit histograms for the pipelined sort: `width`-bit digits,
@@ -554,21 +599,30 @@ __global__ void __launch_bounds__(R) radix_bases_w_kernel(const u64* __restrict_
     bases[pass * R + threadIdx.x] = block_exclusive_scan<u64, R>(hist[pass * R + threadIdx.x], all, scan_tmp);
 }
 
-template <int RB>
-void launch_pipe(Ctx& c, const u64* src, u64* dst, u64 pb, u64 pn, u32 shift, u32 width, const u64* rd, u64* wr,
-                 u32* w) {
-    const size_t smem = sizeof(PipeSmem<RB>);
+template <int RB, bool IP, bool BALLOT>
+void launch_pipe_ip(Ctx& c, const u64* src, u64* dst, u64 pb, u64 pn, u32 shift, u32 width, const u64* rd, u64* wr,
+                    u32* w) {
+    const size_t smem = sizeof(PipeSmem<RB, IP>);
+    auto kern = onesweep_pipe_kernel<RB, IP, BALLOT>;
     static int per_sm = -1;  // co-resident CTAs per SM (one device per process)
     if (per_sm < 0) {
-        GD_CUDA(cudaFuncSetAttribute(onesweep_pipe_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_pipe_kernel<RB>, kPT, smem));
+        GD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPT, smem));
         if (per_sm < 1) throw Error(GD_ERR_CUDA, "onesweep_pipe_kernel does not fit an SM");
     }
     const u64 tiles = (pn + kPTile - 1) / kPTile;
     const u64 grid = std::min<u64>(tiles, (u64)per_sm * c.num_sms);
-    onesweep_pipe_kernel<RB><<<(unsigned)grid, kPT, smem, c.stream>>>(src, dst, pb, pn, shift, width, rd, wr, w,
-                                                                      (u32)tiles);
+    kern<<<(unsigned)grid, kPT, smem, c.stream>>>(src, dst, pb, pn, shift, width, rd, wr, w, (u32)tiles);
+}
+
+template <int RB>
+void launch_pipe(Ctx& c, const u64* src, u64* dst, u64 pb, u64 pn, u32 shift, u32 width, const u64* rd, u64* wr,
+                 u32* w) {
+    switch (c.cfg.sort_pipeline) {
+        case 2: launch_pipe_ip<RB, false, true>(c, src, dst, pb, pn, shift, width, rd, wr, w); break;
+        case 3: launch_pipe_ip<RB, true, false>(c, src, dst, pb, pn, shift, width, rd, wr, w); break;
+        default: launch_pipe_ip<RB, true, true>(c, src, dst, pb, pn, shift, width, rd, wr, w);
+    }
 }
 
 // Pipelined LSD sort of u64 keys (gd_device_config.sort_digit_bits > 8 or
@@ -629,7 +683,7 @@ template <typename K>
 K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
     if (n <= 1 || nbits == 0) return a;
     if constexpr (sizeof(K) == 8) {
-        if (c.cfg.sort_pipeline && n >= c.cfg.sort_pipeline_min_keys)
+        if (c.cfg.sort_pipeline && c.cfg.sort_pipeline != 4 && n >= c.cfg.sort_pipeline_min_keys)
             return reinterpret_cast<K*>(radix_sort_pipe(c, reinterpret_cast<u64*>(a), reinterpret_cast<u64*>(b), n,
                                                         nbits));
     }

@@ -22,13 +22,18 @@ from paper_2311_02206_b200 import arraylog as al
 def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     sizes = [int(float(a) * 1e6) for a in args] or [16_000_000, 771_000_000]
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a real stream: the context must launch where the events are recorded
+    torch.cuda.set_stream(stream)
     ctx = al.Context(0, stream.cuda_stream)
     lib = ctx.lib
     flush = torch.empty(256 << 20 >> 2, dtype=torch.int32, device="cuda")
-    modes = [("classic", {"sort_pipeline": 0}), ("pipe8", {"sort_pipeline": 1, "sort_digit_bits": 8}),
+    modes = [("classic", {"sort_pipeline": 0, "sort_pipeline_min_keys": 0}), ("pipe8", {"sort_pipeline": 1, "sort_digit_bits": 8}),
              ("pipe9", {"sort_pipeline": 1, "sort_digit_bits": 9}),
-             ("pipe10", {"sort_pipeline": 1, "sort_digit_bits": 10})]
+             ("pipe10", {"sort_pipeline": 1, "sort_digit_bits": 10}),
+             ("pipe8s", {"sort_pipeline": 2, "sort_digit_bits": 8}),
+             ("pipe10s", {"sort_pipeline": 2, "sort_digit_bits": 10}),
+             ("pipe10m", {"sort_pipeline": 3, "sort_digit_bits": 10}),
+             ("classicb", {"sort_pipeline": 4})]
     out = []
     for n in sizes:
         g = torch.Generator(device="cuda").manual_seed(1)
@@ -53,8 +58,10 @@ def main():
             res = b if it.value else a
             ok = bool(torch.equal(res, ref))
             ms = float(np.median(ts[1:]))
-            rec = {"n": n, "mode": name, "ms": round(ms, 3), "ok": ok,
-                   "gbs_per_pass": None}
+            nb = 46
+            npass = {"classic": 6, "classicb": 6}.get(name, -(-nb // cfg.get("sort_digit_bits", 8)))
+            rec = {"n": n, "mode": name, "ms": round(ms, 3), "ok": ok, "passes": npass,
+                   "gbs_per_pass": round(2 * 8 * n * npass / (ms / 1e3) / 1e9 / npass, 1)}
             print(json.dumps(rec), flush=True)
             out.append(rec)
         del src, ref, a, b

@@ -11,8 +11,11 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 CLASSES = [  # kernel-name substring -> bench/profiler class (ctx.h KClass)
-    ("onesweep_kernel", "sort_pass"), ("radix_hist_kernel", "sort_hist"), ("radix_bases", "sort_hist"),
-    ("loop_probe_kernel", "join_probe"), ("join_probe_kernel", "join_probe"),
+    ("onesweep_kernel", "sort_pass"), ("onesweep_pipe_kernel", "sort_pass"), ("radix_hist", "sort_hist"),
+    ("radix_bases", "sort_hist"),
+    ("loop_probe_kernel", "join_probe"), ("join_probe_kernel", "join_probe"), ("loop_count_kernel", "join_probe"),
+    ("loop_expand_insert", "join_insert"), ("loop_insert_keys", "join_insert"), ("loop_expand_route", "exchange"),
+    ("loop_route_keys", "exchange"), ("loop_peer_sync", "loop_ctl"),
     ("loop_scan_kernel", "select"), ("scan_tiles", "select"), ("apply_offsets", "select"), ("select_kernel", "select"),
     ("loop_materialize_insert", "join_insert"), ("loop_select_insert", "join_insert"),
     ("loop_materialize_temp", "join_materialize"), ("join_materialize_kernel", "join_materialize"),

@@ -4,10 +4,18 @@
 logic, gloo multi-process); `-m gpu` tests are the parity tests proper and
 call libgdlog_b200.so through the C-ABI on a B200.
 """
+import os
 import sys
 from pathlib import Path
 
 import pytest
+
+# The loopback ranks of the peer-memory partition tests run P CUDA graphs
+# concurrently on one GPU, their device barriers spinning until every rank
+# arrives: each rank's stream needs its own hardware queue, or a spinning
+# barrier kernel blocks another rank's work queued behind it.  (Set before
+# the first CUDA context of the process.)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 ROOT = Path(__file__).resolve().parent.parent
 if str(ROOT) not in sys.path:

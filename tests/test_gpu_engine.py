@@ -105,9 +105,15 @@ def test_ebm_saves_allocations(ref):
     assert_same(off, run_ref(ref, "reach", {"Edge": chain_edges(60)}, cfg), ["Reach"])
 
 
-def test_budget_error_names_a_phase(ref):
+LOOPS = {"resident": {}, "host": {"resident_loop": 0}}
+
+
+@pytest.mark.parametrize("loop", list(LOOPS))
+def test_budget_error_names_a_phase(ref, loop):
+    """Finite budgets run on both loops: the resident device loop replays
+    the reference's charges after the fixpoint and raises the same error."""
     cfg = al.engine_config(memory_budget_bytes=400)
-    with pytest.raises(al.budget_error) as ei:
+    with pytest.raises(al.budget_error) as ei, al.default_context().configured(**LOOPS[loop]):
         run_gpu("reach", {"Edge": chain_edges(30)}, cfg)
     from oracle.bindings import OracleError
     with pytest.raises(OracleError) as er:
@@ -116,8 +122,9 @@ def test_budget_error_names_a_phase(ref):
     assert ei.value.phase() in A.PHASES
 
 
+@pytest.mark.parametrize("loop", list(LOOPS))
 @pytest.mark.parametrize("budget", [2000, 6000, 20000, 60000])
-def test_budget_errors_match_reference_phase(ref, budget):
+def test_budget_errors_match_reference_phase(ref, budget, loop):
     cfg = al.engine_config(memory_budget_bytes=budget)
     from oracle.bindings import OracleError
     edges = chain_edges(40)
@@ -127,11 +134,34 @@ def test_budget_errors_match_reference_phase(ref, budget):
     except OracleError as e:
         ref_phase = e.phase
     try:
-        run_gpu("reach", {"Edge": edges}, cfg)
+        with al.default_context().configured(**LOOPS[loop]):
+            run_gpu("reach", {"Edge": edges}, cfg)
         gpu_phase = None
     except al.budget_error as e:
         gpu_phase = e.phase()
     assert gpu_phase == ref_phase
+
+
+@pytest.mark.parametrize("loop", list(LOOPS))
+@pytest.mark.parametrize("prog,budget", [("reach", 3 << 20), ("sg", 1 << 20), ("reach", 200_000)])
+def test_finite_budget_runs_match_reference(ref, prog, budget, loop):
+    """A finite budget that the run fits (EBM shrinks K to fit it): result,
+    Δ history, iterations, peaks and buffer allocations equal the
+    reference's on both loops (the resident loop under a budget)."""
+    from oracle.bindings import OracleError
+    rng = np.random.default_rng(budget)
+    edges = random_relation(rng, 2, 3000, 1200) if prog == "reach" else random_relation(rng, 2, 900, 700)
+    cfg = al.engine_config(memory_budget_bytes=budget)
+    try:
+        r = run_ref(ref, prog, {"Edge": edges}, cfg)
+    except OracleError as e:
+        with pytest.raises(al.budget_error) as ei, al.default_context().configured(**LOOPS[loop]):
+            run_gpu(prog, {"Edge": edges}, cfg)
+        assert ei.value.phase() == e.phase
+        return
+    with al.default_context().configured(**LOOPS[loop]):
+        g = run_gpu(prog, {"Edge": edges}, cfg)
+    assert_same(g, r, [{"reach": "Reach", "sg": "SG"}[prog]])
 
 
 def test_load_errors_and_config_validation():

@@ -31,6 +31,12 @@ MODES = {  # gd_device_config fields of each mode
     # segment) items of 3 outputs (the heavy-row path on small inputs)
     "heavy": {"heavy_rows": 3},
     "tiny_heavy": {"min_capacities": 1, "heavy_rows": 2},
+    # chain temps above 7 rows are materialized in windows of 7 (the
+    # windowed iteration of SURVEY §8f rank 2), with and without the rest
+    # of the capacities at their minimum
+    "window": {"temp_limit_rows": 7},
+    "tiny_window": {"min_capacities": 1, "temp_limit_rows": 5},
+    "window_noxp": {"temp_limit_rows": 16, "warp_expand": 0},
 }
 
 
@@ -64,14 +70,15 @@ def test_c1_all_modes(ref, mode):
     assert g.raw_stats().join_tuples == 190496  # SURVEY §6 probe: ΣJ over 46 iterations
 
 
-@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "hashindex", "split", "noxp", "heavy", "tiny_heavy"])
+@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "hashindex", "split", "noxp", "heavy", "tiny_heavy",
+                                  "window", "tiny_window", "window_noxp"])
 @pytest.mark.parametrize("idx", [0, 17, 55])
 def test_sg_corpus_modes(ref, mode, idx):
     g, _ = corpus(ref, 1, idx)
     assert_same(run_mode(mode, "sg", {"Edge": g}), run_ref(ref, "sg", {"Edge": g}), ["SG"])
 
 
-@pytest.mark.parametrize("mode", ["graph", "tiny", "tiny_split", "heavy"])
+@pytest.mark.parametrize("mode", ["graph", "tiny", "tiny_split", "heavy", "window", "tiny_window"])
 @pytest.mark.parametrize("case", sorted(CUSTOM))
 def test_custom_programs_modes(ref, mode, case):
     src, db = CUSTOM[case]
@@ -181,3 +188,25 @@ def test_wide_slots(ref, mode):
     enc = g.encoding()
     assert enc["bits"] == 31 and not enc["dictionary"]
     assert_same(g, run_ref(ref, "reach", {"Edge": edges}), ["Reach"])
+
+
+@pytest.mark.parametrize("limit", [64, 1000, 20000])
+def test_sg_windowed_chain_temps_vs_reference(ref, limit):
+    """SG on a bushy random DAG whose step-1 temps reach tens of thousands of
+    rows per iteration, with chain temps capped at `limit` rows: the
+    iterations whose temp exceeds the cap run in windows; relation, Δ
+    history, iteration records and accountant statistics (the reference's
+    charges for the whole temp) equal the reference's."""
+    rng = np.random.default_rng(limit)
+    n = 3000
+    child = np.arange(1, n, dtype=np.uint64)
+    parent = (child - 1 - rng.integers(0, 40, size=n - 1).astype(np.uint64) % child).astype(np.uint64)
+    edges = np.stack([parent, child], 1)
+    r = run_ref(ref, "sg", {"Edge": edges})
+    with configured(temp_limit_rows=limit):
+        g = run_gpu("sg", {"Edge": edges})
+    assert_same(g, r, ["SG"])
+    with configured(resident_loop=0):
+        h = run_gpu("sg", {"Edge": edges})
+    assert g.iter_log("SG") == h.iter_log("SG")
+    assert g.raw_stats().join_tuples == h.raw_stats().join_tuples

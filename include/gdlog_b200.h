@@ -147,17 +147,22 @@ typedef struct gd_device_config {
     uint32_t sort_digit_bits;       /* pipelined sort: widest digit, 8..10 (10) */
     uint64_t heavy_rows;            /* ... rows with more outputs are expanded as segments of this many (4096) */
     int32_t sort_pipeline;          /* u64 sorts: 0 classic onesweep; 1 pipelined (bulk-copy prefetch, wide
-                                       digits, ballot multi-split, keys staged in place); 2 the same with a
+                                       digits, ballot multi-split, keys staged in place, static tile order, cooperative launch); 2 the same with a
                                        separate staging buffer; 3 in place with MATCH.ANY ranking;
-                                       4 classic onesweep with ballot ranking (1) */
+                                       4 classic onesweep with ballot ranking (0) */
     uint32_t partition_exchange;    /* gd_engine_run_partitioned: gd_partition_exchange (GD_EXCHANGE_PEER) */
     uint64_t sort_pipeline_min_keys; /* ... for sorts of at least this many keys (1 << 20) */
     uint64_t temp_limit_rows;       /* resident loop: a chain temp above this many rows is materialized
                                        in windows of at most this many (0: half the free HBM) */
     uint32_t peer_timeout_ms;       /* peer exchange: a device barrier waiting longer fails the run with
                                        GD_ERR_NCCL instead of hanging the GPU (60000) */
-    uint32_t insert_slots;          /* head-index inserts: slots of the 4-slot home bucket read at the
-                                       first probe, 1, 2 or 4 (2) */
+    uint32_t insert_slots;          /* head-index inserts: slots read before the claiming CAS, 1, 2 or 4;
+                                       0 = CAS first, no read (1) */
+    uint32_t l2_hints;              /* head-index accesses L2 evict-first, join inputs evict-last:
+                                       0 never, 1 when the index exceeds 256 MB, 2 always (0:
+                                       measured slower on C2) */
+    uint32_t l2_fetch_bytes;        /* cudaLimitMaxL2FetchGranularity set for the device when the context
+                                       is configured: 32 / 64 / 128 bytes, 0 = leave the driver's (0) */
 } gd_device_config;
 
 void gd_device_config_default(gd_device_config* cfg);

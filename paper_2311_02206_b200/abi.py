@@ -80,6 +80,8 @@ class gd_device_config(C.Structure):
         ("temp_limit_rows", u64),
         ("peer_timeout_ms", u32),
         ("insert_slots", u32),
+        ("l2_hints", u32),
+        ("l2_fetch_bytes", u32),
     ]
 
 

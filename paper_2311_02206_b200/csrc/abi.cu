@@ -281,8 +281,16 @@ gd_status gd_ctx_set_device_config(gd_ctx* ctx, const gd_device_config* cfg) {
         if (cfg->partition_exchange > GD_EXCHANGE_NCCL) throw_config("partition_exchange out of range");
         if (cfg->sort_pipeline < 0 || cfg->sort_pipeline > 4) throw_config("sort_pipeline must be in [0, 4]");
         if (cfg->peer_timeout_ms == 0) throw_config("peer_timeout_ms must be positive");
-        if (cfg->insert_slots != 1 && cfg->insert_slots != 2 && cfg->insert_slots != 4)
-            throw_config("insert_slots must be 1, 2 or 4");
+        if (cfg->insert_slots > 4 || cfg->insert_slots == 3)
+            throw_config("insert_slots must be 0 (CAS first), 1, 2 or 4");
+        if (cfg->l2_hints > 2) throw_config("l2_hints must be 0, 1 or 2");
+        if (cfg->l2_fetch_bytes && cfg->l2_fetch_bytes != 32 && cfg->l2_fetch_bytes != 64 &&
+            cfg->l2_fetch_bytes != 128)
+            throw_config("l2_fetch_bytes must be 0, 32, 64 or 128");
+        if (cfg->l2_fetch_bytes && cfg->l2_fetch_bytes != ctx->c->cfg.l2_fetch_bytes) {
+            GD_CUDA(cudaSetDevice(ctx->c->device));
+            GD_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, cfg->l2_fetch_bytes));
+        }
         ctx->c->cfg = *cfg;
     });
 }
@@ -786,8 +794,15 @@ gd_status gd_nccl_comm_destroy(gd_comm* comm) {
 
 gd_status gd_engine_run_partitioned(gd_engine* eng, gd_comm* comm, uint64_t max_iters, uint64_t* iterations) {
     if (!comm) return GD_ERR_INVALID_ARG;
-    ENG_GUARD(const u64 it = eng->e->partition_run(comm->c, max_iters ? max_iters : ~0ull);
-              if (iterations) *iterations = it);
+    if (!eng) return GD_ERR_INVALID_ARG;
+    const gd_status st = guard(eng->ctx, [&] {
+        const u64 it = eng->e->partition_run(comm->c, max_iters ? max_iters : ~0ull);
+        if (iterations) *iterations = it;
+    });
+    // a failed rank must not leave its peers waiting in a host-side
+    // collective of the transport (loopback ranks share one process)
+    if (st != GD_OK) comm->t->abort();
+    return st;
 }
 
 }  // extern "C"

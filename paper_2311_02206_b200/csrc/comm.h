@@ -32,6 +32,10 @@ struct Transport {
     virtual void map_peers(void* local, std::vector<void*>& out, cudaStream_t s) = 0;
     // Releases mappings made by map_peers (not the local allocation).
     virtual void unmap_peers(const std::vector<void*>& ptrs) { (void)ptrs; }
+    // This rank failed: peers blocked in a collective of the transport
+    // return with an error instead of waiting forever (NCCL: nothing to do,
+    // its own timeouts / the process exit end the job).
+    virtual void abort() {}
 };
 
 struct Comm {
@@ -163,21 +167,30 @@ struct LoopbackHub {
     uint64_t gen = 0;
     uint32_t arrived = 0;
     explicit LoopbackHub(uint32_t p) : P(p), out((size_t)p * p), mapped(p) {}
+    bool aborted = false;
     void barrier() {
         std::unique_lock<std::mutex> l(m);
+        if (aborted) throw Error(GD_ERR_NCCL, "loopback transport: a peer rank failed");
         const uint64_t g = gen;
         if (++arrived == P) {
             arrived = 0;
             ++gen;
             cv.notify_all();
         } else {
-            cv.wait(l, [&] { return gen != g; });
+            cv.wait(l, [&] { return gen != g || aborted; });
+            if (gen == g) throw Error(GD_ERR_NCCL, "loopback transport: a peer rank failed");
         }
+    }
+    void abort() {
+        std::lock_guard<std::mutex> l(m);
+        aborted = true;
+        cv.notify_all();
     }
 };
 
 struct LoopbackTransport : Transport {
     LoopbackHub* hub = nullptr;
+    void abort() override { hub->abort(); }
     struct Want {
         unsigned long long* dst;
         uint64_t n;

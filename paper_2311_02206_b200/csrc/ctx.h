@@ -135,12 +135,14 @@ inline gd_device_config default_device_config() {
     d.warp_expand = 1;
     d.sort_digit_bits = 10;
     d.heavy_rows = 4096;
-    d.sort_pipeline = 1;
+    d.sort_pipeline = 0;
     d.partition_exchange = GD_EXCHANGE_PEER;
     d.sort_pipeline_min_keys = 1u << 20;
     d.temp_limit_rows = 0;
     d.peer_timeout_ms = 60000;
-    d.insert_slots = 2;
+    d.insert_slots = 1;
+    d.l2_hints = 0;
+    d.l2_fetch_bytes = 0;
     return d;
 }
 

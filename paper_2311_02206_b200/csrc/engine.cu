@@ -611,7 +611,15 @@ public:
         u32 proj_arity = 0;
         DevBuf<u64> row_start, row_off, splits, temp;
         u64 rows_cap = 0, splits_cap = 0, temp_cap = 0;
-        LoopStepBufs bufs() const { return LoopStepBufs{row_start.p, row_off.p, rows_cap, splits.p, splits_cap}; }
+        DevBuf<u64> rc;  // xp steps: each outer row's inner range (start << 32 | count), from loop_count
+        LoopStepBufs bufs() const {
+            return LoopStepBufs{row_start.p, row_off.p, rows_cap, splits.p, splits_cap, xp ? rc.p : nullptr};
+        }
+        void alloc_rows(Ctx& c) {
+            row_start = DevBuf<u64>(c, rows_cap);
+            row_off = DevBuf<u64>(c, rows_cap);
+            if (xp) rc = DevBuf<u64>(c, rows_cap);
+        }
     };
     struct LHead {
         u32 rel = 0;
@@ -622,7 +630,6 @@ public:
         // clear = false: the caller writes every slot (loop_table_rehash)
         void alloc_tab(Ctx& c, u64 cap, bool dense = false, bool clear = true) {
             tab.release();
-            cap = std::max<u64>((cap + 3) & ~3ull, 4);  // whole 4-slot buckets (loop.cu hs_home)
             tab_cap = cap;
             tab_limit = dense ? cap / 4 * 3 : tab_limit_of(cap);
             tab = DevBuf<u64>(c, cap * loop_slot_bytes(sbits) / 8);
@@ -633,6 +640,11 @@ public:
     // sector scan) at load <= 1/2; a full table grows 4x (to load 1/8), so
     // the re-spreads move about a third of the final key count in total.
     static u64 tab_limit_of(u64 cap) { return cap / 2; }
+    // L2 eviction hints on the head index once it is larger than L2 (the
+    // join inputs, not the table lines, are what L2 should keep then).
+    u32 l2_hints_for(u64 tab_bytes) const {
+        return c.cfg.l2_hints == 1 ? (tab_bytes > (256ull << 20) ? 1u : 0u) : c.cfg.l2_hints == 2 ? 1u : 0u;
+    }
 
     // The recursive variants as loop steps (plan order, variant order): outer
     // source, join descriptor, inner copy and index (dense form when
@@ -748,8 +760,7 @@ public:
             L.rows_cap = tiny ? 2 : std::max<u64>(d0 + 1, 1 << 12);
             L.splits_cap = tiny ? 2 : std::max<u64>(2 * d0 / kLoopMatTile + 2, 1 << 12);
             if (!L.select) {
-                L.row_start = DevBuf<u64>(c, L.rows_cap);
-                L.row_off = DevBuf<u64>(c, L.rows_cap);
+                L.alloc_rows(c);
                 L.splits = DevBuf<u64>(c, L.splits_cap);
             }
             if (!L.final || (L.split_insert && !L.select)) {  // chain temps / split-insert input
@@ -793,7 +804,8 @@ public:
         };
         auto bufs_of = [&](u32 h) {
             return LoopHeadBufs{heads[h].log.p, heads[h].log_cap, heads[h].tab.p, heads[h].tab_cap,
-                                heads[h].tab_limit, heads[h].sbits, 0};
+                                heads[h].tab_limit, heads[h].sbits,
+                                l2_hints_for(heads[h].tab_cap * loop_slot_bytes(heads[h].sbits))};
         };
         // One iteration's kernel sequence (captured into the graph, or
         // launched eagerly when profiling).  The gate runs in the last CTA
@@ -961,8 +973,7 @@ public:
                 LStep& L = steps[i];
                 if (hc->need_rows[i] > L.rows_cap) {
                     L.rows_cap = hc->need_rows[i] + hc->need_rows[i] / 2;
-                    L.row_start = DevBuf<u64>(c, L.rows_cap);
-                    L.row_off = DevBuf<u64>(c, L.rows_cap);
+                    L.alloc_rows(c);
                 }
                 if (hc->need_splits[i] > L.splits_cap) {
                     L.splits_cap = hc->need_splits[i] + hc->need_splits[i] / 2;
@@ -1123,18 +1134,31 @@ public:
             // Per-step counters of the steps about to run (again): the
             // candidate counts accumulate atomically; finals keep their
             // post-filter totals (inserted rows of earlier windows / phase A).
+            // (phase B keeps step wi's candidate count and scan: the windows
+            // are cut from them)
             auto clear_steps = [&](bool phase_b) {
                 for (u32 j = 0; j < ns; ++j) {
-                    const bool runs = phase_b ? in_v(j) && j >= wi : !in_v(j) || j <= wi;
+                    const bool runs = phase_b ? in_v(j) && j > wi : !in_v(j) || j <= wi;
                     if (!runs) continue;
                     hc->step_cand[j] = hc->heavy_n[j] = 0;
                     if (!steps[j].final) hc->step_total[j] = 0;
                 }
             };
+            u32 redos = 0;
             auto settle = [&](bool phase_b) {  // false: overflowed, grown, state cleared for a redo
                 c.d2h(hc, ctl.p, sizeof(LoopCtl));
                 c.sync();
                 if (!hc->overflow) return true;
+                if (++redos > 256) {
+                    std::string need;
+                    for (u32 j = 0; j < ns; ++j)
+                        need += " step" + std::to_string(j) + "(rows " + std::to_string(hc->need_rows[j]) + "/" +
+                                std::to_string(steps[j].rows_cap) + " splits " + std::to_string(hc->need_splits[j]) +
+                                "/" + std::to_string(steps[j].splits_cap) + " temp " +
+                                std::to_string(hc->need_temp[j]) + "/" + std::to_string(steps[j].temp_cap) + ")";
+                    throw_logic("windowed iteration: overflow persists after growth:" + need + " log " +
+                                std::to_string(hc->need_log[0]) + " tab " + std::to_string(hc->need_tab[0]));
+                }
                 grow_after_overflow();
                 hc->overflow = 0;
                 clear_steps(phase_b);
@@ -1457,8 +1481,7 @@ public:
             const bool tiny = c.cfg.min_capacities != 0;
             L.rows_cap = tiny ? 2 : std::max<u64>(f0 + 1, 1 << 12);
             L.splits_cap = tiny ? 2 : std::max<u64>(2 * f0 / kLoopMatTile + 2, 1 << 12);
-            L.row_start = DevBuf<u64>(c, L.rows_cap);
-            L.row_off = DevBuf<u64>(c, L.rows_cap);
+            L.alloc_rows(c);
             L.splits = DevBuf<u64>(c, L.splits_cap);
             L.temp_cap = tiny ? 1 : std::max<u64>(4 * f0, 1 << 16);
             L.temp = DevBuf<u64>(c, L.temp_cap);
@@ -1492,6 +1515,7 @@ public:
         b.tab_cap = H.tab_cap;
         b.tab_limit = H.tab_limit;
         b.sbits = H.sbits;
+        b.l2_hints = l2_hints_for(H.tab_cap * loop_slot_bytes(H.sbits));
         return b;
     }
 
@@ -1528,8 +1552,7 @@ public:
                 LStep& L = P.steps[i];
                 if (hc->need_rows[i] > L.rows_cap) {
                     L.rows_cap = hc->need_rows[i] + hc->need_rows[i] / 2;
-                    L.row_start = DevBuf<u64>(c, L.rows_cap);
-                    L.row_off = DevBuf<u64>(c, L.rows_cap);
+                    L.alloc_rows(c);
                 }
                 if (hc->need_splits[i] > L.splits_cap) {
                     L.splits_cap = hc->need_splits[i] + hc->need_splits[i] / 2;
@@ -1686,8 +1709,7 @@ public:
                     LStep& L = P.steps[i];
                     if (hc->need_rows[i] > L.rows_cap) {
                         L.rows_cap = hc->need_rows[i] + hc->need_rows[i] / 2;
-                        L.row_start = DevBuf<u64>(c, L.rows_cap);
-                        L.row_off = DevBuf<u64>(c, L.rows_cap);
+                        L.alloc_rows(c);
                     }
                     if (hc->need_splits[i] > L.splits_cap) {
                         L.splits_cap = hc->need_splits[i] + hc->need_splits[i] / 2;
@@ -1788,12 +1810,18 @@ public:
         u64* inbox = nullptr;
         u64 inbox_cap = 0;
         std::vector<void*> mails, inboxes;
+        // inboxes replaced by a regrow: freed only when the run ends (a
+        // cudaFree synchronizes the device, and loopback ranks sharing it
+        // may be spinning in a device barrier)
+        std::vector<std::pair<u64*, std::vector<void*>>> retired;
         DevBuf<PeerTab> tab;
         ~PeerState() {
             if (t) {
                 t->unmap_peers(inboxes);
                 t->unmap_peers(mails);
+                for (auto& r : retired) t->unmap_peers(r.second);
             }
+            for (auto& r : retired) cudaFree(r.first);
             if (inbox) cudaFree(inbox);
             if (mail) cudaFree(mail);
         }
@@ -1824,8 +1852,8 @@ public:
 
     void peer_map_inbox(Comm& comm, PeerState& ps, u64 cap) {
         if (ps.inbox) {
-            comm.t->unmap_peers(ps.inboxes);
-            cudaFree(ps.inbox);
+            ps.retired.emplace_back(ps.inbox, std::move(ps.inboxes));
+            ps.inboxes.clear();
             ps.inbox = nullptr;
         }
         GD_CUDA(cudaMalloc(&ps.inbox, std::max<u64>(cap, 1) * sizeof(u64)));
@@ -2011,11 +2039,20 @@ public:
 
         u32 done_iters = hc->iter;
         const u64 iter_limit = hist0 + max_iters;
+        // Every rank has its graph built (and its buffers set) before any
+        // rank launches: a rank spinning in a device barrier must never wait
+        // on a peer stuck in a host call that synchronizes the device
+        // (loopback ranks share one GPU).
+        auto ready = [&]() {
+            if (!eager && !exec) build_graph();
+            u64 bar = 0;
+            host_allreduce(comm, &bar, 1, 0);
+        };
+        ready();
         for (;;) {
             if (eager) {
                 record_iteration(c.stream, false, 0);
             } else {
-                if (!exec) build_graph();
                 GD_CUDA(cudaGraphLaunch(exec, c.stream));
             }
             c.d2h(hc, P.ctl.p, sizeof(LoopCtl));
@@ -2025,14 +2062,17 @@ public:
             if (hc->part_timeout)
                 throw Error(GD_ERR_NCCL, "partitioned loop: a peer did not reach the device barrier within " +
                                              std::to_string(c.cfg.peer_timeout_ms) + " ms (rank " +
-                                             std::to_string(comm.rank) + ", iteration " + std::to_string(hc->iter) + ")");
+                                             std::to_string(comm.rank) + ", iteration " + std::to_string(hc->iter) +
+                                             ": waiting for epoch " + std::to_string(hc->dbg_epoch) + ", rank " +
+                                             std::to_string(hc->dbg_rank) + " at " + std::to_string(hc->dbg_flag) +
+                                             "; stall " + std::to_string(hc->part_stall) + " over " +
+                                             std::to_string(hc->part_over) + ")");
             if (hc->part_over) {  // every rank rolled the iteration back: grow, remap, rerun
                 for (u32 i = 0; i < ns; ++i) {
                     LStep& L = P.steps[i];
                     if (hc->need_rows[i] > L.rows_cap) {
                         L.rows_cap = hc->need_rows[i] + hc->need_rows[i] / 2;
-                        L.row_start = DevBuf<u64>(c, L.rows_cap);
-                        L.row_off = DevBuf<u64>(c, L.rows_cap);
+                        L.alloc_rows(c);
                     }
                     if (hc->need_splits[i] > L.splits_cap) {
                         L.splits_cap = hc->need_splits[i] + hc->need_splits[i] / 2;
@@ -2054,10 +2094,9 @@ public:
                 hc->h[0].J = hc->h[0].N = hc->h[0].D = 0;
                 c.h2d(P.ctl.p, hc, sizeof(LoopCtl));
                 GD_CUDA(cudaMemsetAsync(&ps.mail->cursor, 0, sizeof(unsigned long long), c.stream));
-                u64 bar = 0;
-                host_allreduce(comm, &bar, 1, 0);  // every cursor reset before any rank routes again
                 c.sync();
                 destroy_graph();
+                ready();  // every cursor reset and every graph rebuilt before any rank routes again
                 continue;
             }
             if (hc->part_stall_any) {
@@ -2092,12 +2131,17 @@ public:
                 destroy_graph();
                 if (D == 0) break;
                 if (hc->iter >= iter_limit) break;
+                ready();
                 continue;
             }
             if (hc->done || hc->iter >= iter_limit) break;
             if (eager) continue;
             // a graph that stopped without a reason: cannot happen
             throw_logic("partitioned loop: graph stopped without termination, overflow or stall");
+        }
+        {  // no rank frees its mailbox / inboxes while a peer may still write them
+            u64 bar = 0;
+            host_allreduce(comm, &bar, 1, 0);
         }
         const u64 it = hc->iter - hist0;
         E.join_tuples += hc->part_join;

@@ -59,14 +59,11 @@ __device__ __forceinline__ void resolve(const LoopOuter& o, const LoopCtl* ctl, 
     }
 }
 
-// Home of a key: the first slot of its 4-slot bucket (one 32-byte sector of
-// packed slots; table capacities are multiples of 4).  Probing is linear
-// from the bucket start, so one sector read settles a key unless its whole
-// bucket is taken by other keys.  Homes are monotone in the hash (the zone
-// growth pass relies on it).
-__device__ __forceinline__ u64 hs_home(u64 key, u64 cap) {
-    return __umul64hi(fmix64(key ^ kHashSeed), cap) & ~3ull;
-}
+// Home slot of a key; homes are monotone in the hash (the zone growth pass
+// relies on it).  (4-slot aligned buckets read whole were measured slower on
+// C2: 118 ms with 2-slot and 129 ms with 4-slot first reads vs 104 ms for
+// exact homes — keys crowd the bucket starts and the wider reads spill.)
+__device__ __forceinline__ u64 hs_home(u64 key, u64 cap) { return __umul64hi(fmix64(key ^ kHashSeed), cap); }
 
 // Rare paths of a packed-slot insertion, out of line (register pressure of
 // the batched fast path): the key was seen in an earlier iteration (stamp
@@ -111,6 +108,11 @@ __device__ __noinline__ u32 insert_slow_packed(u64* __restrict__ tab, u64 cap, u
     }
 }
 
+// The same from the home slot (the caller's home-slot read or CAS returned o).
+__device__ __noinline__ u32 insert_slow_home(u64* __restrict__ tab, u64 cap, u32 sb, u64 st, u64 key, u64 o) {
+    return insert_slow_packed(tab, cap, sb, st, key, hs_home(key, cap), o);
+}
+
 __device__ __noinline__ u32 insert_slow_wide(HSlot* __restrict__ tab, u64 cap, u32 st, u64 key, u64 o) {
     u64 p = hs_home(key, cap);
     while (o != kEmptySlot && o != key) {
@@ -129,64 +131,101 @@ __device__ __noinline__ u32 insert_slow_wide(HSlot* __restrict__ tab, u64 cap, u
 // fresh: bit k = key k is new (appended by the caller); first: bit k = first
 // occurrence of key k in this iteration (stamp st) — the distinct count of
 // the join output.
-template <int PER, int NSLOT = 2>
+// L2 policy of the head-index reads of the NSLOT >= 2 path: evict-first
+// when hb.l2_hints (gd_device_config.l2_hints; measured slower on C2, off by
+// default); 0 = no hint.
+__device__ __forceinline__ u64 make_policy_first() {
+    u64 p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ u64 tab_policy(const LoopHeadBufs& hb) { return hb.l2_hints ? make_policy_first() : 0ull; }
+__device__ __forceinline__ u64 ld_tab(const u64* p, u64 pol) {
+    if (!pol) return __ldcg(p);
+    u64 v;
+    asm volatile("ld.global.cg.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol) : "memory");
+    return v;
+}
+
+template <int PER, int NSLOT = 1>
 __device__ __forceinline__ void hs_insert(const LoopHeadBufs& hb, u32 st, const u64 (&key)[PER], u32 ok,
                                           u32& fresh, u32& first) {
-    static_assert(NSLOT == 1 || NSLOT == 2 || NSLOT == 4, "bucket reads of 1, 2 or 4 slots");
+    static_assert(NSLOT == 0 || NSLOT == 1 || NSLOT == 2 || NSLOT == 4, "first reads of 0, 1, 2 or 4 slots");
     fresh = first = 0;
     u64 old[PER];
-    if (hb.sbits) {
+    if constexpr (NSLOT <= 1) {
+      if (hb.sbits) {
         u64* tab = static_cast<u64*>(hb.tab);
         const u32 sb = hb.sbits;
-        // Read the first NSLOT slots of every key's home bucket (16-byte
-        // loads inside one 32-byte sector) first — all of a thread's reads in
-        // flight together — then settle each key there: its own slot (seen
-        // before), or the first empty slot, claimed with one CAS that hits
-        // the line the read brought into L2.  Only keys whose slots read are
-        // all taken by other keys, or whose CAS lost a race, probe further
-        // (out of line).
-        u64 pos[PER];
-#pragma unroll
-        for (int k = 0; k < PER; ++k) pos[k] = hs_home(key[k], hb.tab_cap);
-        constexpr int NV = NSLOT > 1 ? NSLOT / 2 : 1;  // 16-byte vectors (or one 8-byte slot)
-        ulonglong2 b[PER][NV];
+        // NSLOT = 1 (default): load the home slots first, then CAS only the
+        // empty ones — the CAS hits the line the load brought into L2.
+        // NSLOT = 0: CAS first (one round trip, the CAS misses to DRAM).
+        u64 home[PER];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-            const ulonglong2* q = reinterpret_cast<const ulonglong2*>(tab + pos[k]);
+            home[k] = hs_home(key[k], hb.tab_cap);
+            if (NSLOT) old[k] = (ok >> k & 1) ? __ldcg(&tab[home[k]]) : 0ull;
+            else old[k] = (ok >> k & 1) ? atomicCAS(&tab[home[k]], kEmptySlot, key[k] << sb | st) : 0ull;
+        }
+        if (NSLOT) {
 #pragma unroll
-            for (int h = 0; h < NV; ++h) {
-                if (NSLOT == 1) b[k][h].x = (ok >> k & 1) ? __ldcg(tab + pos[k]) : 0ull;
-                else b[k][h] = (ok >> k & 1) ? __ldcg(q + h) : make_ulonglong2(0, 0);
+            for (int k = 0; k < PER; ++k)
+                if ((ok >> k & 1) && old[k] == kEmptySlot)
+                    old[k] = atomicCAS(&tab[home[k]], kEmptySlot, key[k] << sb | st);
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            if (!(ok >> k & 1)) continue;
+            u32 r;
+            if (old[k] == kEmptySlot) r = 3;
+            else if (old[k] == (key[k] << sb | st)) r = 0;
+            else r = insert_slow_home(tab, hb.tab_cap, sb, st, key[k], old[k]);
+            fresh |= (r & 1u) << k;
+            first |= (r >> 1) << k;
+        }
+        return;
+      }
+    } else if (hb.sbits) {
+        // NSLOT = 2 / 4: the first NSLOT slots from home read together, the
+        // key settled among them when they hold it or an empty slot (fewer
+        // slow-path round trips at the cost of registers; measured slower on
+        // C2 than NSLOT = 1).
+        u64* tab = static_cast<u64*>(hb.tab);
+        const u32 sb = hb.sbits;
+        const u64 pol = tab_policy(hb);
+        u64 pos[PER];
+        u64 b[PER][NSLOT ? NSLOT : 1];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            pos[k] = hs_home(key[k], hb.tab_cap);
+#pragma unroll
+            for (int h = 0; h < NSLOT; ++h) {
+                u64 q = pos[k] + h;
+                q = q >= hb.tab_cap ? q - hb.tab_cap : q;
+                b[k][h] = (ok >> k & 1) ? ld_tab(tab + q, pol) : 0ull;
             }
         }
         u32 cas = 0, slow = 0;
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             if (!(ok >> k & 1)) continue;
-            u64 w[NSLOT];
-#pragma unroll
-            for (int h = 0; h < NV; ++h) {
-                w[2 * h] = b[k][h].x;
-                if (NSLOT > 1) w[(2 * h + 1) % NSLOT] = b[k][h].y;
-            }
             u32 q = NSLOT;
             bool empty = false;
 #pragma unroll
             for (int j = NSLOT - 1; j >= 0; --j)  // first slot holding the key or empty
-                if (w[j] == kEmptySlot || (w[j] >> sb) == key[k]) {
+                if (b[k][j] == kEmptySlot || (b[k][j] >> sb) == key[k]) {
                     q = j;
-                    empty = w[j] == kEmptySlot;
+                    empty = b[k][j] == kEmptySlot;
                 }
-            if (q == NSLOT) {  // slots read all hold other keys: probe on from the last one
-                pos[k] += NSLOT - 1;
-                old[k] = w[NSLOT - 1];
-                slow |= 1u << k;
-            } else {
-                pos[k] += q;
-                old[k] = w[q];
-                if (empty) cas |= 1u << k;
-                else if (w[q] != (key[k] << sb | st)) slow |= 1u << k;  // seen before: stamp update
-            }
+            const u32 qq = q == (u32)NSLOT ? (u32)NSLOT - 1 : q;
+            old[k] = b[k][0];
+#pragma unroll
+            for (int j = 1; j < NSLOT; ++j)
+                if ((u32)j == qq) old[k] = b[k][j];
+            pos[k] += qq;
+            pos[k] = pos[k] >= hb.tab_cap ? pos[k] - hb.tab_cap : pos[k];
+            if (q == (u32)NSLOT || (!empty && old[k] != (key[k] << sb | st))) slow |= 1u << k;
+            else if (empty) cas |= 1u << k;
         }
 #pragma unroll
         for (int k = 0; k < PER; ++k)
@@ -202,7 +241,9 @@ __device__ __forceinline__ void hs_insert(const LoopHeadBufs& hb, u32 st, const 
             fresh |= (r & 1u) << k;
             first |= (r >> 1) << k;
         }
-    } else {
+        return;
+    }
+    {  // wide slots
         HSlot* tab = static_cast<HSlot*>(hb.tab);
 #pragma unroll
         for (int k = 0; k < PER; ++k)
@@ -860,6 +901,13 @@ __global__ void __launch_bounds__(kLT) loop_count_kernel(LoopCtl* ctl, u32 step,
         u64 n;
         resolve(o, ctl, outer, n);
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->step_n[step] = n;
+        if (sb.rc && n > sb.rows_cap) {  // the row ranges need n entries
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                atomicMax((unsigned long long*)&ctl->need_rows[step], (unsigned long long)(n + 1));
+                ctl->overflow = 1;
+            }
+            n = 0;
+        }
         u64 sum = 0;
         for (u64 base = (u64)blockIdx.x * kLTile; base < n; base += (u64)gridDim.x * kLTile) {
             u64 pre[kLItems];
@@ -875,6 +923,7 @@ __global__ void __launch_bounds__(kLT) loop_count_kernel(LoopCtl* ctl, u32 step,
             for (int j = 0; j < kLItems; ++j) {
                 const u64 r = base + threadIdx.x + (u64)j * kLT;
                 if (r >= n) continue;
+                if (sb.rc) sb.rc[r] = a[j] << 32 | c[j];  // the expansion reads it instead of re-probing
                 sum += c[j];
                 if (c[j] > heavy_min) {
                     const u64 segs = (c[j] + heavy_min - 1) / heavy_min;
@@ -907,7 +956,7 @@ struct XWarp {
 // head's index and appends the new keys to the log.
 template <int NS>
 struct InsertSink {
-    LoopHeadBufs hb;
+    const LoopHeadBufs& hb;  // the kernel parameter itself (a copy would take registers)
     u32 it;
     unsigned long long* log_n;
     __device__ __forceinline__ void round(XWarp& w, u32 m) {
@@ -1043,35 +1092,53 @@ __device__ __forceinline__ void expand_rows(const LoopCtl* ctl, u32 step, const 
         const u64 r = base + lane;
         u64 ov = 0, a = 0, c = 0;
         if (r < n) {
-            ov = outer[r];
-            dense_range(dv, outer_prefix(jd, ov), a, c);
+            if (sb.rc) {  // the row's range from loop_count: both loads independent
+                ov = outer[r];
+                const u64 v = __ldcg(sb.rc + r);
+                a = v >> 32;
+                c = v & 0xffffffffull;
+            } else {
+                ov = outer[r];
+                dense_range(dv, outer_prefix(jd, ov), a, c);
+            }
             if (c > heavy_min) c = 0;  // a heavy item (loop_count queued it)
         }
         const u64 incl = warp_inclusive_scan(c);
         const u64 T = __shfl_sync(0xffffffffu, incl, 31);
         const u64 excl = incl - c;
-        for (u64 j0 = 0; j0 < T; j0 += 32) {
-            const u64 j = j0 + lane;
-            // source lane: the last s with excl_s <= j (rows without
-            // output share the next row's excl and are never last)
-            u32 s = 0;
+        // kXB outputs per lane at a time: their inner loads in flight together
+        constexpr int kXB = 4;
+        for (u64 j0 = 0; j0 < T; j0 += 32 * kXB) {
+            u64 iv[kXB], so[kXB];
 #pragma unroll
-            for (u32 d = 16; d; d >>= 1) {
-                const u64 ex = __shfl_sync(0xffffffffu, excl, s + d);
-                if (ex <= j) s += d;
+            for (int q = 0; q < kXB; ++q) {
+                const u64 j = j0 + 32 * q + lane;
+                // source lane: the last s with excl_s <= j (rows without
+                // output share the next row's excl and are never last)
+                u32 s = 0;
+#pragma unroll
+                for (u32 d = 16; d; d >>= 1) {
+                    const u64 ex = __shfl_sync(0xffffffffu, excl, s + d);
+                    if (ex <= j) s += d;
+                }
+                const u64 sa = __shfl_sync(0xffffffffu, a, s);
+                const u64 se = __shfl_sync(0xffffffffu, excl, s);
+                so[q] = __shfl_sync(0xffffffffu, ov, s);
+                iv[q] = j < T ? inner[sa + (j - se)] : 0ull;
             }
-            const u64 sa = __shfl_sync(0xffffffffu, a, s);
-            const u64 se = __shfl_sync(0xffffffffu, excl, s);
-            const u64 so = __shfl_sync(0xffffffffu, ov, s);
-            bool have = false;
-            u64 key = 0;
-            if (j < T) {
-                const u64 iv = inner[sa + (j - se)];
-                have = passes(jd, so, iv);
-                key = project(jd, so, iv);
+#pragma unroll
+            for (int q = 0; q < kXB; ++q) {
+                if (j0 + 32 * q >= T) break;  // warp-uniform
+                const u64 j = j0 + 32 * q + lane;
+                bool have = false;
+                u64 key = 0;
+                if (j < T) {
+                    have = passes(jd, so[q], iv[q]);
+                    key = project(jd, so[q], iv[q]);
+                }
+                w.J += have;
+                x_emit(w, have, key, sink);
             }
-            w.J += have;
-            x_emit(w, have, key, sink);
         }
     }
     for (u64 i = gw; i < nheavy; i += nw) {  // heavy items: one segment of heavy_min outputs per warp
@@ -1199,7 +1266,7 @@ __device__ __forceinline__ u64 global_ns() {
 // until every rank reached the same epoch; out[s] = rank s's payload.
 // Returns false when a rank did not arrive within timeout_ns (a dead peer
 // must not hang the GPU: the caller stops the graph, the host reports it).
-__device__ bool peer_barrier(const PeerTab* tab, u64 epoch, const u64 (&val)[kPeerVals],
+__device__ bool peer_barrier(LoopCtl* ctl, const PeerTab* tab, u64 epoch, const u64 (&val)[kPeerVals],
                              u64 (&out)[kLoopMaxRanks][kPeerVals], u64 timeout_ns) {
     const u32 P = tab->P, me = tab->rank;
     for (u32 q = 0; q < P; ++q) {
@@ -1212,9 +1279,15 @@ __device__ bool peer_barrier(const PeerTab* tab, u64 epoch, const u64 (&val)[kPe
     PeerMail* mine = tab->mail[me];
     const u64 t0 = global_ns();
     for (u32 s = 0; s < P; ++s) {
-        while (ld_acquire_sys(&mine->flag[s]) < epoch) {
+        u64 f;
+        while ((f = ld_acquire_sys(&mine->flag[s])) < epoch) {
             __nanosleep(64);
-            if (global_ns() - t0 > timeout_ns) return false;
+            if (global_ns() - t0 > timeout_ns) {
+                ctl->dbg_rank = s;
+                ctl->dbg_flag = f;
+                ctl->dbg_epoch = epoch;
+                return false;
+            }
         }
 #pragma unroll
         for (u32 k = 0; k < kPeerVals; ++k) out[s][k] = __ldcv(&mine->val[s][k]);
@@ -1234,7 +1307,7 @@ __global__ void loop_peer_sync1_kernel(LoopCtl* ctl, PeerSyncDesc d) {
     ctl->part_epoch = epoch;
     const u64 mine[kPeerVals] = {(u64)(ctl->overflow | ctl->part_inbox_over), 0, 0, 0};
     __shared__ u64 got[kLoopMaxRanks][kPeerVals];
-    if (!peer_barrier(tab, epoch, mine, got, d.timeout_ns)) {
+    if (!peer_barrier(ctl, tab, epoch, mine, got, d.timeout_ns)) {
         ctl->part_timeout = 1;
         ctl->overflow = 1;
         if (d.use_cond) cudaGraphSetConditional(cond, 0);
@@ -1287,7 +1360,7 @@ __global__ void loop_peer_sync2_kernel(LoopCtl* ctl, PeerSyncDesc d) {
     ctl->part_epoch = epoch;
     const u64 mine[kPeerVals] = {D, (u64)stall, 0, 0};
     __shared__ u64 got[kLoopMaxRanks][kPeerVals];
-    if (!peer_barrier(tab, epoch, mine, got, d.timeout_ns)) {
+    if (!peer_barrier(ctl, tab, epoch, mine, got, d.timeout_ns)) {
         ctl->part_timeout = 1;
         if (d.use_cond) cudaGraphSetConditional(cond, 0);
         return;
@@ -1607,18 +1680,19 @@ int loop_grid(const Ctx& c) { return c.num_sms * 4; }
 // Slots read per key at the first probe (gd_device_config.insert_slots).
 #define SLOT_DISPATCH(c, kern, ...)                                      \
     do {                                                                 \
-        if ((c).cfg.insert_slots == 1) kern<1> __VA_ARGS__;              \
+        if ((c).cfg.insert_slots == 2) kern<2> __VA_ARGS__;              \
         else if ((c).cfg.insert_slots == 4) kern<4> __VA_ARGS__;         \
-        else kern<2> __VA_ARGS__;                                        \
+        else if ((c).cfg.insert_slots == 0) kern<0> __VA_ARGS__;         \
+        else kern<1> __VA_ARGS__;                                        \
     } while (0)
 
 void loop_prepare() {
     if (g_occ_temp) return;
     g_occ_temp = occupancy(loop_materialize_temp_kernel);
-    g_occ_insert = occupancy(loop_materialize_insert_kernel<2>);
-    g_occ_keys = occupancy(loop_insert_keys_kernel<2>);
-    g_occ_select = occupancy(loop_select_insert_kernel<2>);
-    g_occ_expand = occupancy(loop_expand_insert_kernel<2>);
+    g_occ_insert = occupancy(loop_materialize_insert_kernel<1>);
+    g_occ_keys = occupancy(loop_insert_keys_kernel<1>);
+    g_occ_select = occupancy(loop_select_insert_kernel<1>);
+    g_occ_expand = occupancy(loop_expand_insert_kernel<1>);
     g_occ_xroute = occupancy(loop_expand_route_kernel);
     g_occ_route = occupancy(loop_route_keys_kernel);
     g_occ_xtemp = occupancy(loop_expand_temp_kernel);

@@ -95,7 +95,8 @@ struct LoopCtl {
     u32 part_stall;       // this rank's insert did not fit its log / index: the host finishes it
     u32 part_stall_any;   // some rank stalled (the graph stopped on every rank)
     u32 part_timeout;     // a device barrier waited past its limit (the host raises GD_ERR_NCCL)
-    u32 pad3;
+    u32 dbg_rank;         // ... the first rank missing, its flag and the epoch waited for
+    u64 dbg_flag, dbg_epoch;
     // output window of a chain temp (host-driven windowed iteration, when a
     // step's temp exceeds gd_device_config.temp_limit_rows): step win_step
     // materializes only its outputs [win_lo, win_hi); win_hi = 0: no window
@@ -142,7 +143,7 @@ struct LoopHeadBufs {
     u64 tab_cap;
     u64 tab_limit;  // max keys before the table must grow
     u32 sbits;      // stamp bits of packed slots; 0 = wide HSlot
-    u32 pad;
+    u32 l2_hints;   // table accesses evict-first, join inputs evict-last (gd_device_config.l2_hints)
 };
 inline u64 loop_slot_bytes(u32 sbits) { return sbits ? 8 : sizeof(HSlot); }
 // Stamp bits for keys of `key_bits` bits (0: wide slots).
@@ -173,6 +174,7 @@ struct LoopStepBufs {
     u64 rows_cap;
     u64* splits;
     u64 splits_cap;
+    u64* rc;  // warp-expanded steps: row r's inner range, start << 32 | count (loop_count writes it)
 };
 
 // Candidate bound of the final steps -> overflow check of every head.

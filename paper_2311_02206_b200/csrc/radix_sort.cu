@@ -354,7 +354,13 @@ __global__ void __launch_bounds__(kPT, IP ? 2 : 1) onesweep_pipe_kernel(const u6
         mbar_init(&sm.mbar[0]);
         mbar_init(&sm.mbar[1]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const u32 first = atomicAdd(counter, 1u);
+        // static round-robin tiles (b, b + G, ...): every CTA of the grid is
+        // co-resident (sized from the occupancy), so a tile's predecessors
+        // are always being processed in the same round and the prefetched
+        // next tile never holds up another CTA's look-back (an atomic claim
+        // made at prefetch time did: measured 2x slower)
+        (void)counter;
+        const u32 first = blockIdx.x;
         sm.tile[0] = first;
         if (first < ntiles) issue(0, first);
     }
@@ -363,8 +369,8 @@ __global__ void __launch_bounds__(kPT, IP ? 2 : 1) onesweep_pipe_kernel(const u6
         __syncthreads();  // (A) previous tile fully written out; tile ids visible
         const u32 tile = sm.tile[cur];
         if (tile >= ntiles) break;
-        if (t == 0) {  // claim and prefetch the next tile into the other buffer
-            const u32 nx = atomicAdd(counter, 1u);
+        if (t == 0) {  // prefetch this CTA's next tile into the other buffer
+            const u32 nx = tile + gridDim.x;
             sm.tile[cur ^ 1] = nx;
             if (nx < ntiles) issue(cur ^ 1, nx);
         }
@@ -612,7 +618,12 @@ void launch_pipe_ip(Ctx& c, const u64* src, u64* dst, u64 pb, u64 pn, u32 shift,
     }
     const u64 tiles = (pn + kPTile - 1) / kPTile;
     const u64 grid = std::min<u64>(tiles, (u64)per_sm * c.num_sms);
-    kern<<<(unsigned)grid, kPT, smem, c.stream>>>(src, dst, pb, pn, shift, width, rd, wr, w, (u32)tiles);
+    // cooperative launch: the static round-robin tile order needs every CTA
+    // of the grid co-resident (the driver guarantees it or fails the launch)
+    u32 nt = (u32)tiles;
+    void* args[] = {(void*)&src, (void*)&dst, (void*)&pb, (void*)&pn, (void*)&shift, (void*)&width, (void*)&rd,
+                    (void*)&wr, (void*)&w, (void*)&nt};
+    GD_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(kPT), args, smem, c.stream));
 }
 
 template <int RB>

@@ -1,9 +1,10 @@
 #!/bin/bash
-# Round 2d: insert variants (bucket slots 1/2/4, split insert) and sort variants on C2.
+# Round 2d: targeted hang check, insert variants, sort variants on C2.
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
-timeout 600 python -m pytest tests/test_gpu_loop.py tests/test_gpu_sort.py -q -x -k "c1_all_modes or sg_corpus or sort" > gpurun_out/pytest_quick.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_quick.log
-for v in "GD_INSERT_SLOTS=2" "GD_INSERT_SLOTS=1" "GD_INSERT_SLOTS=4" "GD_LOOP_SPLIT=1" "GD_SORT_PIPE=0" "GD_SORT_PIPE=1 GD_SORT_DIGIT_BITS=8" "GD_SORT_PIPE=2"; do
+GD_LOOP_TRACE=1 timeout 120 python -m pytest tests/test_gpu_loop.py -x -q -k "sg_corpus_modes and window" > gpurun_out/pytest_window.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_window.log
+timeout 300 python scripts/sort_micro.py 200 771 > gpurun_out/sort_micro.log 2>&1
+for v in "GD_INSERT_SLOTS=2" "GD_INSERT_SLOTS=1" "GD_INSERT_SLOTS=4" "GD_LOOP_SPLIT=1" "GD_LOOP_SPLIT=1 GD_INSERT_SLOTS=1" "GD_SORT_PIPE=4"; do
   tag=$(echo $v | tr ' =' '__')
-  env $v timeout 600 python bench.py --steps 4 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err
+  env GD_SORT_PIPE=0 $v timeout 300 python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err
 done

@@ -150,10 +150,16 @@ def test_native_driver_multi_rank_loopback(prog, head, P, seed, n, dom, tiny, ex
 
     from paper_2311_02206_b200.partition import LoopbackComms, run_partitioned_native
 
-    cfg = dict(EXCHANGES[exchange], **({"min_capacities": 1} if tiny else {}))
+    import gc
+
+    cfg = dict(EXCHANGES[exchange], peer_timeout_ms=20000, **({"min_capacities": 1} if tiny else {}))
     rng = np.random.default_rng(seed)
     edges = random_relation(rng, 2, n, dom)
     ref = single(prog, edges)
+    # No context of an earlier test may be torn down (cudaFree: a device-wide
+    # synchronization holding the driver) while the ranks' device barriers
+    # spin: collect them now.
+    gc.collect()
     ctxs = [al.Context(0, config=cfg) for _ in range(P)]
     lb = LoopbackComms(ctxs[0], P)
     engines = []
@@ -175,7 +181,14 @@ def test_native_driver_multi_rank_loopback(prog, head, P, seed, n, dom, tiny, ex
     for t in th:
         t.start()
     for t in th:
-        t.join(timeout=120)
+        t.join(timeout=150)
+    if errs or any(t.is_alive() for t in th):
+        for t in th:  # failed ranks abort the transport: every rank returns
+            t.join(timeout=60)
+        if all(not t.is_alive() for t in th):  # orderly teardown before failing
+            for e in engines:
+                e.close()
+            lb.close()
     assert not errs, errs
     assert all(not t.is_alive() for t in th)
     assert iters == [ref.stats().iterations] * P
@@ -189,6 +202,8 @@ def test_native_driver_multi_rank_loopback(prog, head, P, seed, n, dom, tiny, ex
     for e in engines:
         e.close()
     lb.close()
+    for cx in ctxs:
+        cx.close()
 
 
 def test_native_driver_rejects_host_path():

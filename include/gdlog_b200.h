@@ -143,7 +143,8 @@ typedef struct gd_device_config {
     uint64_t download_chunk_rows;   /* staging chunk of packed downloads (1 << 20) */
     uint32_t sort_items;            /* onesweep keys per thread: 4, 8 or 16 (16) */
     uint32_t trace;                 /* stderr traces: bit 0 resident loop, bit 1 downloads (0) */
-    int32_t warp_expand;            /* final steps over a dense inner: count + warp-expanded insert (1) */
+    int32_t warp_expand;            /* final steps over a dense inner: count + warp-expanded insert (0:
+                                       the merge-path fused insert measured faster on C2, 163 vs 172 ms) */
     uint32_t sort_digit_bits;       /* pipelined sort: widest digit, 8..10 (10) */
     uint64_t heavy_rows;            /* ... rows with more outputs are expanded as segments of this many (4096) */
     int32_t sort_pipeline;          /* u64 sorts: 0 classic onesweep; 1 pipelined (bulk-copy prefetch, wide
@@ -156,11 +157,14 @@ typedef struct gd_device_config {
                                        in windows of at most this many (0: half the free HBM) */
     uint32_t peer_timeout_ms;       /* peer exchange: a device barrier waiting longer fails the run with
                                        GD_ERR_NCCL instead of hanging the GPU (60000) */
-    uint32_t insert_slots;          /* head-index inserts: slots read before the claiming CAS, 1, 2 or 4;
-                                       0 = CAS first, no read (1) */
-    uint32_t l2_hints;              /* head-index accesses L2 evict-first, join inputs evict-last:
-                                       0 never, 1 when the index exceeds 256 MB, 2 always (0:
-                                       measured slower on C2) */
+    uint32_t insert_slots;          /* head-index insert: 0 CAS first; 1 home slot loaded, then CAS, collisions
+                                       probed one key after another; 2 the same with every key's probe
+                                       steps batched (1) */
+    uint32_t insert_pipeline;       /* inserts of materialized keys (split final steps, partition inboxes):
+                                       two batches in flight per thread, batched probing (0) */
+    uint32_t insert_per_thread;     /* materialized-key inserts (insert_pipeline = 0): keys per thread,
+                                       8 (4 CTAs/SM), 4 (6 CTAs/SM) or 2 (8 CTAs/SM) (8) */
+    uint32_t reserved4;
     uint32_t l2_fetch_bytes;        /* cudaLimitMaxL2FetchGranularity set for the device when the context
                                        is configured: 32 / 64 / 128 bytes, 0 = leave the driver's (0) */
 } gd_device_config;

@@ -80,7 +80,9 @@ class gd_device_config(C.Structure):
         ("temp_limit_rows", u64),
         ("peer_timeout_ms", u32),
         ("insert_slots", u32),
-        ("l2_hints", u32),
+        ("insert_pipeline", u32),
+        ("insert_per_thread", u32),
+        ("reserved4", u32),
         ("l2_fetch_bytes", u32),
     ]
 

@@ -219,8 +219,9 @@ _ENV_KNOBS = {
     "GD_SORT_PIPE_MIN": ("sort_pipeline_min_keys", int),
     "GD_TEMP_LIMIT_ROWS": ("temp_limit_rows", int),
     "GD_INSERT_SLOTS": ("insert_slots", int),
-    "GD_L2_HINTS": ("l2_hints", int),
     "GD_L2_FETCH": ("l2_fetch_bytes", int),
+    "GD_INSERT_PIPE": ("insert_pipeline", int),
+    "GD_INSERT_PER": ("insert_per_thread", int),
     "GD_PART_EXCHANGE": ("partition_exchange", lambda v: {"peer": 0, "nccl": 1}[v]),
 }
 

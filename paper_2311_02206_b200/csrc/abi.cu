@@ -281,9 +281,7 @@ gd_status gd_ctx_set_device_config(gd_ctx* ctx, const gd_device_config* cfg) {
         if (cfg->partition_exchange > GD_EXCHANGE_NCCL) throw_config("partition_exchange out of range");
         if (cfg->sort_pipeline < 0 || cfg->sort_pipeline > 4) throw_config("sort_pipeline must be in [0, 4]");
         if (cfg->peer_timeout_ms == 0) throw_config("peer_timeout_ms must be positive");
-        if (cfg->insert_slots > 4 || cfg->insert_slots == 3)
-            throw_config("insert_slots must be 0 (CAS first), 1, 2 or 4");
-        if (cfg->l2_hints > 2) throw_config("l2_hints must be 0, 1 or 2");
+        if (cfg->insert_slots > 2) throw_config("insert_slots must be 0 (CAS first), 1 (load first) or 2 (batched)");
         if (cfg->l2_fetch_bytes && cfg->l2_fetch_bytes != 32 && cfg->l2_fetch_bytes != 64 &&
             cfg->l2_fetch_bytes != 128)
             throw_config("l2_fetch_bytes must be 0, 32, 64 or 128");

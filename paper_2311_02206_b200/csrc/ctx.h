@@ -132,7 +132,7 @@ inline gd_device_config default_device_config() {
     d.download_chunk_rows = 1u << 20;
     d.sort_items = 16;
     d.trace = 0;
-    d.warp_expand = 1;
+    d.warp_expand = 0;
     d.sort_digit_bits = 10;
     d.heavy_rows = 4096;
     d.sort_pipeline = 0;
@@ -141,7 +141,9 @@ inline gd_device_config default_device_config() {
     d.temp_limit_rows = 0;
     d.peer_timeout_ms = 60000;
     d.insert_slots = 1;
-    d.l2_hints = 0;
+    d.insert_pipeline = 0;
+    d.insert_per_thread = 8;
+    d.reserved4 = 0;
     d.l2_fetch_bytes = 0;
     return d;
 }

@@ -640,11 +640,6 @@ public:
     // sector scan) at load <= 1/2; a full table grows 4x (to load 1/8), so
     // the re-spreads move about a third of the final key count in total.
     static u64 tab_limit_of(u64 cap) { return cap / 2; }
-    // L2 eviction hints on the head index once it is larger than L2 (the
-    // join inputs, not the table lines, are what L2 should keep then).
-    u32 l2_hints_for(u64 tab_bytes) const {
-        return c.cfg.l2_hints == 1 ? (tab_bytes > (256ull << 20) ? 1u : 0u) : c.cfg.l2_hints == 2 ? 1u : 0u;
-    }
 
     // The recursive variants as loop steps (plan order, variant order): outer
     // source, join descriptor, inner copy and index (dense form when
@@ -804,8 +799,7 @@ public:
         };
         auto bufs_of = [&](u32 h) {
             return LoopHeadBufs{heads[h].log.p, heads[h].log_cap, heads[h].tab.p, heads[h].tab_cap,
-                                heads[h].tab_limit, heads[h].sbits,
-                                l2_hints_for(heads[h].tab_cap * loop_slot_bytes(heads[h].sbits))};
+                                heads[h].tab_limit, heads[h].sbits, 0};
         };
         // One iteration's kernel sequence (captured into the graph, or
         // launched eagerly when profiling).  The gate runs in the last CTA
@@ -1515,7 +1509,6 @@ public:
         b.tab_cap = H.tab_cap;
         b.tab_limit = H.tab_limit;
         b.sbits = H.sbits;
-        b.l2_hints = l2_hints_for(H.tab_cap * loop_slot_bytes(H.sbits));
         return b;
     }
 

@@ -131,26 +131,10 @@ __device__ __noinline__ u32 insert_slow_wide(HSlot* __restrict__ tab, u64 cap, u
 // fresh: bit k = key k is new (appended by the caller); first: bit k = first
 // occurrence of key k in this iteration (stamp st) — the distinct count of
 // the join output.
-// L2 policy of the head-index reads of the NSLOT >= 2 path: evict-first
-// when hb.l2_hints (gd_device_config.l2_hints; measured slower on C2, off by
-// default); 0 = no hint.
-__device__ __forceinline__ u64 make_policy_first() {
-    u64 p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ u64 tab_policy(const LoopHeadBufs& hb) { return hb.l2_hints ? make_policy_first() : 0ull; }
-__device__ __forceinline__ u64 ld_tab(const u64* p, u64 pol) {
-    if (!pol) return __ldcg(p);
-    u64 v;
-    asm volatile("ld.global.cg.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol) : "memory");
-    return v;
-}
-
 template <int PER, int NSLOT = 1>
 __device__ __forceinline__ void hs_insert(const LoopHeadBufs& hb, u32 st, const u64 (&key)[PER], u32 ok,
                                           u32& fresh, u32& first) {
-    static_assert(NSLOT == 0 || NSLOT == 1 || NSLOT == 2 || NSLOT == 4, "first reads of 0, 1, 2 or 4 slots");
+    static_assert(NSLOT == 0 || NSLOT == 1 || NSLOT == 2, "insert mode 0 (CAS first), 1 (load first), 2 (batched)");
     fresh = first = 0;
     u64 old[PER];
     if constexpr (NSLOT <= 1) {
@@ -186,60 +170,52 @@ __device__ __forceinline__ void hs_insert(const LoopHeadBufs& hb, u32 st, const 
         return;
       }
     } else if (hb.sbits) {
-        // NSLOT = 2 / 4: the first NSLOT slots from home read together, the
-        // key settled among them when they hold it or an empty slot (fewer
-        // slow-path round trips at the cost of registers; measured slower on
-        // C2 than NSLOT = 1).
+        // NSLOT = 2: load-first with BATCHED probing.  Every unresolved key
+        // of the thread advances one step per pass — a claiming CAS on an
+        // empty slot, a stamp CAS on its own slot, or the load of the next
+        // slot after another key — and a pass issues all of them before
+        // consuming any, so a thread (and its warp) pays the longest probe
+        // chain among its keys instead of the sum of its collisions.
         u64* tab = static_cast<u64*>(hb.tab);
         const u32 sb = hb.sbits;
-        const u64 pol = tab_policy(hb);
+        const u64 smask = (1ull << sb) - 1;
         u64 pos[PER];
-        u64 b[PER][NSLOT ? NSLOT : 1];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             pos[k] = hs_home(key[k], hb.tab_cap);
-#pragma unroll
-            for (int h = 0; h < NSLOT; ++h) {
-                u64 q = pos[k] + h;
-                q = q >= hb.tab_cap ? q - hb.tab_cap : q;
-                b[k][h] = (ok >> k & 1) ? ld_tab(tab + q, pol) : 0ull;
-            }
+            old[k] = (ok >> k & 1) ? __ldcg(&tab[pos[k]]) : 0ull;
         }
-        u32 cas = 0, slow = 0;
+        u32 pend = ok;
+        while (pend) {
+            u32 cas = 0;
 #pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            if (!(ok >> k & 1)) continue;
-            u32 q = NSLOT;
-            bool empty = false;
-#pragma unroll
-            for (int j = NSLOT - 1; j >= 0; --j)  // first slot holding the key or empty
-                if (b[k][j] == kEmptySlot || (b[k][j] >> sb) == key[k]) {
-                    q = j;
-                    empty = b[k][j] == kEmptySlot;
+            for (int k = 0; k < PER; ++k) {
+                if (!(pend >> k & 1)) continue;
+                if (old[k] == kEmptySlot) {
+                    cas |= 1u << k;
+                } else if ((old[k] >> sb) == key[k]) {
+                    if ((old[k] & smask) == st) pend &= ~(1u << k);  // seen this iteration already
+                    else cas |= 1u << k;                               // stamp update
+                } else {  // another key: the next slot
+                    pos[k] = pos[k] + 1 == hb.tab_cap ? 0 : pos[k] + 1;
+                    old[k] = __ldcg(&tab[pos[k]]);
                 }
-            const u32 qq = q == (u32)NSLOT ? (u32)NSLOT - 1 : q;
-            old[k] = b[k][0];
+            }
+            u64 res[PER];
 #pragma unroll
-            for (int j = 1; j < NSLOT; ++j)
-                if ((u32)j == qq) old[k] = b[k][j];
-            pos[k] += qq;
-            pos[k] = pos[k] >= hb.tab_cap ? pos[k] - hb.tab_cap : pos[k];
-            if (q == (u32)NSLOT || (!empty && old[k] != (key[k] << sb | st))) slow |= 1u << k;
-            else if (empty) cas |= 1u << k;
-        }
+            for (int k = 0; k < PER; ++k)
+                if (cas >> k & 1) res[k] = atomicCAS(&tab[pos[k]], old[k], key[k] << sb | st);
 #pragma unroll
-        for (int k = 0; k < PER; ++k)
-            if (cas >> k & 1) old[k] = atomicCAS(&tab[pos[k]], kEmptySlot, key[k] << sb | st);
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            if (!(ok >> k & 1)) continue;
-            u32 r;
-            if ((cas >> k & 1) && old[k] == kEmptySlot) r = 3;
-            else if (!(cas >> k & 1) && !(slow >> k & 1)) r = 0;  // already stamped this iteration
-            else if ((cas >> k & 1) && old[k] == (key[k] << sb | st)) r = 0;
-            else r = insert_slow_packed(tab, hb.tab_cap, sb, st, key[k], pos[k], old[k]);
-            fresh |= (r & 1u) << k;
-            first |= (r >> 1) << k;
+            for (int k = 0; k < PER; ++k) {
+                if (!(cas >> k & 1)) continue;
+                if (res[k] == old[k]) {  // claimed: a new key (was empty) or this iteration's first sight
+                    fresh |= (u32)(old[k] == kEmptySlot) << k;
+                    first |= 1u << k;
+                    pend &= ~(1u << k);
+                } else {
+                    old[k] = res[k];  // lost a race: look at what is there now
+                }
+            }
         }
         return;
     }
@@ -724,6 +700,29 @@ __device__ __forceinline__ void append_cta(u64* __restrict__ log, unsigned long 
     }
 }
 
+// Appends the warp's new keys to the log with one atomic per warp: no CTA
+// barrier, so a warp's next keys do not wait for the slowest warp's probes.
+template <int PER>
+__device__ __forceinline__ void append_warp(u64* __restrict__ log, unsigned long long* log_n, const u64 (&key)[PER],
+                                            u32 fresh) {
+    u32 m[PER];
+    u32 tot = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        m[k] = __ballot_sync(0xffffffffu, fresh >> k & 1);
+        tot += __popc(m[k]);
+    }
+    unsigned long long base = 0;
+    if (lane_id() == 0 && tot) base = atomicAdd(log_n, (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const u32 lt = lanemask_lt();
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        if (fresh >> k & 1) log[base + __popc(m[k] & lt)] = key[k];
+        base += __popc(m[k]);
+    }
+}
+
 // Flushes per-thread J / N / D counts of a CTA (once, at exit).
 __device__ __forceinline__ void flush_counts(LoopCtl* ctl, u32 head, u32 step, u64 J, u64 N, u64 D, u64* red,
                                              bool step_total = true) {
@@ -797,14 +796,11 @@ __global__ void __launch_bounds__(kLT, 6) loop_materialize_insert_kernel(
 // `keys` by loop_materialize_temp): each thread keeps kInsPer CASes in flight
 // (the random-CAS rate needs ~8 K in flight per SM; a fused materialize
 // kernel holds too many registers to get there).
-constexpr int kInsPer = 8;
-template <int NS>
-__global__ void __launch_bounds__(kLT, 4) loop_insert_keys_kernel(LoopCtl* ctl, u32 step, u32 head,
+template <int NS, int kInsPer = 8, int kMinCta = 4>
+__global__ void __launch_bounds__(kLT, kMinCta) loop_insert_keys_kernel(LoopCtl* ctl, u32 step, u32 head,
                                                                   const u64* __restrict__ keys, LoopHeadBufs hb,
                                                                   LoopEndDesc e, int do_end) {
     __shared__ u64 red[kLT / 32];
-    __shared__ u32 s_warp[kLT / 32];
-    __shared__ u64 s_base;
     __shared__ u32 s_flag;
     if (!cta_stopped(ctl, &s_flag)) {
         const u64 n = ctl->step_total[step];
@@ -825,7 +821,107 @@ __global__ void __launch_bounds__(kLT, 4) loop_insert_keys_kernel(LoopCtl* ctl, 
             J += __popc(ok);
             N += __popc(first);
             D += __popc(fresh);
-            append_cta<kInsPer>(hb.log, &ctl->h[head].log_n, key, fresh, s_warp, &s_base);
+            append_warp<kInsPer>(hb.log, &ctl->h[head].log_n, key, fresh);
+        }
+        flush_counts(ctl, head, step, J, N, D, red, false);
+    }
+    if (do_end && last_cta(ctl, &s_flag) && threadIdx.x == 0) end_body(ctl, e);
+}
+
+// Pipelined insert of materialized keys (packed slots; split final steps and
+// the partitioned inbox): each thread keeps two batches of kPP keys — the
+// next batch's key reads and home-slot reads are issued before the current
+// batch's CASes, probes and log append run, so DRAM latency overlaps the
+// L2 round trips instead of adding to them.  Probing is batched (every
+// unresolved key advances one step per pass) and the append is one atomic
+// per warp.
+constexpr int kPP = 4;
+struct PipeBatch {
+    u64 key[kPP];
+    u64 old[kPP];
+    u32 ok;
+};
+
+__device__ __forceinline__ void pipe_issue(PipeBatch& b, const u64* __restrict__ keys, u64 base, u64 n,
+                                           const u64* tab, u64 cap) {
+    b.ok = 0;
+#pragma unroll
+    for (int k = 0; k < kPP; ++k) {
+        const u64 j = base + (u64)k * kLT + threadIdx.x;
+        b.key[k] = j < n ? __ldcs(keys + j) : 0ull;
+        b.ok |= (u32)(j < n) << k;
+    }
+#pragma unroll
+    for (int k = 0; k < kPP; ++k) b.old[k] = (b.ok >> k & 1) ? __ldcg(tab + hs_home(b.key[k], cap)) : 0ull;
+}
+
+// Settles batch b (its home slots already read) and appends its new keys.
+__device__ __forceinline__ void pipe_resolve(PipeBatch& b, u64* tab, u64 cap, u32 sb, u32 st, u64* __restrict__ log,
+                                             unsigned long long* log_n, u64& J, u64& N, u64& D) {
+    const u64 smask = (1ull << sb) - 1;
+    u64 pos[kPP];
+#pragma unroll
+    for (int k = 0; k < kPP; ++k) pos[k] = hs_home(b.key[k], cap);
+    u32 pend = b.ok, fresh = 0, first = 0;
+    while (pend) {
+        u32 cas = 0;
+#pragma unroll
+        for (int k = 0; k < kPP; ++k) {
+            if (!(pend >> k & 1)) continue;
+            if (b.old[k] == kEmptySlot) {
+                cas |= 1u << k;
+            } else if ((b.old[k] >> sb) == b.key[k]) {
+                if ((b.old[k] & smask) == st) pend &= ~(1u << k);
+                else cas |= 1u << k;
+            } else {
+                pos[k] = pos[k] + 1 == cap ? 0 : pos[k] + 1;
+                b.old[k] = __ldcg(tab + pos[k]);
+            }
+        }
+        u64 res[kPP];
+#pragma unroll
+        for (int k = 0; k < kPP; ++k)
+            if (cas >> k & 1) res[k] = atomicCAS(tab + pos[k], b.old[k], b.key[k] << sb | st);
+#pragma unroll
+        for (int k = 0; k < kPP; ++k) {
+            if (!(cas >> k & 1)) continue;
+            if (res[k] == b.old[k]) {
+                fresh |= (u32)(b.old[k] == kEmptySlot) << k;
+                first |= 1u << k;
+                pend &= ~(1u << k);
+            } else {
+                b.old[k] = res[k];
+            }
+        }
+    }
+    J += __popc(b.ok);
+    N += __popc(first);
+    D += __popc(fresh);
+    append_warp<kPP>(log, log_n, b.key, fresh);
+}
+
+__global__ void __launch_bounds__(kLT, 3) loop_insert_keys_pipe_kernel(LoopCtl* ctl, u32 step, u32 head,
+                                                                       const u64* __restrict__ keys, LoopHeadBufs hb,
+                                                                       LoopEndDesc e, int do_end) {
+    __shared__ u64 red[kLT / 32];
+    __shared__ u32 s_flag;
+    if (!cta_stopped(ctl, &s_flag)) {
+        const u64 n = ctl->step_total[step];
+        const u32 st = ctl->iter + 1 - ctl->epoch_base;
+        u64* tab = static_cast<u64*>(hb.tab);
+        unsigned long long* log_n = reinterpret_cast<unsigned long long*>(&ctl->h[head].log_n);
+        constexpr u64 kChunk = (u64)kLT * kPP;
+        const u64 stride = (u64)gridDim.x * kChunk;
+        u64 J = 0, N = 0, D = 0;
+        u64 base = (u64)blockIdx.x * kChunk;
+        PipeBatch a, b;
+        pipe_issue(a, keys, base, n, tab, hb.tab_cap);
+        while (base < n) {
+            const u64 next = base + stride;
+            pipe_issue(b, keys, next, n, tab, hb.tab_cap);  // in flight while a settles
+            pipe_resolve(a, tab, hb.tab_cap, hb.sbits, st, hb.log, log_n, J, N, D);
+            a = b;
+            base = next;
         }
         flush_counts(ctl, head, step, J, N, D, red, false);
     }
@@ -1665,7 +1761,7 @@ int occupancy(Kern k, size_t smem = 0) {
 }
 
 int g_occ_temp = 0, g_occ_insert = 0, g_occ_select = 0, g_occ_keys = 0, g_occ_expand = 0, g_occ_xroute = 0,
-    g_occ_route = 0, g_occ_xtemp = 0;
+    g_occ_route = 0, g_occ_xtemp = 0, g_occ_keys_pipe = 0, g_occ_keys4 = 0, g_occ_keys2 = 0;
 // Insert grid = waves x resident CTAs: CTAs beyond the resident set start as
 // others finish, so the hardware balances the iteration's tiles.  Large
 // relations (log capacity >= kWideLog rows) run 3 waves (C2 -2.8%, SG
@@ -1677,11 +1773,11 @@ constexpr u64 kWideLog = 64ull << 20;
 
 int loop_grid(const Ctx& c) { return c.num_sms * 4; }
 
-// Slots read per key at the first probe (gd_device_config.insert_slots).
+// Insert mode (gd_device_config.insert_slots): 0 CAS first, 1 load first,
+// 2 load first with batched probing.
 #define SLOT_DISPATCH(c, kern, ...)                                      \
     do {                                                                 \
         if ((c).cfg.insert_slots == 2) kern<2> __VA_ARGS__;              \
-        else if ((c).cfg.insert_slots == 4) kern<4> __VA_ARGS__;         \
         else if ((c).cfg.insert_slots == 0) kern<0> __VA_ARGS__;         \
         else kern<1> __VA_ARGS__;                                        \
     } while (0)
@@ -1691,11 +1787,14 @@ void loop_prepare() {
     g_occ_temp = occupancy(loop_materialize_temp_kernel);
     g_occ_insert = occupancy(loop_materialize_insert_kernel<1>);
     g_occ_keys = occupancy(loop_insert_keys_kernel<1>);
+    g_occ_keys4 = occupancy(loop_insert_keys_kernel<1, 4, 6>);
+    g_occ_keys2 = occupancy(loop_insert_keys_kernel<1, 2, 8>);
     g_occ_select = occupancy(loop_select_insert_kernel<1>);
     g_occ_expand = occupancy(loop_expand_insert_kernel<1>);
     g_occ_xroute = occupancy(loop_expand_route_kernel);
     g_occ_route = occupancy(loop_route_keys_kernel);
     g_occ_xtemp = occupancy(loop_expand_temp_kernel);
+    g_occ_keys_pipe = occupancy(loop_insert_keys_pipe_kernel);
 }
 
 void loop_fill_u64(Ctx& c, u64* p, u64 n, u64 v) {
@@ -1855,8 +1954,18 @@ void loop_insert_keys(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, 
                       const LoopHeadBufs& hb, const LoopEndDesc* end) {
     LoopEndDesc e{};
     if (end) e = *end;
-    SLOT_DISPATCH(c, loop_insert_keys_kernel, <<<c.num_sms * g_occ_keys, kLT, 0, s>>>(ctl, step, head, keys, hb, e,
-                                                                                      end ? 1 : 0));
+    if (hb.sbits && c.cfg.insert_pipeline)
+        loop_insert_keys_pipe_kernel<<<c.num_sms * g_occ_keys_pipe, kLT, 0, s>>>(ctl, step, head, keys, hb, e,
+                                                                                end ? 1 : 0);
+    else if (c.cfg.insert_per_thread == 4)
+        loop_insert_keys_kernel<1, 4, 6><<<c.num_sms * g_occ_keys4, kLT, 0, s>>>(ctl, step, head, keys, hb, e,
+                                                                                end ? 1 : 0);
+    else if (c.cfg.insert_per_thread == 2)
+        loop_insert_keys_kernel<1, 2, 8><<<c.num_sms * g_occ_keys2, kLT, 0, s>>>(ctl, step, head, keys, hb, e,
+                                                                                end ? 1 : 0);
+    else
+        SLOT_DISPATCH(c, loop_insert_keys_kernel, <<<c.num_sms * g_occ_keys, kLT, 0, s>>>(ctl, step, head, keys, hb,
+                                                                                          e, end ? 1 : 0));
     c.check_launch();
 }
 

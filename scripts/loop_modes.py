@@ -13,19 +13,19 @@ import torch  # noqa: E402
 from paper_2311_02206_b200 import arraylog as al  # noqa: E402
 from paper_2311_02206_b200 import workloads as W  # noqa: E402
 
-ctx = al.Context(0, torch.cuda.current_stream().cuda_stream)
+_s = torch.cuda.Stream()
+torch.cuda.set_stream(_s)
+ctx = al.Context(0, _s.cuda_stream)
 cases = {"chain3000": np.stack([np.arange(2999), np.arange(1, 3000)], 1).astype(np.uint64)}
 if len(sys.argv) > 1:
     cases["c2"] = W.tc_pl(5_000_000, 5_000_000, 200, 1.05, 1)
-modes = {"graph": {"GD_LOOP_MODE": "graph"}, "batch16": {"GD_LOOP_MODE": "batch", "GD_LOOP_BATCH": "16"},
-         "batch64": {"GD_LOOP_MODE": "batch", "GD_LOOP_BATCH": "64"}, "eager": {"GD_LOOP_MODE": "eager"},
-         "host": {"GD_LOOP": "0"}}
+modes = {"graph": {"loop_mode": 0}, "batch16": {"loop_mode": 2, "loop_batch": 16},
+         "batch64": {"loop_mode": 2, "loop_batch": 64}, "eager": {"loop_mode": 1},
+         "host": {"resident_loop": 0}, "graph_noxp": {"loop_mode": 0, "warp_expand": 0}}
 for name, edges in cases.items():
     d = torch.from_numpy(edges.view(np.int64)).cuda()
     for m, kv in modes.items():
-        for k in ("GD_LOOP_MODE", "GD_LOOP_BATCH", "GD_LOOP"):
-            os.environ.pop(k, None)
-        os.environ.update(kv)
+        ctx.set_config(**{"loop_mode": 0, "loop_batch": 16, "resident_loop": 1, "warp_expand": 1, **kv})
         ts = []
         for rep in range(3):
             e = al.engine("reach", ctx=ctx)

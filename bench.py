@@ -375,6 +375,17 @@ def main():
             gbs = roof["traffic"] / (roof["avg_launch_ms"] / 1e3) / 1e9
             roof["random_access"] = {"dram_gbs": gbs, "ceiling_gbs": ceil["cas_dram_tbps"] * 1e3,
                                      "frac": gbs / (ceil["cas_dram_tbps"] * 1e3), "ceiling_source": ceil["source"]}
+        # op-rate view of the fused insert: join rows settled per second of
+        # insert-kernel time against the measured random 8-byte access
+        # ceilings of this B200 (every join row is one random slot access)
+        if dom == "join_insert" and rc.exists():
+            ceil = json.loads(rc.read_text())
+            ins_ms = prof["join_insert"][0]
+            rate = float(np.mean(joins)) / (ins_ms / 1e3) / 1e9 if ins_ms else 0.0
+            roof["op_rate"] = {"achieved_gops": rate, "unit": "G join rows/s",
+                               "ceiling_load_gops": ceil["load_gops"], "ceiling_cas_gops": ceil["cas_gops"],
+                               "frac_of_load_ceiling": rate / ceil["load_gops"],
+                               "frac_of_cas_ceiling": rate / ceil["cas_gops"], "ceiling_source": ceil["source"]}
         jm = [k for k in ("join_probe", "join_materialize", "join_insert", "diff_merge", "difference")]
         jm_ms = sum(prof[k][0] for k in jm)
         jm_by = sum(prof[k][2] for k in jm)

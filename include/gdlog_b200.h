@@ -164,9 +164,13 @@ typedef struct gd_device_config {
                                        two batches in flight per thread, batched probing (0) */
     uint32_t insert_per_thread;     /* materialized-key inserts (insert_pipeline = 0): keys per thread,
                                        8 (4 CTAs/SM), 4 (6 CTAs/SM) or 2 (8 CTAs/SM) (8) */
-    uint32_t reserved4;
+    uint32_t sort_ballot;           /* classic sort of >= 16 x sort_pipeline_min_keys keys: ballot ranking on
+                                       passes whose digits are spread, MATCH.ANY on skewed ones (1) */
     uint32_t l2_fetch_bytes;        /* cudaLimitMaxL2FetchGranularity set for the device when the context
                                        is configured: 32 / 64 / 128 bytes, 0 = leave the driver's (0) */
+    uint32_t sort_min_ctas;         /* classic onesweep: 4 = registers capped for 4 CTAs per SM, else the
+                                       compiler's choice (3 per SM) (0) */
+    uint32_t reserved5;
 } gd_device_config;
 
 void gd_device_config_default(gd_device_config* cfg);

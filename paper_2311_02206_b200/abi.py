@@ -82,8 +82,10 @@ class gd_device_config(C.Structure):
         ("insert_slots", u32),
         ("insert_pipeline", u32),
         ("insert_per_thread", u32),
-        ("reserved4", u32),
+        ("sort_ballot", u32),
         ("l2_fetch_bytes", u32),
+        ("sort_min_ctas", u32),
+        ("reserved5", u32),
     ]
 
 

@@ -222,6 +222,8 @@ _ENV_KNOBS = {
     "GD_L2_FETCH": ("l2_fetch_bytes", int),
     "GD_INSERT_PIPE": ("insert_pipeline", int),
     "GD_INSERT_PER": ("insert_per_thread", int),
+    "GD_SORT_BALLOT": ("sort_ballot", int),
+    "GD_SORT_MIN_CTAS": ("sort_min_ctas", int),
     "GD_PART_EXCHANGE": ("partition_exchange", lambda v: {"peer": 0, "nccl": 1}[v]),
 }
 

@@ -176,6 +176,7 @@ def device_rows(e, head):
 def check_invariants(e, head, program, edges):
     """Device-side checks of a full-size result (no CPU engine at this size)."""
     import torch
+    e.ctx.trim()  # the fixpoint's cached device blocks back to the driver (torch allocates below)
     rows = device_rows(e, head)
     n = rows.shape[0]
     hist = e.delta_history(head)
@@ -209,11 +210,15 @@ def record_of(e, head):
             "delta_history_sha": hist_sha(e.delta_history(head))}
 
 
-def run_loopback(program, head, edges, P):
+def run_loopback(program, head, edges, P, name=None):
     """The native partitioned driver over P loopback ranks (threads, one
-    context each); returns the union record (shard digests add up)."""
+    context each); returns the union record (shard digests add up).  Up to
+    3 ranks use the peer exchange, more the NCCL exchange (peer-exchange
+    ranks sharing one GPU need a hardware queue each, test_gpu_partition)."""
+    import gc
+    gc.collect()
     from paper_2311_02206_b200.partition import LoopbackComms, run_partitioned_native
-    ctxs = [al.Context(0) for _ in range(P)]
+    ctxs = [al.Context(0, config={"partition_exchange": 0 if P <= 3 else 1}) for _ in range(P)]
     lb = LoopbackComms(ctxs[0], P)
     engines = []
     for r in range(P):
@@ -271,7 +276,7 @@ def scale_records(name, check=True):
         h.close()
         al.default_context().trim()
     for P in cfg["parts"]:
-        out[f"loopback_p{P}"] = run_loopback(cfg["program"], cfg["head"], edges, P)
+        out[f"loopback_p{P}"] = run_loopback(cfg["program"], cfg["head"], edges, P, name)
     return out
 
 

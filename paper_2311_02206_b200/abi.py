@@ -85,7 +85,7 @@ class gd_device_config(C.Structure):
         ("sort_ballot", u32),
         ("l2_fetch_bytes", u32),
         ("sort_min_ctas", u32),
-        ("reserved5", u32),
+        ("download_delta", u32),
     ]
 
 

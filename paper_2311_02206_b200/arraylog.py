@@ -224,6 +224,7 @@ _ENV_KNOBS = {
     "GD_INSERT_PER": ("insert_per_thread", int),
     "GD_SORT_BALLOT": ("sort_ballot", int),
     "GD_SORT_MIN_CTAS": ("sort_min_ctas", int),
+    "GD_DL_DELTA": ("download_delta", int),
     "GD_PART_EXCHANGE": ("partition_exchange", lambda v: {"peer": 0, "nccl": 1}[v]),
 }
 

@@ -354,6 +354,13 @@ public:
                 c.d2h_bytes += nd * ar * sizeof(u64);
             }
         }
+        const bool trace = (c.cfg.trace & 2) != 0;
+        double t_wait = 0, t_unpack = 0;
+        const unsigned hw = std::thread::hardware_concurrency();
+        const unsigned nt = std::max(1u, std::min(hw ? hw : 8u, 32u));
+        if (c.cfg.download_delta && n > 0) {
+            download_delta_rows(keys, n, ar, out, nt, t_wait, t_unpack);
+        } else {
         const u64 kChunk = c.cfg.download_chunk_rows;
         u64* stage[2];
         void* area = c.pinned_staging(2 * kChunk * sizeof(u64));
@@ -363,16 +370,12 @@ public:
         GD_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
         const u32 bits = E.enc.e.bits;
         const u64 mask = bits >= 64 ? ~0ull : (1ull << bits) - 1;
-        const unsigned hw = std::thread::hardware_concurrency();
-        const unsigned nt = std::max(1u, std::min(hw ? hw : 8u, 32u));
         const u64 nchunks = (n + kChunk - 1) / kChunk;
         auto issue = [&](u64 k) {
             const u64 b = k * kChunk, m = std::min(kChunk, n - b);
             c.d2h(stage[k & 1], keys + b, m * sizeof(u64));
             GD_CUDA(cudaEventRecord(ev[k & 1], c.stream));
         };
-        const bool trace = (c.cfg.trace & 2) != 0;
-        double t_wait = 0, t_unpack = 0;
         // one pool of nt threads for the whole download; chunk k is handed
         // out by a generation counter once its copy has landed
         std::atomic<u64> gen{0};
@@ -456,6 +459,7 @@ public:
         quit.store(true, std::memory_order_release);
         for (auto& th : pool) th.join();
         pool.clear();
+        }
         double t_direct = 0;
         if (s2) {
             const double td = Ctx::now_s();
@@ -468,6 +472,136 @@ public:
                     "direct tail %.1f ms\n",
                     (unsigned long long)n_all, (unsigned long long)(n_all - n), nt, t_wait * 1e3, t_unpack * 1e3,
                     t_direct * 1e3);
+    }
+
+    // Delta-compressed download of n canonical keys into rows (download_delta):
+    // the device bit-packs the gaps of every 64-key block (delta.cu), chunks
+    // of 16 K blocks cross PCIe into two pinned staging areas (heads, widths,
+    // payload), and nt host threads rebuild the keys — a running sum per
+    // block — and unpack them into the caller's rows while the next chunk is
+    // in flight.  C2: ~3 bytes per row over PCIe instead of 8.
+    void download_delta_rows(const u64* keys, u64 n, u32 ar, u64* out, unsigned nt, double& t_wait,
+                             double& t_unpack) {
+        DeltaPacked d;
+        delta_pack(c, keys, n, d);
+        constexpr u64 kBPC = 16384;  // blocks per chunk (1 M keys)
+        const u64 nchunks = (d.nb + kBPC - 1) / kBPC;
+        std::vector<u64> coff(nchunks + 1);
+        {
+            DevBuf<u64> dco(c, nchunks + 1);
+            delta_chunk_offsets(c, d, kBPC, nchunks, dco.p);
+            c.d2h(coff.data(), dco.p, (nchunks + 1) * sizeof(u64));
+            c.sync();
+        }
+        u64 maxw = 0;
+        for (u64 k = 0; k < nchunks; ++k) maxw = std::max(maxw, coff[k + 1] - coff[k]);
+        // staging area per buffer: heads | widths (padded to words) | payload
+        const u64 area = kBPC + kBPC / 8 + maxw + 8;
+        u64* stage0 = static_cast<u64*>(c.pinned_staging(2 * area * sizeof(u64)));
+        u64* stage[2] = {stage0, stage0 + area};
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        std::vector<std::thread> pool;
+        std::atomic<bool> quit{false};
+        struct Cleanup {
+            std::function<void()> f;
+            ~Cleanup() { f(); }
+        } cleanup{[&] {
+            quit.store(true, std::memory_order_release);
+            for (auto& th : pool)
+                if (th.joinable()) th.join();
+            cudaStreamSynchronize(c.stream);
+            for (auto e : ev)
+                if (e) cudaEventDestroy(e);
+        }};
+        GD_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+        GD_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+        auto issue = [&](u64 k) {
+            const u64 b0 = k * kBPC, nbk = std::min(kBPC, d.nb - b0);
+            u64* st = stage[k & 1];
+            c.d2h(st, d.heads.p + b0, nbk * sizeof(u64));
+            c.d2h(st + kBPC, d.widths.p + b0, nbk);
+            if (coff[k + 1] > coff[k])
+                c.d2h(st + kBPC + kBPC / 8, d.payload.p + coff[k], (coff[k + 1] - coff[k]) * sizeof(u64));
+            GD_CUDA(cudaEventRecord(ev[k & 1], c.stream));
+        };
+        const u32 bits = E.enc.e.bits;
+        const u64 cmask = bits >= 64 ? ~0ull : (1ull << bits) - 1;
+        std::atomic<u64> gen{0};
+        std::atomic<unsigned> left{0};
+        u64 cur_k = 0;
+        auto decode = [&](unsigned t) {
+            const u64 k = cur_k, b0 = k * kBPC, nbk = std::min(kBPC, d.nb - b0);
+            const u64 lo = nbk * t / nt, hi = nbk * (t + 1) / nt;
+            const u64* st = stage[k & 1];
+            const u64* heads = st;
+            const uint8_t* widths = reinterpret_cast<const uint8_t*>(st + kBPC);
+            const u64* pay = st + kBPC + kBPC / 8;
+            u64 wo = 0;  // payload word offset of block lo within the chunk
+            for (u64 b = 0; b < lo; ++b) {
+                const u64 cnt = std::min<u64>(kDeltaBlock, n - (b0 + b) * kDeltaBlock);
+                wo += ((cnt - 1) * widths[b] + 63) / 64;
+            }
+            for (u64 b = lo; b < hi; ++b) {
+                const u64 first = (b0 + b) * kDeltaBlock;
+                const u64 cnt = std::min<u64>(kDeltaBlock, n - first);
+                const u32 w = widths[b];
+                const u64 wm = w >= 64 ? ~0ull : (1ull << w) - 1;
+                const u64* p = pay + wo;
+                u64 key = heads[b];
+                u64* dst = out + first * ar;
+                for (u64 i = 0;; ++i) {
+                    if (ar == 2) {
+#if defined(__x86_64__)
+                        _mm_stream_si64(reinterpret_cast<long long*>(dst), (long long)((key >> bits) & cmask));
+                        _mm_stream_si64(reinterpret_cast<long long*>(dst + 1), (long long)(key & cmask));
+#else
+                        dst[0] = (key >> bits) & cmask;
+                        dst[1] = key & cmask;
+#endif
+                    } else {
+                        for (u32 col = 0; col < ar; ++col) dst[col] = (key >> ((ar - 1 - col) * bits)) & cmask;
+                    }
+                    dst += ar;
+                    if (i + 1 >= cnt) break;
+                    const u64 pos = i * w;
+                    const u32 q = (u32)(pos >> 6), sh = (u32)(pos & 63);
+                    u64 v = p[q] >> sh;
+                    if (sh && sh + w > 64) v |= p[q + 1] << (64 - sh);
+                    key += v & wm;
+                }
+                wo += ((cnt - 1) * w + 63) / 64;
+            }
+#if defined(__x86_64__)
+            _mm_sfence();
+#endif
+        };
+        for (unsigned t = 1; t < nt; ++t)
+            pool.emplace_back([&, t] {
+                u64 seen = 0;
+                while (true) {
+                    u64 g;
+                    while ((g = gen.load(std::memory_order_acquire)) == seen && !quit.load(std::memory_order_acquire))
+                        std::this_thread::yield();
+                    if (quit.load(std::memory_order_acquire)) return;
+                    seen = g;
+                    decode(t);
+                    left.fetch_sub(1, std::memory_order_acq_rel);
+                }
+            });
+        issue(0);
+        for (u64 k = 0; k < nchunks; ++k) {
+            const double tw = Ctx::now_s();
+            GD_CUDA(cudaEventSynchronize(ev[k & 1]));
+            t_wait += Ctx::now_s() - tw;
+            const double tu = Ctx::now_s();
+            if (k + 1 < nchunks) issue(k + 1);  // stage[(k+1)&1] was decoded at step k-1
+            cur_k = k;
+            left.store(nt - 1, std::memory_order_release);
+            gen.fetch_add(1, std::memory_order_acq_rel);
+            decode(0);
+            while (left.load(std::memory_order_acquire) != 0) std::this_thread::yield();
+            t_unpack += Ctx::now_s() - tu;
+        }
     }
 
     u64 digest(u32 r) override {

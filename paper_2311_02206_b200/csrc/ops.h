@@ -33,6 +33,20 @@ inline u32 bitwidth(u64 v) {  // bits needed to represent v (0 -> 0)
 template <typename K>
 K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits);
 
+// ---- delta.cu (download compression) ----------------------------------
+constexpr u32 kDeltaBlock = 64;  // keys per delta block
+struct DeltaPacked {
+    u64 n = 0, nb = 0, words = 0;
+    DevBuf<u64> heads;        // first key of each block
+    DevBuf<uint8_t> widths;   // bits per gap of each block
+    DevBuf<u64> offs;         // first payload word of each block (nb + 1)
+    DevBuf<u64> payload;      // gaps, bit-packed per block
+};
+// Delta bit-packs n strictly increasing keys; returns the payload words.
+u64 delta_pack(Ctx& c, const u64* keys, u64 n, DeltaPacked& out);
+// dev_out[k] = d.offs[min(k * blocks_per_chunk, nb)] for k = 0..nchunks.
+void delta_chunk_offsets(Ctx& c, const DeltaPacked& d, u64 blocks_per_chunk, u64 nchunks, u64* dev_out);
+
 // ---- primitives.cu --------------------------------------------------
 u64 max_value(Ctx& c, const u64* vals, u64 n);  // 0 for n == 0
 

@@ -18,8 +18,11 @@ def canonical(a):
     return np.unique(a, axis=0)
 
 
+@pytest.mark.parametrize("delta", [1, 0])
 @pytest.mark.parametrize("arity,n,hi", [(2, 3_000_000, 1 << 20), (3, 2_100_000, 1 << 14), (2, 40_000_000, 1 << 30)])
-def test_host_unpack_matches(ref, arity, n, hi):
+def test_host_unpack_matches(ref, arity, n, hi, delta):
+    """Downloads of packed keys (delta-compressed or plain) unpacked by host
+    threads equal the device-unpacked rows and the canonical input."""
     src = COPY2 if arity == 2 else COPY3
     r = ref.engine(src)
     prog = program_from_ref(r)
@@ -27,7 +30,7 @@ def test_host_unpack_matches(ref, arity, n, hi):
     e = rng.integers(0, hi, size=(n, arity), dtype=np.uint64)
     outs = {}
     for mode in ("1", "0"):
-        with al.default_context().configured(host_unpack=int(mode)):
+        with al.default_context().configured(host_unpack=int(mode), download_delta=delta):
             g = al.engine(prog)
             g.load_edb("E", al.tuple_array(arity, e))
             g.run()
@@ -38,6 +41,8 @@ def test_host_unpack_matches(ref, arity, n, hi):
 
 @pytest.mark.parametrize("frac", ["0.25", "0.6"])
 def test_pinned_destination_direct_tail(ref, frac):
+    """(download_delta = 0: the transfer counter is checked against the
+    plain packed-key formula; the delta path is covered below.)"""
     """Into a pinned destination the tail rows are unpacked on the device
     and DMA'd straight into the caller's rows on a second stream while the
     host unpacks the head (download_packed): same bytes as a pageable
@@ -58,10 +63,75 @@ def test_pinned_destination_direct_tail(ref, frac):
     want = canonical(e)
     assert n == len(want)
     pinned = torch.empty((n, 2), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
-    with g.ctx.configured(download_direct_frac=float(frac)):
+    with g.ctx.configured(download_direct_frac=float(frac), download_delta=0):
         h0, d0 = g.ctx.transfer_bytes()
         g.ctx.check(g.ctx.lib.gd_engine_relation_download(g.h, rid, pinned.ctypes.data_as(C.c_void_p), n))
         h1, d1 = g.ctx.transfer_bytes()
     assert np.array_equal(pinned, want)
     nd = int(n * float(frac))
     assert d1 - d0 == (n - nd) * 8 + nd * 16  # packed head + unpacked direct tail
+
+
+@pytest.mark.parametrize("case", ["dense", "sparse", "mixed", "wide3", "tail"])
+def test_delta_download_gap_widths(ref, case):
+    """Delta-compressed download across gap widths: runs of consecutive keys
+    (1-bit gaps), sparse keys (wide gaps), blocks mixing both, arity-3 keys
+    with 60-bit packed values (gaps up to 60 bits) and sizes that end in a
+    partial block — rows equal the canonical input; the compressed transfer
+    is smaller than 8 bytes per row for dense data."""
+    rng = np.random.default_rng(hash(case) & 0xffff)
+    if case == "dense":
+        e = np.stack([np.repeat(np.arange(1500, dtype=np.uint64), 1000), np.tile(np.arange(1000, dtype=np.uint64), 1500)], 1)
+        arity = 2
+    elif case == "sparse":
+        e = rng.integers(0, 1 << 31, size=(1_500_000, 2), dtype=np.uint64)
+        arity = 2
+    elif case == "mixed":
+        a = np.stack([np.zeros(1_000_000, np.uint64), np.arange(1_000_000, dtype=np.uint64)], 1)
+        b = rng.integers(1, 1 << 30, size=(600_000, 2), dtype=np.uint64)
+        e = np.vstack([a, b])
+        arity = 2
+    elif case == "wide3":
+        e = rng.integers(0, 1 << 20, size=(1_200_000, 3), dtype=np.uint64)
+        arity = 3
+    else:
+        e = rng.integers(0, 1 << 22, size=(1_048_576 + 37, 2), dtype=np.uint64)
+        arity = 2
+    prog = program_from_ref(ref.engine(COPY2 if arity == 2 else COPY3))
+    want = canonical(e)
+    outs = {}
+    for delta in (1, 0):
+        with al.default_context().configured(download_delta=delta):
+            g = al.engine(prog)
+            g.load_edb("E", al.tuple_array(arity, e))
+            g.run()
+            h0, d0 = g.ctx.transfer_bytes()
+            outs[delta] = g.relation("C").data.copy()
+            h1, d1 = g.ctx.transfer_bytes()
+            outs[f"bytes{delta}"] = d1 - d0
+    assert np.array_equal(outs[1].reshape(-1, arity), want)
+    assert np.array_equal(outs[0], outs[1])
+    if case == "dense":
+        assert outs["bytes1"] < 2 * len(want)  # ~1.2 bits per gap + block headers
+
+
+@pytest.mark.parametrize("frac", ["0.0", "0.1", "0.5"])
+def test_pinned_destination_delta(ref, frac):
+    """Delta-compressed head + device-unpacked direct tail into a pinned
+    destination: same rows as the canonical input."""
+    import ctypes as C
+
+    import torch
+
+    prog = program_from_ref(ref.engine(COPY2))
+    rng = np.random.default_rng(78)
+    e = rng.integers(0, 1 << 22, size=(3_000_000, 2), dtype=np.uint64)
+    g = al.engine(prog)
+    g.load_edb("E", al.tuple_array(2, e))
+    g.run()
+    rid = g._rid("C")
+    n = g.relation_count("C")
+    pinned = torch.empty((n, 2), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    with g.ctx.configured(download_direct_frac=float(frac), download_delta=1):
+        g.ctx.check(g.ctx.lib.gd_engine_relation_download(g.h, rid, pinned.ctypes.data_as(C.c_void_p), n))
+    assert np.array_equal(pinned, canonical(e))

@@ -140,7 +140,7 @@ typedef struct gd_device_config {
     int32_t dedup_split;            /* split large dedup sets into L2-sized parts (1) */
     int32_t host_unpack;            /* downloads move packed keys, host threads unpack (1) */
     double download_direct_frac;    /* pinned destinations: share of rows unpacked on the device and DMA'd
-                                       into the caller's rows (0.1: with delta-compressed keys the host's
+                                       into the caller's rows (0.15: with delta-compressed keys the host's
                                        row writes, not PCIe, bound the download) */
     uint64_t download_chunk_rows;   /* staging chunk of packed downloads (1 << 20) */
     uint32_t sort_items;            /* onesweep keys per thread: 4, 8 or 16 (16) */
@@ -173,6 +173,9 @@ typedef struct gd_device_config {
                                        is configured: 32 / 64 / 128 bytes, 0 = leave the driver's (0) */
     uint32_t sort_min_ctas;         /* classic onesweep: 4 = registers capped for 4 CTAs per SM, else the
                                        compiler's choice (3 per SM) (0) */
+    uint32_t expand_keys_per_lane;  /* warp-expanded insert: keys per lane per insert round, 8 (3 CTAs/SM)
+                                       or 4 (5 CTAs/SM) (8) */
+    uint32_t reserved6;
     uint32_t download_delta;        /* host downloads of canonical u64 keys: gaps of 64-key blocks bit-packed
                                        on the device, keys rebuilt by host threads (1) */
 } gd_device_config;

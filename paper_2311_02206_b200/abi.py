@@ -85,6 +85,8 @@ class gd_device_config(C.Structure):
         ("sort_ballot", u32),
         ("l2_fetch_bytes", u32),
         ("sort_min_ctas", u32),
+        ("expand_keys_per_lane", u32),
+        ("reserved6", u32),
         ("download_delta", u32),
     ]
 

@@ -128,7 +128,7 @@ inline gd_device_config default_device_config() {
     d.dedup_part_slots = 8u << 20;
     d.dedup_split = 1;
     d.host_unpack = 1;
-    d.download_direct_frac = 0.1;
+    d.download_direct_frac = 0.15;
     d.download_chunk_rows = 1u << 20;
     d.sort_items = 16;
     d.trace = 0;
@@ -146,6 +146,8 @@ inline gd_device_config default_device_config() {
     d.sort_ballot = 0;
     d.l2_fetch_bytes = 0;
     d.sort_min_ctas = 0;
+    d.expand_keys_per_lane = 8;
+    d.reserved6 = 0;
     d.download_delta = 1;
     return d;
 }

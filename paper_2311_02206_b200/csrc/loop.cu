@@ -1050,30 +1050,31 @@ struct XWarp {
 
 // Sink of the warp expansion: inserts buf[0, m) (m <= kXRound) into the
 // head's index and appends the new keys to the log.
-template <int NS>
+template <int NS, int PER = kXPer>
 struct InsertSink {
+    static constexpr int kRound = 32 * PER;
     const LoopHeadBufs& hb;  // the kernel parameter itself (a copy would take registers)
     u32 it;
     unsigned long long* log_n;
     __device__ __forceinline__ void round(XWarp& w, u32 m) {
         __syncwarp();
         const u32 lane = lane_id();
-        u64 key[kXPer];
+        u64 key[PER];
         u32 ok = 0;
 #pragma unroll
-        for (int k = 0; k < kXPer; ++k) {
+        for (int k = 0; k < PER; ++k) {
             const u32 idx = lane + 32u * k;
             key[k] = idx < m ? w.buf[idx] : 0ull;
             ok |= (u32)(idx < m) << k;
         }
         u32 fresh, first;
-        hs_insert<kXPer, NS>(hb, it, key, ok, fresh, first);
+        hs_insert<PER, NS>(hb, it, key, ok, fresh, first);
         w.N += __popc(first);
         w.D += __popc(fresh);
-        u32 mk[kXPer];
+        u32 mk[PER];
         u32 tot = 0;
 #pragma unroll
-        for (int k = 0; k < kXPer; ++k) {
+        for (int k = 0; k < PER; ++k) {
             mk[k] = __ballot_sync(0xffffffffu, fresh >> k & 1);
             tot += __popc(mk[k]);
         }
@@ -1082,7 +1083,7 @@ struct InsertSink {
         base = __shfl_sync(0xffffffffu, base, 0);
         const u32 lt = lanemask_lt();
 #pragma unroll
-        for (int k = 0; k < kXPer; ++k) {
+        for (int k = 0; k < PER; ++k) {
             if (fresh >> k & 1) hb.log[base + __popc(mk[k] & lt)] = key[k];
             base += __popc(mk[k]);
         }
@@ -1094,6 +1095,7 @@ struct InsertSink {
 // (one atomic per round on the step's row count, coalesced stores); the
 // insert runs as its own kernel (loop_insert_keys) over the temp.
 struct TempSink {
+    static constexpr int kRound = kXRound;
     u64* temp;
     unsigned long long* total;
     __device__ __forceinline__ void round(XWarp& w, u32 m) {
@@ -1113,6 +1115,7 @@ struct TempSink {
 // (peer) stores.  Keys that do not fit raise part_inbox_over; the iteration
 // is rolled back on every rank at the next barrier.
 struct RouteSink {
+    static constexpr int kRound = kXRound;
     const PeerTab* tab;
     LoopCtl* ctl;
     __device__ __forceinline__ void round(XWarp& w, u32 m) {
@@ -1164,11 +1167,11 @@ __device__ __forceinline__ void x_emit(XWarp& w, bool have, u64 key, Sink& sink)
     const u32 mask = __ballot_sync(0xffffffffu, have);
     if (have) w.buf[w.fill + __popc(mask & lanemask_lt())] = key;
     w.fill += __popc(mask);
-    if (w.fill >= (u32)kXRound) {
-        sink.round(w, kXRound);
-        const u32 rest = w.fill - kXRound;
+    if (w.fill >= (u32)Sink::kRound) {
+        sink.round(w, Sink::kRound);
+        const u32 rest = w.fill - Sink::kRound;
         const u32 lane = lane_id();
-        const u64 t = lane < rest ? w.buf[kXRound + lane] : 0ull;
+        const u64 t = lane < rest ? w.buf[Sink::kRound + lane] : 0ull;
         __syncwarp();
         if (lane < rest) w.buf[lane] = t;
         w.fill = rest;
@@ -1259,18 +1262,18 @@ __device__ __forceinline__ void expand_rows(const LoopCtl* ctl, u32 step, const 
     if (w.fill) sink.round(w, w.fill);
 }
 
-template <int NS>
-__global__ void __launch_bounds__(kLT, 3) loop_expand_insert_kernel(
+template <int NS, int PER = kXPer>
+__global__ void __launch_bounds__(kLT, PER >= 8 ? 3 : 5) loop_expand_insert_kernel(
     LoopCtl* ctl, u32 step, u32 head, LoopOuter o, const u64* __restrict__ inner, DevJoin jd, LoopDense dv,
     LoopStepBufs sb, u64 heavy_min, LoopHeadBufs hb, LoopEndDesc e, int do_end) {
-    __shared__ u64 sbuf[kLT / 32][kXBuf];
+    __shared__ u64 sbuf[kLT / 32][PER >= 8 ? kXBuf : kXBuf / 2];
     __shared__ u64 red[kLT / 32];
     __shared__ u32 s_flag;
     if (!cta_stopped(ctl, &s_flag)) {
         const u64* outer;
         u64 n;
         resolve(o, ctl, outer, n);
-        InsertSink<NS> sink{hb, ctl->iter + 1 - ctl->epoch_base,
+        InsertSink<NS, PER> sink{hb, ctl->iter + 1 - ctl->epoch_base,
                         reinterpret_cast<unsigned long long*>(&ctl->h[head].log_n)};
         XWarp w{sbuf[threadIdx.x >> 5], 0, 0, 0, 0};
         expand_rows(ctl, step, outer, n, inner, jd, dv, sb, heavy_min, w, sink);
@@ -1761,7 +1764,7 @@ int occupancy(Kern k, size_t smem = 0) {
 }
 
 int g_occ_temp = 0, g_occ_insert = 0, g_occ_select = 0, g_occ_keys = 0, g_occ_expand = 0, g_occ_xroute = 0,
-    g_occ_route = 0, g_occ_xtemp = 0, g_occ_keys_pipe = 0, g_occ_keys4 = 0, g_occ_keys2 = 0;
+    g_occ_route = 0, g_occ_xtemp = 0, g_occ_keys_pipe = 0, g_occ_keys4 = 0, g_occ_keys2 = 0, g_occ_expand4 = 0;
 // Insert grid = waves x resident CTAs: CTAs beyond the resident set start as
 // others finish, so the hardware balances the iteration's tiles.  Large
 // relations (log capacity >= kWideLog rows) run 3 waves (C2 -2.8%, SG
@@ -1791,6 +1794,7 @@ void loop_prepare() {
     g_occ_keys2 = occupancy(loop_insert_keys_kernel<1, 2, 8>);
     g_occ_select = occupancy(loop_select_insert_kernel<1>);
     g_occ_expand = occupancy(loop_expand_insert_kernel<1>);
+    g_occ_expand4 = occupancy(loop_expand_insert_kernel<1, 4>);
     g_occ_xroute = occupancy(loop_expand_route_kernel);
     g_occ_route = occupancy(loop_route_keys_kernel);
     g_occ_xtemp = occupancy(loop_expand_temp_kernel);
@@ -2024,7 +2028,11 @@ void loop_expand_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head
     LoopEndDesc e{};
     if (end) e = *end;
     const int waves = c.cfg.insert_waves ? (int)c.cfg.insert_waves : 1;
-    SLOT_DISPATCH(c, loop_expand_insert_kernel, <<<c.num_sms * g_occ_expand * waves, kLT, 0, s>>>(
+    if (c.cfg.expand_keys_per_lane == 4)
+        loop_expand_insert_kernel<1, 4><<<c.num_sms * g_occ_expand4 * waves, kLT, 0, s>>>(
+            ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0);
+    else
+        SLOT_DISPATCH(c, loop_expand_insert_kernel, <<<c.num_sms * g_occ_expand * waves, kLT, 0, s>>>(
         ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0));
     c.check_launch();
 }

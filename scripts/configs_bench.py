@@ -12,7 +12,9 @@ import torch  # noqa: E402
 from paper_2311_02206_b200 import arraylog as al  # noqa: E402
 from paper_2311_02206_b200 import workloads as W  # noqa: E402
 
-ctx = al.Context(0, torch.cuda.current_stream().cuda_stream)
+_s = torch.cuda.Stream()  # a real stream: the events below are recorded where the engine runs
+torch.cuda.set_stream(_s)
+ctx = al.Context(0, _s.cuda_stream)
 names = sys.argv[1:] or ["c1_tc_rand", "c3_sg_tree", "c3_sg_tree_w1000", "c3_sg_tree_w4000", "c4_cspa", "c5_tc_dag"]
 for name in names:
     cfg = W.CONFIGS[name]
@@ -25,9 +27,9 @@ for name in names:
             e.load_edb_device(k, dev[k].data_ptr(), len(v))
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+        a.record(_s)
         e.run()
-        b.record()
+        b.record(_s)
         torch.cuda.synchronize()
         if rep:
             times.append(a.elapsed_time(b))

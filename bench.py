@@ -438,7 +438,8 @@ def main():
         # rows by host threads
         e2e = {"value": float(np.mean(joins)) / float(np.mean(e2e_t)), "unit": "tuples/s",
                "h2d_bytes_per_step": int(hb), "d2h_bytes_per_step": int(db),
-               "host_rows_bytes": int(reach_n * 16), "seconds_per_step": float(np.mean(e2e_t))}
+               "host_rows_bytes": int(reach_n * 16), "seconds_per_step": float(np.mean(e2e_t)),
+               "step_s": [round(t, 4) for t in e2e_t]}
 
     # parity of the measured C2 run: the committed full-scale record
     # (tests/golden/scale_digests.json: resident loop == host loop ==

@@ -175,7 +175,8 @@ typedef struct gd_device_config {
                                        compiler's choice (3 per SM) (0) */
     uint32_t expand_keys_per_lane;  /* warp-expanded insert: keys per lane per insert round, 8 (3 CTAs/SM)
                                        or 4 (5 CTAs/SM) (8) */
-    uint32_t reserved6;
+    uint32_t warp_append;           /* merge-path fused insert: log append with one atomic per warp instead
+                                       of one per CTA tile (two CTA barriers fewer per tile) (0) */
     uint32_t download_delta;        /* host downloads of canonical u64 keys: gaps of 64-key blocks bit-packed
                                        on the device, keys rebuilt by host threads (1) */
 } gd_device_config;

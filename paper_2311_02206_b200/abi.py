@@ -86,7 +86,7 @@ class gd_device_config(C.Structure):
         ("l2_fetch_bytes", u32),
         ("sort_min_ctas", u32),
         ("expand_keys_per_lane", u32),
-        ("reserved6", u32),
+        ("warp_append", u32),
         ("download_delta", u32),
     ]
 

@@ -226,6 +226,7 @@ _ENV_KNOBS = {
     "GD_SORT_MIN_CTAS": ("sort_min_ctas", int),
     "GD_DL_DELTA": ("download_delta", int),
     "GD_XP_PER": ("expand_keys_per_lane", int),
+    "GD_WARP_APPEND": ("warp_append", int),
     "GD_PART_EXCHANGE": ("partition_exchange", lambda v: {"peer": 0, "nccl": 1}[v]),
 }
 

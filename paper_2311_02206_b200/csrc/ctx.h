@@ -147,7 +147,7 @@ inline gd_device_config default_device_config() {
     d.l2_fetch_bytes = 0;
     d.sort_min_ctas = 0;
     d.expand_keys_per_lane = 8;
-    d.reserved6 = 0;
+    d.warp_append = 0;
     d.download_delta = 1;
     return d;
 }

@@ -933,7 +933,7 @@ public:
         };
         auto bufs_of = [&](u32 h) {
             return LoopHeadBufs{heads[h].log.p, heads[h].log_cap, heads[h].tab.p, heads[h].tab_cap,
-                                heads[h].tab_limit, heads[h].sbits, 0};
+                                heads[h].tab_limit, heads[h].sbits, c.cfg.warp_append};
         };
         // One iteration's kernel sequence (captured into the graph, or
         // launched eagerly when profiling).  The gate runs in the last CTA
@@ -1643,6 +1643,7 @@ public:
         b.tab_cap = H.tab_cap;
         b.tab_limit = H.tab_limit;
         b.sbits = H.sbits;
+        b.warp_append = c.cfg.warp_append;
         return b;
     }
 

@@ -785,7 +785,8 @@ __global__ void __launch_bounds__(kLT, 6) loop_materialize_insert_kernel(
             J += __popc(ok);
             N += __popc(first);
             D += __popc(fresh);
-            append_cta<kPer>(hb.log, &ctl->h[head].log_n, key, fresh, s_warp, &s_base);
+            if (hb.warp_append) append_warp<kPer>(hb.log, &ctl->h[head].log_n, key, fresh);
+            else append_cta<kPer>(hb.log, &ctl->h[head].log_n, key, fresh, s_warp, &s_base);
         }
         flush_counts(ctl, head, step, J, N, D, red);
     }

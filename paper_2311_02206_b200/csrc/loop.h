@@ -143,7 +143,7 @@ struct LoopHeadBufs {
     u64 tab_cap;
     u64 tab_limit;  // max keys before the table must grow
     u32 sbits;      // stamp bits of packed slots; 0 = wide HSlot
-    u32 pad;
+    u32 warp_append;  // fused inserts append with one atomic per warp instead of per CTA tile
 };
 inline u64 loop_slot_bytes(u32 sbits) { return sbits ? 8 : sizeof(HSlot); }
 // Stamp bits for keys of `key_bits` bits (0: wide slots).

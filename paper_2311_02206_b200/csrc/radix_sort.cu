@@ -179,31 +179,26 @@ __global__ void __launch_bounds__(kSortThreads, MINB) onesweep_kernel(
     // trips instead of one per tile.
     u32 excl = 0;
     if (tile > 0) {
-        constexpr int kLookWindow = 16;
+        // Window of kLookWindow predecessors loaded together, consumed in
+        // order; an unpublished predecessor is waited on alone (one status
+        // word per retry — re-reading the whole window while spinning tripled
+        // the L2 reads of a pass, profiles/r2_ncu_captures.md).
+        constexpr int kLookWindow = 8;
         long long pred = (long long)tile - 1;
-        while (true) {
-            u32 s[kLookWindow];
+        bool found = false;
+        while (!found) {
+            u32 sv[kLookWindow];
 #pragma unroll
             for (int w = 0; w < kLookWindow; ++w)
-                s[w] = pred - w >= 0 ? ld_relaxed32(status + (u64)(pred - w) * kRadix + t) : kSFlagP;
-            int first_inv = kLookWindow, first_p = kLookWindow;
+                sv[w] = pred - w >= 0 ? ld_relaxed32(status + (u64)(pred - w) * kRadix + t) : kSFlagP;
 #pragma unroll
-            for (int w = kLookWindow - 1; w >= 0; --w) {
-                const u32 f = s[w] >> 30;
-                if (f == 0) first_inv = w;
-                if (f == 2) first_p = w;
+            for (int w = 0; w < kLookWindow; ++w) {
+                if (found) break;
+                u32 v = sv[w];
+                while ((v >> 30) == 0) v = ld_relaxed32(status + (u64)(pred - w) * kRadix + t);
+                excl += v & kSMask;
+                found = (v >> 30) == 2;
             }
-            if (first_inv < first_p) {  // an unpublished tile before any prefix: wait on it
-#pragma unroll
-                for (int w = 0; w < kLookWindow; ++w)
-                    if (w < first_inv) excl += s[w] & kSMask;
-                pred -= first_inv;
-                continue;
-            }
-#pragma unroll
-            for (int w = 0; w < kLookWindow; ++w)
-                if (w <= first_p) excl += s[w] & kSMask;
-            if (first_p < kLookWindow) break;
             pred -= kLookWindow;
         }
         st_relaxed32(my_status, kSFlagP | (excl + cnt));

@@ -144,7 +144,7 @@ typedef struct gd_device_config {
                                        row writes, not PCIe, bound the download) */
     uint64_t download_chunk_rows;   /* staging chunk of packed downloads (1 << 20) */
     uint32_t sort_items;            /* onesweep keys per thread: 4, 8 or 16 (16) */
-    uint32_t trace;                 /* stderr traces: bit 0 resident loop, bit 1 downloads (0) */
+    uint32_t trace;                 /* stderr traces: bit 0 resident loop, bit 1 downloads, bit 2 sort (0) */
     int32_t warp_expand;            /* final steps over a dense inner: count + warp-expanded insert (0:
                                        the merge-path fused insert measured faster on C2, 163 vs 172 ms) */
     uint32_t sort_digit_bits;       /* pipelined sort: widest digit, 8..10 (10) */
@@ -166,9 +166,10 @@ typedef struct gd_device_config {
                                        two batches in flight per thread, batched probing (0) */
     uint32_t insert_per_thread;     /* materialized-key inserts (insert_pipeline = 0): keys per thread,
                                        8 (4 CTAs/SM), 4 (6 CTAs/SM) or 2 (8 CTAs/SM) (8) */
-    uint32_t sort_ballot;           /* classic sort of >= 16 x sort_pipeline_min_keys keys: ballot ranking on
-                                       passes whose digits are spread, MATCH.ANY on skewed ones (0: no gain
-                                       measured on C2, 35.7 vs 35.2 ms) */
+    uint32_t sort_ballot;           /* classic sort of >= 16 x sort_pipeline_min_keys keys: a pass whose input
+                                       holds at least this many distinct digits per 32 consecutive keys
+                                       (sampled before the pass) ranks with ballots, else MATCH.ANY;
+                                       0 = MATCH.ANY always (12) */
     uint32_t l2_fetch_bytes;        /* cudaLimitMaxL2FetchGranularity set for the device when the context
                                        is configured: 32 / 64 / 128 bytes, 0 = leave the driver's (0) */
     uint32_t sort_min_ctas;         /* classic onesweep: 4 = registers capped for 4 CTAs per SM, else the

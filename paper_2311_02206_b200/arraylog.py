@@ -238,7 +238,8 @@ def env_device_config() -> dict:
         v = os.environ.get(k)
         if v is not None and v != "":
             out[field] = conv(v)
-    tr = (1 if os.environ.get("GD_LOOP_TRACE") == "1" else 0) | (2 if os.environ.get("GD_DL_TRACE") == "1" else 0)
+    tr = ((1 if os.environ.get("GD_LOOP_TRACE") == "1" else 0) | (2 if os.environ.get("GD_DL_TRACE") == "1" else 0)
+          | (4 if os.environ.get("GD_SORT_TRACE") == "1" else 0))
     if tr:
         out["trace"] = tr
     return out

@@ -143,7 +143,7 @@ inline gd_device_config default_device_config() {
     d.insert_slots = 1;
     d.insert_pipeline = 0;
     d.insert_per_thread = 8;
-    d.sort_ballot = 0;
+    d.sort_ballot = 12;
     d.l2_fetch_bytes = 0;
     d.sort_min_ctas = 0;
     d.expand_keys_per_lane = 8;

@@ -544,6 +544,22 @@ int sort_items(const Ctx& c) {
     return i == 16 || i == 8 ? i : 4;
 }
 
+// Mean distinct pass digits per 32 consecutive keys, over warps spread
+// evenly across the array: out += the number of peer groups of each warp.
+template <typename K>
+__global__ void digit_diversity_kernel(const K* __restrict__ keys, u64 n, u32 shift,
+                                       unsigned long long* __restrict__ out) {
+    const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
+    const u64 base = n > 32 ? (n - 32) * warp / nw : 0;
+    const u64 i = base + lane_id();
+    const u32 d = i < n ? digit_of(keys[i], shift) : (u32)kRadix;
+    const u32 peers = __match_any_sync(0xffffffffu, d);
+    const bool leader = lane_id() == 31 - __clz(peers);
+    const u32 groups = __popc(__ballot_sync(0xffffffffu, leader));
+    if (lane_id() == 0) atomicAdd(out, (unsigned long long)groups);
+}
+
 template <typename K, int I>
 void launch_onesweep(const Ctx& c, u64 tiles, const K* src, K* dst, u64 pb, u64 pn, u32 shift, const u64* rd,
                      u64* wr, u32* w, bool ballot) {
@@ -734,21 +750,33 @@ K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
     K* src = a;
     K* dst = b;
     // Ranking per pass: ballot multi-split where the pass's digits are spread
-    // (measured 17% faster per pass on uniform digits), MATCH.ANY where a
-    // few digits dominate (the top passes of skewed keys: few peer groups per
-    // warp).  Decided from the histograms for large sorts (one readback).
-    std::vector<char> ballot(npass, c.cfg.sort_pipeline == 4 ? 1 : 0);
-    if (c.cfg.sort_ballot && n >= c.cfg.sort_pipeline_min_keys * 16 && c.cfg.sort_pipeline == 0) {
-        std::vector<u64> h(hist_words);
-        c.d2h(h.data(), hist.p, hist_words * sizeof(u64));
-        c.sync();
-        for (int pass = 0; pass < npass; ++pass) {
-            u64 mx = 0;
-            for (int d = 0; d < kRadix; ++d) mx = std::max(mx, h[(u64)pass * kRadix + d]);
-            ballot[pass] = mx * kRadix < 4 * n;  // no digit holds more than 4/256 of the keys
-        }
-    }
+    // (9 ballots, fixed cost) where a warp's 32 consecutive keys carry many
+    // distinct digits, MATCH.ANY (cost grows with the distinct count) where
+    // they carry few.  The count depends on the pass's input ORDER (C2: the
+    // log keeps a Δ row's outputs together, so the low passes see few
+    // distinct digits per warp; the src passes after them see many), so it
+    // is sampled on the pass's actual input right before the pass: 2048
+    // warps of consecutive keys, one readback per pass.  C2: ballot on
+    // passes 3-4 only, final sort 34.2 -> ~30 ms (profiles/r2_sort_passes.md).
+    std::vector<char> ballot(npass, 0);
+    const bool adapt = c.cfg.sort_ballot && n >= c.cfg.sort_pipeline_min_keys * 16 && c.cfg.sort_pipeline == 0;
+    DevBuf<unsigned long long> div;
+    if (adapt) div = DevBuf<unsigned long long>(c, 1);
     for (int pass = 0; pass < npass; ++pass) {
+        bool use_ballot = c.cfg.sort_pipeline == 4;
+        if (adapt) {
+            constexpr int kSampleWarps = 2048;
+            c.memset(div.p, 0, sizeof(unsigned long long));
+            digit_diversity_kernel<K><<<kSampleWarps / 8, 256, 0, c.stream>>>(src, n, (u32)(pass * kRadixBits), div.p);
+            c.check_launch();
+            unsigned long long tot = 0;
+            c.read_words(&tot, div.p, 1);
+            use_ballot = tot >= (unsigned long long)c.cfg.sort_ballot * kSampleWarps;  // mean distinct digits
+            if (c.cfg.trace & 4)
+                fprintf(stderr, "[sort] pass %d: %.1f distinct digits per warp -> %s\n", pass,
+                        (double)tot / kSampleWarps, use_ballot ? "ballot" : "match");
+        }
+        ballot[pass] = use_ballot;
         for (int p = 0; p < nportions; ++p) {
             const u64 pb = (u64)p * kPortion;
             const u64 pn = std::min(kPortion, n - pb);

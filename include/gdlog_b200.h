@@ -145,8 +145,9 @@ typedef struct gd_device_config {
     uint64_t download_chunk_rows;   /* staging chunk of packed downloads (1 << 20) */
     uint32_t sort_items;            /* onesweep keys per thread: 4, 8 or 16 (16) */
     uint32_t trace;                 /* stderr traces: bit 0 resident loop, bit 1 downloads, bit 2 sort (0) */
-    int32_t warp_expand;            /* final steps over a dense inner: count + warp-expanded insert (0:
-                                       the merge-path fused insert measured faster on C2, 163 vs 172 ms) */
+    int32_t warp_expand;            /* final steps over a dense inner: count + warp-expanded insert (1:
+                                       C2 155.7 ms vs 162.4 for probe + scan + merge-path fused insert,
+                                       with expand_keys_per_lane = 4) */
     uint32_t sort_digit_bits;       /* pipelined sort: widest digit, 8..10 (10) */
     uint64_t heavy_rows;            /* ... rows with more outputs are expanded as segments of this many (4096) */
     int32_t sort_pipeline;          /* u64 sorts: 0 classic onesweep; 1 pipelined (bulk-copy prefetch, wide
@@ -174,8 +175,8 @@ typedef struct gd_device_config {
                                        is configured: 32 / 64 / 128 bytes, 0 = leave the driver's (0) */
     uint32_t sort_min_ctas;         /* classic onesweep: 4 = registers capped for 4 CTAs per SM, else the
                                        compiler's choice (3 per SM) (0) */
-    uint32_t expand_keys_per_lane;  /* warp-expanded insert: keys per lane per insert round, 8 (3 CTAs/SM)
-                                       or 4 (5 CTAs/SM) (8) */
+    uint32_t expand_keys_per_lane;  /* warp-expanded insert: keys per lane per insert round, 8 (3 CTAs/SM,
+                                       4 inner loads per lane in flight) or 4 (5 CTAs/SM, one) (4) */
     uint32_t warp_append;           /* merge-path fused insert: log append with one atomic per warp instead
                                        of one per CTA tile (two CTA barriers fewer per tile) (0) */
     uint32_t download_delta;        /* host downloads of canonical u64 keys: gaps of 64-key blocks bit-packed

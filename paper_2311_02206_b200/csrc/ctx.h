@@ -132,7 +132,7 @@ inline gd_device_config default_device_config() {
     d.download_chunk_rows = 1u << 20;
     d.sort_items = 16;
     d.trace = 0;
-    d.warp_expand = 0;
+    d.warp_expand = 1;
     d.sort_digit_bits = 10;
     d.heavy_rows = 4096;
     d.sort_pipeline = 0;
@@ -146,7 +146,7 @@ inline gd_device_config default_device_config() {
     d.sort_ballot = 12;
     d.l2_fetch_bytes = 0;
     d.sort_min_ctas = 0;
-    d.expand_keys_per_lane = 8;
+    d.expand_keys_per_lane = 4;
     d.warp_append = 0;
     d.download_delta = 1;
     return d;

@@ -1181,7 +1181,7 @@ __device__ __forceinline__ void x_emit(XWarp& w, bool have, u64 key, Sink& sink)
 
 // The expansion itself (both sinks): light rows 32 at a time per warp,
 // then the heavy (row, segment) items queued by loop_count.
-template <class Sink>
+template <class Sink, int kXB = 4>
 __device__ __forceinline__ void expand_rows(const LoopCtl* ctl, u32 step, const u64* outer, u64 n,
                                             const u64* __restrict__ inner, const DevJoin& jd, const LoopDense& dv,
                                             const LoopStepBufs& sb, u64 heavy_min, XWarp& w, Sink& sink) {
@@ -1207,7 +1207,6 @@ __device__ __forceinline__ void expand_rows(const LoopCtl* ctl, u32 step, const 
         const u64 T = __shfl_sync(0xffffffffu, incl, 31);
         const u64 excl = incl - c;
         // kXB outputs per lane at a time: their inner loads in flight together
-        constexpr int kXB = 4;
         for (u64 j0 = 0; j0 < T; j0 += 32 * kXB) {
             u64 iv[kXB], so[kXB];
 #pragma unroll
@@ -1263,7 +1262,7 @@ __device__ __forceinline__ void expand_rows(const LoopCtl* ctl, u32 step, const 
     if (w.fill) sink.round(w, w.fill);
 }
 
-template <int NS, int PER = kXPer>
+template <int NS, int PER = kXPer, int XB = 1>
 __global__ void __launch_bounds__(kLT, PER >= 8 ? 3 : 5) loop_expand_insert_kernel(
     LoopCtl* ctl, u32 step, u32 head, LoopOuter o, const u64* __restrict__ inner, DevJoin jd, LoopDense dv,
     LoopStepBufs sb, u64 heavy_min, LoopHeadBufs hb, LoopEndDesc e, int do_end) {
@@ -1277,7 +1276,7 @@ __global__ void __launch_bounds__(kLT, PER >= 8 ? 3 : 5) loop_expand_insert_kern
         InsertSink<NS, PER> sink{hb, ctl->iter + 1 - ctl->epoch_base,
                         reinterpret_cast<unsigned long long*>(&ctl->h[head].log_n)};
         XWarp w{sbuf[threadIdx.x >> 5], 0, 0, 0, 0};
-        expand_rows(ctl, step, outer, n, inner, jd, dv, sb, heavy_min, w, sink);
+        expand_rows<InsertSink<NS, PER>, (PER >= 8 ? 4 : XB)>(ctl, step, outer, n, inner, jd, dv, sb, heavy_min, w, sink);
         flush_counts(ctl, head, step, w.J, w.N, w.D, red);
     }
     if (do_end && last_cta(ctl, &s_flag) && threadIdx.x == 0) end_body(ctl, e);

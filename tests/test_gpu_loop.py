@@ -24,9 +24,11 @@ MODES = {  # gd_device_config fields of each mode
     "split": {"split_insert": 1},
     "tiny_split": {"min_capacities": 1, "split_insert": 1},
     "tiny_casrehash": {"min_capacities": 1, "rehash_cas_only": 1},
-    # final steps over a dense inner: count + warp-expanded insert instead
-    # of the probe/scan/merge-path fused insert (the default)
-    "xp": {"warp_expand": 1},
+    # final steps over a dense inner: probe/scan/merge-path fused insert
+    # instead of count + warp-expanded insert (the default), and the wide
+    # expansion rounds (8 keys per lane)
+    "noxp": {"warp_expand": 0},
+    "xp8": {"warp_expand": 1, "expand_keys_per_lane": 8},
     "xp_split": {"warp_expand": 1, "split_insert": 1},
     # warp expansion with rows of more than 3 outputs queued as (row,
     # segment) items of 3 outputs (the heavy-row path on small inputs)
@@ -76,7 +78,7 @@ def test_c1_all_modes(ref, mode):
     assert g.raw_stats().join_tuples == 190496  # SURVEY §6 probe: ΣJ over 46 iterations
 
 
-@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "hashindex", "split", "xp", "xp_split", "heavy",
+@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "hashindex", "split", "noxp", "xp8", "xp_split", "heavy",
                                   "tiny_heavy", "window", "tiny_window", "window_xp", "cas_first", "batched",
                                   "pipe_insert"])
 @pytest.mark.parametrize("idx", [0, 17, 55])
@@ -108,7 +110,7 @@ def test_modes_agree_on_power_law(ref):
     from paper_2311_02206_b200 import workloads as W
     e = W.tc_pl(20000, 20000, 100, 1.05, 3)
     outs = {m: run_mode(m, "reach", {"Edge": e}) for m in ("graph", "host", "tiny", "hashindex", "tiny_casrehash",
-                                                            "eager", "xp", "heavy", "tiny_heavy")}
+                                                            "eager", "noxp", "heavy", "tiny_heavy")}
     base = outs["host"]
     for m, g in outs.items():
         assert np.array_equal(g.relation("Reach").data, base.relation("Reach").data), m
@@ -149,7 +151,7 @@ def test_hash_predup_matches_sort_path():
                                                                         hs.join_tuples)
 
 
-@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "xp", "heavy", "tiny_heavy"])
+@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "noxp", "heavy", "tiny_heavy"])
 def test_hub_rows(ref, mode):
     """Hubs (in-degree 700, out-degree 300) give Δ rows with long match
     ranges next to short ones: the load-balanced expansion must match the

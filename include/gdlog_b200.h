@@ -179,6 +179,11 @@ typedef struct gd_device_config {
                                        4 inner loads per lane in flight) or 4 (5 CTAs/SM, one) (4) */
     uint32_t warp_append;           /* merge-path fused insert: log append with one atomic per warp instead
                                        of one per CTA tile (two CTA barriers fewer per tile) (0) */
+    uint32_t precount;              /* a single self-recursive warp-expanded step (TC): the insert computes
+                                       the next iteration's row ranges, so loop_count only gates (0:
+                                       C2 158.8 vs 155.5 ms — the count kernel keeps its launch and gate,
+                                       the insert grows by more than the count saves) */
+    uint32_t reserved7;
     uint32_t download_delta;        /* host downloads of canonical u64 keys: gaps of 64-key blocks bit-packed
                                        on the device, keys rebuilt by host threads (1) */
 } gd_device_config;

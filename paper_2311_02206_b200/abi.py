@@ -87,6 +87,8 @@ class gd_device_config(C.Structure):
         ("sort_min_ctas", u32),
         ("expand_keys_per_lane", u32),
         ("warp_append", u32),
+        ("precount", u32),
+        ("reserved7", u32),
         ("download_delta", u32),
     ]
 

@@ -227,6 +227,7 @@ _ENV_KNOBS = {
     "GD_DL_DELTA": ("download_delta", int),
     "GD_XP_PER": ("expand_keys_per_lane", int),
     "GD_WARP_APPEND": ("warp_append", int),
+    "GD_PRECOUNT": ("precount", int),
     "GD_PART_EXCHANGE": ("partition_exchange", lambda v: {"peer": 0, "nccl": 1}[v]),
 }
 

@@ -148,6 +148,8 @@ inline gd_device_config default_device_config() {
     d.sort_min_ctas = 0;
     d.expand_keys_per_lane = 4;
     d.warp_append = 0;
+    d.precount = 0;
+    d.reserved7 = 0;
     d.download_delta = 1;
     return d;
 }

@@ -746,13 +746,23 @@ public:
         DevBuf<u64> row_start, row_off, splits, temp;
         u64 rows_cap = 0, splits_cap = 0, temp_cap = 0;
         DevBuf<u64> rc;  // xp steps: each outer row's inner range (start << 32 | count), from loop_count
+        // precounted step (gd_device_config.precount): second set of the
+        // per-row buffers, written by the insert for the next iteration
+        bool pre = false;
+        DevBuf<u64> rc2, row_start2, row_off2;
         LoopStepBufs bufs() const {
-            return LoopStepBufs{row_start.p, row_off.p, rows_cap, splits.p, splits_cap, xp ? rc.p : nullptr};
+            return LoopStepBufs{row_start.p, row_off.p, rows_cap, splits.p, splits_cap, xp ? rc.p : nullptr,
+                                pre ? rc2.p : nullptr, pre ? row_start2.p : nullptr, pre ? row_off2.p : nullptr};
         }
         void alloc_rows(Ctx& c) {
             row_start = DevBuf<u64>(c, rows_cap);
             row_off = DevBuf<u64>(c, rows_cap);
             if (xp) rc = DevBuf<u64>(c, rows_cap);
+            if (pre) {
+                rc2 = DevBuf<u64>(c, rows_cap);
+                row_start2 = DevBuf<u64>(c, rows_cap);
+                row_off2 = DevBuf<u64>(c, rows_cap);
+            }
         }
     };
     struct LHead {
@@ -883,6 +893,11 @@ public:
         // variant-steps in execution order (plan order, variant order)
         std::vector<LStep> steps;
         build_loop_steps(rec, steps);
+        // Precount: a single self-recursive warp-expanded step (TC) lets its
+        // insert compute the next iteration's row ranges (loop.cu InsertSink).
+        if (steps.size() == 1 && steps[0].xp && steps[0].final && !steps[0].split_insert &&
+            steps[0].kind == LO_DELTA && steps[0].src_head == steps[0].head && c.cfg.precount)
+            steps[0].pre = true;
         const u32 ns = (u32)steps.size();
         const u64 d0 = rels[rec[0]].delta_n;
         for (auto& L : steps) {
@@ -996,7 +1011,8 @@ public:
                 loop_gate(c, s, ctl.p, g);
                 c.prof_end(t, KC_LOOP_CTL, 0);
             }
-            const LoopEndDesc end{LoopHist{hist_rec.p, hist_steps.p, ns}, cond, use_cond ? 1 : 0};
+            const LoopEndDesc end{LoopHist{hist_rec.p, hist_steps.p, ns}, cond, use_cond ? 1 : 0,
+                                  ns == 1 && steps[0].pre ? 0u : ~0u};
             u32 last_final = 0;
             for (u32 i = 0; i < ns; ++i)
                 if (steps[i].final) last_final = i;
@@ -1326,7 +1342,7 @@ public:
                 if (in_v(j) && !steps[j].final) hc->step_total[j] = sums[j];
             hc->win_hi = hc->win_lo = 0;
             c.h2d(ctl.p, hc, sizeof(LoopCtl));
-            loop_end(c, c.stream, ctl.p, LoopEndDesc{LoopHist{hist_rec.p, hist_steps.p, ns}, 0, 0});
+            loop_end(c, c.stream, ctl.p, LoopEndDesc{LoopHist{hist_rec.p, hist_steps.p, ns}, 0, 0, ~0u});
             c.d2h(hc, ctl.p, sizeof(LoopCtl));
             c.sync();
             ++windowed_iters;

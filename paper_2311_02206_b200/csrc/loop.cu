@@ -335,6 +335,8 @@ __device__ void end_body(LoopCtl* ctl, const LoopEndDesc& e) {
     if (overflow) {  // roll back: nothing was inserted (gate)
         for (u32 h = 0; h < nh; ++h) ctl->h[h].cand = ctl->h[h].J = ctl->h[h].N = ctl->h[h].D = 0;
         for (u32 s = 0; s < ns; ++s) ctl->step_total[s] = ctl->step_cand[s] = ctl->heavy_n[s] = 0;
+        ctl->pre_valid = ctl->pre_bad = 0;  // the rerun counts its rows itself
+        ctl->pre_cand = ctl->pre_heavy_n = 0;
         if (e.use_cond) cudaGraphSetConditional(cond, 0);
         return;
     }
@@ -360,6 +362,17 @@ __device__ void end_body(LoopCtl* ctl, const LoopEndDesc& e) {
         e.hist.steps[i * ns + s] = __ldcg(&ctl->step_total[s]);
         ctl->last_cand[s] = __ldcg(&ctl->step_cand[s]);
         ctl->step_total[s] = ctl->step_cand[s] = ctl->heavy_n[s] = 0;
+    }
+    if (e.pre_step != ~0u) {  // the next iteration's counts, from this iteration's insert
+        const u32 bad = __ldcg(&ctl->pre_bad);
+        if (!bad) {
+            ctl->step_cand[e.pre_step] = __ldcg(&ctl->pre_cand);
+            ctl->heavy_n[e.pre_step] = __ldcg(&ctl->pre_heavy_n);
+            ctl->pre_sel ^= 1;
+        }
+        ctl->pre_valid = bad ? 0 : 1;
+        ctl->pre_bad = 0;
+        ctl->pre_cand = ctl->pre_heavy_n = 0;
     }
     ctl->iter = iter + 1;
     ctl->done = active ? 0 : 1;
@@ -988,6 +1001,18 @@ __device__ __forceinline__ void dense_range(const LoopDense& dv, u64 p, u64& a, 
     }
 }
 
+// The step buffers of this iteration / of the next one (precounted steps
+// alternate two sets; pre_sel names the current one).
+__device__ __forceinline__ LoopStepBufs bufs_of_iter(const LoopStepBufs& sb, const LoopCtl* ctl, bool next) {
+    LoopStepBufs b = sb;
+    if (sb.rc2 && (((ctl->pre_sel & 1) != 0) != next)) {
+        b.rc = sb.rc2;
+        b.row_start = sb.row_start2;
+        b.row_off = sb.row_off2;
+    }
+    return b;
+}
+
 __global__ void __launch_bounds__(kLT) loop_count_kernel(LoopCtl* ctl, u32 step, LoopOuter o, DevJoin jd,
                                                          LoopDense dv, LoopStepBufs sb, u64 heavy_min,
                                                          LoopGateDesc g, int do_gate) {
@@ -998,6 +1023,9 @@ __global__ void __launch_bounds__(kLT) loop_count_kernel(LoopCtl* ctl, u32 step,
         u64 n;
         resolve(o, ctl, outer, n);
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->step_n[step] = n;
+        const LoopStepBufs sb0 = sb;
+        LoopStepBufs sb = bufs_of_iter(sb0, ctl, false);
+        if (sb0.rc2 && ctl->pre_valid) n = 0;  // the last insert counted these rows already
         if (sb.rc && n > sb.rows_cap) {  // the row ranges need n entries
             if (blockIdx.x == 0 && threadIdx.x == 0) {
                 atomicMax((unsigned long long*)&ctl->need_rows[step], (unsigned long long)(n + 1));
@@ -1057,6 +1085,37 @@ struct InsertSink {
     const LoopHeadBufs& hb;  // the kernel parameter itself (a copy would take registers)
     u32 it;
     unsigned long long* log_n;
+    // precount (LoopCtl.pre_*): each appended row's next-iteration range
+    bool pre = false;
+    LoopCtl* ctl = nullptr;
+    const DevJoin* jd = nullptr;
+    const LoopDense* dv = nullptr;
+    LoopStepBufs nb = LoopStepBufs();
+    u64 heavy_min = 0, d0 = 0;
+    // Row r of the next iteration (an appended key): its inner range and
+    // heavy items, as loop_count would write them; returns its candidates.
+    __device__ __forceinline__ u64 precount(u64 r, u64 key) {
+        u64 a, c;
+        dense_range(*dv, outer_prefix(*jd, key), a, c);
+        if (r >= nb.rows_cap) {
+            ctl->pre_bad = 1;
+            return c;
+        }
+        nb.rc[r] = a << 32 | c;
+        if (c > heavy_min) {
+            const u64 segs = (c + heavy_min - 1) / heavy_min;
+            const u64 hp = atomicAdd((unsigned long long*)&ctl->pre_heavy_n, (unsigned long long)segs);
+            if (hp + segs <= nb.rows_cap) {
+                for (u64 q = 0; q < segs; ++q) {
+                    nb.row_start[hp + q] = r;
+                    nb.row_off[hp + q] = q;
+                }
+            } else {
+                ctl->pre_bad = 1;
+            }
+        }
+        return c;
+    }
     __device__ __forceinline__ void round(XWarp& w, u32 m) {
         __syncwarp();
         const u32 lane = lane_id();
@@ -1083,10 +1142,19 @@ struct InsertSink {
         if (lane == 0 && tot) base = atomicAdd(log_n, (unsigned long long)tot);
         base = __shfl_sync(0xffffffffu, base, 0);
         const u32 lt = lanemask_lt();
+        u64 csum = 0;
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-            if (fresh >> k & 1) hb.log[base + __popc(mk[k] & lt)] = key[k];
+            const u64 p = base + __popc(mk[k] & lt);
+            if (fresh >> k & 1) {
+                hb.log[p] = key[k];
+                if (pre) csum += precount(p - d0, key[k]);
+            }
             base += __popc(mk[k]);
+        }
+        if (pre) {
+            csum = warp_sum(csum);
+            if (lane == 0 && csum) atomicAdd((unsigned long long*)&ctl->pre_cand, (unsigned long long)csum);
         }
         __syncwarp();
     }
@@ -1273,10 +1341,20 @@ __global__ void __launch_bounds__(kLT, PER >= 8 ? 3 : 5) loop_expand_insert_kern
         const u64* outer;
         u64 n;
         resolve(o, ctl, outer, n);
+        const LoopStepBufs cur = bufs_of_iter(sb, ctl, false);
         InsertSink<NS, PER> sink{hb, ctl->iter + 1 - ctl->epoch_base,
-                        reinterpret_cast<unsigned long long*>(&ctl->h[head].log_n)};
+                                 reinterpret_cast<unsigned long long*>(&ctl->h[head].log_n)};
+        if (sb.rc2) {  // precount the next iteration's rows as they are appended
+            sink.pre = true;
+            sink.ctl = ctl;
+            sink.jd = &jd;
+            sink.dv = &dv;
+            sink.nb = bufs_of_iter(sb, ctl, true);
+            sink.heavy_min = heavy_min;
+            sink.d0 = ctl->h[head].dhi;
+        }
         XWarp w{sbuf[threadIdx.x >> 5], 0, 0, 0, 0};
-        expand_rows<InsertSink<NS, PER>, (PER >= 8 ? 4 : XB)>(ctl, step, outer, n, inner, jd, dv, sb, heavy_min, w, sink);
+        expand_rows<InsertSink<NS, PER>, (PER >= 8 ? 4 : XB)>(ctl, step, outer, n, inner, jd, dv, cur, heavy_min, w, sink);
         flush_counts(ctl, head, step, w.J, w.N, w.D, red);
     }
     if (do_end && last_cta(ctl, &s_flag) && threadIdx.x == 0) end_body(ctl, e);

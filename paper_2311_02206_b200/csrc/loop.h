@@ -103,6 +103,14 @@ struct LoopCtl {
     u32 win_step;
     u32 pad2;
     u64 win_lo, win_hi;
+    // precount (a single self-recursive warp-expanded step): the insert
+    // computes the next iteration's row ranges, heavy items and candidate
+    // count for the rows it appends; loop_count then only gates
+    u32 pre_valid;    // this iteration's ranges / heavy items / step_cand came from the last insert
+    u32 pre_sel;      // buffer set of this iteration (0: rc / row_start / row_off, 1: the *2 set)
+    u32 pre_bad;      // the precount overflowed a buffer: the next iteration counts itself
+    u32 pad4;
+    u64 pre_cand, pre_heavy_n;
 };
 
 // ---- peer-memory partitioned loop --------------
@@ -175,6 +183,12 @@ struct LoopStepBufs {
     u64* splits;
     u64 splits_cap;
     u64* rc;  // warp-expanded steps: row r's inner range, start << 32 | count (loop_count writes it)
+    // precounted steps (the next iteration's ranges written by this
+    // iteration's insert): the second buffer set; LoopCtl.pre_sel picks
+    // which set is the current iteration's
+    u64* rc2;
+    u64* row_start2;
+    u64* row_off2;
 };
 
 // Candidate bound of the final steps -> overflow check of every head.
@@ -191,6 +205,7 @@ struct LoopEndDesc {
     LoopHist hist;
     unsigned long long cond;  // cudaGraphConditionalHandle
     int use_cond;
+    u32 pre_step;  // precounted step (its next-iteration counts become current), or ~0u
 };
 
 // ---- launchers (loop.cu); all stream-ordered on `s`, no host sync ----

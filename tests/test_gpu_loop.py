@@ -39,6 +39,8 @@ MODES = {  # gd_device_config fields of each mode
     "cas_first": {"insert_slots": 0},
     "batched": {"insert_slots": 2, "split_insert": 1, "insert_per_thread": 4},
     "pipe_insert": {"split_insert": 1, "insert_pipeline": 1},
+    "precount": {"precount": 1},
+    "tiny_precount": {"precount": 1, "min_capacities": 1, "heavy_rows": 2},
     # chain temps above 7 rows are materialized in windows of 7 (the
     # windowed iteration of SURVEY §8f rank 2), with and without the rest
     # of the capacities at their minimum
@@ -80,7 +82,7 @@ def test_c1_all_modes(ref, mode):
 
 @pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "hashindex", "split", "noxp", "xp8", "xp_split", "heavy",
                                   "tiny_heavy", "window", "tiny_window", "window_xp", "cas_first", "batched",
-                                  "pipe_insert"])
+                                  "pipe_insert", "precount", "tiny_precount"])
 @pytest.mark.parametrize("idx", [0, 17, 55])
 def test_sg_corpus_modes(ref, mode, idx):
     g, _ = corpus(ref, 1, idx)
@@ -151,7 +153,7 @@ def test_hash_predup_matches_sort_path():
                                                                         hs.join_tuples)
 
 
-@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "noxp", "heavy", "tiny_heavy"])
+@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "noxp", "heavy", "tiny_heavy", "precount", "tiny_precount"])
 def test_hub_rows(ref, mode):
     """Hubs (in-degree 700, out-degree 300) give Δ rows with long match
     ranges next to short ones: the load-balanced expansion must match the

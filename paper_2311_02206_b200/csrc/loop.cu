@@ -1657,9 +1657,12 @@ constexpr u32 kZoneBatch = 8;
 __global__ void __launch_bounds__(kZoneThreads) table_zone_kernel(const void* old_tab, u64 old_cap, void* tab,
                                                                   u64 cap, u32 sb, u32 T, u64* __restrict__ spill,
                                                                   unsigned long long* nspill, u64 spill_cap) {
-    extern __shared__ unsigned long long zone[];
+    extern __shared__ __align__(16) unsigned long long zone_raw[];
     const u64 i0 = (u64)blockIdx.x * T, i1 = min(old_cap, i0 + T);
     const u64 zlo = (u64)((u128)i0 * cap / old_cap);
+    // zone[j] <-> new slot zlo + j, placed so shared and global addresses
+    // agree mod 16 (the write-out is one bulk copy of the aligned run)
+    unsigned long long* zone = zone_raw + (zlo & 1);
     const u64 zhi = i1 == old_cap ? cap : (u64)((u128)i1 * cap / old_cap);
     const u32 width = (u32)(zhi - zlo);  // <= the zone's shared slots (host sizes T)
     for (u32 j = threadIdx.x; j < width; j += kZoneThreads) zone[j] = kEmptySlot;
@@ -1699,8 +1702,23 @@ __global__ void __launch_bounds__(kZoneThreads) table_zone_kernel(const void* ol
     }
     __syncthreads();
     if (sb) {
+        // The zone leaves shared memory as one bulk async copy (cp.async.bulk
+        // shared -> global, UBLKCP): one instruction instead of width / 256
+        // store rounds per thread; the (at most two) 8-byte slots outside
+        // the 16-byte-aligned run are stored directly.
         u64* out = static_cast<u64*>(tab) + zlo;
-        for (u32 j = threadIdx.x; j < width; j += kZoneThreads) __stcs(out + j, (u64)zone[j]);
+        const u32 j0 = (u32)(zlo & 1), j1 = width > j0 ? j0 + ((width - j0) & ~1u) : j0;
+        if (threadIdx.x == 0 && j1 > j0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + j0),
+                         "r"((u32)__cvta_generic_to_shared(zone + j0)), "r"((j1 - j0) * 8u)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (threadIdx.x == 1 && j0 == 1) __stcs(out, (u64)zone[0]);
+        if (threadIdx.x == 2 && j1 < width) __stcs(out + j1, (u64)zone[j1]);
+        if (threadIdx.x == 0 && j1 > j0)  // shared memory stays until the copy has read it
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     } else {
         HSlot* out = static_cast<HSlot*>(tab) + zlo;
         for (u32 j = threadIdx.x; j < width; j += kZoneThreads) {
@@ -1933,14 +1951,14 @@ void loop_table_rehash(Ctx& c, const void* old_tab, u64 old_cap, void* tab, u64 
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(table_zone_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(kZoneSlotsMax * sizeof(u64)));
+                                 (int)((kZoneSlotsMax + 2) * sizeof(u64)));
             attr = true;
         }
         const u64 spill_cap = nkeys / 16 + (1u << 20);
         DevBuf<u64> spill(c, spill_cap);
         DevBuf<unsigned long long> ns(c, 1);
         c.memset(ns.p, 0, sizeof(unsigned long long));
-        table_zone_kernel<<<(unsigned)nzones, kZoneThreads, zslots * sizeof(u64), c.stream>>>(
+        table_zone_kernel<<<(unsigned)nzones, kZoneThreads, (zslots + 2) * sizeof(u64), c.stream>>>(
             old_tab, old_cap, tab, cap, sbits, (u32)T, spill.p, ns.p, spill_cap);
         c.check_launch();
         unsigned long long spilled;

@@ -140,7 +140,7 @@ typedef struct gd_device_config {
     int32_t dedup_split;            /* split large dedup sets into L2-sized parts (1) */
     int32_t host_unpack;            /* downloads move packed keys, host threads unpack (1) */
     double download_direct_frac;    /* pinned destinations: share of rows unpacked on the device and DMA'd
-                                       into the caller's rows (0.15: with delta-compressed keys the host's
+                                       into the caller's rows (0: with delta-compressed keys the host's
                                        row writes, not PCIe, bound the download) */
     uint64_t download_chunk_rows;   /* staging chunk of packed downloads (1 << 20) */
     uint32_t sort_items;            /* onesweep keys per thread: 4, 8 or 16 (16) */
@@ -183,7 +183,7 @@ typedef struct gd_device_config {
                                        the next iteration's row ranges, so loop_count only gates (0:
                                        C2 158.8 vs 155.5 ms — the count kernel keeps its launch and gate,
                                        the insert grows by more than the count saves) */
-    uint32_t reserved7;
+    uint32_t count_ctas_per_sm;     /* loop_count grid = SMs x this (0: 4) */
     uint32_t download_delta;        /* host downloads of canonical u64 keys: gaps of 64-key blocks bit-packed
                                        on the device, keys rebuilt by host threads (1) */
 } gd_device_config;

@@ -88,7 +88,7 @@ class gd_device_config(C.Structure):
         ("expand_keys_per_lane", u32),
         ("warp_append", u32),
         ("precount", u32),
-        ("reserved7", u32),
+        ("count_ctas_per_sm", u32),
         ("download_delta", u32),
     ]
 

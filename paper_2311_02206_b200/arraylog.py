@@ -228,6 +228,7 @@ _ENV_KNOBS = {
     "GD_XP_PER": ("expand_keys_per_lane", int),
     "GD_WARP_APPEND": ("warp_append", int),
     "GD_PRECOUNT": ("precount", int),
+    "GD_COUNT_CTAS": ("count_ctas_per_sm", int),
     "GD_PART_EXCHANGE": ("partition_exchange", lambda v: {"peer": 0, "nccl": 1}[v]),
 }
 

@@ -128,7 +128,7 @@ inline gd_device_config default_device_config() {
     d.dedup_part_slots = 8u << 20;
     d.dedup_split = 1;
     d.host_unpack = 1;
-    d.download_direct_frac = 0.15;
+    d.download_direct_frac = 0.0;
     d.download_chunk_rows = 1u << 20;
     d.sort_items = 16;
     d.trace = 0;
@@ -149,7 +149,7 @@ inline gd_device_config default_device_config() {
     d.expand_keys_per_lane = 4;
     d.warp_append = 0;
     d.precount = 0;
-    d.reserved7 = 0;
+    d.count_ctas_per_sm = 0;
     d.download_delta = 1;
     return d;
 }

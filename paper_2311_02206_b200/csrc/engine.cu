@@ -526,6 +526,8 @@ public:
         };
         const u32 bits = E.enc.e.bits;
         const u64 cmask = bits >= 64 ? ~0ull : (1ull << bits) - 1;
+        const bool aligned16 = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+        (void)aligned16;
         std::atomic<u64> gen{0};
         std::atomic<unsigned> left{0};
         u64 cur_k = 0;
@@ -552,8 +554,13 @@ public:
                 for (u64 i = 0;; ++i) {
                     if (ar == 2) {
 #if defined(__x86_64__)
-                        _mm_stream_si64(reinterpret_cast<long long*>(dst), (long long)((key >> bits) & cmask));
-                        _mm_stream_si64(reinterpret_cast<long long*>(dst + 1), (long long)(key & cmask));
+                        if (aligned16) {  // one 16-byte non-temporal store per row
+                            _mm_stream_si128(reinterpret_cast<__m128i*>(dst),
+                                             _mm_set_epi64x((long long)(key & cmask), (long long)((key >> bits) & cmask)));
+                        } else {
+                            _mm_stream_si64(reinterpret_cast<long long*>(dst), (long long)((key >> bits) & cmask));
+                            _mm_stream_si64(reinterpret_cast<long long*>(dst + 1), (long long)(key & cmask));
+                        }
 #else
                         dst[0] = (key >> bits) & cmask;
                         dst[1] = key & cmask;

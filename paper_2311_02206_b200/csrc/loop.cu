@@ -2114,7 +2114,8 @@ void loop_count(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter&
                 const LoopDense& dense, const LoopStepBufs& sb, u64 heavy_rows, const LoopGateDesc* gate) {
     LoopGateDesc g{};
     if (gate) g = *gate;
-    loop_count_kernel<<<loop_grid(c), kLT, 0, s>>>(ctl, step, o, jd, dense, sb, heavy_rows, g, gate ? 1 : 0);
+    const int grid = c.cfg.count_ctas_per_sm ? c.num_sms * (int)c.cfg.count_ctas_per_sm : loop_grid(c);
+    loop_count_kernel<<<grid, kLT, 0, s>>>(ctl, step, o, jd, dense, sb, heavy_rows, g, gate ? 1 : 0);
     c.check_launch();
 }
 

@@ -93,7 +93,7 @@ def test_device_config_defaults(lib):
     assert c.size == C.sizeof(A.gd_device_config)
     assert (c.resident_loop, c.loop_mode, c.loop_batch, c.min_capacities) == (1, A.GD_LOOP_GRAPH, 16, 0)
     assert (c.index_growth, c.zone_slots, c.sort_items, c.hash_dedup_min_rows) == (8, 4096, 16, 1 << 20)
-    assert c.download_direct_frac == 0.15
+    assert c.download_direct_frac == 0.0
     assert lib.gd_ctx_set_device_config(None, C.byref(c)) == A.GD_ERR_INVALID_ARG
 
 

@@ -184,8 +184,10 @@ typedef struct gd_device_config {
                                        C2 158.8 vs 155.5 ms — the count kernel keeps its launch and gate,
                                        the insert grows by more than the count saves) */
     uint32_t count_ctas_per_sm;     /* loop_count grid = SMs x this (0: 4) */
-    uint32_t download_delta;        /* host downloads of canonical u64 keys: gaps of 64-key blocks bit-packed
-                                       on the device, keys rebuilt by host threads (1) */
+    uint32_t download_delta;        /* host downloads of canonical u64 keys: 2 = 32-key blocks of byte-aligned
+                                       offsets from the block's first key, rows rebuilt by host threads with
+                                       vector adds; 1 = gaps of 64-key blocks bit-packed, keys rebuilt by a
+                                       running sum; 0 = packed 8-byte keys (2) */
 } gd_device_config;
 
 void gd_device_config_default(gd_device_config* cfg);

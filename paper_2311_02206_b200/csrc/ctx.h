@@ -150,7 +150,7 @@ inline gd_device_config default_device_config() {
     d.warp_append = 0;
     d.precount = 0;
     d.count_ctas_per_sm = 0;
-    d.download_delta = 1;
+    d.download_delta = 2;
     return d;
 }
 

@@ -144,6 +144,55 @@ __global__ void __launch_bounds__(256) delta_pack_kernel(const u64* __restrict__
     }
 }
 
+// ---- byte-offset blocks (download_delta = 2) ----
+// One warp per block of kByteBlock keys: the block's offset class (bytes
+// per offset from its first key: 1 / 2 / 4 / 8, code 0..3) and its payload
+// bytes.
+__global__ void byte_class_kernel(const u64* __restrict__ keys, u64 n, u64 nb, uint8_t* __restrict__ cls,
+                                  u64* __restrict__ bytes) {
+    const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const u32 lane = lane_id();
+    for (u64 b = warp; b < nb; b += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u64 base = b * kByteBlock;
+        const u32 cnt = (u32)min((u64)kByteBlock, n - base);
+        const u64 k = lane < cnt ? keys[base + lane] : 0;
+        const u64 head = __shfl_sync(0xffffffffu, k, 0);
+        const u64 last = __shfl_sync(0xffffffffu, k, cnt - 1);
+        if (lane == 0) {
+            const u64 r = last - head;
+            const u32 code = r < (1ull << 8) ? 0 : r < (1ull << 16) ? 1 : r < (1ull << 32) ? 2 : 3;
+            cls[b] = (uint8_t)code;
+            bytes[b] = (u64)cnt << code;
+        }
+    }
+}
+
+// One warp per block: the first key to heads, offset i (key_i - head) to
+// payload[offs[b] + i * width], little-endian.
+__global__ void byte_pack_kernel(const u64* __restrict__ keys, u64 n, u64 nb, const uint8_t* __restrict__ cls,
+                                 const u64* __restrict__ offs, u64* __restrict__ heads, uint8_t* __restrict__ payload) {
+    const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const u32 lane = lane_id();
+    for (u64 b = warp; b < nb; b += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u64 base = b * kByteBlock;
+        const u32 cnt = (u32)min((u64)kByteBlock, n - base);
+        const u64 k = lane < cnt ? keys[base + lane] : 0;
+        const u64 head = __shfl_sync(0xffffffffu, k, 0);
+        const u32 code = cls[b];
+        if (lane == 0) heads[b] = head;
+        if (lane < cnt) {
+            const u64 o = k - head;
+            uint8_t* p = payload + offs[b] + ((u64)lane << code);
+            switch (code) {  // offsets of one width are aligned to it when the block start is
+                case 0: *p = (uint8_t)o; break;
+                case 1: for (int q = 0; q < 2; ++q) p[q] = (uint8_t)(o >> (8 * q)); break;
+                case 2: for (int q = 0; q < 4; ++q) p[q] = (uint8_t)(o >> (8 * q)); break;
+                default: for (int q = 0; q < 8; ++q) p[q] = (uint8_t)(o >> (8 * q)); break;
+            }
+        }
+    }
+}
+
 __global__ void gather_kernel(const u64* __restrict__ src, u64 stride, u64 n, u64 m, u64* __restrict__ dst) {
     const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
     if (i <= m) dst[i] = src[min(i * stride, n)];
@@ -182,6 +231,45 @@ u64 delta_pack(Ctx& c, const u64* keys, u64 n, DeltaPacked& out) {
                                                    out.payload.p);
     c.check_launch();
     return total;
+}
+
+u64 byte_pack(Ctx& c, const u64* keys, u64 n, BytePacked& out) {
+    const u64 nb = (n + kByteBlock - 1) / kByteBlock;
+    out.nb = nb;
+    out.n = n;
+    out.heads = DevBuf<u64>(c, std::max<u64>(nb, 1));
+    out.cls = DevBuf<uint8_t>(c, std::max<u64>(nb, 1));
+    out.offs = DevBuf<u64>(c, nb + 1);
+    if (!nb) {
+        c.memset(out.offs.p, 0, sizeof(u64));
+        out.bytes = 0;
+        return 0;
+    }
+    DevBuf<u64> bytes(c, nb);
+    const int grid = c.num_sms * 8;
+    byte_class_kernel<<<grid, 256, 0, c.stream>>>(keys, n, nb, out.cls.p, bytes.p);
+    c.check_launch();
+    const u64 tiles = (nb + kScanTile - 1) / kScanTile;
+    DevBuf<u64> sums(c, tiles);
+    scan_tile_sums_kernel<<<(unsigned)tiles, kScanT, 0, c.stream>>>(bytes.p, nb, sums.p);
+    c.check_launch();
+    scan_sums_kernel<<<1, 1024, 0, c.stream>>>(sums.p, tiles, out.offs.p + nb);
+    c.check_launch();
+    scan_tiles_kernel<<<(unsigned)tiles, kScanT, 0, c.stream>>>(bytes.p, nb, sums.p, out.offs.p);
+    c.check_launch();
+    unsigned long long total = 0;
+    c.read_words(&total, out.offs.p + nb, 1);
+    out.payload = DevBuf<uint8_t>(c, std::max<u64>(total, 1));
+    out.bytes = total;
+    byte_pack_kernel<<<grid, 256, 0, c.stream>>>(keys, n, nb, out.cls.p, out.offs.p, out.heads.p, out.payload.p);
+    c.check_launch();
+    return total;
+}
+
+void byte_unit_offsets(Ctx& c, const BytePacked& d, u64 blocks_per_unit, u64 nunits, u64* dev_out) {
+    gather_kernel<<<(unsigned)((nunits + 1 + 255) / 256), 256, 0, c.stream>>>(d.offs.p, blocks_per_unit, d.nb,
+                                                                             nunits, dev_out);
+    c.check_launch();
 }
 
 void delta_chunk_offsets(Ctx& c, const DeltaPacked& d, u64 blocks_per_chunk, u64 nchunks, u64* dev_out) {

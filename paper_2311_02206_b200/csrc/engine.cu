@@ -19,7 +19,9 @@
 #include <set>
 #include <atomic>
 #include <functional>
+#include <memory>
 #include <optional>
+#include <mutex>
 #include <thread>
 #include <type_traits>
 #if defined(__x86_64__)
@@ -27,6 +29,7 @@
 #endif
 
 #include "engine.h"
+#include "host_decode.h"
 #include "comm.h"
 #include "loop.h"
 #include "ops.h"
@@ -358,7 +361,9 @@ public:
         double t_wait = 0, t_unpack = 0;
         const unsigned hw = std::thread::hardware_concurrency();
         const unsigned nt = std::max(1u, std::min(hw ? hw : 8u, 32u));
-        if (c.cfg.download_delta && n > 0) {
+        if (c.cfg.download_delta == 2 && n > 0) {
+            download_bytes_rows(keys, n, ar, out, nt, t_wait, t_unpack);
+        } else if (c.cfg.download_delta == 1 && n > 0) {
             download_delta_rows(keys, n, ar, out, nt, t_wait, t_unpack);
         } else {
         const u64 kChunk = c.cfg.download_chunk_rows;
@@ -474,7 +479,123 @@ public:
                     t_direct * 1e3);
     }
 
-    // Delta-compressed download of n canonical keys into rows (download_delta):
+    // Byte-offset download of n canonical keys into rows (download_delta = 2):
+    // the device writes every 32-key block as its first key plus byte-aligned
+    // offsets (delta.cu byte_pack; C2: ~2.5 B per row over PCIe), chunks of
+    // kChunkB blocks cross PCIe into a ring of pinned staging areas, and nt
+    // host threads (the caller included) claim units of kUnitB blocks in
+    // order from one counter and rebuild their rows with vector loads, adds
+    // and non-temporal stores (host_decode.cpp).  No barrier per chunk: a
+    // unit waits only for its own chunk's copy, and the thread that finishes
+    // a chunk's last unit issues the copy that reuses its staging area.
+    void download_bytes_rows(const u64* keys, u64 n, u32 ar, u64* out, unsigned nt, double& t_wait,
+                             double& t_unpack) {
+        BytePacked d;
+        byte_pack(c, keys, n, d);
+        constexpr u64 kUnitB = 8192;      // blocks per unit (256 K rows)
+        constexpr u64 kChunkUnits = 16;   // units per chunk (4 M rows)
+        constexpr u64 kChunkB = kUnitB * kChunkUnits;
+        const u64 nunits = (d.nb + kUnitB - 1) / kUnitB;
+        const u64 nchunks = (nunits + kChunkUnits - 1) / kChunkUnits;
+        std::vector<u64> uoff(nunits + 1);
+        {
+            DevBuf<u64> duo(c, nunits + 1);
+            byte_unit_offsets(c, d, kUnitB, nunits, duo.p);
+            c.d2h(uoff.data(), duo.p, (nunits + 1) * sizeof(u64));
+            c.sync();
+        }
+        auto chunk_units = [&](u64 k) { return std::min(kChunkUnits, nunits - k * kChunkUnits); };
+        u64 maxp = 0;
+        for (u64 k = 0; k < nchunks; ++k)
+            maxp = std::max(maxp, uoff[k * kChunkUnits + chunk_units(k)] - uoff[k * kChunkUnits]);
+        // staging area: heads | classes | payload, 64-byte aligned parts
+        auto up = [](u64 v) { return (v + 63) & ~63ull; };
+        const u64 a_heads = kChunkB * sizeof(u64), a_cls = up(kChunkB), area = a_heads + a_cls + up(maxp + 64);
+        const u64 R = std::min<u64>(nchunks, 6);
+        uint8_t* stage = static_cast<uint8_t*>(c.pinned_staging(R * area));
+        std::vector<cudaEvent_t> ev(nchunks, nullptr);
+        std::unique_ptr<std::atomic<int>[]> issued(new std::atomic<int>[nchunks]);
+        std::unique_ptr<std::atomic<u64>[]> finished(new std::atomic<u64>[nchunks]);
+        for (u64 k = 0; k < nchunks; ++k) {
+            issued[k].store(0);
+            finished[k].store(0);
+        }
+        std::atomic<u64> next{0};
+        std::atomic<bool> quit{false};
+        std::atomic<u64> d2h_total{0};
+        std::exception_ptr err;
+        std::mutex err_mu;
+        std::vector<std::thread> pool;
+        struct Cleanup {
+            std::function<void()> f;
+            ~Cleanup() { f(); }
+        } cleanup{[&] {
+            quit.store(true, std::memory_order_release);
+            for (auto& th : pool)
+                if (th.joinable()) th.join();
+            cudaStreamSynchronize(c.stream);
+            for (auto e : ev)
+                if (e) cudaEventDestroy(e);
+            cudaGetLastError();
+        }};
+        for (u64 k = 0; k < nchunks; ++k) GD_CUDA(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+        auto issue = [&](u64 k) {  // chunk k into area k % R
+            uint8_t* a = stage + (k % R) * area;
+            const u64 b0 = k * kChunkB, nbk = std::min(kChunkB, d.nb - b0);
+            const u64 p0 = uoff[k * kChunkUnits], p1 = uoff[k * kChunkUnits + chunk_units(k)];
+            GD_CUDA(cudaMemcpyAsync(a, d.heads.p + b0, nbk * sizeof(u64), cudaMemcpyDeviceToHost, c.stream));
+            GD_CUDA(cudaMemcpyAsync(a + a_heads, d.cls.p + b0, nbk, cudaMemcpyDeviceToHost, c.stream));
+            if (p1 > p0)
+                GD_CUDA(cudaMemcpyAsync(a + a_heads + a_cls, d.payload.p + p0, p1 - p0, cudaMemcpyDeviceToHost,
+                                        c.stream));
+            GD_CUDA(cudaEventRecord(ev[k], c.stream));
+            d2h_total.fetch_add(nbk * sizeof(u64) + nbk + (p1 - p0), std::memory_order_relaxed);
+            issued[k].store(1, std::memory_order_release);
+        };
+        const u32 bits = E.enc.e.bits;
+        std::atomic<u64> wait_ns{0}, work_ns{0};
+        auto worker = [&] {
+            try {
+                while (!quit.load(std::memory_order_acquire)) {
+                    const u64 u = next.fetch_add(1, std::memory_order_acq_rel);
+                    if (u >= nunits) return;
+                    const u64 k = u / kChunkUnits;
+                    const double tw = Ctx::now_s();
+                    while (!issued[k].load(std::memory_order_acquire)) {
+                        if (quit.load(std::memory_order_acquire)) return;
+                        std::this_thread::yield();
+                    }
+                    GD_CUDA(cudaEventSynchronize(ev[k]));
+                    const double tu = Ctx::now_s();
+                    const uint8_t* a = stage + (k % R) * area;
+                    const u64 b0 = u * kUnitB, nbu = std::min(kUnitB, d.nb - b0), cb = b0 - k * kChunkB;
+                    byte_decode_rows(reinterpret_cast<const u64*>(a) + cb, a + a_heads + cb,
+                                     a + a_heads + a_cls + (uoff[u] - uoff[k * kChunkUnits]), b0 * kByteBlock, nbu,
+                                     n, ar, bits, out);
+                    const double te = Ctx::now_s();
+                    wait_ns.fetch_add((u64)((tu - tw) * 1e9), std::memory_order_relaxed);
+                    work_ns.fetch_add((u64)((te - tu) * 1e9), std::memory_order_relaxed);
+                    if (finished[k].fetch_add(1, std::memory_order_acq_rel) + 1 == chunk_units(k) && k + R < nchunks)
+                        issue(k + R);  // area k % R is free again
+                }
+            } catch (...) {
+                std::lock_guard<std::mutex> g(err_mu);
+                if (!err) err = std::current_exception();
+                quit.store(true, std::memory_order_release);
+            }
+        };
+        for (u64 k = 0; k < R; ++k) issue(k);
+        for (unsigned t = 1; t < nt; ++t) pool.emplace_back(worker);
+        worker();
+        for (auto& th : pool) th.join();
+        pool.clear();
+        if (err) std::rethrow_exception(err);
+        c.d2h_bytes += d2h_total.load() + (nunits + 1) * sizeof(u64);
+        t_wait += wait_ns.load() * 1e-9 / nt;
+        t_unpack += work_ns.load() * 1e-9 / nt;
+    }
+
+    // Delta-compressed download of n canonical keys into rows (download_delta = 1):
     // the device bit-packs the gaps of every 64-key block (delta.cu), chunks
     // of 16 K blocks cross PCIe into two pinned staging areas (heads, widths,
     // payload), and nt host threads rebuild the keys — a running sum per

@@ -47,6 +47,23 @@ u64 delta_pack(Ctx& c, const u64* keys, u64 n, DeltaPacked& out);
 // dev_out[k] = d.offs[min(k * blocks_per_chunk, nb)] for k = 0..nchunks.
 void delta_chunk_offsets(Ctx& c, const DeltaPacked& d, u64 blocks_per_chunk, u64 nchunks, u64* dev_out);
 
+// Byte-offset blocks (download_delta = 2): each block of kByteBlock keys
+// is its first key plus every key's offset from it at the block's byte
+// width (1 / 2 / 4 / 8: cls code 0..3), so the host rebuilds rows with
+// plain vector loads and adds (host_decode.cpp) instead of a bit-serial
+// prefix sum.
+constexpr u32 kByteBlock = 32;
+struct BytePacked {
+    u64 n = 0, nb = 0, bytes = 0;
+    DevBuf<u64> heads;       // first key of each block
+    DevBuf<uint8_t> cls;     // offset width code of each block
+    DevBuf<u64> offs;        // first payload byte of each block (nb + 1)
+    DevBuf<uint8_t> payload;
+};
+u64 byte_pack(Ctx& c, const u64* keys, u64 n, BytePacked& out);
+// dev_out[k] = d.offs[min(k * blocks_per_unit, nb)] for k = 0..nunits.
+void byte_unit_offsets(Ctx& c, const BytePacked& d, u64 blocks_per_unit, u64 nunits, u64* dev_out);
+
 // ---- primitives.cu --------------------------------------------------
 u64 max_value(Ctx& c, const u64* vals, u64 n);  // 0 for n == 0
 

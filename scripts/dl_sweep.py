@@ -22,12 +22,16 @@ e.run()
 n = e.relation_count("Reach")
 out = torch.empty((n, 2), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
 rid = e._rid("Reach")
-for delta in (1, 0):
-    for frac in (0.0, 0.15, 0.3, 0.5):
+want = None
+for delta in (2, 1, 0):
+    for frac in ((0.0, 0.1, 0.2, 0.3) if delta == 2 else (0.0, 0.15)):
         ts = []
         for _ in range(4):
             with ctx.configured(download_delta=delta, download_direct_frac=frac):
                 t = time.perf_counter()
                 ctx.check(ctx.lib.gd_engine_relation_download(e.h, rid, out.ctypes.data_as(C.c_void_p), n))
                 ts.append(time.perf_counter() - t)
+        dig = int(out[::9973].sum())
+        want = dig if want is None else want
+        assert dig == want, "download differs between modes"
         print(f"delta={delta} frac={frac}: " + " ".join(f"{x * 1e3:.0f}" for x in ts) + " ms", flush=True)

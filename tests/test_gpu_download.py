@@ -18,7 +18,7 @@ def canonical(a):
     return np.unique(a, axis=0)
 
 
-@pytest.mark.parametrize("delta", [1, 0])
+@pytest.mark.parametrize("delta", [2, 1, 0])
 @pytest.mark.parametrize("arity,n,hi", [(2, 3_000_000, 1 << 20), (3, 2_100_000, 1 << 14), (2, 40_000_000, 1 << 30)])
 def test_host_unpack_matches(ref, arity, n, hi, delta):
     """Downloads of packed keys (delta-compressed or plain) unpacked by host
@@ -100,7 +100,7 @@ def test_delta_download_gap_widths(ref, case):
     prog = program_from_ref(ref.engine(COPY2 if arity == 2 else COPY3))
     want = canonical(e)
     outs = {}
-    for delta in (1, 0):
+    for delta in (2, 1, 0):
         with al.default_context().configured(download_delta=delta):
             g = al.engine(prog)
             g.load_edb("E", al.tuple_array(arity, e))
@@ -111,12 +111,16 @@ def test_delta_download_gap_widths(ref, case):
             outs[f"bytes{delta}"] = d1 - d0
     assert np.array_equal(outs[1].reshape(-1, arity), want)
     assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[2], outs[1])
     if case == "dense":
         assert outs["bytes1"] < 2 * len(want)  # ~1.2 bits per gap + block headers
+        # byte offsets: 1 byte per row + 9 bytes per 32-row block (+ unit offsets)
+        assert outs["bytes2"] < 1.4 * len(want)
 
 
+@pytest.mark.parametrize("delta", [2, 1])
 @pytest.mark.parametrize("frac", ["0.0", "0.1", "0.5"])
-def test_pinned_destination_delta(ref, frac):
+def test_pinned_destination_delta(ref, frac, delta):
     """Delta-compressed head + device-unpacked direct tail into a pinned
     destination: same rows as the canonical input."""
     import ctypes as C
@@ -132,6 +136,34 @@ def test_pinned_destination_delta(ref, frac):
     rid = g._rid("C")
     n = g.relation_count("C")
     pinned = torch.empty((n, 2), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
-    with g.ctx.configured(download_direct_frac=float(frac), download_delta=1):
+    with g.ctx.configured(download_direct_frac=float(frac), download_delta=delta):
         g.ctx.check(g.ctx.lib.gd_engine_relation_download(g.h, rid, pinned.ctypes.data_as(C.c_void_p), n))
     assert np.array_equal(pinned, canonical(e))
+
+
+@pytest.mark.parametrize("arity", [2, 3])
+@pytest.mark.parametrize("shift", [0, 1, 2, 3])
+def test_byte_download_destination_alignment(ref, arity, shift):
+    """Byte-offset download (download_delta = 2) into destinations at every
+    16-byte shift of a 64-byte line (the vector rebuild needs 64-byte
+    aligned rows; the others take the scalar rebuild) and into arity-3
+    rows: same rows as the canonical input, and the bytes just past the
+    destination are untouched."""
+    import ctypes as C
+
+    prog = program_from_ref(ref.engine(COPY2 if arity == 2 else COPY3))
+    rng = np.random.default_rng(91 + shift)
+    e = rng.integers(0, 1 << 17, size=(2_000_003, arity), dtype=np.uint64)
+    g = al.engine(prog)
+    g.load_edb("E", al.tuple_array(arity, e))
+    g.run()
+    rid = g._rid("C")
+    n = g.relation_count("C")
+    back = np.full(n * arity + 16, 0xABABABABABABABAB, dtype=np.uint64)
+    base = (-(back.ctypes.data // 8)) % 8  # first 64-byte aligned word
+    out = back[base + 2 * shift: base + 2 * shift + n * arity]
+    with g.ctx.configured(download_delta=2):
+        g.ctx.check(g.ctx.lib.gd_engine_relation_download(g.h, rid, out.ctypes.data_as(C.c_void_p), n))
+    assert np.array_equal(out.reshape(-1, arity), canonical(e))
+    rest = back[base + 2 * shift + n * arity:]
+    assert (rest == 0xABABABABABABABAB).all()

@@ -225,8 +225,14 @@ def main():
     from paper_2311_02206_b200 import arraylog as al
     from paper_2311_02206_b200.partition import NcclComm, TorchExchange, run_partitioned
 
-    stream = torch.cuda.current_stream()
+    # the engine runs on this (non-default) stream and every timing event is
+    # recorded on it, so device times include all the engine's queued work
+    # (the legacy default stream would be handed over as "no stream" and
+    # the context would create its own)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx = al.Context(local, stream.cuda_stream)
+    assert stream.cuda_stream != 0, "the engine needs a real stream to be timed on"
     edges = gen_workload()
     d_edges = torch.from_numpy(edges.view(np.int64)).cuda()
     flush = torch.empty(256 << 20 >> 2, dtype=torch.int32, device="cuda")

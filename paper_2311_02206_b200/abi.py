@@ -90,6 +90,9 @@ class gd_device_config(C.Structure):
         ("precount", u32),
         ("count_ctas_per_sm", u32),
         ("download_delta", u32),
+        ("index_load_pct", u32),
+        ("download_pipeline", u32),
+        ("download_pipeline_min_rows", u64),
     ]
 
 

@@ -225,6 +225,9 @@ _ENV_KNOBS = {
     "GD_SORT_BALLOT": ("sort_ballot", int),
     "GD_SORT_MIN_CTAS": ("sort_min_ctas", int),
     "GD_DL_DELTA": ("download_delta", int),
+    "GD_INDEX_LOAD_PCT": ("index_load_pct", int),
+    "GD_DL_PIPELINE": ("download_pipeline", int),
+    "GD_DL_PIPELINE_MIN": ("download_pipeline_min_rows", int),
     "GD_XP_PER": ("expand_keys_per_lane", int),
     "GD_WARP_APPEND": ("warp_append", int),
     "GD_PRECOUNT": ("precount", int),

@@ -151,6 +151,8 @@ inline gd_device_config default_device_config() {
     d.precount = 0;
     d.count_ctas_per_sm = 0;
     d.download_delta = 2;
+    d.download_pipeline = 0;
+    d.download_pipeline_min_rows = 1ull << 24;
     return d;
 }
 

@@ -266,6 +266,30 @@ u64 byte_pack(Ctx& c, const u64* keys, u64 n, BytePacked& out) {
     return total;
 }
 
+void byte_pack_into(Ctx& c, const u64* keys, u64 n, u64* heads, uint8_t* cls, u64* offs, uint8_t* payload,
+                    u64 blocks_per_unit, u64* unit_offs) {
+    const u64 nb = (n + kByteBlock - 1) / kByteBlock;
+    if (!nb) return;
+    DevBuf<u64> bytes(c, nb);
+    const int grid = (int)std::min<u64>((u64)c.num_sms * 8, (nb + 7) / 8);
+    byte_class_kernel<<<grid, 256, 0, c.stream>>>(keys, n, nb, cls, bytes.p);
+    c.check_launch();
+    const u64 tiles = (nb + kScanTile - 1) / kScanTile;
+    DevBuf<u64> sums(c, tiles);
+    scan_tile_sums_kernel<<<(unsigned)tiles, kScanT, 0, c.stream>>>(bytes.p, nb, sums.p);
+    c.check_launch();
+    scan_sums_kernel<<<1, 1024, 0, c.stream>>>(sums.p, tiles, offs + nb);
+    c.check_launch();
+    scan_tiles_kernel<<<(unsigned)tiles, kScanT, 0, c.stream>>>(bytes.p, nb, sums.p, offs);
+    c.check_launch();
+    byte_pack_kernel<<<grid, 256, 0, c.stream>>>(keys, n, nb, cls, offs, heads, payload);
+    c.check_launch();
+    const u64 nunits = (nb + blocks_per_unit - 1) / blocks_per_unit;
+    gather_kernel<<<(unsigned)((nunits + 1 + 255) / 256), 256, 0, c.stream>>>(offs, blocks_per_unit, nb, nunits,
+                                                                             unit_offs);
+    c.check_launch();
+}
+
 void byte_unit_offsets(Ctx& c, const BytePacked& d, u64 blocks_per_unit, u64 nunits, u64* dev_out) {
     gather_kernel<<<(unsigned)((nunits + 1 + 255) / 256), 256, 0, c.stream>>>(d.offs.p, blocks_per_unit, d.nb,
                                                                              nunits, dev_out);

@@ -87,8 +87,39 @@ struct Run {
 // kTierRatio times the rows of the next smaller one.
 constexpr u64 kTierRatio = 4;
 
+// Segmented final sort with the download packed per segment
+// (gd_device_config.download_pipeline): the loop's log is
+// sorted by its top digit first (one stable pass), then every top-digit
+// segment by its low digits, and each sorted segment is byte-offset packed
+// (delta.cu byte_pack_into) into the other sort buffer with an event
+// recorded behind it — a host download then copies and rebuilds segment s
+// while the device still sorts the segments after it.
+struct PipedPack {
+    const u64* keys = nullptr;  // the sorted relation this pack belongs to (RelDev::full)
+    u64 n = 0;
+    DevBuf<u64> spare;          // the other sort buffer: segment s's payload at byte 8 * key_off
+    DevBuf<u64> heads, offs, uoffs;
+    DevBuf<uint8_t> cls;
+    struct Seg {
+        u64 key_off, cnt;    // rows [key_off, key_off + cnt)
+        u64 blk_off, nblk;   // heads / cls entries (offs: blk_off + index, nblk + 1 of them)
+        u64 unit_off, nunits;  // uoffs: unit_off + index, nunits + 1 entries
+    };
+    std::vector<Seg> segs;
+    std::vector<cudaEvent_t> ev;  // ev[s]: segment s sorted and packed (context stream)
+    static constexpr u64 kUnitB = 8192;  // blocks of 32 keys per download unit
+    PipedPack() = default;
+    PipedPack(const PipedPack&) = delete;
+    PipedPack& operator=(const PipedPack&) = delete;
+    ~PipedPack() {
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
 template <typename K>
 struct RelDev {
+    std::unique_ptr<PipedPack> piped;  // set by the resident loop's segmented final sort
     // full relation = `full` (the base run) U every run of `tail`; all
     // sorted and pairwise disjoint.  `tail` stays empty unless `lsm`.
     DevBuf<K> full, full_alt;
@@ -271,6 +302,12 @@ public:
         for (auto& st : rels) compact(st);
     }
 
+    bool output_pending() const override {
+        for (const auto& st : rels)
+            if (st.piped) return true;
+        return false;
+    }
+
     u64 count(u32 r) override {
         if (pl && pl->heads[0].rel == r) return pl->hc->h[0].log_n;
         return total_n(rels[r]);
@@ -290,6 +327,13 @@ public:
         if constexpr (std::is_same_v<K, u64>) {
             if (!E.enc.e.dict && ar > 1 && st.full_n >= (1u << 20) &&
                 c.cfg.host_unpack) {
+                std::unique_ptr<PipedPack> pp = std::move(st.piped);
+                if (pp && pp->keys == st.full.p && pp->n == st.full_n && st.tail.empty() &&
+                    c.cfg.download_delta == 2 && c.cfg.download_direct_frac == 0.0) {
+                    download_piped_rows(*pp, ar, out);
+                    return;
+                }
+                pp.reset();
                 download_packed(st.full.p, st.full_n, ar, out);
                 return;
             }
@@ -477,6 +521,142 @@ public:
                     "direct tail %.1f ms\n",
                     (unsigned long long)n_all, (unsigned long long)(n_all - n), nt, t_wait * 1e3, t_unpack * 1e3,
                     t_direct * 1e3);
+    }
+
+    // Download of a segment-packed relation (PipedPack): the calling thread
+    // issues, segment by segment as each one's event completes, the copies of
+    // its units (heads | classes | payload) on a side stream into a ring of
+    // pinned staging areas; nt - 1 threads claim units in order and rebuild
+    // their rows (host_decode.cpp) — so the host rebuild of segment s overlaps
+    // the device sort of the segments after it.
+    void download_piped_rows(PipedPack& pp, u32 ar, u64* out) {
+        const bool trace = (c.cfg.trace & 2) != 0;
+        const double t_start = Ctx::now_s();
+        constexpr u64 kUnitB = PipedPack::kUnitB;
+        const u64 nseg = pp.segs.size();
+        u64 nunits = 0;
+        for (const auto& sg : pp.segs) nunits += sg.nunits;
+        std::vector<u64> uo(nunits + nseg);  // per segment: its nunits + 1 unit offsets
+        struct Unit { u64 seg, j; };
+        std::vector<Unit> units;
+        units.reserve(nunits);
+        for (u64 sgi = 0; sgi < nseg; ++sgi)
+            for (u64 j = 0; j < pp.segs[sgi].nunits; ++j) units.push_back({sgi, j});
+        const u64 R = std::min<u64>(std::max<u64>(nunits, 1), 32);
+        auto up = [](u64 v) { return (v + 63) & ~63ull; };
+        const u64 a_heads = kUnitB * sizeof(u64), a_cls = up(kUnitB);
+        const u64 area = a_heads + a_cls + up(kUnitB * kByteBlock * sizeof(u64) + 64);
+        uint8_t* stage = static_cast<uint8_t*>(c.pinned_staging(R * area));
+        const uint8_t* payload = reinterpret_cast<const uint8_t*>(pp.spare.p);
+        cudaStream_t s2 = nullptr, sm = nullptr;
+        std::vector<cudaEvent_t> ev(R, nullptr);
+        std::unique_ptr<std::atomic<int>[]> issued(new std::atomic<int>[nunits + 1]);
+        std::unique_ptr<std::atomic<int>[]> finished(new std::atomic<int>[nunits + 1]);
+        for (u64 u = 0; u <= nunits; ++u) {
+            issued[u].store(0);
+            finished[u].store(0);
+        }
+        std::atomic<u64> next{0};
+        std::atomic<bool> quit{false};
+        std::exception_ptr err;
+        std::mutex err_mu;
+        std::vector<std::thread> pool;
+        struct Cleanup {
+            std::function<void()> f;
+            ~Cleanup() { f(); }
+        } cleanup{[&] {
+            quit.store(true, std::memory_order_release);
+            for (auto& th : pool)
+                if (th.joinable()) th.join();
+            if (s2) {
+                cudaStreamSynchronize(s2);
+                cudaStreamDestroy(s2);
+            }
+            if (sm) {
+                cudaStreamSynchronize(sm);
+                cudaStreamDestroy(sm);
+            }
+            cudaStreamSynchronize(c.stream);
+            for (auto e : ev)
+                if (e) cudaEventDestroy(e);
+            cudaGetLastError();
+        }};
+        GD_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        GD_CUDA(cudaStreamCreateWithFlags(&sm, cudaStreamNonBlocking));
+        for (auto& e : ev) GD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        const u32 bits = E.enc.e.bits;
+        auto worker = [&] {
+            try {
+                while (!quit.load(std::memory_order_acquire)) {
+                    const u64 u = next.fetch_add(1, std::memory_order_acq_rel);
+                    if (u >= nunits) return;
+                    while (!issued[u].load(std::memory_order_acquire)) {
+                        if (quit.load(std::memory_order_acquire)) return;
+                        std::this_thread::yield();
+                    }
+                    GD_CUDA(cudaEventSynchronize(ev[u % R]));
+                    const PipedPack::Seg& sg = pp.segs[units[u].seg];
+                    const u64 j = units[u].j, b0 = j * kUnitB, nbu = std::min(kUnitB, sg.nblk - b0);
+                    const uint8_t* a = stage + (u % R) * area;
+                    byte_decode_rows(reinterpret_cast<const u64*>(a), a + a_heads, a + a_heads + a_cls,
+                                     sg.key_off + b0 * kByteBlock, nbu, sg.key_off + sg.cnt, ar, bits, out);
+                    finished[u].store(1, std::memory_order_release);
+                }
+            } catch (...) {
+                std::lock_guard<std::mutex> g(err_mu);
+                if (!err) err = std::current_exception();
+                quit.store(true, std::memory_order_release);
+            }
+        };
+        const unsigned hw = std::thread::hardware_concurrency();
+        const unsigned nt = std::max(2u, std::min(hw ? hw : 8u, 32u));
+        for (unsigned t = 1; t < nt; ++t) pool.emplace_back(worker);
+        u64 bytes = 0;
+        double t_seg_wait = 0;
+        u64 u = 0;
+        for (u64 sgi = 0; sgi < nseg && !quit.load(std::memory_order_acquire); ++sgi) {
+            const PipedPack::Seg& sg = pp.segs[sgi];
+            u64* suo = uo.data() + sg.unit_off + sgi;
+            const double tw = Ctx::now_s();
+            GD_CUDA(cudaStreamWaitEvent(sm, pp.ev[sgi], 0));
+            GD_CUDA(cudaMemcpyAsync(suo, pp.uoffs.p + sg.unit_off + sgi, (sg.nunits + 1) * sizeof(u64),
+                                    cudaMemcpyDeviceToHost, sm));
+            GD_CUDA(cudaStreamSynchronize(sm));
+            t_seg_wait += Ctx::now_s() - tw;
+            bytes += (sg.nunits + 1) * sizeof(u64);
+            GD_CUDA(cudaStreamWaitEvent(s2, pp.ev[sgi], 0));
+            for (u64 j = 0; j < sg.nunits; ++j, ++u) {
+                if (u >= R) {  // area u % R is free once unit u - R is rebuilt
+                    while (!finished[u - R].load(std::memory_order_acquire)) {
+                        if (quit.load(std::memory_order_acquire)) break;
+                        std::this_thread::yield();
+                    }
+                    if (quit.load(std::memory_order_acquire)) break;
+                }
+                uint8_t* a = stage + (u % R) * area;
+                const u64 b0 = j * kUnitB, nbu = std::min(kUnitB, sg.nblk - b0);
+                const u64 p0 = suo[j], p1 = suo[j + 1];
+                GD_CUDA(cudaMemcpyAsync(a, pp.heads.p + sg.blk_off + b0, nbu * sizeof(u64), cudaMemcpyDeviceToHost,
+                                        s2));
+                GD_CUDA(cudaMemcpyAsync(a + a_heads, pp.cls.p + sg.blk_off + b0, nbu, cudaMemcpyDeviceToHost, s2));
+                if (p1 > p0)
+                    GD_CUDA(cudaMemcpyAsync(a + a_heads + a_cls, payload + sg.key_off * sizeof(u64) + p0, p1 - p0,
+                                            cudaMemcpyDeviceToHost, s2));
+                GD_CUDA(cudaEventRecord(ev[u % R], s2));
+                bytes += nbu * (sizeof(u64) + 1) + (p1 - p0);
+                issued[u].store(1, std::memory_order_release);
+            }
+        }
+        for (auto& th : pool) th.join();
+        pool.clear();
+        if (err) std::rethrow_exception(err);
+        if (quit.load() && next.load() < nunits) throw Error(GD_ERR_CUDA, "segmented download stopped early");
+        c.d2h_bytes += bytes;
+        if (trace)
+            fprintf(stderr, "[download] %llu rows in %llu segments (%llu units), %u threads: %.1f ms, waiting on "
+                            "segments %.1f ms\n",
+                    (unsigned long long)pp.n, (unsigned long long)nseg, (unsigned long long)nunits, nt,
+                    (Ctx::now_s() - t_start) * 1e3, t_seg_wait * 1e3);
     }
 
     // Byte-offset download of n canonical keys into rows (download_delta = 2):
@@ -903,7 +1083,7 @@ public:
         void alloc_tab(Ctx& c, u64 cap, bool dense = false, bool clear = true) {
             tab.release();
             tab_cap = cap;
-            tab_limit = dense ? cap / 4 * 3 : tab_limit_of(cap);
+            tab_limit = dense ? cap / 4 * 3 : tab_limit_of(c, cap);
             tab = DevBuf<u64>(c, cap * loop_slot_bytes(sbits) / 8);
             if (clear) loop_table_clear(c, tab.p, cap, sbits);
         }
@@ -911,7 +1091,10 @@ public:
     // Linear probing stays short (~1.5 slot reads per new key with the
     // sector scan) at load <= 1/2; a full table grows 4x (to load 1/8), so
     // the re-spreads move about a third of the final key count in total.
-    static u64 tab_limit_of(u64 cap) { return cap / 2; }
+    static u64 tab_limit_of(const Ctx& c, u64 cap) {
+        const u64 pct = c.cfg.index_load_pct ? c.cfg.index_load_pct : 50;
+        return cap / 100 * pct + cap % 100 * pct / 100;
+    }
 
     // The recursive variants as loop steps (plan order, variant order): outer
     // source, join descriptor, inner copy and index (dense form when
@@ -1574,6 +1757,12 @@ public:
             const u64 f = hc->h[h].log_n;
             const u32 ar = E.info_[rec[h]].arity;
             DevBuf<u64> scratch(c, std::max<u64>(f, 1));
+            st.piped.reset();
+            if (c.cfg.download_pipeline && f >= c.cfg.download_pipeline_min_rows && ar * bits > 8 && ar > 1 &&
+                !E.enc.e.dict && c.cfg.sort_pipeline == 0) {
+                segmented_final_sort(st, H.log, scratch, f, ar * bits);
+                continue;
+            }
             u64* sorted = radix_sort<u64>(c, H.log.p, scratch.p, f, ar * bits);
             DevBuf<u64>& res = sorted == H.log.p ? H.log : scratch;
             st.full.release();
@@ -1587,6 +1776,82 @@ public:
             st.delta_n = 0;
             st.new_n = 0;
         }
+    }
+
+    // Segmented final sort (PipedPack): the top digit first (one stable pass,
+    // its histogram read back for the segment bounds), then each top-digit
+    // segment on its low digits (the ranking choice sampled on the first
+    // segment and reused), each sorted segment packed for the download with
+    // an event behind it.  Same passes and the same sorted keys as
+    // radix_sort; the relation's full array is the buffer the segments end
+    // in, the other one holds the packed payloads until the download.
+    void segmented_final_sort(RelDev<K>& st, DevBuf<u64>& log, DevBuf<u64>& scratch, u64 f, u32 nbits) {
+        const u32 npass = (nbits + 7) / 8;
+        std::vector<u64> top;
+        u64* msd = radix_sort_passes<u64>(c, log.p, scratch.p, f, nbits, npass - 1, npass, nullptr, &top);
+        DevBuf<u64>& mbuf = msd == log.p ? log : scratch;
+        DevBuf<u64>& obuf = msd == log.p ? scratch : log;
+        // the low passes ping-pong between the two buffers: odd counts end in obuf
+        DevBuf<u64>& tbuf = (npass - 1) % 2 ? obuf : mbuf;
+        auto pp = std::make_unique<PipedPack>();
+        u64 off = 0, blk = 0, unit = 0;
+        for (u64 d = 0; d < top.size(); ++d) {
+            if (!top[d]) continue;
+            PipedPack::Seg sg;
+            sg.key_off = off;
+            sg.cnt = top[d];
+            sg.blk_off = blk;
+            sg.nblk = (sg.cnt + kByteBlock - 1) / kByteBlock;
+            sg.unit_off = unit;
+            sg.nunits = (sg.nblk + PipedPack::kUnitB - 1) / PipedPack::kUnitB;
+            pp->segs.push_back(sg);
+            off += sg.cnt;
+            blk += sg.nblk;
+            unit += sg.nunits;
+        }
+        if (off != f) throw Error(GD_ERR_CUDA, "segmented sort: digit counts do not add up to the row count");
+        const u64 nseg = pp->segs.size();
+        pp->heads = DevBuf<u64>(c, std::max<u64>(blk, 1));
+        pp->cls = DevBuf<uint8_t>(c, std::max<u64>(blk, 1));
+        pp->offs = DevBuf<u64>(c, blk + nseg);
+        pp->uoffs = DevBuf<u64>(c, unit + nseg);
+        pp->ev.assign(nseg, nullptr);
+        for (auto& e : pp->ev) GD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        std::vector<char> ballot;
+        const bool trace = (c.cfg.trace & 4) != 0;
+        const double t0 = Ctx::now_s();
+        for (u64 i = 0; i < nseg; ++i) {
+            if (trace && (i < 4 || i % 16 == 0 || i + 1 == nseg))
+                fprintf(stderr, "[segsort] segment %llu/%llu (%llu keys) enqueued at +%.2f ms\n",
+                        (unsigned long long)i, (unsigned long long)nseg, (unsigned long long)pp->segs[i].cnt,
+                        (Ctx::now_s() - t0) * 1e3);
+            const PipedPack::Seg& sg = pp->segs[i];
+            u64* r = npass > 1 ? radix_sort_passes<u64>(c, mbuf.p + sg.key_off, obuf.p + sg.key_off, sg.cnt, nbits, 0,
+                                                        npass - 1, &ballot, nullptr)
+                               : mbuf.p + sg.key_off;
+            if (r != tbuf.p + sg.key_off) c.d2d(tbuf.p + sg.key_off, r, sg.cnt * sizeof(u64));
+            DevBuf<u64>& sbuf = &tbuf == &mbuf ? obuf : mbuf;
+            byte_pack_into(c, tbuf.p + sg.key_off, sg.cnt, pp->heads.p + sg.blk_off, pp->cls.p + sg.blk_off,
+                           pp->offs.p + sg.blk_off + i, reinterpret_cast<uint8_t*>(sbuf.p + sg.key_off),
+                           PipedPack::kUnitB, pp->uoffs.p + sg.unit_off + i);
+            GD_CUDA(cudaEventRecord(pp->ev[i], c.stream));
+        }
+        if (trace) fprintf(stderr, "[segsort] all segments enqueued at +%.2f ms\n", (Ctx::now_s() - t0) * 1e3);
+        DevBuf<u64>& sbuf = &tbuf == &mbuf ? obuf : mbuf;
+        st.full.release();
+        st.full.ctx = tbuf.ctx;
+        st.full.p = reinterpret_cast<K*>(tbuf.p);
+        st.full.cap = tbuf.cap;
+        tbuf.p = nullptr;
+        tbuf.cap = 0;
+        st.full_n = f;
+        st.tail.clear();
+        st.delta_n = 0;
+        st.new_n = 0;
+        pp->keys = reinterpret_cast<const u64*>(st.full.p);
+        pp->n = f;
+        pp->spare = std::move(sbuf);
+        st.piped = std::move(pp);
     }
 
     // The reference's per-iteration bookkeeping (engine.hpp:196-251) from the
@@ -3088,7 +3353,8 @@ void Engine::iterate() {  // engine.hpp:181-257
     if (!seeded) seed();
     const auto t0 = std::chrono::steady_clock::now();
     impl->iterate();
-    c.sync();
+    if (c.cfg.trace & 4) fprintf(stderr, "[segsort] iterate returns (pending %d)\n", (int)impl->output_pending());
+    if (!impl->output_pending()) c.sync();
     total_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 

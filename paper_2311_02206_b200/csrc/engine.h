@@ -33,6 +33,10 @@ public:
     virtual ~ImplBase() = default;
     virtual void seed() = 0;
     virtual void iterate() = 0;
+    // True when the canonical output is still being sorted / packed on the
+    // stream (segmented final sort): iterate() returns without a sync and
+    // the download waits per segment.
+    virtual bool output_pending() const { return false; }
     virtual u64 count(u32 rel) = 0;
     virtual void download(u32 rel, u64* out, bool device) = 0;
     virtual u64 digest(u32 rel) = 0;

@@ -51,8 +51,9 @@ void decode_block_scalar(uint64_t head, uint32_t code, const uint8_t* p, uint32_
 }
 
 #if defined(__x86_64__)
-// Arity 2, destination 64-byte aligned, full blocks.
-__attribute__((target("avx512f"))) void decode_avx512(const uint64_t* heads, const uint8_t* cls,
+// Arity 2, 16-byte aligned rows, full blocks (64-byte stores where a block's
+// rows start a line).
+__attribute__((target("avx512f,avx512dq"))) void decode_avx512(const uint64_t* heads, const uint8_t* cls,
                                                       const uint8_t* payload, uint64_t first_row, uint64_t nblocks,
                                                       uint64_t n_total, uint32_t bits, uint64_t mask, uint64_t* out) {
     const __m512i vmask = _mm512_set1_epi64((long long)mask);
@@ -71,6 +72,7 @@ __attribute__((target("avx512f"))) void decode_avx512(const uint64_t* heads, con
             continue;
         }
         const __m512i head = _mm512_set1_epi64((long long)heads[b]);
+        const bool line = !(reinterpret_cast<uintptr_t>(dst) & 63);  // else 16-byte aligned rows
 #pragma GCC unroll 4
         for (int q = 0; q < 4; ++q) {
             __m512i off;
@@ -83,8 +85,21 @@ __attribute__((target("avx512f"))) void decode_avx512(const uint64_t* heads, con
             const __m512i key = _mm512_add_epi64(head, off);
             const __m512i hi = _mm512_and_si512(_mm512_srl_epi64(key, sh), vmask);
             const __m512i lo = _mm512_and_si512(key, vmask);
-            _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + 16 * q), _mm512_permutex2var_epi64(hi, i0, lo));
-            _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + 16 * q + 8), _mm512_permutex2var_epi64(hi, i1, lo));
+            const __m512i r0 = _mm512_permutex2var_epi64(hi, i0, lo), r1 = _mm512_permutex2var_epi64(hi, i1, lo);
+            if (line) {
+                _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + 16 * q), r0);
+                _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + 16 * q + 8), r1);
+            } else {  // rows of a segment that starts off a 64-byte line: one 16-byte store per row
+                __m128i* d = reinterpret_cast<__m128i*>(dst + 16 * q);
+                _mm_stream_si128(d + 0, _mm512_extracti64x2_epi64(r0, 0));
+                _mm_stream_si128(d + 1, _mm512_extracti64x2_epi64(r0, 1));
+                _mm_stream_si128(d + 2, _mm512_extracti64x2_epi64(r0, 2));
+                _mm_stream_si128(d + 3, _mm512_extracti64x2_epi64(r0, 3));
+                _mm_stream_si128(d + 4, _mm512_extracti64x2_epi64(r1, 0));
+                _mm_stream_si128(d + 5, _mm512_extracti64x2_epi64(r1, 1));
+                _mm_stream_si128(d + 6, _mm512_extracti64x2_epi64(r1, 2));
+                _mm_stream_si128(d + 7, _mm512_extracti64x2_epi64(r1, 3));
+            }
         }
         p += (uint64_t)kBlock << code;
     }
@@ -92,7 +107,7 @@ __attribute__((target("avx512f"))) void decode_avx512(const uint64_t* heads, con
 }
 
 bool has_avx512() {
-    static const bool v = __builtin_cpu_supports("avx512f");
+    static const bool v = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512dq");
     return v;
 }
 #endif
@@ -115,7 +130,7 @@ void byte_decode_rows(const unsigned long long* heads_, const uint8_t* cls, cons
     uint64_t* out = reinterpret_cast<uint64_t*>(out_);
     const uint64_t mask = bits >= 64 ? ~0ull : (1ull << bits) - 1;
 #if defined(__x86_64__)
-    if (ar == 2 && !(reinterpret_cast<uintptr_t>(out) & 63) && has_avx512()) {
+    if (ar == 2 && !(reinterpret_cast<uintptr_t>(out) & 15) && has_avx512()) {
         decode_avx512(heads, cls, payload, first_row, nblocks, n_total, bits, mask, out);
         return;
     }

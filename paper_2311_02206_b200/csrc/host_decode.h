@@ -15,7 +15,7 @@ namespace gd {
 void byte_decode_rows(const unsigned long long* heads, const uint8_t* cls, const uint8_t* payload, uint64_t first_row,
                       uint64_t nblocks, uint64_t n_total, uint32_t ar, uint32_t bits, unsigned long long* out);
 
-// True when the AVX-512 decoder is used (x86-64 host with AVX-512F).
+// True when the AVX-512 decoder is used (x86-64 host with AVX-512F/DQ).
 bool byte_decode_vectorized();
 
 }  // namespace gd

@@ -32,6 +32,14 @@ inline u32 bitwidth(u64 v) {  // bits needed to represent v (0 -> 0)
 // Uses b as scratch; returns the buffer holding the sorted keys (a or b).
 template <typename K>
 K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits);
+// Only the LSD passes [pass_lo, pass_hi) of the same sort (8-bit digits;
+// higher key bits are ignored by a pass, so a segment whose top digits are
+// equal sorts on its low passes alone).  ballot_io: per-pass ranking choice
+// to use, or empty to sample each pass and return the choices; top_hist:
+// receives the digit counts of pass pass_hi - 1 (one host sync).
+template <typename K>
+K* radix_sort_passes(Ctx& c, K* a, K* b, u64 n, u32 nbits, u32 pass_lo, u32 pass_hi, std::vector<char>* ballot_io,
+                     std::vector<u64>* top_hist);
 
 // ---- delta.cu (download compression) ----------------------------------
 constexpr u32 kDeltaBlock = 64;  // keys per delta block
@@ -61,6 +69,12 @@ struct BytePacked {
     DevBuf<uint8_t> payload;
 };
 u64 byte_pack(Ctx& c, const u64* keys, u64 n, BytePacked& out);
+// The same into caller buffers, stream-ordered with no host sync (segmented
+// final sort, engine.cu): heads / cls get ceil(n / 32) entries, offs one
+// more, payload up to 8 n bytes, unit_offs[k] = offs[min(k * blocks_per_unit,
+// nb)] for k = 0..ceil(nb / blocks_per_unit).
+void byte_pack_into(Ctx& c, const u64* keys, u64 n, u64* heads, uint8_t* cls, u64* offs, uint8_t* payload,
+                    u64 blocks_per_unit, u64* unit_offs);
 // dev_out[k] = d.offs[min(k * blocks_per_unit, nb)] for k = 0..nunits.
 void byte_unit_offsets(Ctx& c, const BytePacked& d, u64 blocks_per_unit, u64 nunits, u64* dev_out);
 

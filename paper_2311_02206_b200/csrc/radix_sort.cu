@@ -709,14 +709,17 @@ u64* radix_sort_pipe(Ctx& c, u64* a, u64* b, u64 n, u32 nbits) {
 }
 
 template <typename K>
-K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
+K* radix_sort_passes(Ctx& c, K* a, K* b, u64 n, u32 nbits, u32 pass_lo, u32 pass_hi, std::vector<char>* ballot_io,
+                     std::vector<u64>* top_hist) {
     if (n <= 1 || nbits == 0) return a;
+    const bool whole = pass_lo == 0 && pass_hi == ~0u && !ballot_io && !top_hist;
     if constexpr (sizeof(K) == 8) {
-        if (c.cfg.sort_pipeline && c.cfg.sort_pipeline != 4 && n >= c.cfg.sort_pipeline_min_keys)
+        if (whole && c.cfg.sort_pipeline && c.cfg.sort_pipeline != 4 && n >= c.cfg.sort_pipeline_min_keys)
             return reinterpret_cast<K*>(radix_sort_pipe(c, reinterpret_cast<u64*>(a), reinterpret_cast<u64*>(b), n,
                                                         nbits));
     }
     const int npass = (int)((nbits + kRadixBits - 1) / kRadixBits);
+    const int p_lo = (int)std::min<u32>(pass_lo, (u32)npass), p_hi = (int)std::min<u32>(pass_hi, (u32)npass);
     const int nportions = (int)((n + kPortion - 1) / kPortion);
     const int items = sort_items<K>(c);
     const u64 TILE = (u64)kSortThreads * items;
@@ -737,6 +740,11 @@ K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
     radix_bases_kernel<<<npass, kRadix, 0, c.stream>>>(hist.p, bases.p);
     c.check_launch();
     u64* pp[2] = {bases.p + hist_words, bases.p + hist_words + kRadix};
+    if (top_hist && p_hi > 0) {  // digit counts of the last requested pass
+        top_hist->assign(kRadix, 0);
+        c.d2h(top_hist->data(), hist.p + (u64)(p_hi - 1) * kRadix, kRadix * sizeof(u64));
+        c.sync();
+    }
 
     const u64 max_tiles = (std::min(n, kPortion) + TILE - 1) / TILE;
     const u64 ws_words = 1 + max_tiles * kRadix;
@@ -758,12 +766,17 @@ K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
     // is sampled on the pass's actual input right before the pass: 2048
     // warps of consecutive keys, one readback per pass.  C2: ballot on
     // passes 3-4 only, final sort 34.2 -> ~30 ms (profiles/r2_sort_passes.md).
+    // ballot_io: decisions given by the caller (sized npass), or empty: sample
+    // every pass (from 1 M keys) and hand the decisions back — the segments
+    // of a segmented sort sample once, on their first segment.
     std::vector<char> ballot(npass, 0);
-    const bool adapt = c.cfg.sort_ballot && n >= c.cfg.sort_pipeline_min_keys * 16 && c.cfg.sort_pipeline == 0;
+    const bool given = ballot_io && (int)ballot_io->size() == npass;
+    const u64 adapt_min = ballot_io ? (1ull << 20) : c.cfg.sort_pipeline_min_keys * 16;
+    const bool adapt = !given && c.cfg.sort_ballot && n >= adapt_min && c.cfg.sort_pipeline == 0;
     DevBuf<unsigned long long> div;
     if (adapt) div = DevBuf<unsigned long long>(c, 1);
-    for (int pass = 0; pass < npass; ++pass) {
-        bool use_ballot = c.cfg.sort_pipeline == 4;
+    for (int pass = p_lo; pass < p_hi; ++pass) {
+        bool use_ballot = given ? (*ballot_io)[pass] != 0 : c.cfg.sort_pipeline == 4;
         if (adapt) {
             constexpr int kSampleWarps = 2048;
             c.memset(div.p, 0, sizeof(unsigned long long));
@@ -795,10 +808,17 @@ K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
         }
         std::swap(src, dst);
     }
+    if (ballot_io && !given) *ballot_io = ballot;
     return src;
 }
 
+template <typename K>
+K* radix_sort(Ctx& c, K* a, K* b, u64 n, u32 nbits) {
+    return radix_sort_passes<K>(c, a, b, n, nbits, 0, ~0u, nullptr, nullptr);
+}
+
 template u64* radix_sort<u64>(Ctx&, u64*, u64*, u64, u32);
+template u64* radix_sort_passes<u64>(Ctx&, u64*, u64*, u64, u32, u32, u32, std::vector<char>*, std::vector<u64>*);
 template u128* radix_sort<u128>(Ctx&, u128*, u128*, u64, u32);
 
 }  // namespace gd

@@ -145,49 +145,73 @@ __global__ void __launch_bounds__(256) delta_pack_kernel(const u64* __restrict__
 }
 
 // ---- byte-offset blocks (download_delta = 2) ----
-// One warp per block of kByteBlock keys: the block's offset class (bytes
-// per offset from its first key: 1 / 2 / 4 / 8, code 0..3) and its payload
-// bytes.
+// A warp takes kBW consecutive blocks of kByteBlock keys per step, their
+// loads issued together (one key per lane per block).
+constexpr int kBW = 4;
+
+// The block's offset class (bytes per offset from its first key: 1 / 2 / 4
+// / 8, code 0..3) and its payload bytes.
 __global__ void byte_class_kernel(const u64* __restrict__ keys, u64 n, u64 nb, uint8_t* __restrict__ cls,
                                   u64* __restrict__ bytes) {
     const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
     const u32 lane = lane_id();
-    for (u64 b = warp; b < nb; b += ((u64)gridDim.x * blockDim.x) >> 5) {
-        const u64 base = b * kByteBlock;
-        const u32 cnt = (u32)min((u64)kByteBlock, n - base);
-        const u64 k = lane < cnt ? keys[base + lane] : 0;
-        const u64 head = __shfl_sync(0xffffffffu, k, 0);
-        const u64 last = __shfl_sync(0xffffffffu, k, cnt - 1);
-        if (lane == 0) {
-            const u64 r = last - head;
-            const u32 code = r < (1ull << 8) ? 0 : r < (1ull << 16) ? 1 : r < (1ull << 32) ? 2 : 3;
-            cls[b] = (uint8_t)code;
-            bytes[b] = (u64)cnt << code;
+    for (u64 b0 = warp * kBW; b0 < nb; b0 += nw * kBW) {
+        u64 k[kBW];
+        u32 cnt[kBW];
+#pragma unroll
+        for (int q = 0; q < kBW; ++q) {
+            const u64 b = b0 + q;
+            cnt[q] = b < nb ? (u32)min((u64)kByteBlock, n - b * kByteBlock) : 0u;
+            k[q] = lane < cnt[q] ? keys[b * kByteBlock + lane] : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < kBW; ++q) {
+            if (!cnt[q]) break;  // warp-uniform
+            const u64 head = __shfl_sync(0xffffffffu, k[q], 0);
+            const u64 last = __shfl_sync(0xffffffffu, k[q], cnt[q] - 1);
+            if (lane == q) {
+                const u64 r = last - head;
+                const u32 code = r < (1ull << 8) ? 0 : r < (1ull << 16) ? 1 : r < (1ull << 32) ? 2 : 3;
+                cls[b0 + q] = (uint8_t)code;
+                bytes[b0 + q] = (u64)cnt[q] << code;
+            }
         }
     }
 }
 
-// One warp per block: the first key to heads, offset i (key_i - head) to
-// payload[offs[b] + i * width], little-endian.
+// The first key to heads, offset i (key_i - head) to payload[offs[b] + i *
+// width], little-endian.
 __global__ void byte_pack_kernel(const u64* __restrict__ keys, u64 n, u64 nb, const uint8_t* __restrict__ cls,
                                  const u64* __restrict__ offs, u64* __restrict__ heads, uint8_t* __restrict__ payload) {
     const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
     const u32 lane = lane_id();
-    for (u64 b = warp; b < nb; b += ((u64)gridDim.x * blockDim.x) >> 5) {
-        const u64 base = b * kByteBlock;
-        const u32 cnt = (u32)min((u64)kByteBlock, n - base);
-        const u64 k = lane < cnt ? keys[base + lane] : 0;
-        const u64 head = __shfl_sync(0xffffffffu, k, 0);
-        const u32 code = cls[b];
-        if (lane == 0) heads[b] = head;
-        if (lane < cnt) {
-            const u64 o = k - head;
-            uint8_t* p = payload + offs[b] + ((u64)lane << code);
-            switch (code) {  // offsets of one width are aligned to it when the block start is
-                case 0: *p = (uint8_t)o; break;
-                case 1: for (int q = 0; q < 2; ++q) p[q] = (uint8_t)(o >> (8 * q)); break;
-                case 2: for (int q = 0; q < 4; ++q) p[q] = (uint8_t)(o >> (8 * q)); break;
-                default: for (int q = 0; q < 8; ++q) p[q] = (uint8_t)(o >> (8 * q)); break;
+    for (u64 b0 = warp * kBW; b0 < nb; b0 += nw * kBW) {
+        u64 k[kBW], base[kBW];
+        u32 cnt[kBW], code[kBW];
+#pragma unroll
+        for (int q = 0; q < kBW; ++q) {
+            const u64 b = b0 + q;
+            cnt[q] = b < nb ? (u32)min((u64)kByteBlock, n - b * kByteBlock) : 0u;
+            k[q] = lane < cnt[q] ? keys[b * kByteBlock + lane] : 0;
+            code[q] = cnt[q] ? cls[b] : 0u;
+            base[q] = cnt[q] ? offs[b] : 0ull;
+        }
+#pragma unroll
+        for (int q = 0; q < kBW; ++q) {
+            if (!cnt[q]) break;  // warp-uniform
+            const u64 head = __shfl_sync(0xffffffffu, k[q], 0);
+            if (lane == 0) heads[b0 + q] = head;
+            if (lane < cnt[q]) {
+                const u64 o = k[q] - head;
+                uint8_t* p = payload + base[q] + ((u64)lane << code[q]);
+                switch (code[q]) {
+                    case 0: *p = (uint8_t)o; break;
+                    case 1: for (int i = 0; i < 2; ++i) p[i] = (uint8_t)(o >> (8 * i)); break;
+                    case 2: for (int i = 0; i < 4; ++i) p[i] = (uint8_t)(o >> (8 * i)); break;
+                    default: for (int i = 0; i < 8; ++i) p[i] = (uint8_t)(o >> (8 * i)); break;
+                }
             }
         }
     }
@@ -271,7 +295,7 @@ void byte_pack_into(Ctx& c, const u64* keys, u64 n, u64* heads, uint8_t* cls, u6
     const u64 nb = (n + kByteBlock - 1) / kByteBlock;
     if (!nb) return;
     DevBuf<u64> bytes(c, nb);
-    const int grid = (int)std::min<u64>((u64)c.num_sms * 8, (nb + 7) / 8);
+    const int grid = (int)std::min<u64>((u64)c.num_sms * 8, (nb + 8 * kBW - 1) / (8 * kBW));
     byte_class_kernel<<<grid, 256, 0, c.stream>>>(keys, n, nb, cls, bytes.p);
     c.check_launch();
     const u64 tiles = (nb + kScanTile - 1) / kScanTile;

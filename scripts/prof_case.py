@@ -1,5 +1,5 @@
 """One fixpoint run of a named case for ncu captures
-(python scripts/prof_case.py chain|c2|c2log|<workloads.CONFIGS name>|cspa:<n>)."""
+(python scripts/prof_case.py chain|c2|c2dl|c2log|<workloads.CONFIGS name>|cspa:<n>)."""
 import sys
 from pathlib import Path
 
@@ -30,6 +30,9 @@ e = al.engine("reach")
 e.load_edb("Edge", al.tuple_array(2, edges))
 e.run()
 print("iterations", e.stats().iterations, "|Reach|", e.relation_count("Reach"))
+if case == "c2dl":  # plus the host download (byte-offset packing on the device)
+    rows = e.relation("Reach").data
+    print("downloaded", rows.shape)
 if case == "c2log":
     log = e.iter_log("Reach")
     big = sorted(range(len(log)), key=lambda i: -log[i][1])[:10]

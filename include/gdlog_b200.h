@@ -197,6 +197,8 @@ typedef struct gd_device_config {
                                        155.2 ms of device time, e2e only 6 ms shorter — 75% of C2's rows
                                        share one top digit, so the first segment is most of the sort) */
     uint64_t download_pipeline_min_rows;  /* (1 << 24) */
+    uint32_t gate_in_insert;        /* a single warp-expanded step (TC): the capacity gate is evaluated by every
+                                       CTA of the insert kernel instead of loop_count's last CTA (1) */
 } gd_device_config;
 
 void gd_device_config_default(gd_device_config* cfg);

@@ -93,6 +93,7 @@ class gd_device_config(C.Structure):
         ("index_load_pct", u32),
         ("download_pipeline", u32),
         ("download_pipeline_min_rows", u64),
+        ("gate_in_insert", u32),
     ]
 
 

@@ -153,6 +153,7 @@ inline gd_device_config default_device_config() {
     d.download_delta = 2;
     d.download_pipeline = 0;
     d.download_pipeline_min_rows = 1ull << 24;
+    d.gate_in_insert = 1;
     return d;
 }
 

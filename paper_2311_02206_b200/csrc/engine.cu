@@ -1305,6 +1305,10 @@ public:
                 if (heads[h].sbits) g.stamp_max = std::min<u32>(g.stamp_max, (1u << heads[h].sbits) - 1);
             }
             const bool fuse_gate = !steps[ns - 1].select;
+            // a single warp-expanded step (TC): its insert kernel evaluates the gate
+            // in every CTA, so loop_count needs no last-CTA epilogue
+            const bool gate_ins = c.cfg.gate_in_insert && ns == 1 && steps[0].xp && !steps[0].split_insert &&
+                                  steps[0].final && !steps[0].pre && fuse_gate;
             for (u32 i = 0; i < ns; ++i) {
                 LStep& L = steps[i];
                 const LoopOuter o = outer_of(L);
@@ -1317,7 +1321,7 @@ public:
                 cudaEvent_t t = br();
                 if (L.xp) {
                     loop_count(c, s, ctl.p, i, o, L.jd, L.dv, L.bufs(), c.cfg.heavy_rows,
-                               fuse_gate && i + 1 == ns ? &g : nullptr);
+                               fuse_gate && !gate_ins && i + 1 == ns ? &g : nullptr);
                     prof_recs.push_back({c.prof_end(t, KC_PROBE, 0), 4, i});
                     continue;
                 }
@@ -1357,7 +1361,7 @@ public:
                     loop_insert_keys(c, s, ctl.p, i, L.head, L.temp.p, bufs_of(L.head), e);
                 } else if (L.xp)
                     loop_expand_insert(c, s, ctl.p, i, L.head, o, L.inner, L.jd, L.dv, L.bufs(), c.cfg.heavy_rows,
-                                       bufs_of(L.head), e);
+                                       bufs_of(L.head), e, gate_ins ? &g : nullptr);
                 else if (L.split_insert)
                     loop_insert_keys(c, s, ctl.p, i, L.head, L.temp.p, bufs_of(L.head), e);
                 else

@@ -323,6 +323,52 @@ __device__ void gate_body(LoopCtl* ctl, const LoopGateDesc& g) {
     if (over) ctl->overflow = 1;
 }
 
+// The gate evaluated by every CTA of the insert kernel itself (gate in the
+// insert, gd_device_config.gate_in_insert): the same decision as gate_body
+// from fields that stay fixed while the iteration inserts — the log size
+// before any insert is the Δ window's end (log_n == dhi until the first
+// append) — so every CTA reaches the same answer without a barrier; the
+// caller's CTA 0 also writes the capacities it asks for (write = true).
+// Returns true when the iteration must not insert.
+__device__ bool gate_eval(LoopCtl* ctl, const LoopGateDesc& g, bool write) {
+    const u32 overflow = __ldcg(&ctl->overflow), done = __ldcg(&ctl->done), iter = __ldcg(&ctl->iter);
+    const u32 nh = __ldcg(&ctl->nheads), epoch = __ldcg(&ctl->epoch_base);
+    const u64 hist_cap = __ldcg(&ctl->hist_cap);
+    if (overflow | done) return true;
+    if (iter >= hist_cap) {
+        if (write) {
+            ctl->need_hist = hist_cap * 2;
+            ctl->overflow = 1;
+        }
+        return true;
+    }
+    if (iter + 1 - epoch > g.stamp_max) {
+        if (write) {
+            ctl->need_restamp = 1;
+            ctl->overflow = 1;
+        }
+        return true;
+    }
+    bool over = false;
+    for (u32 h = 0; h < nh; ++h) {
+        u64 add = 0;
+        for (u32 f = 0; f < g.nfinal; ++f)
+            if (g.final_head[f] == h) add += __ldcg(&ctl->step_cand[g.final_step[f]]);
+        const u64 need = __ldcg(&ctl->h[h].dhi) + add;
+        if (write) ctl->h[h].cand = add;
+        if (need > g.log_cap[h]) {
+            if (write) ctl->need_log[h] = need;
+            over = true;
+        }
+        if (need > g.tab_limit[h]) {
+            if (write) ctl->need_tab[h] = need;
+            over = true;
+        }
+    }
+    if (over && write) ctl->overflow = 1;
+    return over;
+}
+
 __device__ void end_body(LoopCtl* ctl, const LoopEndDesc& e) {
     const cudaGraphConditionalHandle cond = (cudaGraphConditionalHandle)e.cond;
     const u32 overflow = __ldcg(&ctl->overflow), done = __ldcg(&ctl->done), iter = __ldcg(&ctl->iter);
@@ -1333,11 +1379,19 @@ __device__ __forceinline__ void expand_rows(const LoopCtl* ctl, u32 step, const 
 template <int NS, int PER = kXPer, int XB = 1>
 __global__ void __launch_bounds__(kLT, PER >= 8 ? 3 : 5) loop_expand_insert_kernel(
     LoopCtl* ctl, u32 step, u32 head, LoopOuter o, const u64* __restrict__ inner, DevJoin jd, LoopDense dv,
-    LoopStepBufs sb, u64 heavy_min, LoopHeadBufs hb, LoopEndDesc e, int do_end) {
+    LoopStepBufs sb, u64 heavy_min, LoopHeadBufs hb, LoopEndDesc e, int do_end, LoopGateDesc g, int do_gate) {
     __shared__ u64 sbuf[kLT / 32][PER >= 8 ? kXBuf : kXBuf / 2];
     __shared__ u64 red[kLT / 32];
     __shared__ u32 s_flag;
-    if (!cta_stopped(ctl, &s_flag)) {
+    bool stopped;
+    if (do_gate) {  // the iteration's gate, evaluated here instead of in loop_count's last CTA
+        if (threadIdx.x == 0) s_flag = gate_eval(ctl, g, blockIdx.x == 0) ? 1u : 0u;
+        __syncthreads();
+        stopped = s_flag != 0;
+    } else {
+        stopped = cta_stopped(ctl, &s_flag);
+    }
+    if (!stopped) {
         const u64* outer;
         u64 n;
         resolve(o, ctl, outer, n);
@@ -2121,16 +2175,18 @@ void loop_count(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter&
 
 void loop_expand_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
                         const u64* inner, const DevJoin& jd, const LoopDense& dense, const LoopStepBufs& sb,
-                        u64 heavy_rows, const LoopHeadBufs& hb, const LoopEndDesc* end) {
+                        u64 heavy_rows, const LoopHeadBufs& hb, const LoopEndDesc* end, const LoopGateDesc* gate) {
     LoopEndDesc e{};
     if (end) e = *end;
+    LoopGateDesc g{};
+    if (gate) g = *gate;
     const int waves = c.cfg.insert_waves ? (int)c.cfg.insert_waves : 1;
     if (c.cfg.expand_keys_per_lane == 4)
         loop_expand_insert_kernel<1, 4><<<c.num_sms * g_occ_expand4 * waves, kLT, 0, s>>>(
-            ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0);
+            ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0, g, gate ? 1 : 0);
     else
         SLOT_DISPATCH(c, loop_expand_insert_kernel, <<<c.num_sms * g_occ_expand * waves, kLT, 0, s>>>(
-        ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0));
+        ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0, g, gate ? 1 : 0));
     c.check_launch();
 }
 

@@ -300,9 +300,13 @@ void loop_count(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter&
 // Expansion fused with dedup + difference + append: every warp expands 32
 // outer rows at a time into a shared buffer and inserts 256 keys at a
 // time, then the heavy items; loop_end in the last CTA when `end`.
+// gate: the iteration's capacity gate, evaluated by every CTA at its start
+// (the step must be the iteration's only candidate producer, nothing
+// inserted before it in the iteration).
 void loop_expand_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
                         const u64* inner, const DevJoin& jd, const LoopDense& dense, const LoopStepBufs& sb,
-                        u64 heavy_rows, const LoopHeadBufs& hb, const LoopEndDesc* end);
+                        u64 heavy_rows, const LoopHeadBufs& hb, const LoopEndDesc* end,
+                        const LoopGateDesc* gate = nullptr);
 
 // The same expansion appended to the step's temp (split final step, then
 // loop_insert_keys over the temp).

@@ -199,6 +199,8 @@ typedef struct gd_device_config {
     uint64_t download_pipeline_min_rows;  /* (1 << 24) */
     uint32_t gate_in_insert;        /* a single warp-expanded step (TC): the capacity gate is evaluated by every
                                        CTA of the insert kernel instead of loop_count's last CTA (1) */
+    uint32_t pdl;                   /* the warp-expanded insert is a programmatic dependent launch of loop_count
+                                       (its CTAs take SM slots as the count's retire, then wait for it) (0) */
 } gd_device_config;
 
 void gd_device_config_default(gd_device_config* cfg);

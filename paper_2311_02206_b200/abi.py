@@ -94,6 +94,7 @@ class gd_device_config(C.Structure):
         ("download_pipeline", u32),
         ("download_pipeline_min_rows", u64),
         ("gate_in_insert", u32),
+        ("pdl", u32),
     ]
 
 

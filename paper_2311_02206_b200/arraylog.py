@@ -229,6 +229,7 @@ _ENV_KNOBS = {
     "GD_DL_PIPELINE": ("download_pipeline", int),
     "GD_DL_PIPELINE_MIN": ("download_pipeline_min_rows", int),
     "GD_GATE_IN_INSERT": ("gate_in_insert", int),
+    "GD_PDL": ("pdl", int),
     "GD_XP_PER": ("expand_keys_per_lane", int),
     "GD_WARP_APPEND": ("warp_append", int),
     "GD_PRECOUNT": ("precount", int),

@@ -1690,8 +1690,19 @@ public:
                     prof_recs.clear();
                     record_iteration(c.stream, false, 0);
                 } else {
+                    const double tb = Ctx::now_s();
+                    const bool built = !exec;
                     if (!exec) build_graph();
+                    const double tl = Ctx::now_s();
                     for (int b = 0; b < (batch ? batch_n : 1); ++b) GD_CUDA(cudaGraphLaunch(exec, c.stream));
+                    if (trace) {
+                        const double te = Ctx::now_s();
+                        c.d2h(hc, ctl.p, sizeof(LoopCtl));
+                        c.sync();
+                        fprintf(stderr, "[loop] graph%s: build %.3f ms, launch %.3f ms, run to iter %u %.3f ms\n",
+                                built ? " (new)" : "", (tl - tb) * 1e3, (te - tl) * 1e3, hc->iter,
+                                (Ctx::now_s() - te) * 1e3);
+                    }
                 }
                 c.d2h(hc, ctl.p, sizeof(LoopCtl));
                 c.sync();

@@ -1064,6 +1064,10 @@ __global__ void __launch_bounds__(kLT) loop_count_kernel(LoopCtl* ctl, u32 step,
                                                          LoopGateDesc g, int do_gate) {
     __shared__ u64 red[kLT / 32];
     __shared__ u32 s_flag;
+    // the insert launched behind this kernel (programmatic dependent launch,
+    // gd_device_config.pdl) may take SM slots as this grid's CTAs retire; it
+    // waits for this grid's completion before reading anything
+    asm volatile("griddepcontrol.launch_dependents;");
     if (!cta_stopped(ctl, &s_flag)) {
         const u64* outer;
         u64 n;
@@ -1383,6 +1387,9 @@ __global__ void __launch_bounds__(kLT, PER >= 8 ? 3 : 5) loop_expand_insert_kern
     __shared__ u64 sbuf[kLT / 32][PER >= 8 ? kXBuf : kXBuf / 2];
     __shared__ u64 red[kLT / 32];
     __shared__ u32 s_flag;
+    // launched as a programmatic dependent of loop_count (pdl): wait for its
+    // completion and memory (a no-op under a plain launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     bool stopped;
     if (do_gate) {  // the iteration's gate, evaluated here instead of in loop_count's last CTA
         if (threadIdx.x == 0) s_flag = gate_eval(ctl, g, blockIdx.x == 0) ? 1u : 0u;
@@ -2181,7 +2188,20 @@ void loop_expand_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head
     LoopGateDesc g{};
     if (gate) g = *gate;
     const int waves = c.cfg.insert_waves ? (int)c.cfg.insert_waves : 1;
-    if (c.cfg.expand_keys_per_lane == 4)
+    if (c.cfg.expand_keys_per_lane == 4 && c.cfg.pdl) {
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3((unsigned)(c.num_sms * g_occ_expand4 * waves));
+        lc.blockDim = dim3(kLT);
+        lc.dynamicSmemBytes = 0;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        GD_CUDA(cudaLaunchKernelEx(&lc, loop_expand_insert_kernel<1, 4>, ctl, step, head, o, inner, jd, dense, sb,
+                                   heavy_rows, hb, e, end ? 1 : 0, g, gate ? 1 : 0));
+    } else if (c.cfg.expand_keys_per_lane == 4)
         loop_expand_insert_kernel<1, 4><<<c.num_sms * g_occ_expand4 * waves, kLT, 0, s>>>(
             ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0, g, gate ? 1 : 0);
     else

@@ -201,6 +201,13 @@ typedef struct gd_device_config {
                                        CTA of the insert kernel instead of loop_count's last CTA (1) */
     uint32_t pdl;                   /* the warp-expanded insert is a programmatic dependent launch of loop_count
                                        (its CTAs take SM slots as the count's retire, then wait for it) (0) */
+    uint32_t count_ahead;           /* a single self-recursive warp-expanded step over light inner groups (TC):
+                                       the insert sums the next iteration's candidates as it appends its rows,
+                                       so the graph iteration is the insert kernel alone (0: C2 152.7-152.9
+                                       vs 152.1-152.4 ms; a near-empty iteration 22.5 -> 20.6 us) */
+    uint64_t chain_chunk_rows;      /* host-driven loop: a final join step with more output rows than this runs
+                                       in row ranges of about this many outputs, the sink hash-deduplicated
+                                       between them (0: an eighth of the free HBM) */
 } gd_device_config;
 
 void gd_device_config_default(gd_device_config* cfg);

@@ -95,6 +95,8 @@ class gd_device_config(C.Structure):
         ("download_pipeline_min_rows", u64),
         ("gate_in_insert", u32),
         ("pdl", u32),
+        ("count_ahead", u32),
+        ("chain_chunk_rows", u64),
     ]
 
 

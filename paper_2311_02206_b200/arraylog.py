@@ -230,6 +230,8 @@ _ENV_KNOBS = {
     "GD_DL_PIPELINE_MIN": ("download_pipeline_min_rows", int),
     "GD_GATE_IN_INSERT": ("gate_in_insert", int),
     "GD_PDL": ("pdl", int),
+    "GD_COUNT_AHEAD": ("count_ahead", int),
+    "GD_CHAIN_CHUNK_ROWS": ("chain_chunk_rows", int),
     "GD_XP_PER": ("expand_keys_per_lane", int),
     "GD_WARP_APPEND": ("warp_append", int),
     "GD_PRECOUNT": ("precount", int),

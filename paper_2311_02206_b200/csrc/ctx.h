@@ -155,6 +155,7 @@ inline gd_device_config default_device_config() {
     d.download_pipeline_min_rows = 1ull << 24;
     d.gate_in_insert = 1;
     d.pdl = 0;
+    d.count_ahead = 0;
     return d;
 }
 

@@ -314,6 +314,24 @@ void byte_pack_into(Ctx& c, const u64* keys, u64 n, u64* heads, uint8_t* cls, u6
     c.check_launch();
 }
 
+__global__ void rebase_kernel(const u64* __restrict__ off, u64 lo, u64 n1, u64* __restrict__ out) {
+    const u64 base = off[lo];
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n1; i += (u64)gridDim.x * blockDim.x)
+        out[i] = off[lo + i] - base;
+}
+
+void gather_strided(Ctx& c, const u64* src, u64 stride, u64 n, u64 m, u64* dst) {
+    gather_kernel<<<(unsigned)((m + 1 + 255) / 256), 256, 0, c.stream>>>(src, stride, n, m, dst);
+    c.check_launch();
+}
+
+void offsets_rebase(Ctx& c, const u64* off, u64 lo, u64 n1, u64* out) {
+    if (!n1) return;
+    const int grid = (int)std::max<u64>(1, std::min<u64>((n1 + 255) / 256, (u64)c.num_sms * 8));
+    rebase_kernel<<<grid, 256, 0, c.stream>>>(off, lo, n1, out);
+    c.check_launch();
+}
+
 void byte_unit_offsets(Ctx& c, const BytePacked& d, u64 blocks_per_unit, u64 nunits, u64* dev_out) {
     gather_kernel<<<(unsigned)((nunits + 1 + 255) / 256), 256, 0, c.stream>>>(d.offs.p, blocks_per_unit, d.nb,
                                                                              nunits, dev_out);

@@ -1258,6 +1258,25 @@ public:
         }
         c.h2d(ctl.p, hc, sizeof(LoopCtl));
 
+        // Count ahead (gd_device_config.count_ahead): a single self-recursive
+        // warp-expanded step whose inner groups are all light (no heavy
+        // segments possible) drops loop_count from the iteration: the insert
+        // sums the next iteration's candidates as it appends the rows, loop_end
+        // makes that the next gate's total, the insert evaluates the gate, and
+        // the rows' ranges are read inline.  loop_count runs eagerly only
+        // before the first graph launch and after a rollback.
+        const bool loop_eager = c.prof.on || c.cfg.loop_mode == GD_LOOP_EAGER;
+        const bool count_ahead = c.cfg.count_ahead && c.cfg.gate_in_insert && !loop_eager &&
+                                 c.cfg.loop_mode != GD_LOOP_BATCH && ns == 1 && steps[0].xp && steps[0].final &&
+                                 !steps[0].split_insert && !steps[0].pre && steps[0].kind == LO_DELTA &&
+                                 steps[0].src_head == steps[0].head &&
+                                 loop_dense_max_group(c, steps[0].dv) <= c.cfg.heavy_rows;
+        auto light_bufs = [&](const LStep& L) {  // no row ranges handed over: read inline
+            LoopStepBufs b = L.bufs();
+            b.rc = b.rc2 = nullptr;
+            return b;
+        };
+
         auto outer_of = [&](const LStep& L) {
             LoopOuter o{};
             o.kind = L.kind;
@@ -1320,6 +1339,7 @@ public:
                 }
                 cudaEvent_t t = br();
                 if (L.xp) {
+                    if (count_ahead) continue;  // the last insert counted this iteration's rows
                     loop_count(c, s, ctl.p, i, o, L.jd, L.dv, L.bufs(), c.cfg.heavy_rows,
                                fuse_gate && !gate_ins && i + 1 == ns ? &g : nullptr);
                     prof_recs.push_back({c.prof_end(t, KC_PROBE, 0), 4, i});
@@ -1343,7 +1363,7 @@ public:
                 c.prof_end(t, KC_LOOP_CTL, 0);
             }
             const LoopEndDesc end{LoopHist{hist_rec.p, hist_steps.p, ns}, cond, use_cond ? 1 : 0,
-                                  ns == 1 && steps[0].pre ? 0u : ~0u};
+                                  ns == 1 && (steps[0].pre || count_ahead) ? 0u : ~0u};
             u32 last_final = 0;
             for (u32 i = 0; i < ns; ++i)
                 if (steps[i].final) last_final = i;
@@ -1359,7 +1379,10 @@ public:
                     loop_expand_temp(c, s, ctl.p, i, o, L.inner, L.jd, L.dv, L.bufs(), c.cfg.heavy_rows, L.temp.p,
                                      L.temp_cap);
                     loop_insert_keys(c, s, ctl.p, i, L.head, L.temp.p, bufs_of(L.head), e);
-                } else if (L.xp)
+                } else if (L.xp && count_ahead)
+                    loop_expand_insert(c, s, ctl.p, i, L.head, o, L.inner, L.jd, L.dv, light_bufs(L), ~0ull,
+                                       bufs_of(L.head), e, &g, true);
+                else if (L.xp)
                     loop_expand_insert(c, s, ctl.p, i, L.head, o, L.inner, L.jd, L.dv, L.bufs(), c.cfg.heavy_rows,
                                        bufs_of(L.head), e, gate_ins ? &g : nullptr);
                 else if (L.split_insert)
@@ -1681,6 +1704,7 @@ public:
 
         u64 rollbacks = 0;
         u32 done_iters = 0;
+        bool need_count = true;  // count_ahead: the current Δ has no candidate total yet
         std::vector<u64> prev_log_n(nh);
         for (u32 h = 0; h < nh; ++h) prev_log_n[h] = hc->h[h].log_n;
         {
@@ -1690,6 +1714,11 @@ public:
                     prof_recs.clear();
                     record_iteration(c.stream, false, 0);
                 } else {
+                    if (count_ahead && need_count) {  // this iteration's candidates, counted once here
+                        const LStep& L = steps[0];
+                        loop_count(c, c.stream, ctl.p, 0, outer_of(L), L.jd, L.dv, light_bufs(L), ~0ull, nullptr);
+                        need_count = false;
+                    }
                     const double tb = Ctx::now_s();
                     const bool built = !exec;
                     if (!exec) build_graph();
@@ -1748,6 +1777,7 @@ public:
                         if (!steps[i].final && hc->need_temp[i] > temp_limit && wstep == UINT32_MAX) wstep = i;
                     grow_after_overflow();
                     hc->overflow = 0;
+                    need_count = true;  // the rollback cleared the candidate totals
                     c.h2d(ctl.p, hc, sizeof(LoopCtl));
                     c.sync();
                     destroy_graph();
@@ -2950,6 +2980,21 @@ private:
                 }
             }
             Tracked out_charge(E.acct, Accountant::kTemp, total * st.proj_arity * 8ull, "join");
+            if constexpr (std::is_same_v<K, u64>) {
+                // output-bounded final step (engine.hpp:401-484,
+                // PAPER.md:429-478): a final step whose output would not fit runs in
+                // row ranges of bounded output, the sink deduplicated between them
+                // (hash set, dedup.cu) so it holds about the distinct rows; the
+                // logical counts and charges stay the reference's
+                const u64 limit = chain_chunk_rows();
+                if (last && st.nfilters == 0 && c.cfg.hash_dedup && total > limit && cur_n > 1) {
+                    PhaseTimer t(E, "join");
+                    chunked_final_step(cur, cur_n, inner, jd, row_start.p, row_off.p, total, limit, sink, sink_n);
+                    E.join_tuples += total;
+                    *produced = total;
+                    break;
+                }
+            }
             K* dst;
             DevBuf<K> out;
             if (last) {
@@ -2979,6 +3024,80 @@ private:
             cur_n = total;
             cur_ar = st.proj_arity;
             for (u32 i = 0; i < kMaxArity; ++i) cur_perm[i] = i;
+        }
+    }
+
+    // Output rows one chunk of a chained final step may materialize
+    // (gd_device_config.chain_chunk_rows; 0: an eighth of the free HBM).
+    u64 chain_chunk_rows() const {
+        if (c.cfg.chain_chunk_rows) return c.cfg.chain_chunk_rows;
+        return std::max<u64>(1ull << 24, c.available_bytes() / 8 / sizeof(u64));
+    }
+
+    // The final step of a chain over outer rows [0, n) in row ranges whose
+    // output stays near `limit` rows (range ends from offsets sampled at
+    // 64 K points; one sampled interval is the smallest range), appended
+    // to the sink, which is hash-deduplicated whenever it passes `limit`.
+    void chunked_final_step(const u64* outer, u64 n, const u64* inner, const DevJoin& jd, const u64* row_start,
+                            const u64* row_off, u64 total, u64 limit, DevBuf<u64>& sink, u64& sink_n) {
+        const u64 S = std::min<u64>(n, 1ull << 16);
+        const u64 stride = (n + S - 1) / S;
+        const u64 m = (n + stride - 1) / stride;  // samples k * stride < n, plus row_off[n]
+        std::vector<u64> off(m + 1);
+        {
+            DevBuf<u64> d(c, m + 1);
+            gather_strided(c, row_off, stride, n, m, d.p);
+            c.d2h(off.data(), d.p, (m + 1) * sizeof(u64));
+            c.sync();
+        }
+        auto row_of = [&](u64 k) { return std::min(k * stride, n); };
+        std::vector<u64> ends;  // sample indices ending each range
+        u64 k0 = 0;
+        for (u64 k = 1; k <= m; ++k) {
+            if (off[k] - off[k0] > limit && k - 1 > k0) {
+                ends.push_back(k - 1);
+                k0 = k - 1;
+            }
+        }
+        ends.push_back(m);
+        u64 max_rows = 0;
+        k0 = 0;
+        for (u64 k : ends) {
+            max_rows = std::max(max_rows, row_of(k) - row_of(k0));
+            k0 = k;
+        }
+        DevBuf<u64> roff(c, max_rows + 1);
+        const bool trace = (c.cfg.trace & 1) != 0;
+        k0 = 0;
+        for (u64 k : ends) {
+            const u64 r0 = row_of(k0), r1 = row_of(k), cnt = off[k] - off[k0];
+            k0 = k;
+            if (!cnt) continue;
+            offsets_rebase(c, row_off, r0, r1 - r0 + 1, roff.p);
+            ensure_keep(c, sink, sink_n + cnt, sink_n);
+            join_materialize<u64>(c, outer + r0, r1 - r0, inner, jd, row_start + r0, roff.p, cnt, sink.p + sink_n,
+                                  nullptr);
+            sink_n += cnt;
+            if (sink_n > limit) compact_sink(sink, sink_n);
+            if (trace)
+                fprintf(stderr, "[chain] rows [%llu, %llu): %llu outputs, sink %llu rows\n",
+                        (unsigned long long)r0, (unsigned long long)r1, (unsigned long long)cnt,
+                        (unsigned long long)sink_n);
+        }
+        (void)total;
+    }
+
+    // Sink rows -> their distinct rows (hash set; the set grows until it fits).
+    void compact_sink(DevBuf<u64>& sink, u64& sink_n) {
+        for (u64 expect = std::max<u64>(sink_n / 4, 1 << 16);; expect *= 2) {
+            DevBuf<u64> uniq(c, std::min<u64>(sink_n, 2 * expect + 1));
+            const u64 u = hash_dedup(c, sink.p, sink_n, expect, uniq.p, uniq.cap);
+            if (u != ~0ull) {
+                sink = std::move(uniq);
+                sink_n = u;
+                return;
+            }
+            if (expect >= sink_n) return;  // no set fits: keep the rows as they are
         }
     }
 
@@ -3028,7 +3147,9 @@ private:
         DevBuf<K> rows;
         u64 m = 0, produced = 0;
         execute_chain(v, rows, m, &produced);
-        Tracked rows_charge(E.acct, Accountant::kTemp, rb(m, ar), "join");
+        // charges follow the logical rows (a chunked final step leaves them deduplicated)
+        const u64 mlog = std::max<u64>(m, produced);
+        Tracked rows_charge(E.acct, Accountant::kTemp, rb(mlog, ar), "join");
         if (m == 0) return;
         auto& head = rels[h];
         K* sorted;
@@ -3043,7 +3164,7 @@ private:
             mr = difference_full(head, sorted, m, gained.p);
         }
         {
-            Tracked scratch(E.acct, Accountant::kTemp, m * 8 + rb(m, ar), "dedup");
+            Tracked scratch(E.acct, Accountant::kTemp, mlog * 8 + rb(mlog, ar), "dedup");
         }
         Tracked fresh_charge(E.acct, Accountant::kTemp, rb(mr.unique_new, ar), "dedup");
         rows_charge.reset();
@@ -3066,6 +3187,9 @@ private:
         RelInfo& ri = E.info_[r];
         const u32 ar = ri.arity;
         const u64 m = st.new_n;
+        // the reference's charges follow the logical join rows (a chunked final
+        // step leaves fewer, deduplicated rows in new_acc)
+        const u64 mlog = std::max<u64>(m, (u64)log.join);
         MergeResult mr;
         if (m > 0) {
             K* sorted;
@@ -3100,7 +3224,7 @@ private:
             ensure_discard(c, st.delta_alt, ms);
             mr = difference_full(st, sorted, ms, st.delta_alt.p);
             st.last_unique = mr.unique_new;
-            Tracked scratch(E.acct, Accountant::kTemp, m * 8 + rb(m, ar), "dedup");
+            Tracked scratch(E.acct, Accountant::kTemp, mlog * 8 + rb(mlog, ar), "dedup");
         }
         Tracked fresh_charge(E.acct, Accountant::kTemp, rb(mr.unique_new, ar), "dedup");
         // clear_new, engine.hpp:497-501

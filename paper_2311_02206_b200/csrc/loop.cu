@@ -1142,11 +1142,13 @@ struct InsertSink {
     const LoopDense* dv = nullptr;
     LoopStepBufs nb = LoopStepBufs();
     u64 heavy_min = 0, d0 = 0;
+    bool cand_only = false;  // count ahead: only the next iteration's candidate total
     // Row r of the next iteration (an appended key): its inner range and
     // heavy items, as loop_count would write them; returns its candidates.
     __device__ __forceinline__ u64 precount(u64 r, u64 key) {
         u64 a, c;
         dense_range(*dv, outer_prefix(*jd, key), a, c);
+        if (cand_only) return c;
         if (r >= nb.rows_cap) {
             ctl->pre_bad = 1;
             return c;
@@ -1383,7 +1385,8 @@ __device__ __forceinline__ void expand_rows(const LoopCtl* ctl, u32 step, const 
 template <int NS, int PER = kXPer, int XB = 1>
 __global__ void __launch_bounds__(kLT, PER >= 8 ? 3 : 5) loop_expand_insert_kernel(
     LoopCtl* ctl, u32 step, u32 head, LoopOuter o, const u64* __restrict__ inner, DevJoin jd, LoopDense dv,
-    LoopStepBufs sb, u64 heavy_min, LoopHeadBufs hb, LoopEndDesc e, int do_end, LoopGateDesc g, int do_gate) {
+    LoopStepBufs sb, u64 heavy_min, LoopHeadBufs hb, LoopEndDesc e, int do_end, LoopGateDesc g, int do_gate,
+    int count_ahead) {
     __shared__ u64 sbuf[kLT / 32][PER >= 8 ? kXBuf : kXBuf / 2];
     __shared__ u64 red[kLT / 32];
     __shared__ u32 s_flag;
@@ -1405,7 +1408,14 @@ __global__ void __launch_bounds__(kLT, PER >= 8 ? 3 : 5) loop_expand_insert_kern
         const LoopStepBufs cur = bufs_of_iter(sb, ctl, false);
         InsertSink<NS, PER> sink{hb, ctl->iter + 1 - ctl->epoch_base,
                                  reinterpret_cast<unsigned long long*>(&ctl->h[head].log_n)};
-        if (sb.rc2) {  // precount the next iteration's rows as they are appended
+        if (count_ahead) {  // the next iteration's candidate total, summed as its rows are appended
+            sink.pre = true;
+            sink.cand_only = true;
+            sink.ctl = ctl;
+            sink.jd = &jd;
+            sink.dv = &dv;
+            sink.d0 = ctl->h[head].dhi;
+        } else if (sb.rc2) {  // precount the next iteration's rows as they are appended
             sink.pre = true;
             sink.ctl = ctl;
             sink.jd = &jd;
@@ -2071,6 +2081,27 @@ __global__ void dense_offsets_kernel(const u64* __restrict__ rows, u64 n, u32 ar
 }
 }  // namespace
 
+__global__ void dense_max_group_kernel(const u32* __restrict__ off, u64 span, unsigned long long* out) {
+    u32 m = 0;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < span; i += (u64)gridDim.x * blockDim.x)
+        m = max(m, off[i + 1] - off[i]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, (unsigned long long)m);
+}
+
+u64 loop_dense_max_group(Ctx& c, const LoopDense& dv) {
+    if (!dv.off || !dv.span) return 0;
+    DevBuf<unsigned long long> m(c, 1);
+    c.memset(m.p, 0, sizeof(unsigned long long));
+    const int grid = (int)std::max<u64>(1, std::min<u64>((dv.span + 255) / 256, (u64)c.num_sms * 8));
+    dense_max_group_kernel<<<grid, 256, 0, c.stream>>>(dv.off, dv.span, m.p);
+    c.check_launch();
+    unsigned long long v = 0;
+    c.read_words(&v, m.p, 1);
+    return v;
+}
+
 bool loop_dense_build(Ctx& c, const u64* rows, u64 n, u32 arity, u32 bits, DevBuf<u32>& off, u64& lo, u64& span) {
     if (n == 0 || n >= (1ull << 32)) return false;
     unsigned long long first = 0, last = 0;
@@ -2182,7 +2213,8 @@ void loop_count(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter&
 
 void loop_expand_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
                         const u64* inner, const DevJoin& jd, const LoopDense& dense, const LoopStepBufs& sb,
-                        u64 heavy_rows, const LoopHeadBufs& hb, const LoopEndDesc* end, const LoopGateDesc* gate) {
+                        u64 heavy_rows, const LoopHeadBufs& hb, const LoopEndDesc* end, const LoopGateDesc* gate,
+                        bool count_ahead) {
     LoopEndDesc e{};
     if (end) e = *end;
     LoopGateDesc g{};
@@ -2200,13 +2232,15 @@ void loop_expand_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head
         lc.attrs = at;
         lc.numAttrs = 1;
         GD_CUDA(cudaLaunchKernelEx(&lc, loop_expand_insert_kernel<1, 4>, ctl, step, head, o, inner, jd, dense, sb,
-                                   heavy_rows, hb, e, end ? 1 : 0, g, gate ? 1 : 0));
+                                   heavy_rows, hb, e, end ? 1 : 0, g, gate ? 1 : 0, count_ahead ? 1 : 0));
     } else if (c.cfg.expand_keys_per_lane == 4)
         loop_expand_insert_kernel<1, 4><<<c.num_sms * g_occ_expand4 * waves, kLT, 0, s>>>(
-            ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0, g, gate ? 1 : 0);
+            ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0, g, gate ? 1 : 0,
+            count_ahead ? 1 : 0);
     else
         SLOT_DISPATCH(c, loop_expand_insert_kernel, <<<c.num_sms * g_occ_expand * waves, kLT, 0, s>>>(
-        ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0, g, gate ? 1 : 0));
+        ctl, step, head, o, inner, jd, dense, sb, heavy_rows, hb, e, end ? 1 : 0, g, gate ? 1 : 0,
+        count_ahead ? 1 : 0));
     c.check_launch();
 }
 

@@ -306,7 +306,9 @@ void loop_count(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, const LoopOuter&
 void loop_expand_insert(Ctx& c, cudaStream_t s, LoopCtl* ctl, u32 step, u32 head, const LoopOuter& o,
                         const u64* inner, const DevJoin& jd, const LoopDense& dense, const LoopStepBufs& sb,
                         u64 heavy_rows, const LoopHeadBufs& hb, const LoopEndDesc* end,
-                        const LoopGateDesc* gate = nullptr);
+                        const LoopGateDesc* gate = nullptr, bool count_ahead = false);
+// Largest inner group of a dense index (max off[i + 1] - off[i]; one host sync).
+u64 loop_dense_max_group(Ctx& c, const LoopDense& dv);
 
 // The same expansion appended to the step's temp (split final step, then
 // loop_insert_keys over the temp).

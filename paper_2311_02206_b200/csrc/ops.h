@@ -75,6 +75,10 @@ u64 byte_pack(Ctx& c, const u64* keys, u64 n, BytePacked& out);
 // nb)] for k = 0..ceil(nb / blocks_per_unit).
 void byte_pack_into(Ctx& c, const u64* keys, u64 n, u64* heads, uint8_t* cls, u64* offs, uint8_t* payload,
                     u64 blocks_per_unit, u64* unit_offs);
+// dst[k] = src[min(k * stride, n)] for k = 0..m.
+void gather_strided(Ctx& c, const u64* src, u64 stride, u64 n, u64 m, u64* dst);
+// out[i] = off[lo + i] - off[lo] for i < n1 (a row range's join offsets from 0).
+void offsets_rebase(Ctx& c, const u64* off, u64 lo, u64 n1, u64* out);
 // dev_out[k] = d.offs[min(k * blocks_per_unit, nb)] for k = 0..nunits.
 void byte_unit_offsets(Ctx& c, const BytePacked& d, u64 blocks_per_unit, u64 nunits, u64* dev_out);
 

@@ -298,3 +298,44 @@ def test_cspa_random_medium(ref):
     rng = np.random.default_rng(8)
     db = {"assign": random_relation(rng, 2, 400, 120), "dereference": random_relation(rng, 2, 500, 120)}
     assert_same(run_gpu("cspa", db), run_ref(ref, "cspa", db), ["ValueFlow", "ValueAlias", "MemoryAlias"])
+
+
+@pytest.mark.parametrize("chunk", [40, 700, 20000])
+@pytest.mark.parametrize("prog", ["cspa", "sg", "reach"])
+def test_chunked_final_steps_match_reference(ref, prog, chunk):
+    """Host-driven loop with every final join step above `chunk` output rows
+    run in row ranges of about that many outputs (chain_chunk_rows), the
+    join sink hash-deduplicated between the ranges (engine.cu
+    chunked_final_step): relations, Δ history, iterations and the
+    reference's charge events, peaks and EBM allocations are unchanged
+    (the charges follow the logical join rows)."""
+    rng = np.random.default_rng(chunk + len(prog))
+    if prog == "cspa":
+        db = {"assign": random_relation(rng, 2, 400, 120), "dereference": random_relation(rng, 2, 500, 120)}
+        names = ["ValueFlow", "ValueAlias", "MemoryAlias"]
+    else:
+        db = {"Edge": random_relation(rng, 2, 3000, 1200) if prog == "reach" else random_relation(rng, 2, 900, 700)}
+        names = [{"reach": "Reach", "sg": "SG"}[prog]]
+    with al.default_context().configured(resident_loop=0, chain_chunk_rows=chunk):
+        g = run_gpu(prog, db)
+    assert_same(g, run_ref(ref, prog, db), names)
+
+
+def test_chunked_final_steps_under_budget(ref):
+    """Chunked final steps under a finite budget: the reference's budget
+    outcome (error phase or peaks) is unchanged."""
+    from oracle.bindings import OracleError
+    rng = np.random.default_rng(77)
+    db = {"assign": random_relation(rng, 2, 300, 100), "dereference": random_relation(rng, 2, 400, 100)}
+    for budget in (20_000, 200_000, 2_000_000):
+        cfg = al.engine_config(memory_budget_bytes=budget)
+        try:
+            r = run_ref(ref, "cspa", db, cfg)
+        except OracleError as e:
+            with pytest.raises(al.budget_error) as ei, al.default_context().configured(chain_chunk_rows=64):
+                run_gpu("cspa", db, cfg)
+            assert ei.value.phase() == e.phase
+            continue
+        with al.default_context().configured(chain_chunk_rows=64):
+            g = run_gpu("cspa", db, cfg)
+        assert_same(g, r, ["ValueFlow", "ValueAlias", "MemoryAlias"])

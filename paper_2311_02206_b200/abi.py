@@ -97,6 +97,7 @@ class gd_device_config(C.Structure):
         ("pdl", u32),
         ("count_ahead", u32),
         ("chain_chunk_rows", u64),
+        ("log_growth", u32),
     ]
 
 

@@ -232,6 +232,7 @@ _ENV_KNOBS = {
     "GD_PDL": ("pdl", int),
     "GD_COUNT_AHEAD": ("count_ahead", int),
     "GD_CHAIN_CHUNK_ROWS": ("chain_chunk_rows", int),
+    "GD_LOG_GROWTH": ("log_growth", int),
     "GD_XP_PER": ("expand_keys_per_lane", int),
     "GD_WARP_APPEND": ("warp_append", int),
     "GD_PRECOUNT": ("precount", int),

@@ -276,6 +276,7 @@ gd_status gd_ctx_set_device_config(gd_ctx* ctx, const gd_device_config* cfg) {
         if (cfg->download_chunk_rows < (1u << 16)) throw_config("download_chunk_rows must be at least 65536");
         if (cfg->download_delta > 2) throw_config("download_delta must be 0, 1 or 2");
         if (cfg->index_load_pct > 90) throw_config("index_load_pct must be at most 90");
+        if (cfg->log_growth == 1 || cfg->log_growth > 64) throw_config("log_growth must be 0 or 2..64");
         if (cfg->sort_items != 4 && cfg->sort_items != 8 && cfg->sort_items != 16)
             throw_config("sort_items must be 4, 8 or 16");
         if (cfg->heavy_rows == 0) throw_config("heavy_rows must be positive");

@@ -156,6 +156,7 @@ inline gd_device_config default_device_config() {
     d.gate_in_insert = 1;
     d.pdl = 0;
     d.count_ahead = 0;
+    d.log_growth = 4;
     return d;
 }
 

@@ -1514,9 +1514,10 @@ public:
                 if (hc->need_log[h] > H.log_cap) {
                     const u64 need = hc->need_log[h];
                     u64 avail = c.available_bytes();
-                    if (2 * need * sizeof(u64) + reserve > avail / 2) avail = c.available_bytes(true);
+                    const u64 lg = c.cfg.log_growth ? c.cfg.log_growth : 2;
+                    if (lg * need * sizeof(u64) + reserve > avail / 2) avail = c.available_bytes(true);
                     const u64 fit = avail > reserve ? (avail - reserve) / sizeof(u64) : 0;
-                    const u64 cap = std::max(need + need / 16 + 1024, std::min(2 * need, fit));
+                    const u64 cap = std::max(need + need / 16 + 1024, std::min(lg * need, fit));
                     DevBuf<u64> nl(c, cap);
                     if (ln) loop_copy_u64(c, nl.p, H.log.p, ln);
                     H.log = std::move(nl);

@@ -449,8 +449,8 @@ def main():
             torch.distributed.all_reduce(sb)
             hb, db = int(sb[0].item()), int(sb[1].item())
         # bytes that crossed PCIe (the C-ABI counts every copy); the Reach
-        # download moves packed 8-byte keys, unpacked into the caller's u64
-        # rows by host threads
+        # download moves 32-key blocks of byte-aligned offsets, rebuilt into
+        # the caller's u64 rows by host threads (DESIGN.md §7 download)
         e2e = {"value": float(np.mean(joins)) / float(np.mean(e2e_t)), "unit": "tuples/s",
                "h2d_bytes_per_step": int(hb), "d2h_bytes_per_step": int(db),
                "host_rows_bytes": int(reach_n * 16), "seconds_per_step": float(np.mean(e2e_t)),

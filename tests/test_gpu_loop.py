@@ -47,6 +47,14 @@ MODES = {  # gd_device_config fields of each mode
     "window": {"temp_limit_rows": 7},
     "tiny_window": {"min_capacities": 1, "temp_limit_rows": 5},
     "window_xp": {"temp_limit_rows": 16, "warp_expand": 1},
+    # end-of-round insert variants: count ahead (no loop_count in the graph
+    # iteration; eager counts after every rollback), the insert as a
+    # programmatic dependent launch, the gate back in loop_count, 2x logs
+    "count_ahead": {"count_ahead": 1},
+    "tiny_count_ahead": {"count_ahead": 1, "min_capacities": 1},
+    "pdl": {"pdl": 1},
+    "gate_in_count": {"gate_in_insert": 0},
+    "log2": {"log_growth": 2},
 }
 
 
@@ -153,7 +161,8 @@ def test_hash_predup_matches_sort_path():
                                                                         hs.join_tuples)
 
 
-@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "noxp", "heavy", "tiny_heavy", "precount", "tiny_precount"])
+@pytest.mark.parametrize("mode", ["graph", "tiny", "eager", "noxp", "heavy", "tiny_heavy", "precount", "tiny_precount",
+                                  "count_ahead", "tiny_count_ahead", "pdl", "gate_in_count"])
 def test_hub_rows(ref, mode):
     """Hubs (in-degree 700, out-degree 300) give Δ rows with long match
     ranges next to short ones: the load-balanced expansion must match the

@@ -55,6 +55,8 @@ MODES = {  # gd_device_config fields of each mode
     "pdl": {"pdl": 1},
     "gate_in_count": {"gate_in_insert": 0},
     "log2": {"log_growth": 2},
+    "load35": {"index_load_pct": 35},
+    "tiny_load80": {"index_load_pct": 80, "min_capacities": 1},
 }
 
 

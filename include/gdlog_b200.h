@@ -211,6 +211,9 @@ typedef struct gd_device_config {
     uint32_t log_growth;            /* resident loop: a full head log grows to this many times the rows it must
                                        hold, when free HBM allows (4: C2 149.6 vs 152.9-153.2 ms at 2x,
                                        3 rollbacks instead of 8; 0 means 2) */
+    uint32_t download_overlap_pack;  /* byte-offset downloads: pack per 4 M-row chunk with an event behind each,
+                                       the host rebuilding chunk 0 while the device packs the rest (needs
+                                       8 B per row of scratch) (0) */
 } gd_device_config;
 
 void gd_device_config_default(gd_device_config* cfg);

@@ -98,6 +98,7 @@ class gd_device_config(C.Structure):
         ("count_ahead", u32),
         ("chain_chunk_rows", u64),
         ("log_growth", u32),
+        ("download_overlap_pack", u32),
     ]
 
 

@@ -233,6 +233,7 @@ _ENV_KNOBS = {
     "GD_COUNT_AHEAD": ("count_ahead", int),
     "GD_CHAIN_CHUNK_ROWS": ("chain_chunk_rows", int),
     "GD_LOG_GROWTH": ("log_growth", int),
+    "GD_DL_OVERLAP": ("download_overlap_pack", int),
     "GD_XP_PER": ("expand_keys_per_lane", int),
     "GD_WARP_APPEND": ("warp_append", int),
     "GD_PRECOUNT": ("precount", int),

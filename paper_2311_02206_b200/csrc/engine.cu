@@ -409,7 +409,10 @@ public:
         double t_wait = 0, t_unpack = 0;
         const unsigned hw = std::thread::hardware_concurrency();
         const unsigned nt = std::max(1u, std::min(hw ? hw : 8u, 32u));
-        if (c.cfg.download_delta == 2 && n > 0) {
+        if (c.cfg.download_delta == 2 && n > 0 && c.cfg.download_overlap_pack &&
+            n * sizeof(u64) + (1ull << 30) < c.available_bytes()) {
+            download_bytes_rows_overlap(keys, n, ar, out, nt, t_wait, t_unpack);
+        } else if (c.cfg.download_delta == 2 && n > 0) {
             download_bytes_rows(keys, n, ar, out, nt, t_wait, t_unpack);
         } else if (c.cfg.download_delta == 1 && n > 0) {
             download_delta_rows(keys, n, ar, out, nt, t_wait, t_unpack);
@@ -787,6 +790,142 @@ public:
         pool.clear();
         if (err) std::rethrow_exception(err);
         c.d2h_bytes += d2h_total.load() + (nunits + 1) * sizeof(u64);
+        t_wait += wait_ns.load() * 1e-9 / nt;
+        t_unpack += work_ns.load() * 1e-9 / nt;
+    }
+
+    // The same download with the packing overlapped (download_overlap_pack):
+    // each 4 M-row chunk is packed on its own (byte_pack_into: chunk-relative
+    // offsets, payload at 8 B per row of the chunk's first row) with an event
+    // behind it, every chunk's unit offsets are requested up front on a side
+    // stream behind its pack, and the copies run on a second side stream, so
+    // the host rebuild of chunk 0 starts while the device packs the rest and
+    // no thread is set aside for issuing.
+    void download_bytes_rows_overlap(const u64* keys, u64 n, u32 ar, u64* out, unsigned nt, double& t_wait,
+                                     double& t_unpack) {
+        constexpr u64 kUnitB = 8192;      // blocks per unit (256 K rows)
+        constexpr u64 kChunkUnits = 16;   // units per chunk (4 M rows)
+        constexpr u64 kChunkB = kUnitB * kChunkUnits;
+        const u64 nb = (n + kByteBlock - 1) / kByteBlock;
+        const u64 nunits = (nb + kUnitB - 1) / kUnitB;
+        const u64 nchunks = (nunits + kChunkUnits - 1) / kChunkUnits;
+        auto chunk_units = [&](u64 k) { return std::min(kChunkUnits, nunits - k * kChunkUnits); };
+        DevBuf<u64> heads(c, std::max<u64>(nb, 1)), offs(c, nb + nchunks), uoffs(c, nchunks * (kChunkUnits + 1));
+        DevBuf<uint8_t> cls(c, std::max<u64>(nb, 1));
+        DevBuf<u64> payload(c, std::max<u64>(n, 1));  // chunk k's bytes at 8 * (its first row)
+        auto up = [](u64 v) { return (v + 63) & ~63ull; };
+        const u64 a_heads = kChunkB * sizeof(u64), a_cls = up(kChunkB);
+        const u64 area = a_heads + a_cls + up(kChunkB * kByteBlock * sizeof(u64) + 64);
+        const u64 R = std::min<u64>(nchunks, 6);
+        uint8_t* stage = static_cast<uint8_t*>(c.pinned_staging(R * area + nchunks * (kChunkUnits + 1) * sizeof(u64)));
+        u64* uo = reinterpret_cast<u64*>(stage + R * area);  // chunk k: kChunkUnits + 1 unit offsets
+        std::vector<cudaEvent_t> evp(nchunks, nullptr), evm(nchunks, nullptr), ev(nchunks, nullptr);
+        cudaStream_t s2 = nullptr, sm = nullptr;
+        std::unique_ptr<std::atomic<int>[]> issued(new std::atomic<int>[nchunks]);
+        std::unique_ptr<std::atomic<u64>[]> finished(new std::atomic<u64>[nchunks]);
+        for (u64 k = 0; k < nchunks; ++k) {
+            issued[k].store(0);
+            finished[k].store(0);
+        }
+        std::atomic<u64> next{0};
+        std::atomic<bool> quit{false};
+        std::atomic<u64> d2h_total{0};
+        std::exception_ptr err;
+        std::mutex err_mu;
+        std::mutex issue_mu;  // issue() may run on two threads at once
+        std::vector<std::thread> pool;
+        struct Cleanup {
+            std::function<void()> f;
+            ~Cleanup() { f(); }
+        } cleanup{[&] {
+            quit.store(true, std::memory_order_release);
+            for (auto& th : pool)
+                if (th.joinable()) th.join();
+            for (cudaStream_t st : {s2, sm})
+                if (st) {
+                    cudaStreamSynchronize(st);
+                    cudaStreamDestroy(st);
+                }
+            cudaStreamSynchronize(c.stream);
+            for (auto* v : {&evp, &evm, &ev})
+                for (auto e : *v)
+                    if (e) cudaEventDestroy(e);
+            cudaGetLastError();
+        }};
+        GD_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        GD_CUDA(cudaStreamCreateWithFlags(&sm, cudaStreamNonBlocking));
+        for (u64 k = 0; k < nchunks; ++k) {
+            GD_CUDA(cudaEventCreateWithFlags(&evp[k], cudaEventDisableTiming));
+            GD_CUDA(cudaEventCreateWithFlags(&evm[k], cudaEventDisableTiming));
+            GD_CUDA(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+        }
+        uint8_t* pay = reinterpret_cast<uint8_t*>(payload.p);
+        for (u64 k = 0; k < nchunks; ++k) {
+            const u64 r0 = k * kChunkB * kByteBlock, cnt = std::min(kChunkB * kByteBlock, n - r0);
+            byte_pack_into(c, keys + r0, cnt, heads.p + k * kChunkB, cls.p + k * kChunkB, offs.p + k * kChunkB + k,
+                           pay + r0 * sizeof(u64), kUnitB, uoffs.p + k * (kChunkUnits + 1));
+            GD_CUDA(cudaEventRecord(evp[k], c.stream));
+            GD_CUDA(cudaStreamWaitEvent(sm, evp[k], 0));
+            GD_CUDA(cudaMemcpyAsync(uo + k * (kChunkUnits + 1), uoffs.p + k * (kChunkUnits + 1),
+                                    (chunk_units(k) + 1) * sizeof(u64), cudaMemcpyDeviceToHost, sm));
+            GD_CUDA(cudaEventRecord(evm[k], sm));
+        }
+        auto issue = [&](u64 k) {  // chunk k into area k % R, once its offsets are on the host
+            std::lock_guard<std::mutex> g(issue_mu);
+            GD_CUDA(cudaEventSynchronize(evm[k]));
+            uint8_t* a = stage + (k % R) * area;
+            const u64 b0 = k * kChunkB, nbk = std::min(kChunkB, nb - b0);
+            const u64* ku = uo + k * (kChunkUnits + 1);
+            const u64 p0 = ku[0], p1 = ku[chunk_units(k)];
+            GD_CUDA(cudaMemcpyAsync(a, heads.p + b0, nbk * sizeof(u64), cudaMemcpyDeviceToHost, s2));
+            GD_CUDA(cudaMemcpyAsync(a + a_heads, cls.p + b0, nbk, cudaMemcpyDeviceToHost, s2));
+            if (p1 > p0)
+                GD_CUDA(cudaMemcpyAsync(a + a_heads + a_cls, pay + b0 * kByteBlock * sizeof(u64) + p0, p1 - p0,
+                                        cudaMemcpyDeviceToHost, s2));
+            GD_CUDA(cudaEventRecord(ev[k], s2));
+            d2h_total.fetch_add(nbk * sizeof(u64) + nbk + (p1 - p0) + (chunk_units(k) + 1) * sizeof(u64),
+                                std::memory_order_relaxed);
+            issued[k].store(1, std::memory_order_release);
+        };
+        const u32 bits = E.enc.e.bits;
+        std::atomic<u64> wait_ns{0}, work_ns{0};
+        auto worker = [&] {
+            try {
+                while (!quit.load(std::memory_order_acquire)) {
+                    const u64 u = next.fetch_add(1, std::memory_order_acq_rel);
+                    if (u >= nunits) return;
+                    const u64 k = u / kChunkUnits, j = u - k * kChunkUnits;
+                    const double tw = Ctx::now_s();
+                    while (!issued[k].load(std::memory_order_acquire)) {
+                        if (quit.load(std::memory_order_acquire)) return;
+                        std::this_thread::yield();
+                    }
+                    GD_CUDA(cudaEventSynchronize(ev[k]));
+                    const double tu = Ctx::now_s();
+                    const uint8_t* a = stage + (k % R) * area;
+                    const u64* ku = uo + k * (kChunkUnits + 1);
+                    const u64 b0 = u * kUnitB, nbu = std::min(kUnitB, nb - b0), cb = b0 - k * kChunkB;
+                    byte_decode_rows(reinterpret_cast<const u64*>(a) + cb, a + a_heads + cb,
+                                     a + a_heads + a_cls + (ku[j] - ku[0]), b0 * kByteBlock, nbu, n, ar, bits, out);
+                    const double te = Ctx::now_s();
+                    wait_ns.fetch_add((u64)((tu - tw) * 1e9), std::memory_order_relaxed);
+                    work_ns.fetch_add((u64)((te - tu) * 1e9), std::memory_order_relaxed);
+                    if (finished[k].fetch_add(1, std::memory_order_acq_rel) + 1 == chunk_units(k) && k + R < nchunks)
+                        issue(k + R);  // area k % R is free again
+                }
+            } catch (...) {
+                std::lock_guard<std::mutex> g(err_mu);
+                if (!err) err = std::current_exception();
+                quit.store(true, std::memory_order_release);
+            }
+        };
+        for (unsigned t = 1; t < nt; ++t) pool.emplace_back(worker);
+        for (u64 k = 0; k < R; ++k) issue(k);  // each as soon as its chunk is packed
+        worker();
+        for (auto& th : pool) th.join();
+        pool.clear();
+        if (err) std::rethrow_exception(err);
+        c.d2h_bytes += d2h_total.load();
         t_wait += wait_ns.load() * 1e-9 / nt;
         t_unpack += work_ns.load() * 1e-9 / nt;
     }

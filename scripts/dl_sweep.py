@@ -23,15 +23,15 @@ n = e.relation_count("Reach")
 out = torch.empty((n, 2), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
 rid = e._rid("Reach")
 want = None
-for delta in (2, 1, 0):
-    for frac in ((0.0, 0.1, 0.2, 0.3) if delta == 2 else (0.0, 0.15)):
+for delta, ov in ((2, 1), (2, 0), (1, 0), (0, 0)):
+    for frac in ((0.0, 0.1) if delta == 2 else (0.0,)):
         ts = []
         for _ in range(4):
-            with ctx.configured(download_delta=delta, download_direct_frac=frac):
+            with ctx.configured(download_delta=delta, download_direct_frac=frac, download_overlap_pack=ov):
                 t = time.perf_counter()
                 ctx.check(ctx.lib.gd_engine_relation_download(e.h, rid, out.ctypes.data_as(C.c_void_p), n))
                 ts.append(time.perf_counter() - t)
         dig = int(out[::9973].sum())
         want = dig if want is None else want
         assert dig == want, "download differs between modes"
-        print(f"delta={delta} frac={frac}: " + " ".join(f"{x * 1e3:.0f}" for x in ts) + " ms", flush=True)
+        print(f"delta={delta} overlap={ov} frac={frac}: " + " ".join(f"{x * 1e3:.0f}" for x in ts) + " ms", flush=True)

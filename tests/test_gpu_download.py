@@ -224,3 +224,24 @@ def test_segmented_final_sort_small_relations():
         want, h0 = _reach_rows(edges, None, download_pipeline=0)
         assert h1 == h0
         assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("arity,n,hi", [(2, 3_000_000, 1 << 20), (3, 2_100_000, 1 << 14), (2, 40_000_000, 1 << 30)])
+def test_overlapped_pack_download(ref, arity, n, hi):
+    """Byte-offset download with the packing overlapped (download_overlap_pack:
+    4 M-row chunks packed with events, copies and rebuild starting on chunk
+    0; 40 M rows = 10 chunks through a ring of 6 staging areas): rows equal
+    the canonical input and the whole-array pack."""
+    src = COPY2 if arity == 2 else COPY3
+    prog = program_from_ref(ref.engine(src))
+    rng = np.random.default_rng(arity * 13 + n)
+    e = rng.integers(0, hi, size=(n, arity), dtype=np.uint64)
+    outs = {}
+    for ov in (1, 0):
+        with al.default_context().configured(download_delta=2, download_overlap_pack=ov):
+            g = al.engine(prog)
+            g.load_edb("E", al.tuple_array(arity, e))
+            g.run()
+            outs[ov] = g.relation("C").data.copy()
+    assert np.array_equal(outs[1], outs[0])
+    assert np.array_equal(outs[1].reshape(-1, arity), canonical(e))
